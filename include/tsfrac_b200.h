@@ -1,0 +1,189 @@
+/*
+ * tsfrac_b200 — C ABI of the B200-native FIDS per-time-step solve.
+ *
+ * Drop-in boundary for the reference Python package `tsfrac`
+ * (/root/reference/pkg/src/tsfrac).  Every entry point below names the
+ * reference function it replaces.  Plain pointers and sizes only; all
+ * vector arguments are DEVICE pointers (fp64, contiguous, instance-major
+ * [B][n]) unless documented as host.  `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  Nothing is freed across the ABI: the plan owns
+ * its tables and workspaces, the caller owns every I/O buffer.
+ *
+ * Return value: TSF_SUCCESS (0) or a negative TSF_E* code; the message is
+ * available from tsf_last_error() (thread-local).  Numerical outcomes of
+ * a solve (breakdowns, non-convergence, kappa <= 0, indefinite
+ * preconditioner) are reported per instance in `status` using the
+ * TSF_ST_* codes, which the Python layer maps to the reference's
+ * KrylovReport.breakdown strings and exceptions.
+ */
+#ifndef TSFRAC_B200_H
+#define TSFRAC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSF_ABI_VERSION 1
+
+/* API return codes */
+#define TSF_SUCCESS 0
+#define TSF_E_INVALID (-1)     /* bad argument (reference: ValueError) */
+#define TSF_E_CUDA (-2)        /* CUDA runtime error */
+#define TSF_E_UNSUPPORTED (-3) /* size / mode not built (e.g. non-pow2 n with precond) */
+#define TSF_E_NOMEM (-4)
+
+/* per-instance status codes (solve outcomes) */
+#define TSF_ST_OK 0
+#define TSF_ST_NOT_CONVERGED 1
+#define TSF_ST_RHO_VANISHED 2          /* "rho vanished"               krylov.py:119-121 */
+#define TSF_ST_R0V_VANISHED 3          /* "r0.v vanished"              krylov.py:130-132 */
+#define TSF_ST_OMEGA_DEN_VANISHED 4    /* "omega denominator vanished" krylov.py:141-143 */
+#define TSF_ST_OMEGA_VANISHED 5        /* "omega vanished"             krylov.py:151-152 */
+#define TSF_ST_NONPOS_CURVATURE 6      /* "non-positive curvature"     krylov.py:72-74   */
+#define TSF_ST_KAPPA_NONPOS 7          /* ValueError                   scheme.py:156-160 */
+#define TSF_ST_PRECOND_NONPOS 8        /* PreconditionerError          toeplitz.py:122-124 */
+
+typedef struct tsf_plan tsf_plan;
+
+int tsf_abi_version(void);
+const char* tsf_last_error(void);
+
+/*
+ * Plan for one spatial size n (reference: ToeplitzOperator built by
+ * build_toeplitz, toeplitz.py:34-48, plus the level-independent part of
+ * build_preconditioner, toeplitz.py:101-128).
+ *   L          circulant embedding length (power of two >= 2n-1, >= 32)
+ *   symbol_re  HOST, L reals: Re FFT_L(even embedding of the first column)
+ *   lam        HOST, n reals: Re FFT_n(strang_first_column), or NULL when
+ *              no preconditioner is needed (n need not be a power of two)
+ *   device     CUDA ordinal the plan lives on
+ */
+int tsf_plan_create(tsf_plan** plan, int n, int L, const double* symbol_re,
+                    const double* lam, int device);
+int tsf_plan_destroy(tsf_plan* plan);
+/* out[0]=n out[1]=L out[2]=N_mv(=L/2) out[3]=has_precond out[4]=max_batch_reserved */
+int tsf_plan_info(const tsf_plan* plan, int64_t* out5);
+/* reserve Krylov workspaces for `batch` instances (done lazily otherwise) */
+int tsf_plan_reserve(tsf_plan* plan, int batch);
+
+/*
+ * y = shift*x + kappa .* (A x)  for B instances.
+ * Reference: toeplitz_matvec (toeplitz.py:51-63) and the level closure
+ * apply(v) (scheme.py:129-130).  kappa == NULL gives the bare y = A x.
+ */
+int tsf_toeplitz_matvec(tsf_plan* plan, int B, const double* x, double* y,
+                        const double* kappa, double shift, void* stream);
+
+/*
+ * z = P^{-1} v with P = shift*I + kappa_bar*s(A)  (Strang circulant).
+ * Reference: precond_solve (toeplitz.py:131-136) of build_preconditioner(
+ * d, shift, kappa_bar) (toeplitz.py:101-128).  kappa_bar_dev (device, [B])
+ * overrides kappa_bar per instance when non-NULL.  Requires pow2 n.
+ */
+int tsf_precond_solve(tsf_plan* plan, int B, const double* v, double* z,
+                      double shift, double kappa_bar, const double* kappa_bar_dev,
+                      void* stream);
+
+/*
+ * One level solve (shift*I + diag(kappa) A) x = rhs for B instances, x0 = 0.
+ * Reference: _LevelSolver.solve (scheme.py:120-143) -> solve_bicgstab
+ * (krylov.py:88-153) or solve_cg (krylov.py:43-85).  The preconditioner uses
+ * kappa_bar when > 0, else kappa_bar = mean(kappa) formed on the device
+ * (scheme.py:135).
+ *   method      0 = BiCGSTAB, 1 = CG
+ *   precond     0 = none ("krylov"), 1 = Strang ("pkrylov")
+ *   max_iters   <= 0 means the reference default 10*n
+ *   iters, relres, status: device [B]
+ */
+int tsf_krylov_solve(tsf_plan* plan, int B, int method, int precond,
+                     const double* rhs, double* x, const double* kappa, double shift,
+                     double kappa_bar, double tol, int max_iters, int* iters, double* relres, int* status,
+                     void* stream);
+
+/*
+ * SOE accumulator update fused with the next level's right-hand side.
+ * Reference: history_push (soe.py:209-225) followed by the history term and
+ * RHS assembly of the next level (scheme.py:279-284; fast_caputo_rhs,
+ * soe.py:228-246).
+ *   W        [B][nexp][n] accumulators (updated in place when do_push)
+ *   u, uprev [B][n]  level just solved and the one before (push uses u-uprev)
+ *   decay, coef, hcoef  device [nexp]: e^{-s tau}, -expm1(-s tau)/s,
+ *            w e^{-s tau_next}
+ *   f        [B][n] source at the next level (may be NULL when !do_rhs)
+ *   rhs      [B][n] output: f + (a_next*u - H)/G
+ */
+int tsf_soe_push_rhs(int B, int n, int nexp, double* W, const double* u,
+                     const double* uprev, double tau_push, const double* decay,
+                     const double* coef, const double* hcoef, int do_push, int w_zero,
+                     int do_rhs, double a_next, double G, const double* f, double* rhs,
+                     void* stream);
+
+/* Coefficient field  g(x_i, t_m) = sum_q modes_m[q][b][i] * coef[m][q], where
+ * modes_m = modes + m*t_stride.  Separable fields use t_stride = 0; a field
+ * tabulated per level (arbitrary callables evaluated on the host, as the
+ * reference does at scheme.py:156-160,283) uses one mode, coef = 1 and
+ * t_stride = B*n. */
+typedef struct tsf_field {
+  int nmodes;            /* 0..4 */
+  const double* modes;   /* device; mode q of instance b at modes_m + q*q_stride + b*b_stride */
+  int64_t q_stride;
+  int64_t b_stride;      /* 0 = shared by all instances */
+  int64_t t_stride;      /* per-level offset of the mode block (0 = time-independent modes) */
+  const double* coef;    /* HOST [M+1][nmodes]: coefficients at t_0..t_M */
+} tsf_field;
+
+/*
+ * Native FIDS time march (reference: run_fids loop body, scheme.py:276-294)
+ * for B independent instances that share (gamma, alpha, n, M, r): launches
+ * 2 kernels per level on `stream`, no host synchronisation.
+ *   u_buf0/u_buf1  [B][n]: u^0 in u_buf0 on entry; level m lands in
+ *                  u_buf[m & 1]
+ *   W              [B][nexp][n], zero on entry when m_begin == 1
+ *   shift, a_mm, tau  HOST [M]: level m at index m-1
+ *   soe_tab        device [M][3][nexp]: decay_m, coef_m, hcoef_m
+ *                  (hcoef_m = w e^{-s tau_m}) for levels 1..M
+ *   iters, relres, status  device [M][B]
+ *   hist           device [(M+1)][hist_B][n] or NULL: per-level copy of
+ *                  the first hist_B instances
+ *   Levels m_begin .. m_end-1 are run (1 <= m_begin <= m_end <= M+1); when
+ *   m_end == M+1 the final history push is applied as well.
+ */
+typedef struct tsf_march {
+  int B, M, nexp;
+  int method, precond;
+  double tol;
+  int max_iters;
+  double G;
+  const double* shift;
+  const double* a_mm;
+  const double* tau;
+  const double* soe_tab;
+  tsf_field kappa;
+  tsf_field source;
+  double* u_buf0;
+  double* u_buf1;
+  double* W;
+  double* rhs;
+  double* kwork;
+  int* iters;
+  double* relres;
+  int* status;
+  double* hist;
+  int hist_B;
+  int m_begin;
+  int m_end;
+} tsf_march;
+
+int tsf_fids_march(tsf_plan* plan, const tsf_march* desc, void* stream);
+
+/* Debug / test hook: B complex FFTs of length N (pow2, 16..8192) through the
+ * block Stockham engine.  inverse != 0 gives the unnormalised inverse. */
+int tsf_fft_debug(int N, int inverse, int B, const double* in, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TSFRAC_B200_H */

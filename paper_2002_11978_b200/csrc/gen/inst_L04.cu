@@ -1,0 +1,4 @@
+// generated: explicit instantiation of the N_mv = 2^4 engine
+#include "../tsf_dispatch_impl.cuh"
+
+template struct tsf::Dispatch<4>;

@@ -1,0 +1,4 @@
+// generated: explicit instantiation of the N_mv = 2^7 engine
+#include "../tsf_dispatch_impl.cuh"
+
+template struct tsf::Dispatch<7>;

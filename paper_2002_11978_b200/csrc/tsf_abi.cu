@@ -1,0 +1,438 @@
+// C ABI of the tsfrac B200 engine: plans, tables, dispatch, native march.
+// Declarations and reference mapping: include/tsfrac_b200.h.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tsfrac_b200.h"
+#include "tsf_dispatch.h"
+#include "tsf_soe.cuh"
+
+using namespace tsf;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(TSF_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
+  } while (0)
+
+int ilog2_host(long x) {
+  int r = 0;
+  while ((1L << r) < x) ++r;
+  return r;
+}
+bool is_pow2(long x) { return x > 0 && (x & (x - 1)) == 0; }
+
+
+}  // namespace
+
+namespace tsf {
+int report_cuda(cudaError_t e, const char* what) {
+  return fail(TSF_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+}  // namespace tsf
+
+struct tsf_plan {
+  int n = 0;
+  int L = 0;
+  int nmv = 0;
+  int log_nmv = 0;
+  int has_pc = 0;
+  int device = 0;
+  double2* tw = nullptr;
+  double2* mvab = nullptr;
+  double2* pclam = nullptr;
+  double2* pcsc = nullptr;
+  // Krylov workspaces [cap][n] x 5 + status scratch
+  int cap = 0;
+  double* ws = nullptr;
+  int* ist = nullptr;
+  double* dst = nullptr;
+  FilterTables tables() const { return FilterTables{tw, mvab, pclam, pcsc}; }
+};
+
+// ------------------------------------------------------------- dispatch
+namespace {
+
+template <template <int> class F, int LOG = kMinLogNmv>
+struct ForLog {
+  template <typename... A>
+  static int run(int log, A&&... args) {
+    if (log == LOG) return F<LOG>::call(static_cast<A&&>(args)...);
+    if constexpr (LOG < kMaxLogNmv) return ForLog<F, LOG + 1>::run(log, static_cast<A&&>(args)...);
+    return fail(TSF_E_UNSUPPORTED, "transform size 2^%d not built", log);
+  }
+};
+
+template <int LOG>
+struct MatvecF {
+  template <typename... A>
+  static int call(A... a) { return Dispatch<LOG>::matvec(a...); }
+};
+template <int LOG>
+struct PrecondF {
+  template <typename... A>
+  static int call(A... a) { return Dispatch<LOG>::precond(a...); }
+};
+template <int LOG>
+struct SolveF {
+  template <typename... A>
+  static int call(A... a) { return Dispatch<LOG>::solve(a...); }
+};
+template <int LOG>
+struct FftF {
+  template <typename... A>
+  static int call(A... a) { return Dispatch<LOG>::fft(a...); }
+};
+
+// twiddle table W_N^e, e < N, computed in long double
+std::vector<double2> twiddles(int N) {
+  std::vector<double2> t(N);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int e = 0; e < N; ++e) {
+    long double a = two_pi * (long double)e / (long double)N;
+    t[e] = make_double2((double)cosl(a), (double)-sinl(a));
+  }
+  return t;
+}
+
+
+int ensure_reserved(tsf_plan* p, int B) {
+  if (B <= p->cap) return TSF_SUCCESS;
+  if (p->ws) cudaFree(p->ws);
+  if (p->ist) cudaFree(p->ist);
+  if (p->dst) cudaFree(p->dst);
+  p->ws = nullptr;
+  p->ist = nullptr;
+  p->dst = nullptr;
+  p->cap = 0;
+  CK(cudaSetDevice(p->device));
+  CK(cudaMalloc(&p->ws, sizeof(double) * (size_t)B * p->n * 6));
+  CK(cudaMalloc(&p->ist, sizeof(int) * (size_t)B * 2));
+  CK(cudaMalloc(&p->dst, sizeof(double) * (size_t)B));
+  p->cap = B;
+  return TSF_SUCCESS;
+}
+
+}  // namespace
+
+// ======================================================================
+extern "C" {
+
+int tsf_abi_version(void) { return TSF_ABI_VERSION; }
+
+const char* tsf_last_error(void) { return g_err.c_str(); }
+
+int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const double* lam,
+                    int device) {
+  if (!out) return fail(TSF_E_INVALID, "plan pointer is NULL");
+  *out = nullptr;
+  if (n < 1) return fail(TSF_E_INVALID, "n must be >= 1, got %d", n);
+  if (!is_pow2(L) || L < 2 * n - 1 || L < 32)
+    return fail(TSF_E_INVALID, "L=%d must be a power of two >= max(2n-1, 32)", L);
+  if (!symbol_re) return fail(TSF_E_INVALID, "symbol is NULL");
+  const int nmv = L / 2;
+  const int lg = ilog2_host(nmv);
+  if (lg < kMinLogNmv || lg > kMaxLogNmv)
+    return fail(TSF_E_UNSUPPORTED, "embedding L=%d outside the single-CTA engine (32..16384)", L);
+  if (lam && !(is_pow2(n) && L == 2 * n))
+    return fail(TSF_E_UNSUPPORTED, "Strang preconditioner needs pow2 n with L = 2n (n=%d, L=%d)", n, L);
+  tsf_plan* p = new tsf_plan();
+  p->n = n;
+  p->L = L;
+  p->nmv = nmv;
+  p->log_nmv = lg;
+  p->device = device;
+  p->has_pc = lam != nullptr;
+  auto cleanup = [&](int rc) {
+    tsf_plan_destroy(p);
+    return rc;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return cleanup(fail(TSF_E_CUDA, "cudaSetDevice(%d)", device));
+  // twiddles for the largest transform (N_mv); the N_pc transform uses stride 2
+  std::vector<double2> tw = twiddles(nmv);
+  // Toeplitz symbol -> real-pack filter coefficients (a_k, b_k) / N_mv
+  std::vector<double2> ab(nmv);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int k = 0; k < nmv; ++k) {
+    long double s1 = symbol_re[k], s2 = symbol_re[k + nmv];
+    long double P = 0.5L * (s1 + s2), Q = 0.5L * (s1 - s2);
+    long double th = two_pi * (long double)k / (long double)L;
+    ab[k] = make_double2((double)((P - Q * sinl(th)) / nmv), (double)(Q * cosl(th) / nmv));
+  }
+  std::vector<double2> pl, ps;
+  if (lam) {
+    const int npc = n / 2;
+    pl.resize(npc);
+    ps.resize(npc);
+    for (int k = 0; k < npc; ++k) {
+      pl[k] = make_double2(lam[k], lam[k + npc]);
+      long double th = two_pi * (long double)k / (long double)n;
+      ps[k] = make_double2((double)sinl(th), (double)cosl(th));
+    }
+  }
+  auto up = [&](double2** d, const std::vector<double2>& h) -> int {
+    if (h.empty()) return TSF_SUCCESS;
+    CK(cudaMalloc(d, h.size() * sizeof(double2)));
+    CK(cudaMemcpy(*d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    return TSF_SUCCESS;
+  };
+  int rc;
+  if ((rc = up(&p->tw, tw)) || (rc = up(&p->mvab, ab)) || (rc = up(&p->pclam, pl)) ||
+      (rc = up(&p->pcsc, ps)))
+    return cleanup(rc);
+  *out = p;
+  return TSF_SUCCESS;
+}
+
+int tsf_plan_destroy(tsf_plan* p) {
+  if (!p) return TSF_SUCCESS;
+  cudaSetDevice(p->device);
+  cudaFree(p->tw);
+  cudaFree(p->mvab);
+  cudaFree(p->pclam);
+  cudaFree(p->pcsc);
+  cudaFree(p->ws);
+  cudaFree(p->ist);
+  cudaFree(p->dst);
+  delete p;
+  return TSF_SUCCESS;
+}
+
+int tsf_plan_info(const tsf_plan* p, int64_t* o) {
+  if (!p || !o) return fail(TSF_E_INVALID, "NULL argument");
+  o[0] = p->n;
+  o[1] = p->L;
+  o[2] = p->nmv;
+  o[3] = p->has_pc;
+  o[4] = p->cap;
+  return TSF_SUCCESS;
+}
+
+int tsf_plan_reserve(tsf_plan* p, int B) {
+  if (!p || B < 1) return fail(TSF_E_INVALID, "bad plan or batch");
+  return ensure_reserved(p, B);
+}
+
+int tsf_toeplitz_matvec(tsf_plan* p, int B, const double* x, double* y, const double* kappa,
+                        double shift, void* stream) {
+  if (!p || !x || !y || B < 0) return fail(TSF_E_INVALID, "bad argument");
+  if (B == 0) return TSF_SUCCESS;
+  return ForLog<MatvecF>::run(p->log_nmv, p->n, p->tables(), B, x, y, kappa, shift,
+                              (cudaStream_t)stream);
+}
+
+int tsf_precond_solve(tsf_plan* p, int B, const double* v, double* z, double shift,
+                      double kbar, const double* kbar_dev, void* stream) {
+  if (!p || !v || !z || B < 0) return fail(TSF_E_INVALID, "bad argument");
+  if (!p->has_pc) return fail(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner (non-pow2 n)");
+  if (B == 0) return TSF_SUCCESS;
+  return ForLog<PrecondF>::run(p->log_nmv, p->n, p->tables(), B, v, z, shift, kbar, kbar_dev,
+                               (cudaStream_t)stream);
+}
+
+static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cudaStream_t st) {
+  if (pc && !p->has_pc) return fail(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner");
+  int rc = ensure_reserved(p, B);
+  if (rc) return rc;
+  const size_t vn = (size_t)p->cap * p->n;
+  a.n = p->n;
+  a.B = B;
+  a.r = p->ws;
+  a.p = p->ws + vn;
+  a.v = p->ws + 2 * vn;
+  a.ph = p->ws + 3 * vn;
+  a.s = p->ws + 4 * vn;
+  if (!a.kwork) a.kwork = p->ws + 5 * vn;
+  a.tab = p->tables();
+  if (a.max_iters <= 0) a.max_iters = 10 * p->n;
+  return ForLog<SolveF>::run(p->log_nmv, B, method, pc, (const KrylovArgs&)a, st);
+}
+
+int tsf_krylov_solve(tsf_plan* p, int B, int method, int precond, const double* rhs, double* x,
+                     const double* kappa, double shift, double kappa_bar, double tol, int max_iters, int* iters,
+                     double* relres, int* status, void* stream) {
+  if (!p || !rhs || !x || !kappa || !iters || !relres || !status || B < 0)
+    return fail(TSF_E_INVALID, "bad argument");
+  if (method != 0 && method != 1) return fail(TSF_E_INVALID, "method must be 0 or 1");
+  if (B == 0) return TSF_SUCCESS;
+  KrylovArgs a{};
+  a.rhs = rhs;
+  a.x = x;
+  a.kappa = kappa;
+  a.shift = shift;
+  a.kbar = kappa_bar;
+  a.tol = tol;
+  a.max_iters = max_iters;
+  a.iters = iters;
+  a.relres = relres;
+  a.status = status;
+  return solve_impl(p, B, method, precond, a, (cudaStream_t)stream);
+}
+
+static int soe_launch(int B, SoeArgs& s, cudaStream_t st) {
+  if (B == 0) return TSF_SUCCESS;
+  const int chunks = (s.n + 2 * kSoeThreads - 1) / (2 * kSoeThreads);
+  const int smem = 3 * s.nexp * (int)sizeof(double);
+  if (smem > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_soe_push_rhs<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
+  k_soe_push_rhs<8><<<(unsigned)B * chunks, kSoeThreads, smem, st>>>(s);
+  CK(cudaGetLastError());
+  return TSF_SUCCESS;
+}
+
+int tsf_soe_push_rhs(int B, int n, int nexp, double* W, const double* u,
+                     const double* uprev, double tau_push, const double* decay,
+                     const double* coef, const double* hcoef, int do_push, int w_zero,
+                     int do_rhs, double a_next, double G, const double* f, double* rhs,
+                     void* stream) {
+  if (B < 0 || n < 1 || nexp < 1) return fail(TSF_E_INVALID, "bad argument");
+  if (do_push && (!uprev || !u || !decay || !coef || !(tau_push > 0.0)))
+    return fail(TSF_E_INVALID, "push needs u, uprev, decay, coef and tau_push > 0");
+  if (!w_zero && !W) return fail(TSF_E_INVALID, "W is NULL");
+  if (do_rhs && (!u || !hcoef || !rhs)) return fail(TSF_E_INVALID, "rhs needs u, hcoef, rhs");
+  SoeArgs s{};
+  s.n = n;
+  s.nexp = nexp;
+  s.W = W;
+  s.u = u;
+  s.uprev = uprev;
+  s.tau_push = tau_push;
+  s.decay = decay;
+  s.coef = coef;
+  s.hcoef = hcoef;
+  s.do_push = do_push;
+  s.w_zero = w_zero;
+  s.do_rhs = do_rhs;
+  s.a_next = a_next;
+  s.G = G;
+  s.nf = 0;
+  s.f = f;
+  s.rhs = rhs;
+  return soe_launch(B, s, (cudaStream_t)stream);
+}
+
+int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
+  if (!p || !d) return fail(TSF_E_INVALID, "NULL argument");
+  const int B = d->B, M = d->M, nexp = d->nexp, n = p->n;
+  if (B < 1 || M < 1 || nexp < 1) return fail(TSF_E_INVALID, "bad B/M/nexp");
+  if (d->m_begin < 1 || d->m_end < d->m_begin || d->m_end > M + 1)
+    return fail(TSF_E_INVALID, "bad level range [%d, %d)", d->m_begin, d->m_end);
+  if (d->kappa.nmodes < 1 || d->kappa.nmodes > kMaxModes || d->source.nmodes < 0 ||
+      d->source.nmodes > 4)
+    return fail(TSF_E_INVALID, "kappa needs 1..4 modes, source 0..4");
+  if (!d->u_buf0 || !d->u_buf1 || !d->W || !d->rhs || !d->soe_tab || !d->iters ||
+      !d->relres || !d->status || !d->shift || !d->a_mm || !d->tau)
+    return fail(TSF_E_INVALID, "NULL buffer in march descriptor");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_reserved(p, B);
+  if (rc) return rc;
+  double* ubuf[2] = {d->u_buf0, d->u_buf1};
+  const size_t vn = (size_t)B * n;
+  for (int m = d->m_begin; m < d->m_end; ++m) {
+    // ---- history term + RHS of level m from W^{m-1} (push of level m-1 fused)
+    SoeArgs s{};
+    s.n = n;
+    s.nexp = nexp;
+    s.W = d->W;
+    s.u = ubuf[(m - 1) & 1];   // u^{m-1}
+    s.uprev = ubuf[m & 1];     // u^{m-2} (buffer about to receive u^m)
+    s.do_push = m > 1;
+    s.w_zero = (m == 1);
+    if (m > 1) {
+      const double* tab = d->soe_tab + (size_t)(m - 2) * 3 * nexp;
+      s.tau_push = d->tau[m - 2];
+      s.decay = tab;
+      s.coef = tab + nexp;
+    }
+    s.hcoef = d->soe_tab + (size_t)(m - 1) * 3 * nexp + 2 * nexp;
+    s.do_rhs = 1;
+    s.a_next = d->a_mm[m - 1];
+    s.G = d->G;
+    s.nf = d->source.nmodes;
+    s.fmodes = d->source.modes ? d->source.modes + (size_t)m * d->source.t_stride : nullptr;
+    s.fq_stride = d->source.q_stride;
+    s.fb_stride = d->source.b_stride;
+    for (int q = 0; q < s.nf; ++q) s.fcoef[q] = d->source.coef[(size_t)m * s.nf + q];
+    s.f = nullptr;
+    s.rhs = d->rhs;
+    if ((rc = soe_launch(B, s, st))) return rc;
+    // ---- level solve  -> u^m into ubuf[m & 1]
+    KrylovArgs a{};
+    a.rhs = d->rhs;
+    a.x = ubuf[m & 1];
+    a.kappa = nullptr;
+    a.kmodes = d->kappa.modes + (size_t)m * d->kappa.t_stride;
+    a.kq_stride = d->kappa.q_stride;
+    a.kb_stride = d->kappa.b_stride;
+    a.nk = d->kappa.nmodes;
+    for (int q = 0; q < a.nk; ++q) a.kcoef[q] = d->kappa.coef[(size_t)m * a.nk + q];
+    a.kwork = d->kwork;
+    a.shift = d->shift[m - 1];
+    a.tol = d->tol;
+    a.max_iters = d->max_iters;
+    a.iters = d->iters + (size_t)(m - 1) * B;
+    a.relres = d->relres + (size_t)(m - 1) * B;
+    a.status = d->status + (size_t)(m - 1) * B;
+    if ((rc = solve_impl(p, B, d->method, d->precond, a, st))) return rc;
+    if (d->hist && d->hist_B > 0) {
+      CK(cudaMemcpyAsync(d->hist + (size_t)m * d->hist_B * n, ubuf[m & 1],
+                         sizeof(double) * (size_t)d->hist_B * n, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  if (d->m_end == M + 1 && d->m_begin <= M) {
+    // final push of level M (scheme.py:290 runs after every level)
+    const double* tab = d->soe_tab + (size_t)(M - 1) * 3 * nexp;
+    SoeArgs s{};
+    s.n = n;
+    s.nexp = nexp;
+    s.W = d->W;
+    s.u = ubuf[M & 1];
+    s.uprev = ubuf[(M - 1) & 1];
+    s.do_push = 1;
+    s.w_zero = (M == 1) ? 1 : 0;
+    s.tau_push = d->tau[M - 1];
+    s.decay = tab;
+    s.coef = tab + nexp;
+    s.hcoef = nullptr;
+    s.do_rhs = 0;
+    if ((rc = soe_launch(B, s, st))) return rc;
+  }
+  (void)vn;
+  return TSF_SUCCESS;
+}
+
+int tsf_fft_debug(int N, int inverse, int B, const double* in, double* out, void* stream) {
+  if (!is_pow2(N) || N < 16 || N > 8192 || B < 1 || !in || !out)
+    return fail(TSF_E_INVALID, "bad FFT debug arguments");
+  const int lg = ilog2_host(N);
+  static double2* dtw[kMaxLogNmv + 1] = {};
+  if (!dtw[lg]) {
+    std::vector<double2> t = twiddles(N);
+    CK(cudaMalloc(&dtw[lg], t.size() * sizeof(double2)));
+    CK(cudaMemcpy(dtw[lg], t.data(), t.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  }
+  return ForLog<FftF>::run(lg, inverse, B, (const double2*)in, (double2*)out,
+                           (const double2*)dtw[lg], (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// Common device helpers for the tsfrac B200 kernels (fp64 throughout).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define TSF_HD __host__ __device__ __forceinline__
+#define TSF_D __device__ __forceinline__
+
+// ---------------------------------------------------------------- complex
+TSF_HD double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+TSF_HD double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+TSF_HD double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+TSF_HD double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+TSF_HD double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+TSF_HD double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by -i (forward) / +i (inverse)
+template <bool INV>
+TSF_HD double2 mul_mi(double2 a) {
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+// ---------------------------------------------------------------- status
+// Per-instance status codes; the host maps them to the reference's
+// exceptions / KrylovReport.breakdown strings (krylov.py:72-152,
+// scheme.py:139-142,156-160, toeplitz.py:117-124).
+enum TsfStatus : int {
+  TSF_OK = 0,
+  TSF_NOT_CONVERGED = 1,
+  TSF_BD_RHO = 2,          // "rho vanished"
+  TSF_BD_R0V = 3,          // "r0.v vanished"
+  TSF_BD_OMEGA_DEN = 4,    // "omega denominator vanished"
+  TSF_BD_OMEGA = 5,        // "omega vanished"
+  TSF_BD_CURVATURE = 6,    // "non-positive curvature"
+  TSF_KAPPA_NONPOS = 7,    // kappa <= 0 somewhere on the grid
+  TSF_PRECOND_NONPOS = 8,  // shift + kappa_bar*lambda <= 0
+};
+
+// ---------------------------------------------------------------- reductions
+template <int NV>
+struct Vals {
+  double v[NV];
+};
+
+// Block-wide sum of NV doubles; every thread receives the result.
+// `scratch` must hold NV * 32 doubles.  Contains two __syncthreads.
+template <int NV>
+TSF_D Vals<NV> block_sum(Vals<NV> a, double* scratch) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = a.v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    a.v[k] = x;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) scratch[k * 32 + warp] = a.v[k];
+  }
+  __syncthreads();
+  Vals<NV> r;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = (lane < nwarps) ? scratch[k * 32 + lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    r.v[k] = x;
+  }
+  __syncthreads();
+  return r;
+}
+
+TSF_D double block_sum1(double a, double* scratch) {
+  Vals<1> v;
+  v.v[0] = a;
+  return block_sum<1>(v, scratch).v[0];
+}
+
+TSF_D double block_min1(double a, double* scratch) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+  if (lane == 0) scratch[warp] = a;
+  __syncthreads();
+  double x = (lane < nwarps) ? scratch[lane] : 1e308;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmin(x, __shfl_xor_sync(0xffffffffu, x, o));
+  __syncthreads();
+  return x;
+}

@@ -1,0 +1,39 @@
+// Per-size dispatch of the single-CTA engine.  The bodies live in
+// tsf_dispatch_impl.cuh and are explicitly instantiated one size per
+// translation unit (gen/inst_L*.cu) so the build parallelises.
+#pragma once
+
+#include "tsf_kernels.cuh"
+
+namespace tsf {
+
+constexpr int kMinLogNmv = 4;   // N_mv = 16
+constexpr int kMaxLogNmv = 13;  // N_mv = 8192 (n <= 8192 single-CTA engine)
+
+// sets tsf_last_error() and returns TSF_E_CUDA (defined in tsf_abi.cu)
+int report_cuda(cudaError_t e, const char* what);
+
+template <int LOG>
+struct Dispatch {
+  static int matvec(int n, const FilterTables& t, int B, const double* x, double* y,
+                    const double* kappa, double shift, cudaStream_t st);
+  static int precond(int n, const FilterTables& t, int B, const double* v, double* z,
+                     double shift, double kbar, const double* kbar_dev, cudaStream_t st);
+  static int solve(int B, int method, int pc, const KrylovArgs& a, cudaStream_t st);
+  static int fft(int inverse, int B, const double2* in, double2* out, const double2* tw,
+                 cudaStream_t st);
+};
+
+#define TSF_EXTERN_DISPATCH(L) extern template struct Dispatch<L>;
+TSF_EXTERN_DISPATCH(4)
+TSF_EXTERN_DISPATCH(5)
+TSF_EXTERN_DISPATCH(6)
+TSF_EXTERN_DISPATCH(7)
+TSF_EXTERN_DISPATCH(8)
+TSF_EXTERN_DISPATCH(9)
+TSF_EXTERN_DISPATCH(10)
+TSF_EXTERN_DISPATCH(11)
+TSF_EXTERN_DISPATCH(12)
+TSF_EXTERN_DISPATCH(13)
+
+}  // namespace tsf

@@ -1,0 +1,243 @@
+// Block-level Stockham FFT in shared memory, fp64, sm_100a.
+//
+// One CTA transforms one complex sequence of length N (power of two).  The
+// CTA has T = N/E "owning" threads; thread `tid` owns the complex slots
+// j = tid + c*T, c in [0, E).  The first radix pass reads its butterfly
+// inputs straight from the owning thread's registers and the last pass
+// writes its outputs back to them, so a transform costs (passes-1) shared
+// memory round trips and data can stay in registers between the FFT and the
+// surrounding vector arithmetic (the Krylov updates are done on exactly
+// these slots).
+//
+// Radix passes are chosen greedily (radix <= min(E,16)); twiddles come from
+// a host-computed table W_NT^e (long-double accurate, NT >= N) read through
+// the read-only path.  Shared-memory addresses are padded with
+// pad(i) = i + (i >> log2(R_first)), which makes the strided writes of the
+// first pass and the contiguous accesses of all later passes conflict-free
+// for 16-byte elements.
+//
+// Replaces numpy pocketfft at the reference call sites fourier.py:20-27
+// (used by toeplitz.py:51-63 and toeplitz.py:131-136).
+#pragma once
+
+#include "tsf_common.cuh"
+
+namespace tsf {
+
+// ------------------------------------------------------------ small DFTs
+// All DFTs are in place, natural order in and out; INV selects the +i sign.
+template <bool INV>
+TSF_D void dft2(double2& a0, double2& a1) {
+  double2 t = a0;
+  a0 = cadd(t, a1);
+  a1 = csub(t, a1);
+}
+
+template <bool INV>
+TSF_D void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
+  double2 t0 = cadd(a0, a2), t1 = csub(a0, a2);
+  double2 t2 = cadd(a1, a3), t3 = mul_mi<INV>(csub(a1, a3));
+  a0 = cadd(t0, t2);
+  a2 = csub(t0, t2);
+  a1 = cadd(t1, t3);
+  a3 = csub(t1, t3);
+}
+
+#define TSF_R2 0.70710678118654752440084436210484903928
+#define TSF_C8 0.92387953251128675612818318939678828682
+#define TSF_S8 0.38268343236508977172845998403039886676
+
+// x * W8^1 (fwd: (1-i)/sqrt2 ; inv: (1+i)/sqrt2)
+template <bool INV>
+TSF_D double2 w8_1(double2 x) {
+  return INV ? make_double2((x.x - x.y) * TSF_R2, (x.x + x.y) * TSF_R2)
+             : make_double2((x.x + x.y) * TSF_R2, (x.y - x.x) * TSF_R2);
+}
+// x * W8^3 (fwd: (-1-i)/sqrt2 ; inv: (-1+i)/sqrt2)
+template <bool INV>
+TSF_D double2 w8_3(double2 x) {
+  return INV ? make_double2((-x.x - x.y) * TSF_R2, (x.x - x.y) * TSF_R2)
+             : make_double2((x.y - x.x) * TSF_R2, (-x.x - x.y) * TSF_R2);
+}
+
+template <bool INV>
+TSF_D void dft8(double2* a) {
+  // DIT: even/odd halves of length 4, then combine with W8^k.
+  double2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6];
+  double2 o0 = a[1], o1 = a[3], o2 = a[5], o3 = a[7];
+  dft4<INV>(e0, e1, e2, e3);
+  dft4<INV>(o0, o1, o2, o3);
+  o1 = w8_1<INV>(o1);
+  o2 = mul_mi<INV>(o2);
+  o3 = w8_3<INV>(o3);
+  a[0] = cadd(e0, o0); a[4] = csub(e0, o0);
+  a[1] = cadd(e1, o1); a[5] = csub(e1, o1);
+  a[2] = cadd(e2, o2); a[6] = csub(e2, o2);
+  a[3] = cadd(e3, o3); a[7] = csub(e3, o3);
+}
+
+// x * W16^e for the exponents a 4x4 decomposition needs.
+template <int EXP, bool INV>
+TSF_D double2 w16(double2 x) {
+  if constexpr (EXP == 0) return x;
+  else if constexpr (EXP == 2) return w8_1<INV>(x);
+  else if constexpr (EXP == 4) return mul_mi<INV>(x);
+  else if constexpr (EXP == 6) return w8_3<INV>(x);
+  else {
+    constexpr double c = (EXP == 1) ? TSF_C8 : (EXP == 3) ? TSF_S8 : -TSF_C8;  // 1, 3, 9
+    constexpr double s = (EXP == 1) ? TSF_S8 : (EXP == 3) ? TSF_C8 : -TSF_S8;
+    // W = c - i s (fwd) ; c + i s (inv)
+    return INV ? make_double2(fma(x.x, c, -x.y * s), fma(x.x, s, x.y * c))
+               : make_double2(fma(x.x, c, x.y * s), fma(x.y, c, -x.x * s));
+  }
+}
+
+template <bool INV>
+TSF_D void dft16(double2* a) {
+  // 4x4: columns n2 = 0..3 over n1 (stride 4), twiddle W16^{n2 k1}, rows.
+  dft4<INV>(a[0], a[4], a[8], a[12]);
+  dft4<INV>(a[1], a[5], a[9], a[13]);
+  dft4<INV>(a[2], a[6], a[10], a[14]);
+  dft4<INV>(a[3], a[7], a[11], a[15]);
+  // Y_{n2}[k1] sits at a[n2 + 4 k1]
+  a[5] = w16<1, INV>(a[5]);
+  a[9] = w16<2, INV>(a[9]);
+  a[13] = w16<3, INV>(a[13]);
+  a[6] = w16<2, INV>(a[6]);
+  a[10] = w16<4, INV>(a[10]);
+  a[14] = w16<6, INV>(a[14]);
+  a[7] = w16<3, INV>(a[7]);
+  a[11] = w16<6, INV>(a[11]);
+  a[15] = w16<9, INV>(a[15]);
+  // rows: for k1, DFT4 over n2 -> X[k1 + 4 k2]
+  dft4<INV>(a[0], a[1], a[2], a[3]);
+  dft4<INV>(a[4], a[5], a[6], a[7]);
+  dft4<INV>(a[8], a[9], a[10], a[11]);
+  dft4<INV>(a[12], a[13], a[14], a[15]);
+  // currently X[k1 + 4 k2] at a[4 k1 + k2]: transpose 4x4
+  double2 t;
+  t = a[1]; a[1] = a[4]; a[4] = t;
+  t = a[2]; a[2] = a[8]; a[8] = t;
+  t = a[3]; a[3] = a[12]; a[12] = t;
+  t = a[6]; a[6] = a[9]; a[9] = t;
+  t = a[7]; a[7] = a[13]; a[13] = t;
+  t = a[11]; a[11] = a[14]; a[14] = t;
+}
+
+template <int R, bool INV>
+TSF_D void dft(double2* a) {
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2) {
+    dft2<INV>(a[0], a[1]);
+  } else if constexpr (R == 4) {
+    dft4<INV>(a[0], a[1], a[2], a[3]);
+  } else if constexpr (R == 8) {
+    dft8<INV>(a);
+  } else {
+    static_assert(R == 16, "radix must be 1,2,4,8,16");
+    dft16<INV>(a);
+  }
+}
+
+// ------------------------------------------------------------ pass plan
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+constexpr int imin(int a, int b) { return a < b ? a : b; }
+
+// radix of pass p for an N-point transform with E elements per thread
+template <int N, int E>
+struct FftPlan {
+  static constexpr int LOGN = ilog2(N);
+  static constexpr int LOGR = ilog2(imin(E, 16));
+  static constexpr int NPASS = (LOGN + LOGR - 1) / LOGR;
+  static constexpr int T = N / E;
+  static constexpr int PADSHIFT = imin(LOGR, LOGN);  // log2 of the first radix
+  static constexpr int SMEM_ELEMS = N + (N >> PADSHIFT) + 1;
+  static constexpr int log_radix(int p) {
+    return (p < NPASS - 1) ? LOGR : (LOGN - LOGR * (NPASS - 1));
+  }
+  static constexpr int log_ns(int p) { return p * LOGR; }
+  TSF_HD static int pad(int i) { return i + (i >> PADSHIFT); }
+};
+
+// One Stockham pass: radix R, NS = product of the previous radices.
+//  FROM_REGS: inputs come from v[] (first pass), else from shared memory.
+//  TO_REGS:   outputs go to v[] (last pass), else to shared memory.
+// Every thread of the CTA must call (the in-place pass has a barrier);
+// only owning threads (own == true) touch data.
+template <int N, int E, int P, bool INV, bool FROM_REGS, bool TO_REGS>
+TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
+                         int tw_log_scale, int tid, bool own) {
+  using PL = FftPlan<N, E>;
+  constexpr int R = 1 << PL::log_radix(P);
+  constexpr int NS = 1 << PL::log_ns(P);
+  constexpr int T = PL::T;
+  constexpr int Q = E / R;
+  constexpr int NR = N / R;
+  double2 a[Q][R];
+  if (own) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        if constexpr (FROM_REGS) a[q][m] = v[q + m * Q];
+        else a[q][m] = sm[PL::pad(tid + q * T + m * NR)];
+      }
+    }
+  }
+  if constexpr (!FROM_REGS && !TO_REGS) __syncthreads();  // in place
+  if (!own) return;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int b = tid + q * T;
+    const int k = b & (NS - 1);
+    if constexpr (NS > 1) {
+      // W_{NS R}^{k m} = W_NT^{k m NT/(NS R)}, NT/(NS R) = 2^sh
+      const int sh = tw_log_scale + PL::LOGN - PL::log_ns(P) - PL::log_radix(P);
+#pragma unroll
+      for (int m = 1; m < R; ++m) {
+        double2 w = __ldg(&tw[(k * m) << sh]);
+        a[q][m] = INV ? cmulc(a[q][m], w) : cmul(a[q][m], w);
+      }
+    }
+    dft<R, INV>(a[q]);
+    if constexpr (TO_REGS) {
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[q + m * Q] = a[q][m];
+    } else {
+      const int base = (b / NS) * NS * R + k;
+#pragma unroll
+      for (int m = 0; m < R; ++m) sm[PL::pad(base + m * NS)] = a[q][m];
+    }
+  }
+}
+
+template <int N, int E, int P, bool INV>
+TSF_D void fft_rec(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
+                   int tw_log_scale, int tid, bool own) {
+  using PL = FftPlan<N, E>;
+  constexpr bool FIRST = (P == 0);
+  constexpr bool LAST = (P == PL::NPASS - 1);
+  stockham_pass<N, E, P, INV, FIRST, LAST>(v, sm, tw, tw_log_scale, tid, own);
+  if constexpr (!LAST) {
+    __syncthreads();
+    fft_rec<N, E, P + 1, INV>(v, sm, tw, tw_log_scale, tid, own);
+  }
+}
+
+// Full transform of the owned slots v[c] (j = tid + c*T).  Unnormalised in
+// both directions.  Every thread of the CTA must call; threads with
+// tid >= T own nothing.  Starts with a barrier so the caller may reuse `sm`
+// right before; ends with data in registers (sm may be reused after a
+// barrier).
+// `tw` holds W_NT^e for e < NT with NT = N << tw_log_scale.
+template <int N, int E, bool INV>
+TSF_D void block_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
+                     int tw_log_scale) {
+  using PL = FftPlan<N, E>;
+  const int tid = threadIdx.x;
+  const bool own = tid < PL::T;
+  __syncthreads();
+  fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, own);
+}
+
+}  // namespace tsf

@@ -1,0 +1,242 @@
+"""Krylov level solvers on the B200 (mirror of tsfrac.krylov, krylov.py:19-171).
+
+`solve_bicgstab` / `solve_cg` on a `LevelOperator` (the structured level
+system shift*I + diag(kappa) A of scheme.py:129-130) run the whole solve in
+one sm_100a kernel per instance (csrc/tsf_kernels.cuh, k_krylov_solve):
+the FFT matvec, the Strang preconditioner, the dots/norms and the scalar
+control flow (iteration counting, early ||s|| exit, exact-zero breakdown
+tests) all stay on the device.  Batched right-hand sides [B, n] solve B
+independent systems at once.
+
+For an arbitrary `MatrixFreeOperator` whose `apply` works on torch CUDA
+tensors, a generic device loop restates the same algorithm with torch
+vector ops (not a hot path; used for the reference's dense-operator tests).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Union
+
+import numpy as np
+
+from . import _arrays, _native
+
+
+@dataclass(frozen=True)
+class MatrixFreeOperator:
+    """Dimension plus the action v -> M v (krylov.py:19-24)."""
+
+    n: int
+    apply: Callable
+
+
+@dataclass(frozen=True)
+class KrylovReport:
+    """krylov.py:27-32."""
+
+    iterations: int
+    final_relative_residual: float
+    converged: bool
+    breakdown: Optional[str] = None
+
+
+class LevelOperator(MatrixFreeOperator):
+    """shift*I + diag(kappa) A with A a ToeplitzOperator (scheme.py:129-132)."""
+
+    def __init__(self, toeplitz, shift: float, kappa):
+        object.__setattr__(self, "toeplitz", toeplitz)
+        object.__setattr__(self, "shift", float(shift))
+        object.__setattr__(self, "kappa", kappa)
+        object.__setattr__(self, "n", toeplitz.n)
+        object.__setattr__(self, "apply", self._apply)
+
+    def _apply(self, v):
+        from .toeplitz import toeplitz_matvec
+        return toeplitz_matvec(self.toeplitz, v, kappa=self.kappa, shift=self.shift)
+
+
+def _reports(iters, relres, status) -> List[KrylovReport]:
+    out = []
+    for it, rr, st in zip(iters.tolist(), relres.tolist(), status.tolist()):
+        out.append(KrylovReport(int(it), float(rr), st == _native.ST_OK,
+                                _native.BREAKDOWN.get(int(st))))
+    return out
+
+
+def _device_solve(op: LevelOperator, precond, rhs, tol, max_iters, method):
+    torch = _native.torch_mod()
+    from .toeplitz import CirculantPreconditioner
+    dev = op.toeplitz.device
+    b, as_np = _arrays.to_device(rhs, dev)
+    if b.shape[-1] != op.n or b.dim() not in (1, 2):
+        raise ValueError(f"rhs has shape {tuple(b.shape)}, operator order is {op.n}")
+    B = 1 if b.dim() == 1 else b.shape[0]
+    kap, _ = _arrays.to_device(op.kappa, dev)
+    if kap.shape != b.shape:
+        kap = kap.expand_as(b).contiguous()
+    pc = 0
+    kbar = 0.0
+    if precond is not None:
+        if not isinstance(precond, CirculantPreconditioner):
+            raise TypeError("device solve supports the Strang CirculantPreconditioner or None")
+        if precond.n != op.n:
+            raise ValueError("preconditioner order differs from the operator")
+        pc = 1
+        kbar = float(precond.kappa_bar)
+    x = torch.empty_like(b)
+    iters = torch.empty(B, dtype=torch.int32, device=b.device)
+    relres = torch.empty(B, dtype=torch.float64, device=b.device)
+    status = torch.empty(B, dtype=torch.int32, device=b.device)
+    plan = op.toeplitz.plan
+    if pc and not plan.has_precond:
+        raise NotImplementedError(
+            f"device Strang preconditioner needs a power-of-two n >= 16 (got n={op.n})")
+    _native.check(_native.load().tsf_krylov_solve(
+        plan.handle, B, method, pc, b.data_ptr(), x.data_ptr(), kap.data_ptr(), op.shift,
+        kbar, float(tol), int(max_iters) if max_iters is not None else 0, iters.data_ptr(),
+        relres.data_ptr(), status.data_ptr(), _native.stream_ptr()))
+    reps = _reports(iters.cpu(), relres.cpu(), status.cpu())
+    xs = _arrays.back(x, as_np)
+    return (xs, reps[0]) if b.dim() == 1 else (xs, reps)
+
+
+def _psolve_of(precond):
+    if precond is None:
+        return lambda v: v
+    if hasattr(precond, "solve"):
+        return precond.solve
+    return precond
+
+
+def _generic_bicgstab(op, precond, rhs, tol, max_iters):
+    torch = _native.torch_mod()
+    b, as_np = _arrays.to_device(rhs)
+    n = op.n
+    if b.shape != (n,):
+        raise ValueError(f"rhs has shape {tuple(b.shape)}, operator order is {n}")
+    max_iters = max_iters if max_iters is not None else 10 * n
+    ps = _psolve_of(precond)
+    ap = lambda v: _arrays.to_device(op.apply(v))[0]  # noqa: E731
+    pss = lambda v: _arrays.to_device(ps(v))[0]  # noqa: E731
+    x = torch.zeros_like(b)
+    r = b.clone()
+    r0 = b.clone()
+    nrm0 = float(torch.linalg.norm(r0))
+    if nrm0 == 0.0:
+        return _arrays.back(x, as_np), KrylovReport(0, 0.0, True)
+    rho = alpha = omega = 1.0
+    v = torch.zeros_like(b)
+    p = torch.zeros_like(b)
+    for it in range(1, max_iters + 1):
+        rho_new = float(r0 @ r)
+        if rho_new == 0.0:
+            return _arrays.back(x, as_np), KrylovReport(
+                it, float(torch.linalg.norm(r)) / nrm0, False, "rho vanished")
+        if it == 1:
+            p = r.clone()
+        else:
+            beta = (rho_new / rho) * (alpha / omega)
+            p = r + beta * (p - omega * v)
+        ph = pss(p)
+        v = ap(ph)
+        den = float(r0 @ v)
+        if den == 0.0:
+            return _arrays.back(x, as_np), KrylovReport(
+                it, float(torch.linalg.norm(r)) / nrm0, False, "r0.v vanished")
+        alpha = rho_new / den
+        s = r - alpha * v
+        sn = float(torch.linalg.norm(s)) / nrm0
+        if sn < tol:
+            x += alpha * ph
+            return _arrays.back(x, as_np), KrylovReport(it, sn, True)
+        sh = pss(s)
+        t = ap(sh)
+        tt = float(t @ t)
+        if tt == 0.0:
+            return _arrays.back(x, as_np), KrylovReport(it, sn, False,
+                                                        "omega denominator vanished")
+        omega = float(t @ s) / tt
+        x += alpha * ph + omega * sh
+        r = s - omega * t
+        rho = rho_new
+        rel = float(torch.linalg.norm(r)) / nrm0
+        if rel < tol:
+            return _arrays.back(x, as_np), KrylovReport(it, rel, True)
+        if omega == 0.0:
+            return _arrays.back(x, as_np), KrylovReport(it, rel, False, "omega vanished")
+    return _arrays.back(x, as_np), KrylovReport(
+        max_iters, float(torch.linalg.norm(r)) / nrm0, False)
+
+
+def _generic_cg(op, precond, rhs, tol, max_iters):
+    torch = _native.torch_mod()
+    b, as_np = _arrays.to_device(rhs)
+    n = op.n
+    if b.shape != (n,):
+        raise ValueError(f"rhs has shape {tuple(b.shape)}, operator order is {n}")
+    max_iters = max_iters if max_iters is not None else 10 * n
+    ps = _psolve_of(precond)
+    ap = lambda v: _arrays.to_device(op.apply(v))[0]  # noqa: E731
+    pss = lambda v: _arrays.to_device(ps(v))[0]  # noqa: E731
+    x = torch.zeros_like(b)
+    r = b.clone()
+    nrm0 = float(torch.linalg.norm(r))
+    if nrm0 == 0.0:
+        return _arrays.back(x, as_np), KrylovReport(0, 0.0, True)
+    z = pss(r)
+    p = z.clone()
+    rz = float(r @ z)
+    for it in range(1, max_iters + 1):
+        q = ap(p)
+        curv = float(p @ q)
+        if curv <= 0.0:
+            return _arrays.back(x, as_np), KrylovReport(
+                it, float(torch.linalg.norm(r)) / nrm0, False, "non-positive curvature")
+        a = rz / curv
+        x += a * p
+        r -= a * q
+        rel = float(torch.linalg.norm(r)) / nrm0
+        if rel < tol:
+            return _arrays.back(x, as_np), KrylovReport(it, rel, True)
+        z = pss(r)
+        rz_new = float(r @ z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return _arrays.back(x, as_np), KrylovReport(
+        max_iters, float(torch.linalg.norm(r)) / nrm0, False)
+
+
+def solve_bicgstab(op: MatrixFreeOperator, precond, rhs, tol: float = 1e-10,
+                   max_iters: Optional[int] = None):
+    """Right-preconditioned BiCGSTAB, x0 = 0 (krylov.py:88-153)."""
+    if isinstance(op, LevelOperator):
+        return _device_solve(op, precond, rhs, tol, max_iters, method=0)
+    return _generic_bicgstab(op, precond, rhs, tol, max_iters)
+
+
+def solve_cg(op: MatrixFreeOperator, precond, rhs, tol: float = 1e-10,
+             max_iters: Optional[int] = None):
+    """Preconditioned CG, x0 = 0 (krylov.py:43-85)."""
+    if isinstance(op, LevelOperator):
+        return _device_solve(op, precond, rhs, tol, max_iters, method=1)
+    return _generic_cg(op, precond, rhs, tol, max_iters)
+
+
+DENSE_SOLVE_CAP = 2048
+
+
+def solve_dense(matrix, rhs):
+    """Dense LU on the device (krylov.py:156-171; out of the FIDS hot path)."""
+    torch = _native.torch_mod()
+    A, as_np = _arrays.to_device(matrix)
+    b, _ = _arrays.to_device(rhs)
+    n = A.shape[0]
+    if A.shape != (n, n) or b.shape != (n,):
+        raise ValueError("matrix/rhs shapes are inconsistent")
+    if n > DENSE_SOLVE_CAP:
+        raise ValueError(f"dense solve capped at {DENSE_SOLVE_CAP}, got {n}")
+    x, info = torch.linalg.solve_ex(A, b)
+    if int(info) != 0:
+        raise ValueError("matrix is singular")
+    return _arrays.back(x, as_np)

@@ -1,0 +1,225 @@
+"""GPU parity: the sm_100a path against the oracle and the reference goldens.
+
+Tolerances (BASELINE.json north_star; SURVEY.md §8(c) noise floors):
+  * single matvec / preconditioner solve: 1e-13 relative (max-abs / max)
+  * level solve: iterations within +-1 of the reference, x within 1e-10 rel-l2
+  * march: per-step iterations within +-1 on >= 95% of steps, every recorded
+    step within 1e-10 relative l2 (configs with alpha <= 1.5).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from tsf_testlib import cfg0_fields, golden, rel_err, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2002_11978_b200 as P  # noqa: E402
+from paper_2002_11978_b200 import _native  # noqa: E402
+
+
+def _lin_cases():
+    g = golden("linalg")
+    i = 0
+    while f"tp{i}_col" in g:
+        yield i, g
+        i += 1
+
+
+@pytest.mark.parametrize("N", [16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192])
+@pytest.mark.parametrize("inverse", [0, 1])
+def test_block_fft_matches_numpy(N, inverse):
+    rng = np.random.default_rng(N + inverse)
+    B = 3
+    z = rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))
+    zin = torch.from_numpy(np.ascontiguousarray(z.view(np.float64))).cuda()
+    zout = torch.empty_like(zin)
+    _native.check(_native.load().tsf_fft_debug(N, inverse, B, zin.data_ptr(), zout.data_ptr(),
+                                               _native.stream_ptr()))
+    got = zout.cpu().numpy().view(np.complex128).reshape(B, N)
+    want = np.fft.ifft(z, axis=1) * N if inverse else np.fft.fft(z, axis=1)
+    assert rel_err(got, want) <= 1e-14 * math.log2(N)
+
+
+def test_toeplitz_matvec_vs_reference():
+    for i, g in _lin_cases():
+        col, v = g[f"tp{i}_col"], g[f"tp{i}_v"]
+        op = P.build_toeplitz(col)
+        got = P.toeplitz_matvec(op, v)
+        assert rel_err(got, g[f"tp{i}_Av"]) <= 1e-13, i
+        shift = g[f"tp{i}_shift"][0]
+        got = P.toeplitz_matvec(op, v, kappa=g[f"tp{i}_kappa"], shift=shift)
+        assert rel_err(got, g[f"tp{i}_Mv"]) <= 1e-13, i
+
+
+def test_toeplitz_kats():
+    # pkg/tests/test_toeplitz.py:21-32
+    op = P.build_toeplitz(np.array([2.0, -1.0, 0.0]))
+    np.testing.assert_allclose(op.matvec(np.ones(3)), [1.0, 0.0, 1.0], atol=1e-13)
+    rng = np.random.default_rng(20240817)
+    col = rng.standard_normal(17)
+    e1 = np.zeros(17)
+    e1[0] = 1.0
+    out = P.build_toeplitz(col).matvec(e1)
+    assert np.max(np.abs(out - col)) <= 1e-12 * np.abs(col).max()
+
+
+def test_precond_vs_reference():
+    seen = 0
+    for i, g in _lin_cases():
+        n = g[f"tp{i}_v"].size
+        if n & (n - 1) or n < 16:
+            continue
+        p = P.build_preconditioner(g[f"tp{i}_col"], g[f"tp{i}_shift"][0],
+                                   float(g[f"tp{i}_kappa"].mean()))
+        np.testing.assert_array_equal(p.total_eigs, g[f"tp{i}_total"])
+        got = P.precond_solve(p, g[f"tp{i}_v"])
+        assert rel_err(got, g[f"tp{i}_Pinv_v"]) <= 1e-13, i
+        seen += 1
+    assert seen >= 3
+
+
+def test_level_solve_vs_reference():
+    seen = 0
+    for i, g in _lin_cases():
+        col = g[f"tp{i}_col"]
+        n = col.size
+        op = P.build_toeplitz(col)
+        shift = g[f"tp{i}_shift"][0]
+        kap = g[f"tp{i}_kappa"]
+        lev = P.LevelOperator(op, shift, kap)
+        pow2 = not (n & (n - 1)) and n >= 16
+        if pow2:
+            pc = P.build_preconditioner(col, shift, float(kap.mean()))
+            for tol in (10, 12):
+                key = f"tp{i}_bicg_{tol}"
+                x, rep = P.solve_bicgstab(lev, pc, g[f"{key}_b"], tol=10.0 ** -tol)
+                its = int(g[f"{key}_rep"][0])
+                assert rep.converged
+                assert abs(rep.iterations - its) <= 1, (i, tol, rep.iterations, its)
+                assert rel_l2(x, g[f"{key}_x"]) <= 1e-9 if tol == 10 else 1e-10
+            seen += 1
+        # unpreconditioned BiCGSTAB works for every n
+        x, rep = P.solve_bicgstab(lev, None, g[f"tp{i}_bicg_12_b"], tol=1e-10)
+        its = int(g[f"tp{i}_plain_rep"][0])
+        assert rep.converged and abs(rep.iterations - its) <= max(1, its // 10)
+        assert rel_l2(x, g[f"tp{i}_plain_x"]) <= 1e-8
+    assert seen >= 3
+
+
+def test_zero_rhs_zero_iterations():
+    col = golden("linalg")["tp0_col"]
+    op = P.build_toeplitz(col)
+    lev = P.LevelOperator(op, 3.0, np.ones(col.size))
+    pc = P.build_preconditioner(col, 3.0, 1.0)
+    x, rep = P.solve_bicgstab(lev, pc, np.zeros(col.size))
+    assert rep.converged and rep.iterations == 0
+    np.testing.assert_array_equal(x, 0.0)
+
+
+def test_max_iters_exhaustion():
+    g = golden("linalg")
+    col = g["tp0_col"]
+    lev = P.LevelOperator(P.build_toeplitz(col), g["tp0_shift"][0], g["tp0_kappa"])
+    x, rep = P.solve_bicgstab(lev, None, g["tp0_bicg_12_b"], tol=1e-15, max_iters=1)
+    assert not rep.converged and rep.iterations == 1
+
+
+def test_soe_push_bit_exact():
+    g = golden("linalg")
+    soe = P.build_soe(0.5, 1e-12, (1.0 / 256) ** 3, 1.0)
+    h = P.FastHistory.fresh(soe, g["push_W0"].shape[1])
+    h.W.copy_(torch.from_numpy(g["push_W0"]))
+    tau_push, tau_rhs = g["push_tau"]
+    rhs = P.fast_caputo_rhs(h, 12.5, g["push_uprev"], 0.5, tau_rhs)
+    assert rel_err(rhs, g["push_rhs"]) <= 1e-14
+    P.history_push(h, g["push_du"], tau_push)
+    np.testing.assert_array_equal(h.W.cpu().numpy(), g["push_W1"])
+
+
+@pytest.mark.parametrize("tag", ["s1", "s3", "s5"])
+def test_small_march_vs_reference(tag):
+    g = golden("march")
+    gam, a, M, N, tol, r = g[f"{tag}_args"]
+    k, f, phi = cfg0_fields()
+    spec = P.ProblemSpec(gamma=gam, alpha=a, l=1.0, T=1.0, kappa=k, source=f, initial=phi)
+    hist, rep = P.run_fids(spec, int(M), r, int(N), epsilon=1e-12,
+                           options=P.SolverOptions(solver="pkrylov", tol=tol))
+    its_ref = g[f"{tag}_its"]
+    d = np.abs(rep.iterations - its_ref)
+    assert np.mean(d <= 1) >= 0.95, d
+    errs = [rel_l2(hist[m], g[f"{tag}_hist"][m]) for m in range(1, int(M) + 1)]
+    assert max(errs) <= 1e-10, max(errs)
+
+
+def test_cfg0_march_vs_reference():
+    """BASELINE configs[0] at full size against the reference's own run."""
+    g = golden("march")
+    k, f, phi = cfg0_fields()
+    spec = P.ProblemSpec(gamma=0.5, alpha=1.5, l=1.0, T=1.0, kappa=k, source=f, initial=phi)
+    hist, rep = P.run_fids(spec, 256, 3.0, 1025, epsilon=1e-12,
+                           options=P.SolverOptions(solver="pkrylov", tol=1e-12))
+    d = np.abs(rep.iterations - g["cfg0_its"])
+    assert np.mean(d <= 1) >= 0.95
+    assert abs(rep.avg_iterations - g["cfg0_avg"][0]) <= 0.25
+    errs = np.array([rel_l2(hist[m], g["cfg0_hist"][m]) for m in range(1, 257)])
+    assert errs.max() <= 1e-10, errs.max()
+
+
+def test_cfg0_separable_field_is_bit_identical_kappa():
+    k, f, phi = cfg0_fields()
+    x = np.linspace(-1, 1, 1025)[1:-1]
+    fld = P.SeparableField([np.ones_like(x), 0.5 * np.sin(np.pi * x)],
+                           lambda t: [1.0, math.exp(-t)])
+    for t in (0.0, 0.3, 1.0):
+        np.testing.assert_array_equal(fld(x, t), k(x, t))
+
+
+def test_zero_data_march_exactly_zero():
+    spec = P.ProblemSpec(gamma=0.5, alpha=1.5, l=1.0, T=1.0,
+                         kappa=lambda x, t: np.ones_like(x),
+                         source=lambda x, t: np.zeros_like(x),
+                         initial=lambda x: np.zeros_like(x))
+    hist, rep = P.run_fids(spec, 8, 2.0, 257, epsilon=1e-10)
+    np.testing.assert_array_equal(hist, 0.0)
+    assert rep.avg_iterations == 0.0
+
+
+def test_kappa_positivity_enforced():
+    spec = P.ProblemSpec(gamma=0.5, alpha=1.5, l=1.0, T=1.0,
+                         kappa=lambda x, t: np.where(x > 0, 1.0, -1.0),
+                         source=lambda x, t: np.zeros_like(x),
+                         initial=lambda x: np.zeros_like(x))
+    with pytest.raises(ValueError, match="kappa"):
+        P.run_fids(spec, 4, 1.0, 257, options=P.SolverOptions(solver="pkrylov"))
+
+
+def test_batched_march_matches_single_instances():
+    """Instances in one batched march equal the same instances run alone."""
+    n, M, gam, a = 256, 24, 0.5, 1.5
+    N = n + 1
+    rng = np.random.default_rng(7)
+    B = 5
+    x = -1.0 + (2.0 / N) * np.arange(1, N)
+    kx = np.exp(0.3 * rng.standard_normal((B, 1)) * np.sin(np.pi * x)[None, :])
+    fx = rng.standard_normal((B, 1)) * np.sin(np.pi * x)[None, :]
+    u0 = (1 - x * x) ** 2 * rng.uniform(0.5, 2.0, (B, 1))
+    kap = P.SeparableField([np.ones(n)], lambda t: [1.0 + 0.2 * t])
+    src = P.SeparableField([np.ones(n)], lambda t: [1.0 + t])
+    uB, rep = P.run_fids_batched(gam, a, M, 3.0, N, kap, src, u0, kappa_modes=kx[None],
+                                 source_modes=fx[None], epsilon=1e-12,
+                                 options=P.SolverOptions(solver="pkrylov", tol=1e-12))
+    for b in range(B):
+        rec = O.fids_march(gam, a, 1.0, 1.0, M, 3.0, N,
+                           lambda xx, t, b=b: kx[b] * (1.0 + 0.2 * t),
+                           lambda xx, t, b=b: fx[b] * (1.0 + t),
+                           lambda xx, b=b: u0[b], epsilon=1e-12, tol=1e-12)
+        assert rel_l2(uB[b], rec.hist[-1]) <= 1e-10
+        assert np.mean(np.abs(rep["iterations"][:, b] - rec.iterations) <= 1) >= 0.95
