@@ -53,31 +53,29 @@ int report_cuda(cudaError_t e, const char* what) {
 struct tsf_plan {
   int n = 0;
   int L = 0;
-  int nmv = 0;
-  int log_nmv = 0;
+  int log_L = 0;
   int has_pc = 0;
   int device = 0;
-  double2* tw = nullptr;
-  double2* mvab = nullptr;
-  double2* pclam = nullptr;
-  double2* pcsc = nullptr;
-  // Krylov workspaces [cap][n] x 5 + status scratch
+  double2* tw = nullptr;   // W_L^e
+  double* mvS = nullptr;   // even part of the symbol / L
+  double2* pclam = nullptr;  // (lam_k, lam_{n-k})
+  // Krylov workspaces [cap][n] x 6
   int cap = 0;
   double* ws = nullptr;
   int* ist = nullptr;
   double* dst = nullptr;
-  FilterTables tables() const { return FilterTables{tw, mvab, pclam, pcsc}; }
+  FilterTables tables() const { return FilterTables{tw, mvS, pclam}; }
 };
 
 // ------------------------------------------------------------- dispatch
 namespace {
 
-template <template <int> class F, int LOG = kMinLogNmv>
+template <template <int> class F, int LOG = kMinLogL>
 struct ForLog {
   template <typename... A>
   static int run(int log, A&&... args) {
     if (log == LOG) return F<LOG>::call(static_cast<A&&>(args)...);
-    if constexpr (LOG < kMaxLogNmv) return ForLog<F, LOG + 1>::run(log, static_cast<A&&>(args)...);
+    if constexpr (LOG < kMaxLogL) return ForLog<F, LOG + 1>::run(log, static_cast<A&&>(args)...);
     return fail(TSF_E_UNSUPPORTED, "transform size 2^%d not built", log);
   }
 };
@@ -149,17 +147,15 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
   if (!is_pow2(L) || L < 2 * n - 1 || L < 32)
     return fail(TSF_E_INVALID, "L=%d must be a power of two >= max(2n-1, 32)", L);
   if (!symbol_re) return fail(TSF_E_INVALID, "symbol is NULL");
-  const int nmv = L / 2;
-  const int lg = ilog2_host(nmv);
-  if (lg < kMinLogNmv || lg > kMaxLogNmv)
-    return fail(TSF_E_UNSUPPORTED, "embedding L=%d outside the single-CTA engine (32..16384)", L);
-  if (lam && !(is_pow2(n) && L == 2 * n))
-    return fail(TSF_E_UNSUPPORTED, "Strang preconditioner needs pow2 n with L = 2n (n=%d, L=%d)", n, L);
+  const int lg = ilog2_host(L);
+  if (lg < kMinLogL || lg > kMaxLogL)
+    return fail(TSF_E_UNSUPPORTED, "embedding L=%d outside the single-CTA engine (32..8192, n <= 4096)", L);
+  if (lam && !(is_pow2(n) && n >= 16 && L == 2 * n))
+    return fail(TSF_E_UNSUPPORTED, "Strang preconditioner needs pow2 n >= 16 with L = 2n (n=%d, L=%d)", n, L);
   tsf_plan* p = new tsf_plan();
   p->n = n;
   p->L = L;
-  p->nmv = nmv;
-  p->log_nmv = lg;
+  p->log_L = lg;
   p->device = device;
   p->has_pc = lam != nullptr;
   auto cleanup = [&](int rc) {
@@ -167,37 +163,27 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
     return rc;
   };
   if (cudaSetDevice(device) != cudaSuccess) return cleanup(fail(TSF_E_CUDA, "cudaSetDevice(%d)", device));
-  // twiddles for the largest transform (N_mv); the N_pc transform uses stride 2
-  std::vector<double2> tw = twiddles(nmv);
-  // Toeplitz symbol -> real-pack filter coefficients (a_k, b_k) / N_mv
-  std::vector<double2> ab(nmv);
-  const long double two_pi = 6.283185307179586476925286766559005768L;
-  for (int k = 0; k < nmv; ++k) {
-    long double s1 = symbol_re[k], s2 = symbol_re[k + nmv];
-    long double P = 0.5L * (s1 + s2), Q = 0.5L * (s1 - s2);
-    long double th = two_pi * (long double)k / (long double)L;
-    ab[k] = make_double2((double)((P - Q * sinl(th)) / nmv), (double)(Q * cosl(th) / nmv));
-  }
-  std::vector<double2> pl, ps;
+  // twiddles of the length-L transform; the length-n Strang transform uses stride 2
+  std::vector<double2> tw = twiddles(L);
+  // The reference keeps Re IFFT(S . FFT(pad x)) (toeplitz.py:62-63): its
+  // effective symbol is the even part of S.  1/L of the inverse folded in.
+  std::vector<double> S(L);
+  for (int k = 0; k < L; ++k)
+    S[k] = (double)(0.5L * ((long double)symbol_re[k] + (long double)symbol_re[(L - k) % L]) /
+                    (long double)L);
+  std::vector<double2> pl;
   if (lam) {
-    const int npc = n / 2;
-    pl.resize(npc);
-    ps.resize(npc);
-    for (int k = 0; k < npc; ++k) {
-      pl[k] = make_double2(lam[k], lam[k + npc]);
-      long double th = two_pi * (long double)k / (long double)n;
-      ps[k] = make_double2((double)sinl(th), (double)cosl(th));
-    }
+    pl.resize(n);
+    for (int k = 0; k < n; ++k) pl[k] = make_double2(lam[k], lam[(n - k) % n]);
   }
-  auto up = [&](double2** d, const std::vector<double2>& h) -> int {
+  auto up = [&](auto** d, const auto& h) -> int {
     if (h.empty()) return TSF_SUCCESS;
-    CK(cudaMalloc(d, h.size() * sizeof(double2)));
-    CK(cudaMemcpy(*d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(d, h.size() * sizeof(h[0])));
+    CK(cudaMemcpy(*d, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
     return TSF_SUCCESS;
   };
   int rc;
-  if ((rc = up(&p->tw, tw)) || (rc = up(&p->mvab, ab)) || (rc = up(&p->pclam, pl)) ||
-      (rc = up(&p->pcsc, ps)))
+  if ((rc = up(&p->tw, tw)) || (rc = up(&p->mvS, S)) || (rc = up(&p->pclam, pl)))
     return cleanup(rc);
   *out = p;
   return TSF_SUCCESS;
@@ -207,9 +193,8 @@ int tsf_plan_destroy(tsf_plan* p) {
   if (!p) return TSF_SUCCESS;
   cudaSetDevice(p->device);
   cudaFree(p->tw);
-  cudaFree(p->mvab);
+  cudaFree(p->mvS);
   cudaFree(p->pclam);
-  cudaFree(p->pcsc);
   cudaFree(p->ws);
   cudaFree(p->ist);
   cudaFree(p->dst);
@@ -221,7 +206,7 @@ int tsf_plan_info(const tsf_plan* p, int64_t* o) {
   if (!p || !o) return fail(TSF_E_INVALID, "NULL argument");
   o[0] = p->n;
   o[1] = p->L;
-  o[2] = p->nmv;
+  o[2] = p->L / 16;
   o[3] = p->has_pc;
   o[4] = p->cap;
   return TSF_SUCCESS;
@@ -236,7 +221,7 @@ int tsf_toeplitz_matvec(tsf_plan* p, int B, const double* x, double* y, const do
                         double shift, void* stream) {
   if (!p || !x || !y || B < 0) return fail(TSF_E_INVALID, "bad argument");
   if (B == 0) return TSF_SUCCESS;
-  return ForLog<MatvecF>::run(p->log_nmv, p->n, p->tables(), B, x, y, kappa, shift,
+  return ForLog<MatvecF>::run(p->log_L, p->n, p->tables(), B, x, y, kappa, shift,
                               (cudaStream_t)stream);
 }
 
@@ -245,7 +230,7 @@ int tsf_precond_solve(tsf_plan* p, int B, const double* v, double* z, double shi
   if (!p || !v || !z || B < 0) return fail(TSF_E_INVALID, "bad argument");
   if (!p->has_pc) return fail(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner (non-pow2 n)");
   if (B == 0) return TSF_SUCCESS;
-  return ForLog<PrecondF>::run(p->log_nmv, p->n, p->tables(), B, v, z, shift, kbar, kbar_dev,
+  return ForLog<PrecondF>::run(p->log_L, p->n, p->tables(), B, v, z, shift, kbar, kbar_dev,
                                (cudaStream_t)stream);
 }
 
@@ -264,7 +249,7 @@ static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cud
   if (!a.kwork) a.kwork = p->ws + 5 * vn;
   a.tab = p->tables();
   if (a.max_iters <= 0) a.max_iters = 10 * p->n;
-  return ForLog<SolveF>::run(p->log_nmv, B, method, pc, (const KrylovArgs&)a, st);
+  return ForLog<SolveF>::run(p->log_L, B, method, pc, (const KrylovArgs&)a, st);
 }
 
 int tsf_krylov_solve(tsf_plan* p, int B, int method, int precond, const double* rhs, double* x,
@@ -422,10 +407,10 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
 }
 
 int tsf_fft_debug(int N, int inverse, int B, const double* in, double* out, void* stream) {
-  if (!is_pow2(N) || N < 16 || N > 8192 || B < 1 || !in || !out)
+  if (!is_pow2(N) || N < 32 || N > 8192 || B < 1 || !in || !out)
     return fail(TSF_E_INVALID, "bad FFT debug arguments");
   const int lg = ilog2_host(N);
-  static double2* dtw[kMaxLogNmv + 1] = {};
+  static double2* dtw[kMaxLogL + 1] = {};
   if (!dtw[lg]) {
     std::vector<double2> t = twiddles(N);
     CK(cudaMalloc(&dtw[lg], t.size() * sizeof(double2)));

@@ -7,8 +7,8 @@
 
 namespace tsf {
 
-constexpr int kMinLogNmv = 4;   // N_mv = 16
-constexpr int kMaxLogNmv = 13;  // N_mv = 8192 (n <= 8192 single-CTA engine)
+constexpr int kMinLogL = 5;   // L = 32
+constexpr int kMaxLogL = 13;  // L = 8192 (n <= 4096 single-CTA engine)
 
 // sets tsf_last_error() and returns TSF_E_CUDA (defined in tsf_abi.cu)
 int report_cuda(cudaError_t e, const char* what);
@@ -25,7 +25,6 @@ struct Dispatch {
 };
 
 #define TSF_EXTERN_DISPATCH(L) extern template struct Dispatch<L>;
-TSF_EXTERN_DISPATCH(4)
 TSF_EXTERN_DISPATCH(5)
 TSF_EXTERN_DISPATCH(6)
 TSF_EXTERN_DISPATCH(7)

@@ -19,7 +19,7 @@ inline cudaError_t prep_kernel(K kernel, int smem) {
 template <int LOG>
 int Dispatch<LOG>::matvec(int n, const FilterTables& t, int B, const double* x, double* y,
                           const double* kappa, double shift, cudaStream_t st) {
-  constexpr int NMV = 1 << LOG;
+  constexpr int NMV = 1 << LOG;  // = L
   using S = KShape<NMV>;
   auto k = k_toeplitz_apply<NMV>;
   cudaError_t e = prep_kernel(k, S::SMEM);
@@ -31,7 +31,7 @@ int Dispatch<LOG>::matvec(int n, const FilterTables& t, int B, const double* x, 
 template <int LOG>
 int Dispatch<LOG>::precond(int n, const FilterTables& t, int B, const double* v, double* z,
                            double shift, double kbar, const double* kbar_dev, cudaStream_t st) {
-  constexpr int NMV = 1 << LOG;
+  constexpr int NMV = 1 << LOG;  // = L
   using S = KShape<NMV>;
   auto k = k_strang_apply<NMV>;
   cudaError_t e = prep_kernel(k, S::SMEM);
@@ -52,7 +52,7 @@ int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
 
 template <int LOG>
 int Dispatch<LOG>::solve(int B, int method, int pc, const KrylovArgs& a, cudaStream_t st) {
-  constexpr int NMV = 1 << LOG;
+  constexpr int NMV = 1 << LOG;  // = L
   if (method == 0) return pc ? solve_t<NMV, 1, false>(B, a, st) : solve_t<NMV, 0, false>(B, a, st);
   return pc ? solve_t<NMV, 1, true>(B, a, st) : solve_t<NMV, 0, true>(B, a, st);
 }
@@ -60,7 +60,7 @@ int Dispatch<LOG>::solve(int B, int method, int pc, const KrylovArgs& a, cudaStr
 template <int LOG>
 int Dispatch<LOG>::fft(int inverse, int B, const double2* in, double2* out, const double2* tw,
                        cudaStream_t st) {
-  constexpr int NMV = 1 << LOG;
+  constexpr int NMV = 1 << LOG;  // = L
   using S = KShape<NMV>;
   constexpr int smem = FftPlan<NMV, 16>::SMEM_ELEMS * 16;
   cudaError_t e;

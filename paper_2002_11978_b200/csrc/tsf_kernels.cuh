@@ -1,4 +1,4 @@
-// Batched per-instance kernels (one CTA per problem instance, n <= 8192).
+// Batched per-instance kernels (one CTA per problem instance, n <= 4096).
 //
 //  k_toeplitz_apply : y = shift*x + kappa .* (A x)   (toeplitz.py:51-63 + scheme.py:129-130)
 //  k_strang_apply   : z = P^{-1} v                    (toeplitz.py:131-136)
@@ -9,6 +9,7 @@
 //                     with exactly the reference's control flow, all scalars
 //                     and convergence tests on the device, one CTA per
 //                     instance, no host round trip per iteration.
+// Template parameter L is the circulant embedding length (pow2 >= 2n-1).
 #pragma once
 
 #include "tsf_filters.cuh"
@@ -20,11 +21,9 @@ constexpr int kMaxModes = 4;
 struct KrylovArgs {
   int n;
   int B;
-  // right-hand side [B, n] (R0)
-  const double* rhs;
-  // solution [B, n] (written)
-  double* x;
-  // diffusivity: either given [B, n] (kappa != nullptr), or evaluated from
+  const double* rhs;        // [B, n] (R0)
+  double* x;                // [B, n] solution (written)
+  // diffusivity: given [B, n] (kappa != nullptr), or evaluated from
   // separable modes kappa(x_i) = sum_q kmode_q[b][i] * kcoef[q] into kwork
   const double* kappa;
   const double* kmodes;     // mode q of instance b at kmodes + q*kq_stride + b*kb_stride
@@ -37,88 +36,82 @@ struct KrylovArgs {
   double kbar;              // > 0: preconditioner kappa_bar; else mean(kappa)
   double tol;
   int max_iters;
-  // workspaces [B, n]
-  double* r;
+  double* r;                // workspaces [B, n]
   double* p;
   double* v;
   double* ph;
   double* s;
-  // per-instance outputs
-  int* iters;
+  int* iters;               // per-instance outputs
   double* relres;
   int* status;
   FilterTables tab;
 };
 
-template <int NMV>
+template <int L>
 struct KShape {
-  static constexpr int T = NMV / 16;             // owning threads
+  static constexpr int T = L / 16;               // owning threads
   static constexpr int BLOCK = T < 32 ? 32 : T;  // launched threads
-  static constexpr int SMEM = FftPlan<NMV, 16>::SMEM_ELEMS * 16;
+  static constexpr int SMEM = FftPlan<L, 16>::SMEM_ELEMS * 16;
 };
 
 // --------------------------------------------------------------- matvec
-template <int NMV>
-__global__ void __launch_bounds__(KShape<NMV>::BLOCK)
+template <int L>
+__global__ void __launch_bounds__(KShape<L>::BLOCK)
 k_toeplitz_apply(int n, const double* __restrict__ x, double* __restrict__ y,
                  const double* __restrict__ kappa, double shift, int has_kappa,
                  FilterTables tab) {
   extern __shared__ double2 sm[];
-  constexpr int T = KShape<NMV>::T;
+  constexpr int T = KShape<L>::T;
   const int tid = threadIdx.x;
   const long off = (long)blockIdx.x * n;
-  const double* xb = x + off;
-  double2 xv[8], io[8];
+  double xv[8], io[8];
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) io[c] = xv[c] = ld_pair(xb, n, tid + c * T);
+    for (int c = 0; c < 8; ++c) io[c] = xv[c] = ld_real(x + off, n, tid + c * T);
   }
-  toeplitz_filter<NMV>(io, sm, tab);
+  toeplitz_filter<L>(io, sm, tab);
   if (tid < T) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int j = tid + c * T;
-      double2 out = io[c];
-      if (has_kappa) {
-        const double2 k = ld_pair(kappa + off, n, j);
-        out = make_double2(fma(shift, xv[c].x, k.x * out.x), fma(shift, xv[c].y, k.y * out.y));
-      }
-      st_pair(y + off, n, j, out);
+      double out = io[c];
+      if (has_kappa) out = fma(shift, xv[c], ld_real(kappa + off, n, j) * out);
+      st_real(y + off, n, j, out);
     }
   }
 }
 
 // --------------------------------------------------------------- precond
-template <int NMV>
-__global__ void __launch_bounds__(KShape<NMV>::BLOCK)
+template <int L>
+__global__ void __launch_bounds__(KShape<L>::BLOCK)
 k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ z, double shift,
                double kbar, const double* __restrict__ kbar_dev, FilterTables tab) {
   extern __shared__ double2 sm[];
-  constexpr int T = KShape<NMV>::T;
+  constexpr int T = KShape<L>::T;
   const int tid = threadIdx.x;
   const long off = (long)blockIdx.x * n;
   const double kb = kbar_dev ? kbar_dev[blockIdx.x] : kbar;
-  double2 io[8];
+  double io[8];
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) io[c] = ld_pair(v + off, n, tid + c * T);
+    for (int c = 0; c < 8; ++c) io[c] = ld_real(v + off, n, tid + c * T);
   }
-  strang_filter<NMV>(io, sm, tab, shift, kb);
+  strang_filter<L>(io, sm, tab, shift, kb);
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) st_pair(z + off, n, tid + c * T, io[c]);
+    for (int c = 0; c < 8; ++c) st_real(z + off, n, tid + c * T, io[c]);
   }
 }
 
 // --------------------------------------------------------------- solver
-// PC: 0 = no preconditioner ("krylov"), 1 = Strang ("pkrylov", pow2 n)
+// PC: 0 = no preconditioner ("krylov"), 1 = Strang ("pkrylov", pow2 n = L/2)
 // CG: false = BiCGSTAB, true = PCG (kappa_x_independent)
-template <int NMV, int PC, bool CG>
-__global__ void __launch_bounds__(KShape<NMV>::BLOCK)
+template <int L, int PC, bool CG>
+__global__ void __launch_bounds__(KShape<L>::BLOCK)
 k_krylov_solve(KrylovArgs a) {
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
-  constexpr int T = KShape<NMV>::T;
+  constexpr int T = KShape<L>::T;
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int b = blockIdx.x;
@@ -142,14 +135,10 @@ k_krylov_solve(KrylovArgs a) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int j = tid + c * T;
-        if (2 * j < n) {
-          double2 k = ld_pair(kg, n, j);
-          ksum += k.x;
-          kmin = fmin(kmin, k.x);
-          if (2 * j + 1 < n) {
-            ksum += k.y;
-            kmin = fmin(kmin, k.y);
-          }
+        if (j < n) {
+          const double k = kg[j];
+          ksum += k;
+          kmin = fmin(kmin, k);
         }
       }
     }
@@ -160,22 +149,16 @@ k_krylov_solve(KrylovArgs a) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int j = tid + c * T;
-        if (2 * j < n) {
-          double2 acc = make_double2(0.0, 0.0);
+        if (j < n) {
+          double acc = 0.0;
           for (int q = 0; q < a.nk; ++q) {
-            const double2 mq =
-                ld_pair(a.kmodes + q * a.kq_stride + (long)b * a.kb_stride, n, j);
+            const double mq = a.kmodes[q * a.kq_stride + (long)b * a.kb_stride + j];
             // no contraction: reproduce numpy's  acc + mode*coef  rounding
-            acc.x = __dadd_rn(acc.x, __dmul_rn(mq.x, a.kcoef[q]));
-            acc.y = __dadd_rn(acc.y, __dmul_rn(mq.y, a.kcoef[q]));
+            acc = __dadd_rn(acc, __dmul_rn(mq, a.kcoef[q]));
           }
-          st_pair(kw, n, j, acc);
-          ksum += acc.x;
-          kmin = fmin(kmin, acc.x);
-          if (2 * j + 1 < n) {
-            ksum += acc.y;
-            kmin = fmin(kmin, acc.y);
-          }
+          kw[j] = acc;
+          ksum += acc;
+          kmin = fmin(kmin, acc);
         }
       }
     }
@@ -194,10 +177,7 @@ k_krylov_solve(KrylovArgs a) {
   if constexpr (PC == 1) {
     // total eigenvalues d + kbar*lam > 0  (toeplitz.py:122-124)
     double tmin = 1e308;
-    for (int k = tid; k < n / 2; k += blockDim.x) {
-      const double2 lam = __ldg(&a.tab.pclam[k]);
-      tmin = fmin(tmin, fmin(d + kbar * lam.x, d + kbar * lam.y));
-    }
+    for (int k = tid; k < n; k += blockDim.x) tmin = fmin(tmin, d + kbar * __ldg(&a.tab.pclam[k]).x);
     tmin = block_min1(tmin, red);
     if (tmin <= 0.0) {
       if (tid == 0) {
@@ -209,38 +189,35 @@ k_krylov_solve(KrylovArgs a) {
     }
   }
 
-  auto precond = [&](double2 (&io)[8]) {
-    if constexpr (PC == 1) strang_filter<NMV>(io, sm, a.tab, d, kbar);
+  auto precond = [&](double (&io)[8]) {
+    if constexpr (PC == 1) strang_filter<L>(io, sm, a.tab, d, kbar);
   };
   // y = d*u + kappa .* (A u); u preserved
-  auto apply_op = [&](const double2 (&u)[8], double2 (&y)[8]) {
+  auto apply_op = [&](const double (&u)[8], double (&y)[8]) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) y[c] = u[c];
-    toeplitz_filter<NMV>(y, sm, a.tab);
+    toeplitz_filter<L>(y, sm, a.tab);
     if (own) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const double2 k = ld_pair(kg, n, tid + c * T);
-        y[c] = make_double2(fma(d, u[c].x, k.x * y[c].x), fma(d, u[c].y, k.y * y[c].y));
-      }
+      for (int c = 0; c < 8; ++c) y[c] = fma(d, u[c], ld_real(kg, n, tid + c * T) * y[c]);
     }
   };
-  auto dot_loc = [](const double2 (&u)[8], const double2 (&w)[8]) {
+  auto dot_loc = [](const double (&u)[8], const double (&w)[8]) {
     double acc = 0.0;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc = fma(u[c].x, w[c].x, fma(u[c].y, w[c].y, acc));
+    for (int c = 0; c < 8; ++c) acc = fma(u[c], w[c], acc);
     return acc;
   };
-  auto load = [&](double2 (&u)[8], const double* g) {
+  auto load = [&](double (&u)[8], const double* g) {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) u[c] = ld_pair(g, n, tid + c * T);
+      for (int c = 0; c < 8; ++c) u[c] = ld_real(g, n, tid + c * T);
     }
   };
-  auto store = [&](double* g, const double2 (&u)[8]) {
+  auto store = [&](double* g, const double (&u)[8]) {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) st_pair(g, n, tid + c * T, u[c]);
+      for (int c = 0; c < 8; ++c) st_real(g, n, tid + c * T, u[c]);
     }
   };
   auto finish = [&](int it, double rel, int st) {
@@ -251,18 +228,18 @@ k_krylov_solve(KrylovArgs a) {
     }
   };
 
-  double2 u[8], w[8];
+  double u[8], w[8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) u[c] = w[c] = make_double2(0.0, 0.0);
+  for (int c = 0; c < 8; ++c) u[c] = w[c] = 0.0;
 
   // ---- r = r0 = rhs, x = 0  (krylov.py:107-113 / 64-69)
   load(u, r0g);
   const double ss0 = block_sum1(own ? dot_loc(u, u) : 0.0, red);
   const double nrm0 = sqrt(ss0);
   {
-    double2 zero[8];
+    double zero[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) zero[c] = make_double2(0.0, 0.0);
+    for (int c = 0; c < 8; ++c) zero[c] = 0.0;
     store(xg, zero);
   }
   if (nrm0 == 0.0) {
@@ -275,7 +252,7 @@ k_krylov_solve(KrylovArgs a) {
   if constexpr (!CG) {
     // ================= BiCGSTAB (krylov.py:88-153) =================
     double rho = 1.0, alpha = 1.0, omega = 1.0;
-    double rho_new = ss0;           // r0 . r with r = r0 (same reduction)
+    double rho_new = ss0;           // r0 . r with r = r0
     double rnorm = nrm0;            // ||r|| for breakdown reports
     for (int it = 1; it <= max_iters; ++it) {
       if (rho_new == 0.0) {
@@ -291,9 +268,7 @@ k_krylov_solve(KrylovArgs a) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const int j = tid + c * T;
-            const double2 rr = ld_pair(rg, n, j), pp = ld_pair(pg, n, j), vv = ld_pair(vg, n, j);
-            u[c] = make_double2(rr.x + beta * (pp.x - omega * vv.x),
-                                rr.y + beta * (pp.y - omega * vv.y));
+            u[c] = ld_real(rg, n, j) + beta * (ld_real(pg, n, j) - omega * ld_real(vg, n, j));
           }
         }
       }
@@ -302,7 +277,7 @@ k_krylov_solve(KrylovArgs a) {
       store(phg, u);
       apply_op(u, w);     // w = v = M p_hat
       store(vg, w);
-      double2 r0v[8];
+      double r0v[8];
       load(r0v, r0g);
       const double denom = block_sum1(own ? dot_loc(r0v, w) : 0.0, red);
       if (denom == 0.0) {
@@ -314,8 +289,8 @@ k_krylov_solve(KrylovArgs a) {
       if (own) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const double2 rr = (it == 1) ? r0v[c] : ld_pair(rg, n, tid + c * T);
-          w[c] = make_double2(rr.x - alpha * w[c].x, rr.y - alpha * w[c].y);
+          const double rr = (it == 1) ? r0v[c] : ld_real(rg, n, tid + c * T);
+          w[c] = rr - alpha * w[c];
         }
       }
       const double snorm = sqrt(block_sum1(own ? dot_loc(w, w) : 0.0, red));
@@ -325,8 +300,7 @@ k_krylov_solve(KrylovArgs a) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const int j = tid + c * T;
-            const double2 xx = ld_pair(xg, n, j);
-            st_pair(xg, n, j, make_double2(xx.x + alpha * u[c].x, xx.y + alpha * u[c].y));
+            st_real(xg, n, j, ld_real(xg, n, j) + alpha * u[c]);
           }
         }
         finish(it, snorm / nrm0, TSF_OK);
@@ -335,45 +309,39 @@ k_krylov_solve(KrylovArgs a) {
       store(sg, w);
       precond(w);         // w = s_hat
       apply_op(w, u);     // u = t = M s_hat
-      double tt = 0.0, ts = 0.0;
+      Vals<2> red2;
+      red2.v[0] = 0.0;
+      red2.v[1] = 0.0;
       if (own) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const double2 ss = ld_pair(sg, n, tid + c * T);
-          tt = fma(u[c].x, u[c].x, fma(u[c].y, u[c].y, tt));
-          ts = fma(u[c].x, ss.x, fma(u[c].y, ss.y, ts));
+          const double ss = ld_real(sg, n, tid + c * T);
+          red2.v[0] = fma(u[c], u[c], red2.v[0]);
+          red2.v[1] = fma(u[c], ss, red2.v[1]);
         }
       }
-      Vals<2> red2;
-      red2.v[0] = tt;
-      red2.v[1] = ts;
       red2 = block_sum<2>(red2, red);
-      tt = red2.v[0];
-      ts = red2.v[1];
+      const double tt = red2.v[0], ts = red2.v[1];
       if (tt == 0.0) {
         finish(it, snorm / nrm0, TSF_BD_OMEGA_DEN);
         return;
       }
       omega = ts / tt;
       // x += alpha p_hat + omega s_hat ; r = s - omega t
-      double rr_loc = 0.0, r0r_loc = 0.0;
+      red2.v[0] = 0.0;
+      red2.v[1] = 0.0;
       if (own) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int j = tid + c * T;
-          const double2 xx = ld_pair(xg, n, j), phv = ld_pair(phg, n, j);
-          st_pair(xg, n, j, make_double2(xx.x + (alpha * phv.x + omega * w[c].x),
-                                         xx.y + (alpha * phv.y + omega * w[c].y)));
-          const double2 ss = ld_pair(sg, n, j), r0 = ld_pair(r0g, n, j);
-          const double2 rn = make_double2(ss.x - omega * u[c].x, ss.y - omega * u[c].y);
-          st_pair(rg, n, j, rn);
-          rr_loc = fma(rn.x, rn.x, fma(rn.y, rn.y, rr_loc));
-          r0r_loc = fma(r0.x, rn.x, fma(r0.y, rn.y, r0r_loc));
+          st_real(xg, n, j, ld_real(xg, n, j) + (alpha * ld_real(phg, n, j) + omega * w[c]));
+          const double rn = ld_real(sg, n, j) - omega * u[c];
+          st_real(rg, n, j, rn);
+          red2.v[0] = fma(rn, rn, red2.v[0]);
+          red2.v[1] = fma(ld_real(r0g, n, j), rn, red2.v[1]);
         }
       }
       rho = rho_new;
-      red2.v[0] = rr_loc;
-      red2.v[1] = r0r_loc;
       red2 = block_sum<2>(red2, red);
       rnorm = sqrt(red2.v[0]);
       const double rel = rnorm / nrm0;
@@ -390,17 +358,16 @@ k_krylov_solve(KrylovArgs a) {
     finish(max_iters, rnorm / nrm0, TSF_NOT_CONVERGED);
   } else {
     // ================= PCG (krylov.py:43-85) =================
-    // r = b (kept in rg), z = psolve(r), p = z, rz = r.z
-    store(rg, u);
+    store(rg, u);                    // r = b
     precond(u);                      // u = z
-    store(pg, u);
-    double2 rr[8];
+    store(pg, u);                    // p = z
+    double rr[8];
     load(rr, r0g);
     double rz = block_sum1(own ? dot_loc(rr, u) : 0.0, red);
     double rnorm = nrm0;
     for (int it = 1; it <= max_iters; ++it) {
       load(u, pg);
-      apply_op(u, w);                // w = q = A p
+      apply_op(u, w);                // w = q = M p
       const double curv = block_sum1(own ? dot_loc(u, w) : 0.0, red);
       if (curv <= 0.0) {
         finish(it, rnorm / nrm0, TSF_BD_CURVATURE);
@@ -412,13 +379,11 @@ k_krylov_solve(KrylovArgs a) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int j = tid + c * T;
-          const double2 xx = ld_pair(xg, n, j);
-          st_pair(xg, n, j, make_double2(xx.x + al * u[c].x, xx.y + al * u[c].y));
-          double2 r1 = ld_pair(rg, n, j);
-          r1 = make_double2(r1.x - al * w[c].x, r1.y - al * w[c].y);
-          st_pair(rg, n, j, r1);
+          st_real(xg, n, j, ld_real(xg, n, j) + al * u[c]);
+          const double r1 = ld_real(rg, n, j) - al * w[c];
+          st_real(rg, n, j, r1);
           rr[c] = r1;
-          rr_loc = fma(r1.x, r1.x, fma(r1.y, r1.y, rr_loc));
+          rr_loc = fma(r1, r1, rr_loc);
         }
       }
       rnorm = sqrt(block_sum1(rr_loc, red));
@@ -434,9 +399,7 @@ k_krylov_solve(KrylovArgs a) {
       const double beta = rz_new / rz;
       if (own) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          u[c] = make_double2(w[c].x + beta * u[c].x, w[c].y + beta * u[c].y);
-        }
+        for (int c = 0; c < 8; ++c) u[c] = w[c] + beta * u[c];
       }
       store(pg, u);
       rz = rz_new;
