@@ -1,0 +1,437 @@
+#!/usr/bin/env python3
+"""Benchmark: grid-point time-step solves per second of the FIDS march on B200.
+
+Workload (default, BASELINE.json configs[2]): B independent instances per
+GPU, n = 4096 unknowns (N_ref = 4097), M = 512 graded levels, gamma = 0.5,
+alpha = 1.5, r = (2-gamma)/gamma, SOE tolerance 1e-12 (N_exp = 143),
+Strang-preconditioned BiCGSTAB at tol 1e-12; per-instance seeded
+kappa = exp(0.4 g(x)) (1 + 0.2 t), g = 8 random Fourier modes with
+N(0, 1/k^2) coefficients; f = 8 random sine modes x (1 + t);
+phi = (1 - x^2)^2 U[0.5, 2].  A "step" is one time level of the march over
+the whole batch (fused SOE push + RHS kernel, then the fused level-solve
+kernel).  value = (instances on all ranks) * n * K / max-over-ranks time.
+
+Multi-GPU: one process per GPU (torchrun), B instances per rank (weak
+scaling), no collective on the hot path; barrier + max-over-ranks timing.
+
+--impl reference times the reference's CPU path — the oracle port of
+tsfrac.run_fids (oracle/, numpy pocketfft + OpenBLAS, exactly the
+reference's arithmetic) — on the host cores, one instance per worker
+process, same levels, same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "grid-point time-step solves/sec (B*N*M/s)"
+UNIT = "grid-point solves/s"
+
+
+def workload(args):
+    if args.workload == "cfg2":
+        return dict(name="configs[2] batched FIDS march", n=4096, M=512, gamma=0.5, alpha=1.5,
+                    eps=1e-12, tol=1e-12, B=args.batch or 4096)
+    if args.workload == "cfg0":
+        return dict(name="configs[0] single FIDS march", n=1024, M=256, gamma=0.5, alpha=1.5,
+                    eps=1e-12, tol=1e-12, B=args.batch or 1)
+    raise SystemExit(f"unknown workload {args.workload}")
+
+
+def instance_fields(n, b0, B, seed=2002_11978):
+    """Seeded per-instance fields of configs[2]."""
+    N = n + 1
+    x = -1.0 + (2.0 / N) * np.arange(1, N)
+    k = np.arange(1, 9)
+    cos_b = np.cos(np.pi * np.outer(k, x))
+    sin_b = np.sin(np.pi * np.outer(k, x))
+    sin_f = np.sin(np.pi * np.outer(k, (x + 1.0) / 2.0))
+    A = np.empty((B, 8))
+    Bc = np.empty((B, 8))
+    Cc = np.empty((B, 8))
+    U = np.empty(B)
+    for i in range(B):
+        rng = np.random.default_rng([seed, b0 + i])
+        A[i] = rng.normal(0.0, 1.0 / k)
+        Bc[i] = rng.normal(0.0, 1.0 / k)
+        Cc[i] = rng.normal(0.0, 1.0 / k)
+        U[i] = rng.uniform(0.5, 2.0)
+    g = A @ cos_b + Bc @ sin_b
+    kx = np.exp(0.4 * g)
+    fx = Cc @ sin_f
+    u0 = (1.0 - x * x) ** 2 * U[:, None]
+    return x, kx, fx, u0
+
+
+def cfg0_fields(n):
+    N = n + 1
+    x = -1.0 + (2.0 / N) * np.arange(1, N)
+    return x
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [v.strip() for v in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------- CPU
+def _cpu_worker(args):
+    """One instance of the workload through the oracle port; returns the
+    wall time of levels (warmup, warmup+K]."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    wl, b, warmup, K = args
+    import oracle as O
+    n = wl["n"]
+    if wl.get("cfg2", True):
+        x, kx, fx, u0 = instance_fields(n, b, 1)
+        kf = lambda xx, t: kx[0] * (1.0 + 0.2 * t)  # noqa: E731
+        sf = lambda xx, t: fx[0] * (1.0 + t)  # noqa: E731
+        phi = u0[0]
+    else:
+        kf = lambda xx, t: 1.0 + 0.5 * np.sin(np.pi * xx) * np.exp(-t)  # noqa: E731
+        sf = lambda xx, t: (1.0 + t) * np.sin(np.pi * xx)  # noqa: E731
+        phi = (1.0 - cfg0_fields(n) ** 2) ** 2
+    gam, alpha, M = wl["gamma"], wl["alpha"], wl["M"]
+    r = (2.0 - gam) / gam
+    N = n + 1
+    t, tau = O.graded_mesh(M, r, 1.0)
+    col, h, _ = O.ifl_column(alpha, 1.0 + alpha / 2.0, 1.0, N)
+    xx = -1.0 + h * np.arange(1, N)
+    _, symbol = O.toeplitz_symbol(col)
+    lam = O.strang_eigs(col)
+    G = math.exp(math.lgamma(1.0 - gam))
+    s, w = O.soe_build(gam, wl["eps"], (1.0 / M) ** r, 1.0)
+    u = np.asarray(phi, dtype=float)
+    W = np.zeros((s.size, n))
+    t0 = None
+    its = 0
+    for m in range(1, min(M, warmup + K) + 1):
+        if m == warmup + 1:
+            t0 = time.perf_counter()
+        kap = kf(xx, t[m])
+        f = sf(xx, t[m])
+        u, _, out = O.fids_step(u, W, s, w, tau[m - 1], gam, G, kap, f, symbol, lam, wl["tol"])
+        if m > warmup:
+            its += out.iterations
+    return time.perf_counter() - t0, its
+
+
+def cpu_measure(wl, warmup, K, workers, cfg2=True):
+    from concurrent.futures import ProcessPoolExecutor
+    wl = dict(wl, cfg2=cfg2)
+    K = min(K, wl["M"] - warmup)
+    with ProcessPoolExecutor(max_workers=workers) as ex:
+        res = list(ex.map(_cpu_worker, [(wl, b, warmup, K) for b in range(workers)]))
+    wall = max(r[0] for r in res)
+    value = workers * wl["n"] * K / wall
+    return value, wall, K, sum(r[1] for r in res) / (workers * K)
+
+
+# --------------------------------------------------------------------- GPU
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=509)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--batch", type=int, default=0, help="instances per rank")
+    ap.add_argument("--cpu-workers", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    wl = workload(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    warmup = max(3, args.warmup)
+    cfg2 = args.workload == "cfg2"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        workers = args.cpu_workers or os.cpu_count() or 1
+        value, wall, K, avg_its = cpu_measure(wl, warmup, args.steps, workers, cfg2)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": K, "warmup": warmup,
+            "ms_per_step": wall / K * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "config": {"workload": wl["name"], "instances_sampled": workers, "n": wl["n"],
+                       "M": wl["M"], "gamma": wl["gamma"], "alpha": wl["alpha"],
+                       "tol": wl["tol"], "avg_iterations": avg_its},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                             "sample": f"{workers} instances (one per worker process, "
+                                       f"OPENBLAS_NUM_THREADS=1) x levels {warmup + 1}.."
+                                       f"{warmup + K} of the configs march via oracle/ "
+                                       "(numpy pocketfft/OpenBLAS restatement of tsfrac.run_fids)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_2002_11978_b200 as P
+    from paper_2002_11978_b200 import _native
+    from paper_2002_11978_b200.scheme import FidsMarch, _field_separable
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    n, M, gam, alpha, B = wl["n"], wl["M"], wl["gamma"], wl["alpha"], wl["B"]
+    r = (2.0 - gam) / gam
+    N = n + 1
+    if cfg2:
+        x, kx, fx, u0 = instance_fields(n, rank * B, B)
+        kap = P.SeparableField([np.ones(n)], lambda t: [1.0 + 0.2 * t])
+        src = P.SeparableField([np.ones(n)], lambda t: [1.0 + t])
+        kmodes, fmodes = kx[None], fx[None]
+    else:
+        x = cfg0_fields(n)
+        kap = P.SeparableField([np.ones(n), 0.5 * np.sin(np.pi * x)], lambda t: [1.0, math.exp(-t)])
+        src = P.SeparableField([np.sin(np.pi * x)], lambda t: [1.0 + t])
+        u0 = np.repeat(((1.0 - x * x) ** 2)[None, :], B, axis=0)
+        kmodes = fmodes = None
+    mesh = P.build_mesh(M, r, 1.0)
+    soe = P.build_soe(gam, wl["eps"], (1.0 / M) ** r, 1.0)
+    kdev = _field_separable(kap, x, mesh.t, B, kmodes, dev)
+    fdev = _field_separable(src, x, mesh.t, B, fmodes, dev)
+    u0_d = torch.from_numpy(np.ascontiguousarray(u0)).to(dev)
+    march = FidsMarch(gam, alpha, 1.0, 1.0, M, r, N, soe, method=0, precond=1, tol=wl["tol"],
+                      max_iters=None, B=B, kappa=kdev, source=fdev, u0=u0_d, device=local)
+    K = args.steps
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # segments of at most M levels; a new march (state reset) starts when one ends
+    def plan_levels(start_level, count):
+        segs, lvl = [], start_level
+        while count > 0:
+            if lvl > M:
+                segs.append(("reset", 0))
+                lvl = 1
+            take = min(count, M - lvl + 1)
+            segs.append(("run", take))
+            lvl += take
+            count -= take
+        return segs
+
+    march.reset()
+    march.run(warmup)
+    barrier()
+    nev = 3 * K
+    events = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    t_start.record()
+    ev_i = 0
+    its_sum = 0
+    launches = 0
+    levels_done = []
+    for kind, cnt in plan_levels(warmup + 1, K):
+        if kind == "reset":
+            march.reset()
+            continue
+        m0 = march.next_level
+        march.run(cnt, events=events[ev_i: ev_i + 3 * cnt])
+        ev_i += 3 * cnt
+        launches += 2 * cnt + (1 if march.next_level == M + 1 else 0)
+        levels_done.append((m0, march.next_level))
+    t_end.record()
+    barrier()
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    if dist is not None:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    iters = march.iters.cpu().numpy()
+    for m0, m1 in levels_done:
+        its_sum += int(iters[m0 - 1: m1 - 1].sum())
+    status = march.status.cpu().numpy()
+    if np.any(status != 0):
+        raise SystemExit(f"solver failure in the timed region: status {np.unique(status)}")
+    soe_ms = sum(events[3 * i].elapsed_time(events[3 * i + 1]) for i in range(K))
+    solve_ms = sum(events[3 * i + 1].elapsed_time(events[3 * i + 2]) for i in range(K))
+    nexp = soe.n_exp
+    soe_bytes = (16 * nexp + 32) * n * B  # W read+write; u, u_prev, f-mode read; rhs write
+    solve_bytes = 216 * n * its_sum / K   # per launch: SURVEY §8(d) BiCGSTAB iteration = 216 n B
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    k_soe = {"name": "tsf::k_soe_push_rhs", "avg_ms": soe_ms / K,
+             "GBps": soe_bytes / (soe_ms / K * 1e-3) / 1e9}
+    k_solve = {"name": "tsf::k_krylov_solve<8192,1,false>", "avg_ms": solve_ms / K,
+               "GBps": solve_bytes / (solve_ms / K * 1e-3) / 1e9,
+               "iterations_per_launch": its_sum / K}
+    dom = k_solve if solve_ms >= soe_ms else k_soe
+    dom_bytes = solve_bytes if dom is k_solve else soe_bytes
+    roof = {"kernel": dom["name"], "bound": "hbm", "achieved": dom["GBps"], "peak": hbm,
+            "unit": "GB/s", "frac": dom["GBps"] / hbm, "traffic": None,
+            "algorithmic_bytes_per_launch": dom_bytes, "peak_source": peak_src,
+            "share_of_step": (solve_ms if dom is k_solve else soe_ms) / ms}
+    value = world * B * n * K / (ms * 1e-3)
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        u0_h = torch.from_numpy(np.ascontiguousarray(u0)).pin_memory()
+        km_h = None if kmodes is None else torch.from_numpy(np.ascontiguousarray(kmodes)).pin_memory()
+        fm_h = None if fmodes is None else torch.from_numpy(np.ascontiguousarray(fmodes)).pin_memory()
+        levels = min(M, warmup + K)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h2d = u0_h.numel() * 8
+        march.u0.copy_(u0_h, non_blocking=True)
+        if km_h is not None:
+            kdev.modes.copy_(km_h, non_blocking=True)
+            fdev.modes.copy_(fm_h, non_blocking=True)
+            h2d += (km_h.numel() + fm_h.numel()) * 8
+        march.reset()
+        march.run(levels)
+        u_out = march.u_level(march.next_level - 1).to("cpu", non_blocking=False)
+        its_out = march.iters[:levels].to("cpu")
+        rel_out = march.relres[:levels].to("cpu")
+        e1.record()
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if dist is not None:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        d2h = u_out.numel() * 8 + its_out.numel() * 4 + rel_out.numel() * 8
+        e2e = {"value": world * B * n * levels / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d / levels, "d2h_bytes_per_step": d2h / levels,
+               "levels": levels,
+               "note": "pinned host u0 + coefficient modes -> device, march levels "
+                       f"1..{levels}, final u + per-level iterations/residuals -> host"}
+
+    # ---- standalone Toeplitz matvec throughput (configs[4] point n=4096, B*n=2^26)
+    mv = None
+    if rank == 0:
+        col = P.build_ifl(1.5, 1.75, 1.0, n + 1).first_col
+        op = P.build_toeplitz(col)
+        Bm = (1 << 26) // n
+        xm = torch.randn(Bm, n, dtype=torch.float64, device=dev)
+        km = torch.rand(Bm, n, dtype=torch.float64, device=dev) * 1.5 + 0.5
+        ym = torch.empty_like(xm)
+        lib = _native.load()
+        st = _native.stream_ptr()
+        lib.tsf_toeplitz_matvec(op.plan.handle, Bm, xm.data_ptr(), ym.data_ptr(), km.data_ptr(), 2.0, st)
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(5):
+            lib.tsf_toeplitz_matvec(op.plan.handle, Bm, xm.data_ptr(), ym.data_ptr(), km.data_ptr(),
+                                    2.0, st)
+        a1.record()
+        torch.cuda.synchronize()
+        t_mv = a0.elapsed_time(a1) / 5 * 1e-3
+        gbs = 24.0 * n * Bm / t_mv / 1e9
+        mv = {"n": n, "B": Bm, "GBps": gbs, "frac_hbm": gbs / hbm, "ms": t_mv * 1e3}
+        del xm, km, ym
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = args.cpu_workers or min(os.cpu_count() or 1, 8)
+        cw = min(K, 64)
+        cval, cwall, cK, cits = cpu_measure(wl, warmup, cw, workers, cfg2)
+        cpu = {"value": cval, "unit": UNIT, "cores": workers, "kind": "port",
+               "sample": f"{workers} instances (one per process, 1 BLAS thread) x levels "
+                         f"{warmup + 1}..{warmup + cK} via oracle/ (numpy restatement of "
+                         f"tsfrac.run_fids); avg its {cits:.2f}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": warmup, "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded per instance, SURVEY.md §8(d))",
+            "config": {"workload": wl["name"], "instances_per_gpu": B, "global_batch": B * world,
+                       "n": n, "M": M, "gamma": gam, "alpha": alpha, "r": r, "n_exp": nexp,
+                       "tol": wl["tol"], "soe_eps": wl["eps"],
+                       "levels_timed": [list(v) for v in levels_done],
+                       "avg_iterations": its_sum / (K * B),
+                       "l2": "inputs larger than L2: W is %.1f GB per GPU" % (B * nexp * n * 8 / 1e9),
+                       "parallelism": f"instances sharded over {world} GPU(s), no collectives"},
+            "roofline": roof,
+            "kernels": {"soe_push_rhs": k_soe, "krylov_solve": k_solve},
+            "toeplitz_matvec": mv,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

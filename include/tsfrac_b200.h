@@ -174,6 +174,10 @@ typedef struct tsf_march {
   int hist_B;
   int m_begin;
   int m_end;
+  /* optional per-level timing: 3 cudaEvent_t per level run (before the SOE
+   * kernel, between the SOE and solve kernels, after the solve kernel),
+   * recorded on `stream`; NULL disables */
+  void** events;
 } tsf_march;
 
 int tsf_fids_march(tsf_plan* plan, const tsf_march* desc, void* stream);

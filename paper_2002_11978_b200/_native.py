@@ -61,7 +61,7 @@ class March(C.Structure):
         ("soe_tab", P), ("kappa", Field), ("source", Field), ("u_buf0", P),
         ("u_buf1", P), ("W", P), ("rhs", P), ("kwork", P), ("iters", P),
         ("relres", P), ("status", P), ("hist", P), ("hist_B", I), ("m_begin", I),
-        ("m_end", I),
+        ("m_end", I), ("events", P),
     ]
 
 

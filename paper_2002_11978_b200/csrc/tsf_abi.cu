@@ -333,8 +333,13 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
   if (rc) return rc;
   double* ubuf[2] = {d->u_buf0, d->u_buf1};
   const size_t vn = (size_t)B * n;
+  auto rec = [&](int m, int k) -> int {
+    if (d->events) CK(cudaEventRecord((cudaEvent_t)d->events[3 * (m - d->m_begin) + k], st));
+    return TSF_SUCCESS;
+  };
   for (int m = d->m_begin; m < d->m_end; ++m) {
     // ---- history term + RHS of level m from W^{m-1} (push of level m-1 fused)
+    if ((rc = rec(m, 0))) return rc;
     SoeArgs s{};
     s.n = n;
     s.nexp = nexp;
@@ -361,6 +366,7 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
     s.f = nullptr;
     s.rhs = d->rhs;
     if ((rc = soe_launch(B, s, st))) return rc;
+    if ((rc = rec(m, 1))) return rc;
     // ---- level solve  -> u^m into ubuf[m & 1]
     KrylovArgs a{};
     a.rhs = d->rhs;
@@ -379,6 +385,7 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
     a.relres = d->relres + (size_t)(m - 1) * B;
     a.status = d->status + (size_t)(m - 1) * B;
     if ((rc = solve_impl(p, B, d->method, d->precond, a, st))) return rc;
+    if ((rc = rec(m, 2))) return rc;
     if (d->hist && d->hist_B > 0) {
       CK(cudaMemcpyAsync(d->hist + (size_t)m * d->hist_B * n, ubuf[m & 1],
                          sizeof(double) * (size_t)d->hist_B * n, cudaMemcpyDeviceToDevice, st));

@@ -290,13 +290,26 @@ class FidsMarch:
         d.m_begin, d.m_end = m_begin, m_end
         return d
 
-    def run(self, levels: Optional[int] = None, stream=None):
-        """Launch the next `levels` levels (all remaining by default); async."""
+    def run(self, levels: Optional[int] = None, stream=None, events=None):
+        """Launch the next `levels` levels (all remaining by default); async.
+
+        `events`: optional list of 3 torch.cuda.Event per level run (before
+        the SOE kernel, between SOE and solve, after the solve)."""
         m0 = self.next_level
         m1 = self.M + 1 if levels is None else min(self.M + 1, m0 + levels)
         if m1 <= m0:
             return
         d = self._desc(m0, m1)
+        if events is not None:
+            if len(events) < 3 * (m1 - m0):
+                raise ValueError("need 3 events per level")
+            torch = _native.torch_mod()
+            for e in events:  # materialise the lazily created CUDA events
+                if e.cuda_event == 0:
+                    e.record()
+            torch.cuda.synchronize(self.dev)
+            self._ev = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
+            d.events = C.cast(self._ev, C.c_void_p)
         _native.check(_native.load().tsf_fids_march(self.plan.handle, C.byref(d),
                                                     _native.stream_ptr(stream)))
         self.next_level = m1
