@@ -57,7 +57,7 @@ struct tsf_plan {
   int has_pc = 0;
   int device = 0;
   double2* tw = nullptr;   // W_L^e
-  double* mvS = nullptr;   // even part of the symbol / L
+  double2* mvS = nullptr;  // (S_{2k}, S_{2k+1}) / L, even part of the symbol
   double2* pclam = nullptr;  // (lam_k, lam_{n-k})
   // Krylov workspaces [cap][n] x 6
   int cap = 0;
@@ -123,7 +123,7 @@ int ensure_reserved(tsf_plan* p, int B) {
   p->dst = nullptr;
   p->cap = 0;
   CK(cudaSetDevice(p->device));
-  CK(cudaMalloc(&p->ws, sizeof(double) * (size_t)B * p->n * 6));
+  CK(cudaMalloc(&p->ws, sizeof(double) * (size_t)B * p->n * 8));
   CK(cudaMalloc(&p->ist, sizeof(int) * (size_t)B * 2));
   CK(cudaMalloc(&p->dst, sizeof(double) * (size_t)B));
   p->cap = B;
@@ -149,7 +149,7 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
   if (!symbol_re) return fail(TSF_E_INVALID, "symbol is NULL");
   const int lg = ilog2_host(L);
   if (lg < kMinLogL || lg > kMaxLogL)
-    return fail(TSF_E_UNSUPPORTED, "embedding L=%d outside the single-CTA engine (32..8192, n <= 4096)", L);
+    return fail(TSF_E_UNSUPPORTED, "embedding L=%d outside the single-CTA engine (32..16384, n <= 8192)", L);
   if (lam && !(is_pow2(n) && n >= 16 && L == 2 * n))
     return fail(TSF_E_UNSUPPORTED, "Strang preconditioner needs pow2 n >= 16 with L = 2n (n=%d, L=%d)", n, L);
   tsf_plan* p = new tsf_plan();
@@ -163,14 +163,17 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
     return rc;
   };
   if (cudaSetDevice(device) != cudaSuccess) return cleanup(fail(TSF_E_CUDA, "cudaSetDevice(%d)", device));
-  // twiddles of the length-L transform; the length-n Strang transform uses stride 2
+  // twiddles W_L^e: modulation of the odd-bin half; the length-N transforms use stride 2
   std::vector<double2> tw = twiddles(L);
   // The reference keeps Re IFFT(S . FFT(pad x)) (toeplitz.py:62-63): its
-  // effective symbol is the even part of S.  1/L of the inverse folded in.
-  std::vector<double> S(L);
-  for (int k = 0; k < L; ++k)
-    S[k] = (double)(0.5L * ((long double)symbol_re[k] + (long double)symbol_re[(L - k) % L]) /
+  // effective symbol is the even part of S.  1/L of the inverse folded in;
+  // stored as (S_{2k}, S_{2k+1}) for the even / odd output-bin halves.
+  auto Ssym = [&](int k) -> double {
+    return (double)(0.5L * ((long double)symbol_re[k] + (long double)symbol_re[(L - k) % L]) /
                     (long double)L);
+  };
+  std::vector<double2> S(L / 2);
+  for (int k = 0; k < L / 2; ++k) S[k] = make_double2(Ssym(2 * k), Ssym(2 * k + 1));
   std::vector<double2> pl;
   if (lam) {
     pl.resize(n);
@@ -246,7 +249,9 @@ static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cud
   a.v = p->ws + 2 * vn;
   a.ph = p->ws + 3 * vn;
   a.s = p->ws + 4 * vn;
-  if (!a.kwork) a.kwork = p->ws + 5 * vn;
+  a.sh = p->ws + 5 * vn;
+  a.t = p->ws + 6 * vn;
+  if (!a.kwork) a.kwork = p->ws + 7 * vn;
   a.tab = p->tables();
   if (a.max_iters <= 0) a.max_iters = 10 * p->n;
   return ForLog<SolveF>::run(p->log_L, B, method, pc, (const KrylovArgs&)a, st);
@@ -414,10 +419,10 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
 }
 
 int tsf_fft_debug(int N, int inverse, int B, const double* in, double* out, void* stream) {
-  if (!is_pow2(N) || N < 32 || N > 8192 || B < 1 || !in || !out)
+  if (!is_pow2(N) || N < 16 || N > 8192 || B < 1 || !in || !out)
     return fail(TSF_E_INVALID, "bad FFT debug arguments");
-  const int lg = ilog2_host(N);
-  static double2* dtw[kMaxLogL + 1] = {};
+  const int lg = ilog2_host(N) + 1;  // Dispatch<LOG> transforms N = 2^(LOG-1)
+  static double2* dtw[kMaxLogL + 2] = {};
   if (!dtw[lg]) {
     std::vector<double2> t = twiddles(N);
     CK(cudaMalloc(&dtw[lg], t.size() * sizeof(double2)));

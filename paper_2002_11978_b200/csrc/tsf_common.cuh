@@ -25,6 +25,29 @@ TSF_HD double2 mul_mi(double2 a) {
   return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
 
+// Read-only table load that the compiler may neither hoist across barriers
+// nor CSE between the many inlined transforms of a solve: plain __ldg table
+// reads are identical in every FFT of a Krylov iteration, so ptxas kept all
+// of them live across the whole loop and spilled.  The
+// re-read hits L1.
+TSF_D double2 ldt(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// 1/x for positive normal x without the IEEE division's slow-path call (a
+// call inside an unrolled transform forces every live register to the stack).
+// rcp.approx + two Newton steps + a final residual correction: within 1 ulp
+// of the correctly rounded reciprocal (measured against __drcp_rn in tests).
+TSF_D double rcp_pos(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return fma(r, fma(-x, r, 1.0), r);
+}
+
 // ---------------------------------------------------------------- status
 // Per-instance status codes; the host maps them to the reference's
 // exceptions / KrylovReport.breakdown strings (krylov.py:72-152,

@@ -195,7 +195,7 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
       const int sh = tw_log_scale + PL::LOGN - PL::log_ns(P) - PL::log_radix(P);
 #pragma unroll
       for (int m = 1; m < R; ++m) {
-        double2 w = __ldg(&tw[(k * m) << sh]);
+        double2 w = ldt(&tw[(k * m) << sh]);
         a[q][m] = INV ? cmulc(a[q][m], w) : cmul(a[q][m], w);
       }
     }

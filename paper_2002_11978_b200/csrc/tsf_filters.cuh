@@ -1,4 +1,5 @@
-// Real, even circulant filters applied to real data with full complex FFTs.
+// Real, even circulant filters applied to real data with complex FFTs of
+// length N = L/2 (one CTA, shared memory).
 //
 // Both operators on the hot path multiply by a real, even spectrum:
 //   * Toeplitz matvec  A x = first_n( Re IFFT_L( S . FFT_L(pad_L x) ) ),
@@ -6,25 +7,25 @@
 //     (toeplitz.py:34-63);
 //   * Strang solve     P^{-1} v = Re IFFT_n( FFT_n(v) / (d + kbar lam) )
 //     (toeplitz.py:101-136), lam real and even.
-// Exactly like the reference, each is ONE complex transform pair on the real
-// data (imaginary part zero) followed by taking the real part.  The cheaper
-// real-packed variant (two reals per complex point, half-length transforms)
-// was implemented first and measured: its rounding errors alias bin k with
-// bin k+L/2, and at the Krylov tolerance 1e-12 that biased BiCGSTAB by +0.5
-// iterations per level against the reference, so the hot
-// path keeps the full transforms.
 //
-// Ownership (tsf_fft.cuh): a CTA has T = L/16 owning threads; thread tid
-// owns the real entries j = tid + c*T, c < 8, of every vector (j < L/2 >= n),
-// which are exactly the nonzero inputs / needed outputs of the length-L
-// transform (slots c < 8 of E = 16) and all slots of the length-n Strang
-// transform (E = 8, pow2 n = L/2).
+// Matvec.  x is zero beyond n <= N = L/2, so one radix-2 DIF step splits the
+// length-L transform into two length-N ones (even / odd output bins):
+//   X_{2k}   = FFT_N(x)_k,            X_{2k+1} = FFT_N(x_j w_j)_k,  w_j = W_L^j
+//   y_j = (1/L) [ IFFT_N(S_{2k} X_{2k})_j + conj(w_j) IFFT_N(S_{2k+1} X_{2k+1})_j ],
+// and the real part is kept, as the reference does.  Each half is a full
+// complex transform of the data (imaginary part zero or the modulation) —
+// NOT the cheaper two-reals-per-complex packing: that variant was built and
+// measured first, and its rounding errors alias bin k onto bin k+N, which at
+// the Krylov tolerance 1e-12 biased BiCGSTAB by +0.5 iterations per level
+// against the reference.  The split keeps the shared-memory
+// footprint at N complex points (64 KB for n = 4096).
 //
-// The reference keeps the REAL part of the inverse, which makes its
-// effective filters the even parts of S and of 1/total; those are formed
-// explicitly (host side for S, per bin for 1/total): numpy's lam is even only
-// up to rounding of size eps*max(lam), which is large relative to total at
-// low frequencies where 1/total peaks.
+// Effective spectra are the EVEN parts of S and 1/total, which is what the
+// reference's Re(...) keeps: numpy's FFTs of even sequences are even only up
+// to rounding of size eps*max, large relative to 1/total at low frequency.
+//
+// Ownership (tsf_fft.cuh): T = N/E owning threads; thread tid owns the real
+// entries j = tid + c*T, c < E, of every vector (covering j < N, n <= N).
 #pragma once
 
 #include "tsf_fft.cuh"
@@ -32,9 +33,9 @@
 namespace tsf {
 
 struct FilterTables {
-  const double2* tw;    // W_L^e, e < L
-  const double* mvS;    // even part of the Toeplitz symbol / L, k < L
-  const double2* pclam; // (lam_k, lam_{n-k}), k < n   (pow2 n = L/2 only)
+  const double2* tw;    // W_L^e, e < L  (length-N transforms use stride 2)
+  const double2* mvS;   // (S_{2k}, S_{2k+1}) / L, even part of the symbol, k < N
+  const double2* pclam; // (lam_k, lam_{n-k}), k < n   (pow2 n = N only)
 };
 
 TSF_D double ld_real(const double* __restrict__ base, int n, int j) {
@@ -44,47 +45,63 @@ TSF_D void st_real(double* __restrict__ base, int n, int j, double v) {
   if (j < n) base[j] = v;
 }
 
-// y = A x for the owned entries io[c] (j = tid + c*T); L = 16*T.
-template <int L>
-TSF_D void toeplitz_filter(double (&io)[8], double2* sm, const FilterTables& t) {
-  constexpr int T = L / 16;
-  double2 z[16];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) z[c] = make_double2(io[c], 0.0);
-#pragma unroll
-  for (int c = 8; c < 16; ++c) z[c] = make_double2(0.0, 0.0);
-  block_fft<L, 16, false>(z, sm, t.tw, 0);
+// elements (complex slots) per owning thread: 8 keeps one transform at ~93
+// registers (16 would need ~166)
+constexpr int kE = 8;
+
+template <int N>
+struct FShape {
+  static constexpr int E = kE < N ? kE : N;
+  static constexpr int T = N / E;
+};
+
+// even output bins: z <- IFFT_N( S_even . FFT_N(z) ); caller keeps Re(z)
+template <int N>
+TSF_D void filt_even(double2 (&z)[kE], double2* sm, const FilterTables& t) {
+  constexpr int T = FShape<N>::T;
+  constexpr int E = FShape<N>::E;
+  block_fft<N, E, false>(z, sm, t.tw, 1);
   if (threadIdx.x < T) {
 #pragma unroll
-    for (int c = 0; c < 16; ++c) z[c] = cscale(z[c], __ldg(&t.mvS[threadIdx.x + c * T]));
+    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], ldt(&t.mvS[threadIdx.x + c * T]).x);
   }
-  block_fft<L, 16, true>(z, sm, t.tw, 0);
-#pragma unroll
-  for (int c = 0; c < 8; ++c) io[c] = z[c].x;
+  block_fft<N, E, true>(z, sm, t.tw, 1);
 }
 
-// z = P^{-1} v, P = d I + kbar s(A); n = L/2 (power of two).
-template <int L>
-TSF_D void strang_filter(double (&io)[8], double2* sm, const FilterTables& t, double d,
-                         double kbar) {
-  constexpr int N = L / 2;
-  constexpr int T = N / 8;
-  constexpr double inv_n = 1.0 / N;
-  double2 z[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) z[c] = make_double2(io[c], 0.0);
-  block_fft<N, 8, false>(z, sm, t.tw, 1);
+// odd output bins: z (already modulated by w_j) <- IFFT_N( S_odd . FFT_N(z) );
+// caller keeps Re(conj(w_j) z_j)
+template <int N>
+TSF_D void filt_odd(double2 (&z)[kE], double2* sm, const FilterTables& t) {
+  constexpr int T = FShape<N>::T;
+  constexpr int E = FShape<N>::E;
+  block_fft<N, E, false>(z, sm, t.tw, 1);
   if (threadIdx.x < T) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const double2 lam = __ldg(&t.pclam[threadIdx.x + c * T]);
-      const double s = 0.5 * (1.0 / (d + kbar * lam.x) + 1.0 / (d + kbar * lam.y));
+    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], ldt(&t.mvS[threadIdx.x + c * T]).y);
+  }
+  block_fft<N, E, true>(z, sm, t.tw, 1);
+}
+
+// Strang: z <- IFFT_n( FFT_n(z) . Ssym / n ), n = N; caller keeps Re(z)
+template <int N>
+TSF_D void filt_strang(double2 (&z)[kE], double2* sm, const FilterTables& t, double d,
+                       double kbar) {
+  constexpr int T = FShape<N>::T;
+  constexpr int E = FShape<N>::E;
+  constexpr double inv_n = 1.0 / N;
+  block_fft<N, E, false>(z, sm, t.tw, 1);
+  if (threadIdx.x < T) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const double2 lam = ldt(&t.pclam[threadIdx.x + c * T]);
+      const double s = 0.5 * (rcp_pos(d + kbar * lam.x) + rcp_pos(d + kbar * lam.y));
       z[c] = cscale(z[c], s * inv_n);
     }
   }
-  block_fft<N, 8, true>(z, sm, t.tw, 1);
-#pragma unroll
-  for (int c = 0; c < 8; ++c) io[c] = z[c].x;
+  block_fft<N, E, true>(z, sm, t.tw, 1);
 }
+
+// w_j = W_L^j for the owned slots
+TSF_D double2 modulation(const FilterTables& t, int j) { return ldt(&t.tw[j]); }
 
 }  // namespace tsf

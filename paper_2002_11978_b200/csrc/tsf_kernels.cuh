@@ -1,4 +1,4 @@
-// Batched per-instance kernels (one CTA per problem instance, n <= 4096).
+// Batched per-instance kernels (one CTA per problem instance, n <= N <= 8192).
 //
 //  k_toeplitz_apply : y = shift*x + kappa .* (A x)   (toeplitz.py:51-63 + scheme.py:129-130)
 //  k_strang_apply   : z = P^{-1} v                    (toeplitz.py:131-136)
@@ -9,7 +9,12 @@
 //                     with exactly the reference's control flow, all scalars
 //                     and convergence tests on the device, one CTA per
 //                     instance, no host round trip per iteration.
-// Template parameter L is the circulant embedding length (pow2 >= 2n-1).
+// Template parameter N = L/2 is the transform length (pow2 >= n).
+//
+// Register discipline: during a transform only its 16 complex slots are
+// live; Krylov vectors live in the instance's L2-resident workspace between
+// transforms (re-read where needed), so the kernel runs spill-free at two
+// CTAs per SM for n = 4096.
 #pragma once
 
 #include "tsf_filters.cuh"
@@ -41,185 +46,235 @@ struct KrylovArgs {
   double* v;
   double* ph;
   double* s;
+  double* sh;
+  double* t;
   int* iters;               // per-instance outputs
   double* relres;
   int* status;
   FilterTables tab;
 };
 
-template <int L>
+template <int N>
 struct KShape {
-  static constexpr int T = L / 16;               // owning threads
+  static constexpr int E = FShape<N>::E;
+  static constexpr int T = FShape<N>::T;         // owning threads
   static constexpr int BLOCK = T < 32 ? 32 : T;  // launched threads
-  static constexpr int SMEM = FftPlan<L, 16>::SMEM_ELEMS * 16;
+  static constexpr int FFT_BYTES = FftPlan<N, E>::SMEM_ELEMS * 16;
+  static constexpr int SMEM = FFT_BYTES + N * 8;  // + one real staging vector
+  static constexpr int MIN_BLOCKS = BLOCK >= 512 ? 1 : 512 / BLOCK;  // <= 128 regs
 };
 
-// --------------------------------------------------------------- matvec
-template <int L>
-__global__ void __launch_bounds__(KShape<L>::BLOCK)
-k_toeplitz_apply(int n, const double* __restrict__ x, double* __restrict__ y,
-                 const double* __restrict__ kappa, double shift, int has_kappa,
-                 FilterTables tab) {
-  extern __shared__ double2 sm[];
-  constexpr int T = KShape<L>::T;
+// y = shift*x + kappa .* (A x) on the owned slots (kappa == nullptr: y = A x).
+// x is read from global (twice); result returned in y[].
+template <int N>
+TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restrict__ kg,
+                          double shift, int n, double (&y)[kE], double2* sm, double* aux,
+                          const FilterTables& t) {
+  constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
-  const long off = (long)blockIdx.x * n;
-  double xv[8], io[8];
-  if (tid < T) {
+  const bool own = tid < T;
+  double2 z[kE];
+  if (own) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) io[c] = xv[c] = ld_real(x + off, n, tid + c * T);
+    for (int c = 0; c < KShape<N>::E; ++c) z[c] = make_double2(ld_real(xg, n, tid + c * T), 0.0);
   }
-  toeplitz_filter<L>(io, sm, tab);
-  if (tid < T) {
+  filt_even<N>(z, sm, t);
+  if (own) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < KShape<N>::E; ++c) aux[tid + c * T] = z[c].x;
+#pragma unroll
+    for (int c = 0; c < KShape<N>::E; ++c) {
       const int j = tid + c * T;
-      double out = io[c];
-      if (has_kappa) out = fma(shift, xv[c], ld_real(kappa + off, n, j) * out);
-      st_real(y + off, n, j, out);
+      z[c] = cscale(modulation(t, j), ld_real(xg, n, j));
+    }
+  }
+  filt_odd<N>(z, sm, t);
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < KShape<N>::E; ++c) {
+      const int j = tid + c * T;
+      const double2 w = modulation(t, j);
+      const double ax = aux[j] + fma(z[c].x, w.x, z[c].y * w.y);  // + Re(conj(w) z)
+      y[c] = kg ? fma(shift, ld_real(xg, n, j), ld_real(kg, n, j) * ax) : ax;
     }
   }
 }
 
+// --------------------------------------------------------------- matvec
+template <int N>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
+k_toeplitz_apply(int n, const double* __restrict__ x, double* __restrict__ y,
+                 const double* __restrict__ kappa, double shift, FilterTables tab) {
+  extern __shared__ double2 sm[];
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
+  constexpr int T = KShape<N>::T;
+  const int tid = threadIdx.x;
+  const long off = (long)blockIdx.x * n;
+  double out[kE];
+  apply_level_op<N>(x + off, kappa ? kappa + off : nullptr, shift, n, out, sm, aux, tab);
+  if (tid < T) {
+#pragma unroll
+    for (int c = 0; c < KShape<N>::E; ++c) st_real(y + off, n, tid + c * T, out[c]);
+  }
+}
+
 // --------------------------------------------------------------- precond
-template <int L>
-__global__ void __launch_bounds__(KShape<L>::BLOCK)
-k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ z, double shift,
+template <int N>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
+k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ zo, double shift,
                double kbar, const double* __restrict__ kbar_dev, FilterTables tab) {
   extern __shared__ double2 sm[];
-  constexpr int T = KShape<L>::T;
+  constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   const long off = (long)blockIdx.x * n;
   const double kb = kbar_dev ? kbar_dev[blockIdx.x] : kbar;
-  double io[8];
+  double2 z[kE];
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) io[c] = ld_real(v + off, n, tid + c * T);
+    for (int c = 0; c < KShape<N>::E; ++c) z[c] = make_double2(ld_real(v + off, n, tid + c * T), 0.0);
   }
-  strang_filter<L>(io, sm, tab, shift, kb);
+  filt_strang<N>(z, sm, tab, shift, kb);
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) st_real(z + off, n, tid + c * T, io[c]);
+    for (int c = 0; c < KShape<N>::E; ++c) st_real(zo + off, n, tid + c * T, z[c].x);
   }
 }
 
 // --------------------------------------------------------------- solver
-// PC: 0 = no preconditioner ("krylov"), 1 = Strang ("pkrylov", pow2 n = L/2)
+// Transform phases of the solve are out-of-line device functions with a
+// pointer/scalar interface: vectors live in the instance's L2-resident
+// workspace between phases, so a call boundary carries no vector state and
+// each phase gets the whole register budget (inlining ~10 transforms into
+// one loop body made ptxas interleave them and spill KBs per thread).
+
+// dst = P^{-1} src on the owned slots
+template <int N>
+__device__ __noinline__ void dev_precond(const double* __restrict__ src, double* __restrict__ dst,
+                                         int n, double d, double kbar, double2* sm,
+                                         FilterTables t) {
+  constexpr int T = KShape<N>::T;
+  constexpr int E = KShape<N>::E;
+  const int tid = threadIdx.x;
+  double2 z[kE];
+  if (tid < T) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) z[c] = make_double2(ld_real(src, n, tid + c * T), 0.0);
+  }
+  filt_strang<N>(z, sm, t, d, kbar);
+  if (tid < T) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) st_real(dst, n, tid + c * T, z[c].x);
+  }
+}
+
+// dst = shift*src + kappa .* (A src); returns this thread's partial
+// (sum dst*dst, sum dst*w) (w == nullptr: second entry 0)
+template <int N>
+__device__ __noinline__ double2 dev_apply(const double* __restrict__ src, double* __restrict__ dst,
+                                          const double* __restrict__ kg, double d, int n,
+                                          double2* sm, double* aux, FilterTables t,
+                                          const double* __restrict__ w) {
+  constexpr int T = KShape<N>::T;
+  constexpr int E = KShape<N>::E;
+  const int tid = threadIdx.x;
+  double y[kE];
+  apply_level_op<N>(src, kg, d, n, y, sm, aux, t);
+  double2 part = make_double2(0.0, 0.0);
+  if (tid < T) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      st_real(dst, n, j, y[c]);
+      if (j < n) {
+        part.x = fma(y[c], y[c], part.x);
+        if (w) part.y = fma(y[c], w[j], part.y);
+      }
+    }
+  }
+  return part;
+}
+
+// PC: 0 = no preconditioner ("krylov"), 1 = Strang ("pkrylov", pow2 n = N)
 // CG: false = BiCGSTAB, true = PCG (kappa_x_independent)
-template <int L, int PC, bool CG>
-__global__ void __launch_bounds__(KShape<L>::BLOCK)
+template <int N, int PC, bool CG>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
 k_krylov_solve(KrylovArgs a) {
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
-  constexpr int T = KShape<L>::T;
+  constexpr int T = KShape<N>::T;
+  constexpr int E = KShape<N>::E;
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int b = blockIdx.x;
   const int n = a.n;
   const long off = (long)b * n;
-  const double* r0g = a.rhs + off;
-  double* xg = a.x + off;
-  double* rg = a.r + off;
-  double* pg = a.p + off;
-  double* vg = a.v + off;
-  double* phg = a.ph + off;
-  double* sg = a.s + off;
   const double d = a.shift;
 
   // ---- kappa on the grid (scheme.py:156-160,280) and kappa_bar (scheme.py:135)
-  const double* kg;
-  double ksum = 0.0, kmin = 1e308;
-  if (a.kappa) {
-    kg = a.kappa + off;
+  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
+  double kbar;
+  {
+    double ksum = 0.0, kmin = 1e308;
     if (own) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < E; ++c) {
         const int j = tid + c * T;
         if (j < n) {
-          const double k = kg[j];
+          double k;
+          if (a.kappa) {
+            k = a.kappa[off + j];
+          } else {
+            k = 0.0;
+            for (int q = 0; q < a.nk; ++q) {
+              const double mq = a.kmodes[q * a.kq_stride + (long)b * a.kb_stride + j];
+              // no contraction: reproduce numpy's  acc + mode*coef  rounding
+              k = __dadd_rn(k, __dmul_rn(mq, a.kcoef[q]));
+            }
+            a.kwork[off + j] = k;
+          }
           ksum += k;
           kmin = fmin(kmin, k);
         }
       }
     }
-  } else {
-    double* kw = a.kwork + off;
-    kg = kw;
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int j = tid + c * T;
-        if (j < n) {
-          double acc = 0.0;
-          for (int q = 0; q < a.nk; ++q) {
-            const double mq = a.kmodes[q * a.kq_stride + (long)b * a.kb_stride + j];
-            // no contraction: reproduce numpy's  acc + mode*coef  rounding
-            acc = __dadd_rn(acc, __dmul_rn(mq, a.kcoef[q]));
-          }
-          kw[j] = acc;
-          ksum += acc;
-          kmin = fmin(kmin, acc);
-        }
-      }
-    }
-  }
-  kmin = block_min1(kmin, red);
-  if (kmin <= 0.0) {
-    if (tid == 0) {
-      a.status[b] = TSF_KAPPA_NONPOS;
-      a.iters[b] = 0;
-      a.relres[b] = 0.0;
-    }
-    return;
-  }
-  const double kmean = block_sum1(ksum, red) / n;
-  const double kbar = a.kbar > 0.0 ? a.kbar : kmean;
-  if constexpr (PC == 1) {
-    // total eigenvalues d + kbar*lam > 0  (toeplitz.py:122-124)
-    double tmin = 1e308;
-    for (int k = tid; k < n; k += blockDim.x) tmin = fmin(tmin, d + kbar * __ldg(&a.tab.pclam[k]).x);
-    tmin = block_min1(tmin, red);
-    if (tmin <= 0.0) {
+    kmin = block_min1(kmin, red);
+    if (kmin <= 0.0) {
       if (tid == 0) {
-        a.status[b] = TSF_PRECOND_NONPOS;
+        a.status[b] = TSF_KAPPA_NONPOS;
         a.iters[b] = 0;
         a.relres[b] = 0.0;
       }
       return;
     }
+    const double kmean = block_sum1(ksum, red) / n;
+    kbar = a.kbar > 0.0 ? a.kbar : kmean;
+    if constexpr (PC == 1) {
+      // total eigenvalues d + kbar*lam > 0  (toeplitz.py:122-124)
+      double tmin = 1e308;
+      for (int k = tid; k < n; k += blockDim.x) tmin = fmin(tmin, d + kbar * ldt(&a.tab.pclam[k]).x);
+      tmin = block_min1(tmin, red);
+      if (tmin <= 0.0) {
+        if (tid == 0) {
+          a.status[b] = TSF_PRECOND_NONPOS;
+          a.iters[b] = 0;
+          a.relres[b] = 0.0;
+        }
+        return;
+      }
+    }
   }
 
-  auto precond = [&](double (&io)[8]) {
-    if constexpr (PC == 1) strang_filter<L>(io, sm, a.tab, d, kbar);
-  };
-  // y = d*u + kappa .* (A u); u preserved
-  auto apply_op = [&](const double (&u)[8], double (&y)[8]) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c) y[c] = u[c];
-    toeplitz_filter<L>(y, sm, a.tab);
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) y[c] = fma(d, u[c], ld_real(kg, n, tid + c * T) * y[c]);
-    }
-  };
-  auto dot_loc = [](const double (&u)[8], const double (&w)[8]) {
-    double acc = 0.0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc = fma(u[c], w[c], acc);
-    return acc;
-  };
-  auto load = [&](double (&u)[8], const double* g) {
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) u[c] = ld_real(g, n, tid + c * T);
-    }
-  };
-  auto store = [&](double* g, const double (&u)[8]) {
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) st_real(g, n, tid + c * T, u[c]);
-    }
-  };
+  const double* r0g = a.rhs + off;
+  double* xg = a.x + off;
+  double* rg = a.r + off;
+  double* pg = a.p + off;
+  double* vg = a.v + off;
+  double* sg = a.s + off;
+  double* tg = a.t + off;
+  // without a preconditioner p_hat == p and s_hat == s
+  double* phg = PC ? a.ph + off : pg;
+  double* shg = PC ? a.sh + off : sg;
   auto finish = [&](int it, double rel, int st) {
     if (tid == 0) {
       a.iters[b] = it;
@@ -228,124 +283,112 @@ k_krylov_solve(KrylovArgs a) {
     }
   };
 
-  double u[8], w[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) u[c] = w[c] = 0.0;
-
   // ---- r = r0 = rhs, x = 0  (krylov.py:107-113 / 64-69)
-  load(u, r0g);
-  const double ss0 = block_sum1(own ? dot_loc(u, u) : 0.0, red);
-  const double nrm0 = sqrt(ss0);
-  {
-    double zero[8];
+  double ss0 = 0.0;
+  if (own) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) zero[c] = 0.0;
-    store(xg, zero);
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      const double r0 = ld_real(r0g, n, j);
+      ss0 = fma(r0, r0, ss0);
+      st_real(xg, n, j, 0.0);
+    }
   }
+  ss0 = block_sum1(ss0, red);
+  const double nrm0 = sqrt(ss0);
   if (nrm0 == 0.0) {
     finish(0, 0.0, TSF_OK);
     return;
   }
-  const int max_iters = a.max_iters;
-  const double tol = a.tol;
 
   if constexpr (!CG) {
     // ================= BiCGSTAB (krylov.py:88-153) =================
     double rho = 1.0, alpha = 1.0, omega = 1.0;
-    double rho_new = ss0;           // r0 . r with r = r0
-    double rnorm = nrm0;            // ||r|| for breakdown reports
-    for (int it = 1; it <= max_iters; ++it) {
+    double rho_new = ss0;   // r0 . r with r = r0 (same reduction)
+    double rnorm = nrm0;
+    for (int it = 1; it <= a.max_iters; ++it) {
       if (rho_new == 0.0) {
         finish(it, rnorm / nrm0, TSF_BD_RHO);
         return;
       }
       // p = r  |  p = r + beta (p - omega v)
-      if (it == 1) {
-        load(u, r0g);
-      } else {
+      if (own) {
         const double beta = (rho_new / rho) * (alpha / omega);
-        if (own) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int j = tid + c * T;
-            u[c] = ld_real(rg, n, j) + beta * (ld_real(pg, n, j) - omega * ld_real(vg, n, j));
-          }
+        for (int c = 0; c < E; ++c) {
+          const int j = tid + c * T;
+          const double p = (it == 1) ? ld_real(r0g, n, j)
+                                     : ld_real(rg, n, j) +
+                                           beta * (ld_real(pg, n, j) - omega * ld_real(vg, n, j));
+          st_real(pg, n, j, p);
         }
       }
-      store(pg, u);
-      precond(u);         // u = p_hat
-      store(phg, u);
-      apply_op(u, w);     // w = v = M p_hat
-      store(vg, w);
-      double r0v[8];
-      load(r0v, r0g);
-      const double denom = block_sum1(own ? dot_loc(r0v, w) : 0.0, red);
+      if constexpr (PC == 1) dev_precond<N>(pg, phg, n, d, kbar, sm, a.tab);
+      const double2 pv = dev_apply<N>(phg, vg, kg, d, n, sm, aux, a.tab, r0g);
+      const double denom = block_sum1(pv.y, red);
       if (denom == 0.0) {
         finish(it, rnorm / nrm0, TSF_BD_R0V);
         return;
       }
       alpha = rho_new / denom;
       // s = r - alpha v
+      double part = 0.0;
       if (own) {
+        const double* rc = (it == 1) ? r0g : rg;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const double rr = (it == 1) ? r0v[c] : ld_real(rg, n, tid + c * T);
-          w[c] = rr - alpha * w[c];
+        for (int c = 0; c < E; ++c) {
+          const int j = tid + c * T;
+          const double sv = ld_real(rc, n, j) - alpha * ld_real(vg, n, j);
+          st_real(sg, n, j, sv);
+          if (j < n) part = fma(sv, sv, part);
         }
       }
-      const double snorm = sqrt(block_sum1(own ? dot_loc(w, w) : 0.0, red));
-      if (snorm / nrm0 < tol) {
+      const double snorm = sqrt(block_sum1(part, red));
+      if (snorm / nrm0 < a.tol) {
         // x += alpha p_hat (early exit counts as a full iteration, krylov.py:135-137)
         if (own) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < E; ++c) {
             const int j = tid + c * T;
-            st_real(xg, n, j, ld_real(xg, n, j) + alpha * u[c]);
+            st_real(xg, n, j, ld_real(xg, n, j) + alpha * ld_real(phg, n, j));
           }
         }
         finish(it, snorm / nrm0, TSF_OK);
         return;
       }
-      store(sg, w);
-      precond(w);         // w = s_hat
-      apply_op(w, u);     // u = t = M s_hat
+      if constexpr (PC == 1) dev_precond<N>(sg, shg, n, d, kbar, sm, a.tab);
+      const double2 tp = dev_apply<N>(shg, tg, kg, d, n, sm, aux, a.tab, sg);
       Vals<2> red2;
-      red2.v[0] = 0.0;
-      red2.v[1] = 0.0;
-      if (own) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const double ss = ld_real(sg, n, tid + c * T);
-          red2.v[0] = fma(u[c], u[c], red2.v[0]);
-          red2.v[1] = fma(u[c], ss, red2.v[1]);
-        }
-      }
+      red2.v[0] = tp.x;
+      red2.v[1] = tp.y;
       red2 = block_sum<2>(red2, red);
-      const double tt = red2.v[0], ts = red2.v[1];
-      if (tt == 0.0) {
+      if (red2.v[0] == 0.0) {
         finish(it, snorm / nrm0, TSF_BD_OMEGA_DEN);
         return;
       }
-      omega = ts / tt;
+      omega = red2.v[1] / red2.v[0];
       // x += alpha p_hat + omega s_hat ; r = s - omega t
       red2.v[0] = 0.0;
       red2.v[1] = 0.0;
       if (own) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < E; ++c) {
           const int j = tid + c * T;
-          st_real(xg, n, j, ld_real(xg, n, j) + (alpha * ld_real(phg, n, j) + omega * w[c]));
-          const double rn = ld_real(sg, n, j) - omega * u[c];
+          st_real(xg, n, j,
+                  ld_real(xg, n, j) + (alpha * ld_real(phg, n, j) + omega * ld_real(shg, n, j)));
+          const double rn = ld_real(sg, n, j) - omega * ld_real(tg, n, j);
           st_real(rg, n, j, rn);
-          red2.v[0] = fma(rn, rn, red2.v[0]);
-          red2.v[1] = fma(ld_real(r0g, n, j), rn, red2.v[1]);
+          if (j < n) {
+            red2.v[0] = fma(rn, rn, red2.v[0]);
+            red2.v[1] = fma(r0g[j], rn, red2.v[1]);
+          }
         }
       }
       rho = rho_new;
       red2 = block_sum<2>(red2, red);
       rnorm = sqrt(red2.v[0]);
       const double rel = rnorm / nrm0;
-      if (rel < tol) {
+      if (rel < a.tol) {
         finish(it, rel, TSF_OK);
         return;
       }
@@ -355,56 +398,76 @@ k_krylov_solve(KrylovArgs a) {
       }
       rho_new = red2.v[1];
     }
-    finish(max_iters, rnorm / nrm0, TSF_NOT_CONVERGED);
+    finish(a.max_iters, rnorm / nrm0, TSF_NOT_CONVERGED);
   } else {
     // ================= PCG (krylov.py:43-85) =================
-    store(rg, u);                    // r = b
-    precond(u);                      // u = z
-    store(pg, u);                    // p = z
-    double rr[8];
-    load(rr, r0g);
-    double rz = block_sum1(own ? dot_loc(rr, u) : 0.0, red);
+    // r = b; z = P^{-1} r; p = z  (z kept in s, p written directly)
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) {
+        const int j = tid + c * T;
+        st_real(rg, n, j, ld_real(r0g, n, j));
+        if (!PC) st_real(pg, n, j, ld_real(r0g, n, j));
+      }
+    }
+    if constexpr (PC == 1) dev_precond<N>(rg, pg, n, d, kbar, sm, a.tab);
+    double part = 0.0;
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) {
+        const int j = tid + c * T;
+        if (j < n) part = fma(r0g[j], pg[j], part);
+      }
+    }
+    double rz = block_sum1(part, red);
     double rnorm = nrm0;
-    for (int it = 1; it <= max_iters; ++it) {
-      load(u, pg);
-      apply_op(u, w);                // w = q = M p
-      const double curv = block_sum1(own ? dot_loc(u, w) : 0.0, red);
+    for (int it = 1; it <= a.max_iters; ++it) {
+      const double2 qp = dev_apply<N>(pg, vg, kg, d, n, sm, aux, a.tab, pg);  // q = M p
+      const double curv = block_sum1(qp.y, red);
       if (curv <= 0.0) {
         finish(it, rnorm / nrm0, TSF_BD_CURVATURE);
         return;
       }
       const double al = rz / curv;
-      double rr_loc = 0.0;
+      part = 0.0;
       if (own) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < E; ++c) {
           const int j = tid + c * T;
-          st_real(xg, n, j, ld_real(xg, n, j) + al * u[c]);
-          const double r1 = ld_real(rg, n, j) - al * w[c];
+          st_real(xg, n, j, ld_real(xg, n, j) + al * ld_real(pg, n, j));
+          const double r1 = ld_real(rg, n, j) - al * ld_real(vg, n, j);
           st_real(rg, n, j, r1);
-          rr[c] = r1;
-          rr_loc = fma(r1, r1, rr_loc);
+          if (j < n) part = fma(r1, r1, part);
         }
       }
-      rnorm = sqrt(block_sum1(rr_loc, red));
+      rnorm = sqrt(block_sum1(part, red));
       const double rel = rnorm / nrm0;
-      if (rel < tol) {
+      if (rel < a.tol) {
         finish(it, rel, TSF_OK);
         return;
       }
+      double* zg = PC ? sg : rg;
+      if constexpr (PC == 1) dev_precond<N>(rg, sg, n, d, kbar, sm, a.tab);
+      part = 0.0;
+      if (own) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) w[c] = rr[c];
-      precond(w);                    // w = z
-      const double rz_new = block_sum1(own ? dot_loc(rr, w) : 0.0, red);
+        for (int c = 0; c < E; ++c) {
+          const int j = tid + c * T;
+          if (j < n) part = fma(rg[j], zg[j], part);
+        }
+      }
+      const double rz_new = block_sum1(part, red);
       const double beta = rz_new / rz;
       if (own) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) u[c] = w[c] + beta * u[c];
+        for (int c = 0; c < E; ++c) {
+          const int j = tid + c * T;
+          st_real(pg, n, j, ld_real(zg, n, j) + beta * ld_real(pg, n, j));
+        }
       }
-      store(pg, u);
       rz = rz_new;
     }
-    finish(max_iters, rnorm / nrm0, TSF_NOT_CONVERGED);
+    finish(a.max_iters, rnorm / nrm0, TSF_NOT_CONVERGED);
   }
 }
 
