@@ -62,8 +62,10 @@ struct tsf_plan {
   // Krylov workspaces [cap][n] x 6
   int cap = 0;
   double* ws = nullptr;
-  int* ist = nullptr;
+  int* ist = nullptr;       // [0] = active-instance counter
   double* dst = nullptr;
+  KState* kst = nullptr;    // per-instance Krylov scalars
+  int* h_active = nullptr;  // pinned host mirror of the counter
   FilterTables tables() const { return FilterTables{tw, mvS, pclam}; }
 };
 
@@ -118,14 +120,18 @@ int ensure_reserved(tsf_plan* p, int B) {
   if (p->ws) cudaFree(p->ws);
   if (p->ist) cudaFree(p->ist);
   if (p->dst) cudaFree(p->dst);
+  if (p->kst) cudaFree(p->kst);
   p->ws = nullptr;
   p->ist = nullptr;
   p->dst = nullptr;
+  p->kst = nullptr;
   p->cap = 0;
   CK(cudaSetDevice(p->device));
   CK(cudaMalloc(&p->ws, sizeof(double) * (size_t)B * p->n * 8));
   CK(cudaMalloc(&p->ist, sizeof(int) * (size_t)B * 2));
   CK(cudaMalloc(&p->dst, sizeof(double) * (size_t)B));
+  CK(cudaMalloc(&p->kst, sizeof(KState) * (size_t)B));
+  if (!p->h_active) CK(cudaHostAlloc(&p->h_active, sizeof(int), cudaHostAllocDefault));
   p->cap = B;
   return TSF_SUCCESS;
 }
@@ -149,7 +155,7 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
   if (!symbol_re) return fail(TSF_E_INVALID, "symbol is NULL");
   const int lg = ilog2_host(L);
   if (lg < kMinLogL || lg > kMaxLogL)
-    return fail(TSF_E_UNSUPPORTED, "embedding L=%d outside the single-CTA engine (32..16384, n <= 8192)", L);
+    return fail(TSF_E_UNSUPPORTED, "embedding L=%d outside the single-CTA engine (32..8192, n <= 4096)", L);
   if (lam && !(is_pow2(n) && n >= 16 && L == 2 * n))
     return fail(TSF_E_UNSUPPORTED, "Strang preconditioner needs pow2 n >= 16 with L = 2n (n=%d, L=%d)", n, L);
   tsf_plan* p = new tsf_plan();
@@ -201,6 +207,8 @@ int tsf_plan_destroy(tsf_plan* p) {
   cudaFree(p->ws);
   cudaFree(p->ist);
   cudaFree(p->dst);
+  cudaFree(p->kst);
+  if (p->h_active) cudaFreeHost(p->h_active);
   delete p;
   return TSF_SUCCESS;
 }
@@ -251,6 +259,9 @@ static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cud
   a.s = p->ws + 4 * vn;
   a.sh = p->ws + 5 * vn;
   a.t = p->ws + 6 * vn;
+  a.kst = p->kst;
+  a.active = p->ist;
+  a.h_active = p->h_active;
   if (!a.kwork) a.kwork = p->ws + 7 * vn;
   a.tab = p->tables();
   if (a.max_iters <= 0) a.max_iters = 10 * p->n;
@@ -419,7 +430,7 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
 }
 
 int tsf_fft_debug(int N, int inverse, int B, const double* in, double* out, void* stream) {
-  if (!is_pow2(N) || N < 16 || N > 8192 || B < 1 || !in || !out)
+  if (!is_pow2(N) || N < 16 || N > 4096 || B < 1 || !in || !out)
     return fail(TSF_E_INVALID, "bad FFT debug arguments");
   const int lg = ilog2_host(N) + 1;  // Dispatch<LOG> transforms N = 2^(LOG-1)
   static double2* dtw[kMaxLogL + 2] = {};

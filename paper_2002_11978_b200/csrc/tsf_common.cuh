@@ -36,6 +36,16 @@ TSF_D double2 ldt(const double2* p) {
   return v;
 }
 
+// threadIdx.x that the compiler cannot CSE: each transform pass recomputes
+// its handful of shared-memory addresses instead of ptxas hoisting the
+// addresses of every pass of every transform to kernel entry (where they
+// were spilled).
+TSF_D int tid_x() {
+  int t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
+}
+
 // 1/x for positive normal x without the IEEE division's slow-path call (a
 // call inside an unrolled transform forces every live register to the stack).
 // rcp.approx + two Newton steps + a final residual correction: within 1 ulp

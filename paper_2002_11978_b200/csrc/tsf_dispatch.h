@@ -8,7 +8,7 @@
 namespace tsf {
 
 constexpr int kMinLogL = 5;   // L = 32
-constexpr int kMaxLogL = 14;  // L = 16384 (n <= 8192 single-CTA engine)
+constexpr int kMaxLogL = 13;  // L = 8192 (n <= 4096 single-CTA engine)
 
 // sets tsf_last_error() and returns TSF_E_CUDA (defined in tsf_abi.cu)
 int report_cuda(cudaError_t e, const char* what);
@@ -34,6 +34,5 @@ TSF_EXTERN_DISPATCH(10)
 TSF_EXTERN_DISPATCH(11)
 TSF_EXTERN_DISPATCH(12)
 TSF_EXTERN_DISPATCH(13)
-TSF_EXTERN_DISPATCH(14)
 
 }  // namespace tsf

@@ -41,14 +41,47 @@ int Dispatch<LOG>::precond(int n, const FilterTables& t, int B, const double* v,
   return launch_error(cudaGetLastError());
 }
 
+// Host driver of one level solve for B instances: begin kernel, then the
+// iteration kernels in chunks of kChunk iterations; after each chunk the
+// device count of unfinished instances is read back (one small D2H copy and
+// a stream sync per chunk).  Finished instances' CTAs return immediately, so
+// the overshoot costs at most kChunk-1 near-empty launch pairs.
 template <int N, int PC, bool CG>
 int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
   using S = KShape<N>;
-  auto k = k_krylov_solve<N, PC, CG>;
-  cudaError_t e = prep_kernel(k, S::SMEM);
-  if (e != cudaSuccess) return launch_error(e);
-  k<<<B, S::BLOCK, S::SMEM, st>>>(a);
-  return launch_error(cudaGetLastError());
+  constexpr int kChunk = 4;
+  cudaError_t e;
+  auto kb = k_solve_begin<N, PC, CG>;
+  if ((e = prep_kernel(kb, S::FFT_BYTES)) != cudaSuccess) return launch_error(e);
+  auto kv = k_bicg_v<N, PC>;
+  auto kt = k_bicg_t<N, PC>;
+  auto kc = k_cg_iter<N, PC>;
+  if (!CG) {
+    if ((e = prep_kernel(kv, S::SMEM)) != cudaSuccess) return launch_error(e);
+    if ((e = prep_kernel(kt, S::SMEM)) != cudaSuccess) return launch_error(e);
+  } else if ((e = prep_kernel(kc, S::SMEM)) != cudaSuccess) {
+    return launch_error(e);
+  }
+  k_set_int<<<1, 1, 0, st>>>(a.active, B);
+  kb<<<B, S::BLOCK, S::FFT_BYTES, st>>>(a, a.kst, a.active);
+  if ((e = cudaGetLastError()) != cudaSuccess) return launch_error(e);
+  for (int it = 0; it < a.max_iters; it += kChunk) {
+    for (int k = 0; k < kChunk && it + k < a.max_iters; ++k) {
+      if (!CG) {
+        kv<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
+        kt<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
+      } else {
+        kc<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
+      }
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return launch_error(e);
+    if ((e = cudaMemcpyAsync(a.h_active, a.active, sizeof(int), cudaMemcpyDeviceToHost, st)) !=
+        cudaSuccess)
+      return launch_error(e);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return launch_error(e);
+    if (*a.h_active <= 0) break;
+  }
+  return 0;
 }
 
 template <int LOG>
@@ -63,14 +96,15 @@ int Dispatch<LOG>::fft(int inverse, int B, const double2* in, double2* out, cons
                        cudaStream_t st) {
   constexpr int N = 1 << (LOG - 1);
   using S = KShape<N>;
-  constexpr int smem = FftPlan<N, 16>::SMEM_ELEMS * 16;
+  constexpr int E = FShape<N>::E;
+  constexpr int smem = 2 * FftPlan<N, E>::SMEM_ELEMS * 16;
   cudaError_t e;
   if (inverse) {
-    auto k = k_fft_debug<N, 16, true>;
+    auto k = k_fft_debug<N, E, true>;
     if ((e = prep_kernel(k, smem)) != cudaSuccess) return launch_error(e);
     k<<<B, S::BLOCK, smem, st>>>(in, out, tw, 0);
   } else {
-    auto k = k_fft_debug<N, 16, false>;
+    auto k = k_fft_debug<N, E, false>;
     if ((e = prep_kernel(k, smem)) != cudaSuccess) return launch_error(e);
     k<<<B, S::BLOCK, smem, st>>>(in, out, tw, 0);
   }

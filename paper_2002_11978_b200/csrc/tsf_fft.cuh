@@ -151,7 +151,7 @@ struct FftPlan {
   static constexpr int NPASS = (LOGN + LOGR - 1) / LOGR;
   static constexpr int T = N / E;
   static constexpr int PADSHIFT = imin(LOGR, LOGN);  // log2 of the first radix
-  static constexpr int SMEM_ELEMS = N + (N >> PADSHIFT) + 1;
+  static constexpr int SMEM_ELEMS = N + (N >> PADSHIFT) + 1;  // one of the two buffers
   static constexpr int log_radix(int p) {
     return (p < NPASS - 1) ? LOGR : (LOGN - LOGR * (NPASS - 1));
   }
@@ -162,8 +162,10 @@ struct FftPlan {
 // One Stockham pass: radix R, NS = product of the previous radices.
 //  FROM_REGS: inputs come from v[] (first pass), else from shared memory.
 //  TO_REGS:   outputs go to v[] (last pass), else to shared memory.
-// Every thread of the CTA must call (the in-place pass has a barrier);
-// only owning threads (own == true) touch data.
+// Out of place: pass P reads buffer (P+1)&1 and writes buffer P&1 (two
+// transform buffers), so loaded values never have to survive a barrier —
+// with an in-place pass they did, and inside the Krylov loop ptxas spilled
+// them to local memory.  Only owning threads touch data.
 template <int N, int E, int P, bool INV, bool FROM_REGS, bool TO_REGS>
 TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
                          int tw_log_scale, int tid, bool own) {
@@ -173,21 +175,17 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
   constexpr int T = PL::T;
   constexpr int Q = E / R;
   constexpr int NR = N / R;
-  double2 a[Q][R];
-  if (own) {
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-#pragma unroll
-      for (int m = 0; m < R; ++m) {
-        if constexpr (FROM_REGS) a[q][m] = v[q + m * Q];
-        else a[q][m] = sm[PL::pad(tid + q * T + m * NR)];
-      }
-    }
-  }
-  if constexpr (!FROM_REGS && !TO_REGS) __syncthreads();  // in place
   if (!own) return;
+  const double2* src = sm + ((P + 1) & 1) * PL::SMEM_ELEMS;
+  double2* dst = sm + (P & 1) * PL::SMEM_ELEMS;
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
+    double2 a[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      if constexpr (FROM_REGS) a[m] = v[q + m * Q];
+      else a[m] = src[PL::pad(tid + q * T + m * NR)];
+    }
     const int b = tid + q * T;
     const int k = b & (NS - 1);
     if constexpr (NS > 1) {
@@ -196,17 +194,17 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
 #pragma unroll
       for (int m = 1; m < R; ++m) {
         double2 w = ldt(&tw[(k * m) << sh]);
-        a[q][m] = INV ? cmulc(a[q][m], w) : cmul(a[q][m], w);
+        a[m] = INV ? cmulc(a[m], w) : cmul(a[m], w);
       }
     }
-    dft<R, INV>(a[q]);
+    dft<R, INV>(a);
     if constexpr (TO_REGS) {
 #pragma unroll
-      for (int m = 0; m < R; ++m) v[q + m * Q] = a[q][m];
+      for (int m = 0; m < R; ++m) v[q + m * Q] = a[m];
     } else {
       const int base = (b / NS) * NS * R + k;
 #pragma unroll
-      for (int m = 0; m < R; ++m) sm[PL::pad(base + m * NS)] = a[q][m];
+      for (int m = 0; m < R; ++m) dst[PL::pad(base + m * NS)] = a[m];
     }
   }
 }
@@ -238,6 +236,77 @@ TSF_D void block_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ t
   const bool own = tid < PL::T;
   __syncthreads();
   fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, own);
+}
+
+// ------------------------------------------------------------ real input
+// Forward DFTs of real data: no imaginary zeros are carried (x + 0.0 cannot
+// be folded under IEEE rules, so a complex first pass on real data wastes
+// registers and a quarter of its FLOPs) and the Hermitian half is mirrored.
+TSF_D void dft2_real(const double* x, double2* X) {
+  X[0] = make_double2(x[0] + x[1], 0.0);
+  X[1] = make_double2(x[0] - x[1], 0.0);
+}
+TSF_D void dft4_real(double x0, double x1, double x2, double x3, double2* X) {
+  const double t0 = x0 + x2, t1 = x0 - x2, t2 = x1 + x3, t3 = x1 - x3;
+  X[0] = make_double2(t0 + t2, 0.0);
+  X[1] = make_double2(t1, -t3);
+  X[2] = make_double2(t0 - t2, 0.0);
+  X[3] = make_double2(t1, t3);
+}
+TSF_D void dft8_real(const double* x, double2* X) {
+  double2 Ev[4], Od[4];
+  dft4_real(x[0], x[2], x[4], x[6], Ev);
+  dft4_real(x[1], x[3], x[5], x[7], Od);
+  // X_k = E_k + W8^k O_k, X_{k+4} = E_k - W8^k O_k, X_{8-k} = conj(X_k)
+  X[0] = make_double2(Ev[0].x + Od[0].x, 0.0);
+  X[4] = make_double2(Ev[0].x - Od[0].x, 0.0);
+  const double2 w1 = w8_1<false>(Od[1]);
+  X[1] = cadd(Ev[1], w1);
+  X[5] = csub(Ev[1], w1);
+  X[2] = make_double2(Ev[2].x, -Od[2].x);  // W8^2 = -i, O_2 real
+  X[6] = make_double2(Ev[2].x, Od[2].x);
+  X[3] = cconj(X[5]);
+  X[7] = cconj(X[1]);
+}
+template <int R>
+TSF_D void dft_real(const double* x, double2* X) {
+  if constexpr (R == 2) {
+    dft2_real(x, X);
+  } else if constexpr (R == 4) {
+    dft4_real(x[0], x[1], x[2], x[3], X);
+  } else {
+    static_assert(R == 8, "real first pass supports radix 2, 4, 8");
+    dft8_real(x, X);
+  }
+}
+
+// Forward transform of real owned slots x[c] (j = tid + c*T) into v[c].
+template <int N, int E>
+TSF_D void block_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
+                          const double2* __restrict__ tw, int tw_log_scale) {
+  using PL = FftPlan<N, E>;
+  static_assert(PL::NPASS >= 2, "real-input transform needs at least two passes");
+  constexpr int R = 1 << PL::log_radix(0);
+  constexpr int Q = E / R;
+  constexpr int T = PL::T;
+  __syncthreads();
+  const int tid = threadIdx.x;
+  const bool own = tid < T;
+  if (own) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      double in[R];
+      double2 out[R];
+#pragma unroll
+      for (int m = 0; m < R; ++m) in[m] = x[q + m * Q];
+      dft_real<R>(in, out);
+      const int base = (tid + q * T) * R;  // first pass: NS = 1, no twiddles
+#pragma unroll
+      for (int m = 0; m < R; ++m) sm[PL::pad(base + m)] = out[m];
+    }
+  }
+  __syncthreads();
+  fft_rec<N, E, 1, false>(v, sm, tw, tw_log_scale, tid, own);
 }
 
 }  // namespace tsf

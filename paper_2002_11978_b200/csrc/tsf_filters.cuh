@@ -55,12 +55,13 @@ struct FShape {
   static constexpr int T = N / E;
 };
 
-// even output bins: z <- IFFT_N( S_even . FFT_N(z) ); caller keeps Re(z)
+// even output bins: z <- IFFT_N( S_even . FFT_N(x) ) for real x; caller keeps Re(z)
 template <int N>
-TSF_D void filt_even(double2 (&z)[kE], double2* sm, const FilterTables& t) {
+TSF_D void filt_even(const double (&x)[kE], double2 (&z)[kE], double2* sm,
+                     const FilterTables& t) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
-  block_fft<N, E, false>(z, sm, t.tw, 1);
+  block_fft_real<N, E>(x, z, sm, t.tw, 1);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = cscale(z[c], ldt(&t.mvS[threadIdx.x + c * T]).x);
@@ -82,14 +83,14 @@ TSF_D void filt_odd(double2 (&z)[kE], double2* sm, const FilterTables& t) {
   block_fft<N, E, true>(z, sm, t.tw, 1);
 }
 
-// Strang: z <- IFFT_n( FFT_n(z) . Ssym / n ), n = N; caller keeps Re(z)
+// Strang: z <- IFFT_n( FFT_n(x) . Ssym / n ) for real x, n = N; caller keeps Re(z)
 template <int N>
-TSF_D void filt_strang(double2 (&z)[kE], double2* sm, const FilterTables& t, double d,
-                       double kbar) {
+TSF_D void filt_strang(const double (&x)[kE], double2 (&z)[kE], double2* sm,
+                       const FilterTables& t, double d, double kbar) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
   constexpr double inv_n = 1.0 / N;
-  block_fft<N, E, false>(z, sm, t.tw, 1);
+  block_fft_real<N, E>(x, z, sm, t.tw, 1);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {

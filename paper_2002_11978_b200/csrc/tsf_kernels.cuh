@@ -23,6 +23,8 @@ namespace tsf {
 
 constexpr int kMaxModes = 4;
 
+struct KState;
+
 struct KrylovArgs {
   int n;
   int B;
@@ -48,6 +50,9 @@ struct KrylovArgs {
   double* s;
   double* sh;
   double* t;
+  KState* kst;              // [B] per-instance Krylov scalars (phase kernels)
+  int* active;              // device counter of unfinished instances
+  int* h_active;            // pinned host mirror of *active (driver polling)
   int* iters;               // per-instance outputs
   double* relres;
   int* status;
@@ -59,7 +64,7 @@ struct KShape {
   static constexpr int E = FShape<N>::E;
   static constexpr int T = FShape<N>::T;         // owning threads
   static constexpr int BLOCK = T < 32 ? 32 : T;  // launched threads
-  static constexpr int FFT_BYTES = FftPlan<N, E>::SMEM_ELEMS * 16;
+  static constexpr int FFT_BYTES = 2 * FftPlan<N, E>::SMEM_ELEMS * 16;  // ping-pong
   static constexpr int SMEM = FFT_BYTES + N * 8;  // + one real staging vector
   static constexpr int MIN_BLOCKS = BLOCK >= 512 ? 1 : 512 / BLOCK;  // <= 128 regs
 };
@@ -74,11 +79,14 @@ TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restric
   const int tid = threadIdx.x;
   const bool own = tid < T;
   double2 z[kE];
-  if (own) {
+  {
+    double xr[kE];
+    if (own) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) z[c] = make_double2(ld_real(xg, n, tid + c * T), 0.0);
+      for (int c = 0; c < KShape<N>::E; ++c) xr[c] = ld_real(xg, n, tid + c * T);
+    }
+    filt_even<N>(xr, z, sm, t);
   }
-  filt_even<N>(z, sm, t);
   if (own) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) aux[tid + c * T] = z[c].x;
@@ -129,11 +137,12 @@ k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ zo, dou
   const long off = (long)blockIdx.x * n;
   const double kb = kbar_dev ? kbar_dev[blockIdx.x] : kbar;
   double2 z[kE];
+  double xr[kE];
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) z[c] = make_double2(ld_real(v + off, n, tid + c * T), 0.0);
+    for (int c = 0; c < KShape<N>::E; ++c) xr[c] = ld_real(v + off, n, tid + c * T);
   }
-  filt_strang<N>(z, sm, tab, shift, kb);
+  filt_strang<N>(xr, z, sm, tab, shift, kb);
   if (tid < T) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) st_real(zo + off, n, tid + c * T, z[c].x);
@@ -141,335 +150,417 @@ k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ zo, dou
 }
 
 // --------------------------------------------------------------- solver
-// Transform phases of the solve are out-of-line device functions with a
-// pointer/scalar interface: vectors live in the instance's L2-resident
-// workspace between phases, so a call boundary carries no vector state and
-// each phase gets the whole register budget (inlining ~10 transforms into
-// one loop body made ptxas interleave them and spill KBs per thread).
+// A level solve runs as straight-line PHASE kernels (one CTA per instance):
+//   begin : kappa (+ positivity), kappa_bar, preconditioner check, x = 0,
+//           ||r0||, p = r0, p_hat = P^{-1} p
+//   v     : v = M p_hat, alpha, s = r - alpha v, ||s|| (early exit), s_hat
+//   t     : t = M s_hat, omega, x/r update, ||r||, rho, beta, next p, p_hat
+// (BiCGSTAB, krylov.py:88-153), or begin + one iteration kernel (PCG,
+// krylov.py:43-85), launched repeatedly by the host driver until every
+// instance has finished (converged instances' CTAs return at once).  Each
+// kernel holds one matvec (two transform pairs) and at most one Strang
+// transform pair with no loop around them: ptxas spilled KBs per thread for
+// every single-kernel loop layout tried.  The per-instance
+// Krylov scalars live in KState; CTA-local reductions give every dot
+// product of an instance inside its own CTA.
 
-// dst = P^{-1} src on the owned slots
+struct KState {
+  double rho, rho_new, alpha, omega, nrm0, rnorm, snorm, kbar, rz;
+  int it, done;
+};
+
 template <int N>
-__device__ __noinline__ void dev_precond(const double* __restrict__ src, double* __restrict__ dst,
-                                         int n, double d, double kbar, double2* sm,
-                                         FilterTables t) {
+TSF_D void load_owned(double (&u)[kE], const double* g, int n) {
   constexpr int T = KShape<N>::T;
-  constexpr int E = KShape<N>::E;
   const int tid = threadIdx.x;
+  if (tid < T) {
+#pragma unroll
+    for (int c = 0; c < KShape<N>::E; ++c) u[c] = ld_real(g, n, tid + c * T);
+  }
+}
+template <int N>
+TSF_D void store_owned(double* g, const double (&u)[kE], int n) {
+  constexpr int T = KShape<N>::T;
+  const int tid = threadIdx.x;
+  if (tid < T) {
+#pragma unroll
+    for (int c = 0; c < KShape<N>::E; ++c) st_real(g, n, tid + c * T, u[c]);
+  }
+}
+// dst = P^{-1} u (u real, owned slots)
+template <int N>
+TSF_D void precond_store(const double (&u)[kE], double* dst, int n, double d, double kbar,
+                         double2* sm, const FilterTables& t) {
+  constexpr int T = KShape<N>::T;
   double2 z[kE];
-  if (tid < T) {
+  filt_strang<N>(u, z, sm, t, d, kbar);
+  if (threadIdx.x < T) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) z[c] = make_double2(ld_real(src, n, tid + c * T), 0.0);
-  }
-  filt_strang<N>(z, sm, t, d, kbar);
-  if (tid < T) {
-#pragma unroll
-    for (int c = 0; c < E; ++c) st_real(dst, n, tid + c * T, z[c].x);
+    for (int c = 0; c < KShape<N>::E; ++c) st_real(dst, n, threadIdx.x + c * T, z[c].x);
   }
 }
 
-// dst = shift*src + kappa .* (A src); returns this thread's partial
-// (sum dst*dst, sum dst*w) (w == nullptr: second entry 0)
-template <int N>
-__device__ __noinline__ double2 dev_apply(const double* __restrict__ src, double* __restrict__ dst,
-                                          const double* __restrict__ kg, double d, int n,
-                                          double2* sm, double* aux, FilterTables t,
-                                          const double* __restrict__ w) {
-  constexpr int T = KShape<N>::T;
-  constexpr int E = KShape<N>::E;
-  const int tid = threadIdx.x;
-  double y[kE];
-  apply_level_op<N>(src, kg, d, n, y, sm, aux, t);
-  double2 part = make_double2(0.0, 0.0);
-  if (tid < T) {
-#pragma unroll
-    for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
-      st_real(dst, n, j, y[c]);
-      if (j < n) {
-        part.x = fma(y[c], y[c], part.x);
-        if (w) part.y = fma(y[c], w[j], part.y);
-      }
-    }
+TSF_D void finish_instance(const KrylovArgs& a, KState* st, int* active, int b, int it,
+                           double rel, int status) {
+  if (threadIdx.x == 0) {
+    a.iters[b] = it;
+    a.relres[b] = rel;
+    a.status[b] = status;
+    st[b].done = 1;
+    atomicSub(active, 1);
   }
-  return part;
 }
 
-// PC: 0 = no preconditioner ("krylov"), 1 = Strang ("pkrylov", pow2 n = N)
-// CG: false = BiCGSTAB, true = PCG (kappa_x_independent)
+// ---- begin (both methods)
 template <int N, int PC, bool CG>
 __global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
-k_krylov_solve(KrylovArgs a) {
+k_solve_begin(KrylovArgs a, KState* st, int* active) {
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
   constexpr int T = KShape<N>::T;
   constexpr int E = KShape<N>::E;
-  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int b = blockIdx.x;
   const int n = a.n;
   const long off = (long)b * n;
-  const double d = a.shift;
-
-  // ---- kappa on the grid (scheme.py:156-160,280) and kappa_bar (scheme.py:135)
-  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
-  double kbar;
-  {
-    double ksum = 0.0, kmin = 1e308;
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < E; ++c) {
-        const int j = tid + c * T;
-        if (j < n) {
-          double k;
-          if (a.kappa) {
-            k = a.kappa[off + j];
-          } else {
-            k = 0.0;
-            for (int q = 0; q < a.nk; ++q) {
-              const double mq = a.kmodes[q * a.kq_stride + (long)b * a.kb_stride + j];
-              // no contraction: reproduce numpy's  acc + mode*coef  rounding
-              k = __dadd_rn(k, __dmul_rn(mq, a.kcoef[q]));
-            }
-            a.kwork[off + j] = k;
-          }
-          ksum += k;
-          kmin = fmin(kmin, k);
-        }
-      }
-    }
-    kmin = block_min1(kmin, red);
-    if (kmin <= 0.0) {
-      if (tid == 0) {
-        a.status[b] = TSF_KAPPA_NONPOS;
-        a.iters[b] = 0;
-        a.relres[b] = 0.0;
-      }
-      return;
-    }
-    const double kmean = block_sum1(ksum, red) / n;
-    kbar = a.kbar > 0.0 ? a.kbar : kmean;
-    if constexpr (PC == 1) {
-      // total eigenvalues d + kbar*lam > 0  (toeplitz.py:122-124)
-      double tmin = 1e308;
-      for (int k = tid; k < n; k += blockDim.x) tmin = fmin(tmin, d + kbar * ldt(&a.tab.pclam[k]).x);
-      tmin = block_min1(tmin, red);
-      if (tmin <= 0.0) {
-        if (tid == 0) {
-          a.status[b] = TSF_PRECOND_NONPOS;
-          a.iters[b] = 0;
-          a.relres[b] = 0.0;
-        }
-        return;
-      }
-    }
-  }
-
-  const double* r0g = a.rhs + off;
-  double* xg = a.x + off;
-  double* rg = a.r + off;
-  double* pg = a.p + off;
-  double* vg = a.v + off;
-  double* sg = a.s + off;
-  double* tg = a.t + off;
-  // without a preconditioner p_hat == p and s_hat == s
-  double* phg = PC ? a.ph + off : pg;
-  double* shg = PC ? a.sh + off : sg;
-  auto finish = [&](int it, double rel, int st) {
-    if (tid == 0) {
-      a.iters[b] = it;
-      a.relres[b] = rel;
-      a.status[b] = st;
-    }
-  };
-
-  // ---- r = r0 = rhs, x = 0  (krylov.py:107-113 / 64-69)
-  double ss0 = 0.0;
+  // kappa on the grid (scheme.py:156-160,280) and kappa_bar (scheme.py:135)
+  double ksum = 0.0, kmin = 1e308;
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int j = tid + c * T;
-      const double r0 = ld_real(r0g, n, j);
-      ss0 = fma(r0, r0, ss0);
-      st_real(xg, n, j, 0.0);
+      if (j < n) {
+        double k;
+        if (a.kappa) {
+          k = a.kappa[off + j];
+        } else {
+          k = 0.0;
+          for (int q = 0; q < a.nk; ++q) {
+            const double mq = a.kmodes[q * a.kq_stride + (long)b * a.kb_stride + j];
+            // no contraction: reproduce numpy's  acc + mode*coef  rounding
+            k = __dadd_rn(k, __dmul_rn(mq, a.kcoef[q]));
+          }
+          a.kwork[off + j] = k;
+        }
+        ksum += k;
+        kmin = fmin(kmin, k);
+      }
     }
   }
-  ss0 = block_sum1(ss0, red);
-  const double nrm0 = sqrt(ss0);
-  if (nrm0 == 0.0) {
-    finish(0, 0.0, TSF_OK);
+  kmin = block_min1(kmin, red);
+  if (kmin <= 0.0) {
+    finish_instance(a, st, active, b, 0, 0.0, TSF_KAPPA_NONPOS);
     return;
   }
-
-  if constexpr (!CG) {
-    // ================= BiCGSTAB (krylov.py:88-153) =================
-    double rho = 1.0, alpha = 1.0, omega = 1.0;
-    double rho_new = ss0;   // r0 . r with r = r0 (same reduction)
-    double rnorm = nrm0;
-    for (int it = 1; it <= a.max_iters; ++it) {
-      if (rho_new == 0.0) {
-        finish(it, rnorm / nrm0, TSF_BD_RHO);
-        return;
-      }
-      // p = r  |  p = r + beta (p - omega v)
-      if (own) {
-        const double beta = (rho_new / rho) * (alpha / omega);
+  const double kmean = block_sum1(ksum, red) / n;
+  const double kbar = a.kbar > 0.0 ? a.kbar : kmean;
+  const double d = a.shift;
+  if constexpr (PC == 1) {
+    // total eigenvalues d + kbar*lam > 0  (toeplitz.py:122-124)
+    double tmin = 1e308;
+    for (int k = tid; k < n; k += blockDim.x) tmin = fmin(tmin, d + kbar * ldt(&a.tab.pclam[k]).x);
+    tmin = block_min1(tmin, red);
+    if (tmin <= 0.0) {
+      finish_instance(a, st, active, b, 0, 0.0, TSF_PRECOND_NONPOS);
+      return;
+    }
+  }
+  // r = r0 = rhs, x = 0  (krylov.py:107-113 / 64-69)
+  double u[kE];
+  load_owned<N>(u, a.rhs + off, n);
+  double ss = 0.0;
+  if (own) {
 #pragma unroll
-        for (int c = 0; c < E; ++c) {
-          const int j = tid + c * T;
-          const double p = (it == 1) ? ld_real(r0g, n, j)
-                                     : ld_real(rg, n, j) +
-                                           beta * (ld_real(pg, n, j) - omega * ld_real(vg, n, j));
-          st_real(pg, n, j, p);
-        }
-      }
-      if constexpr (PC == 1) dev_precond<N>(pg, phg, n, d, kbar, sm, a.tab);
-      const double2 pv = dev_apply<N>(phg, vg, kg, d, n, sm, aux, a.tab, r0g);
-      const double denom = block_sum1(pv.y, red);
-      if (denom == 0.0) {
-        finish(it, rnorm / nrm0, TSF_BD_R0V);
-        return;
-      }
-      alpha = rho_new / denom;
-      // s = r - alpha v
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      st_real(a.x + off, n, j, 0.0);
+      if (j < n) ss = fma(u[c], u[c], ss);
+    }
+  }
+  ss = block_sum1(ss, red);
+  if (sqrt(ss) == 0.0) {
+    finish_instance(a, st, active, b, 0, 0.0, TSF_OK);
+    return;
+  }
+  if (CG) store_owned<N>(a.r + off, u, n);        // r = b
+  store_owned<N>(a.p + off, u, n);                // BiCGSTAB: p = r (it 1); CG: p = z (PC=0)
+  double rz = ss;
+  if constexpr (PC == 1) {
+    // BiCGSTAB: p_hat = P^{-1} p ; CG: z = P^{-1} r written to p (p = z)
+    precond_store<N>(u, CG ? a.p + off : a.ph + off, n, d, kbar, sm, a.tab);
+    if (CG) {
       double part = 0.0;
       if (own) {
-        const double* rc = (it == 1) ? r0g : rg;
 #pragma unroll
         for (int c = 0; c < E; ++c) {
           const int j = tid + c * T;
-          const double sv = ld_real(rc, n, j) - alpha * ld_real(vg, n, j);
-          st_real(sg, n, j, sv);
-          if (j < n) part = fma(sv, sv, part);
+          if (j < n) part = fma(u[c], a.p[off + j], part);
         }
       }
-      const double snorm = sqrt(block_sum1(part, red));
-      if (snorm / nrm0 < a.tol) {
-        // x += alpha p_hat (early exit counts as a full iteration, krylov.py:135-137)
-        if (own) {
-#pragma unroll
-          for (int c = 0; c < E; ++c) {
-            const int j = tid + c * T;
-            st_real(xg, n, j, ld_real(xg, n, j) + alpha * ld_real(phg, n, j));
-          }
-        }
-        finish(it, snorm / nrm0, TSF_OK);
-        return;
-      }
-      if constexpr (PC == 1) dev_precond<N>(sg, shg, n, d, kbar, sm, a.tab);
-      const double2 tp = dev_apply<N>(shg, tg, kg, d, n, sm, aux, a.tab, sg);
-      Vals<2> red2;
-      red2.v[0] = tp.x;
-      red2.v[1] = tp.y;
-      red2 = block_sum<2>(red2, red);
-      if (red2.v[0] == 0.0) {
-        finish(it, snorm / nrm0, TSF_BD_OMEGA_DEN);
-        return;
-      }
-      omega = red2.v[1] / red2.v[0];
-      // x += alpha p_hat + omega s_hat ; r = s - omega t
-      red2.v[0] = 0.0;
-      red2.v[1] = 0.0;
-      if (own) {
-#pragma unroll
-        for (int c = 0; c < E; ++c) {
-          const int j = tid + c * T;
-          st_real(xg, n, j,
-                  ld_real(xg, n, j) + (alpha * ld_real(phg, n, j) + omega * ld_real(shg, n, j)));
-          const double rn = ld_real(sg, n, j) - omega * ld_real(tg, n, j);
-          st_real(rg, n, j, rn);
-          if (j < n) {
-            red2.v[0] = fma(rn, rn, red2.v[0]);
-            red2.v[1] = fma(r0g[j], rn, red2.v[1]);
-          }
-        }
-      }
-      rho = rho_new;
-      red2 = block_sum<2>(red2, red);
-      rnorm = sqrt(red2.v[0]);
-      const double rel = rnorm / nrm0;
-      if (rel < a.tol) {
-        finish(it, rel, TSF_OK);
-        return;
-      }
-      if (omega == 0.0) {
-        finish(it, rel, TSF_BD_OMEGA);
-        return;
-      }
-      rho_new = red2.v[1];
+      rz = block_sum1(part, red);
     }
-    finish(a.max_iters, rnorm / nrm0, TSF_NOT_CONVERGED);
-  } else {
-    // ================= PCG (krylov.py:43-85) =================
-    // r = b; z = P^{-1} r; p = z  (z kept in s, p written directly)
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < E; ++c) {
-        const int j = tid + c * T;
-        st_real(rg, n, j, ld_real(r0g, n, j));
-        if (!PC) st_real(pg, n, j, ld_real(r0g, n, j));
-      }
-    }
-    if constexpr (PC == 1) dev_precond<N>(rg, pg, n, d, kbar, sm, a.tab);
-    double part = 0.0;
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < E; ++c) {
-        const int j = tid + c * T;
-        if (j < n) part = fma(r0g[j], pg[j], part);
-      }
-    }
-    double rz = block_sum1(part, red);
-    double rnorm = nrm0;
-    for (int it = 1; it <= a.max_iters; ++it) {
-      const double2 qp = dev_apply<N>(pg, vg, kg, d, n, sm, aux, a.tab, pg);  // q = M p
-      const double curv = block_sum1(qp.y, red);
-      if (curv <= 0.0) {
-        finish(it, rnorm / nrm0, TSF_BD_CURVATURE);
-        return;
-      }
-      const double al = rz / curv;
-      part = 0.0;
-      if (own) {
-#pragma unroll
-        for (int c = 0; c < E; ++c) {
-          const int j = tid + c * T;
-          st_real(xg, n, j, ld_real(xg, n, j) + al * ld_real(pg, n, j));
-          const double r1 = ld_real(rg, n, j) - al * ld_real(vg, n, j);
-          st_real(rg, n, j, r1);
-          if (j < n) part = fma(r1, r1, part);
-        }
-      }
-      rnorm = sqrt(block_sum1(part, red));
-      const double rel = rnorm / nrm0;
-      if (rel < a.tol) {
-        finish(it, rel, TSF_OK);
-        return;
-      }
-      double* zg = PC ? sg : rg;
-      if constexpr (PC == 1) dev_precond<N>(rg, sg, n, d, kbar, sm, a.tab);
-      part = 0.0;
-      if (own) {
-#pragma unroll
-        for (int c = 0; c < E; ++c) {
-          const int j = tid + c * T;
-          if (j < n) part = fma(rg[j], zg[j], part);
-        }
-      }
-      const double rz_new = block_sum1(part, red);
-      const double beta = rz_new / rz;
-      if (own) {
-#pragma unroll
-        for (int c = 0; c < E; ++c) {
-          const int j = tid + c * T;
-          st_real(pg, n, j, ld_real(zg, n, j) + beta * ld_real(pg, n, j));
-        }
-      }
-      rz = rz_new;
-    }
-    finish(a.max_iters, rnorm / nrm0, TSF_NOT_CONVERGED);
+  }
+  if (tid == 0) {
+    KState s;
+    s.rho = s.alpha = s.omega = 1.0;
+    s.rho_new = ss;   // r0 . r with r = r0 (same reduction)
+    s.nrm0 = s.rnorm = s.snorm = sqrt(ss);
+    s.kbar = kbar;
+    s.rz = rz;
+    s.it = 1;
+    s.done = 0;
+    st[b] = s;
   }
 }
+
+// ---- BiCGSTAB v-phase
+template <int N, int PC>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
+k_bicg_v(KrylovArgs a, KState* st, int* active) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  constexpr int T = KShape<N>::T;
+  constexpr int E = KShape<N>::E;
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
+  const int b = blockIdx.x;
+  if (st[b].done) return;
+  const int tid = threadIdx.x;
+  const bool own = tid < T;
+  const int n = a.n;
+  const long off = (long)b * n;
+  const KState s = st[b];
+  const double* phg = (PC ? a.ph : a.p) + off;
+  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
+  double u[kE];
+  apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, a.tab);   // u = v = M p_hat
+  store_owned<N>(a.v + off, u, n);
+  double part = 0.0;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      if (j < n) part = fma(a.rhs[off + j], u[c], part);
+    }
+  }
+  const double denom = block_sum1(part, red);
+  if (denom == 0.0) {
+    finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_R0V);
+    return;
+  }
+  const double alpha = s.rho_new / denom;
+  // s = r - alpha v
+  const double* rc = (s.it == 1 ? a.rhs : a.r) + off;
+  part = 0.0;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      u[c] = ld_real(rc, n, j) - alpha * u[c];
+      if (j < n) part = fma(u[c], u[c], part);
+    }
+  }
+  const double snorm = sqrt(block_sum1(part, red));
+  if (snorm / s.nrm0 < a.tol) {
+    // x += alpha p_hat (early exit counts as a full iteration, krylov.py:135-137)
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) {
+        const int j = tid + c * T;
+        st_real(a.x + off, n, j, ld_real(a.x + off, n, j) + alpha * ld_real(phg, n, j));
+      }
+    }
+    finish_instance(a, st, active, b, s.it, snorm / s.nrm0, TSF_OK);
+    return;
+  }
+  store_owned<N>(a.s + off, u, n);
+  if constexpr (PC == 1) precond_store<N>(u, a.sh + off, n, a.shift, s.kbar, sm, a.tab);
+  if (tid == 0) {
+    st[b].alpha = alpha;
+    st[b].snorm = snorm;
+  }
+}
+
+// ---- BiCGSTAB t-phase (+ next p / p_hat)
+template <int N, int PC>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
+k_bicg_t(KrylovArgs a, KState* st, int* active) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  constexpr int T = KShape<N>::T;
+  constexpr int E = KShape<N>::E;
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
+  const int b = blockIdx.x;
+  if (st[b].done) return;
+  const int tid = threadIdx.x;
+  const bool own = tid < T;
+  const int n = a.n;
+  const long off = (long)b * n;
+  const KState s = st[b];
+  const double* shg = (PC ? a.sh : a.s) + off;
+  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
+  double u[kE];
+  apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, a.tab);   // u = t = M s_hat
+  Vals<2> red2;
+  red2.v[0] = 0.0;
+  red2.v[1] = 0.0;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      if (j < n) {
+        red2.v[0] = fma(u[c], u[c], red2.v[0]);
+        red2.v[1] = fma(u[c], a.s[off + j], red2.v[1]);
+      }
+    }
+  }
+  red2 = block_sum<2>(red2, red);
+  if (red2.v[0] == 0.0) {
+    finish_instance(a, st, active, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN);
+    return;
+  }
+  const double omega = red2.v[1] / red2.v[0];
+  // x += alpha p_hat + omega s_hat ; r = s - omega t
+  const double* phg = (PC ? a.ph : a.p) + off;
+  red2.v[0] = 0.0;
+  red2.v[1] = 0.0;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      st_real(a.x + off, n, j,
+              ld_real(a.x + off, n, j) + (s.alpha * ld_real(phg, n, j) + omega * ld_real(shg, n, j)));
+      u[c] = ld_real(a.s + off, n, j) - omega * u[c];
+      st_real(a.r + off, n, j, u[c]);
+      if (j < n) {
+        red2.v[0] = fma(u[c], u[c], red2.v[0]);
+        red2.v[1] = fma(a.rhs[off + j], u[c], red2.v[1]);
+      }
+    }
+  }
+  red2 = block_sum<2>(red2, red);
+  const double rnorm = sqrt(red2.v[0]);
+  const double rel = rnorm / s.nrm0;
+  if (rel < a.tol) {
+    finish_instance(a, st, active, b, s.it, rel, TSF_OK);
+    return;
+  }
+  if (omega == 0.0) {
+    finish_instance(a, st, active, b, s.it, rel, TSF_BD_OMEGA);
+    return;
+  }
+  if (s.it >= a.max_iters) {
+    finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED);
+    return;
+  }
+  const double rho_new = red2.v[1];
+  if (rho_new == 0.0) {  // the next iteration's first test (krylov.py:118-121)
+    finish_instance(a, st, active, b, s.it + 1, rel, TSF_BD_RHO);
+    return;
+  }
+  // next p = r + beta (p - omega v)
+  const double beta = (rho_new / s.rho_new) * (s.alpha / omega);
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      u[c] = u[c] + beta * (ld_real(a.p + off, n, j) - omega * ld_real(a.v + off, n, j));
+    }
+  }
+  store_owned<N>(a.p + off, u, n);
+  if constexpr (PC == 1) precond_store<N>(u, a.ph + off, n, a.shift, s.kbar, sm, a.tab);
+  if (tid == 0) {
+    st[b].rho = s.rho_new;
+    st[b].rho_new = rho_new;
+    st[b].omega = omega;
+    st[b].rnorm = rnorm;
+    st[b].it = s.it + 1;
+  }
+}
+
+// ---- PCG iteration: q = M p, alpha, x, r, ||r||, z = P^{-1} r, beta, p
+template <int N, int PC>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
+k_cg_iter(KrylovArgs a, KState* st, int* active) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  constexpr int T = KShape<N>::T;
+  constexpr int E = KShape<N>::E;
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
+  const int b = blockIdx.x;
+  if (st[b].done) return;
+  const int tid = threadIdx.x;
+  const bool own = tid < T;
+  const int n = a.n;
+  const long off = (long)b * n;
+  const KState s = st[b];
+  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
+  double u[kE];
+  apply_level_op<N>(a.p + off, kg, a.shift, n, u, sm, aux, a.tab);  // u = q = M p
+  double part = 0.0;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      if (j < n) part = fma(a.p[off + j], u[c], part);
+    }
+  }
+  const double curv = block_sum1(part, red);
+  if (curv <= 0.0) {
+    finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_CURVATURE);
+    return;
+  }
+  const double al = s.rz / curv;
+  part = 0.0;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      st_real(a.x + off, n, j, ld_real(a.x + off, n, j) + al * ld_real(a.p + off, n, j));
+      u[c] = ld_real(a.r + off, n, j) - al * u[c];
+      if (j < n) part = fma(u[c], u[c], part);
+    }
+  }
+  store_owned<N>(a.r + off, u, n);
+  const double rnorm = sqrt(block_sum1(part, red));
+  const double rel = rnorm / s.nrm0;
+  if (rel < a.tol) {
+    finish_instance(a, st, active, b, s.it, rel, TSF_OK);
+    return;
+  }
+  if (s.it >= a.max_iters) {
+    finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED);
+    return;
+  }
+  // z = P^{-1} r (into s), rz_new = r.z, p = z + beta p
+  const double* zg = (PC ? a.s : a.r) + off;
+  if constexpr (PC == 1) precond_store<N>(u, a.s + off, n, a.shift, s.kbar, sm, a.tab);
+  __syncthreads();
+  part = 0.0;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      if (j < n) part = fma(u[c], zg[j], part);
+    }
+  }
+  const double rz_new = block_sum1(part, red);
+  const double beta = rz_new / s.rz;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      st_real(a.p + off, n, j, ld_real(zg, n, j) + beta * ld_real(a.p + off, n, j));
+    }
+  }
+  if (tid == 0) {
+    st[b].rz = rz_new;
+    st[b].rnorm = rnorm;
+    st[b].it = s.it + 1;
+  }
+}
+
+static __global__ void k_set_int(int* p, int v) { *p = v; }
 
 // --------------------------------------------------------------- debug FFT
 template <int N, int E, bool INV>
@@ -477,7 +568,7 @@ __global__ void k_fft_debug(const double2* __restrict__ in, double2* __restrict_
                             const double2* __restrict__ tw, int tw_log_scale) {
   extern __shared__ double2 sm[];
   constexpr int T = N / E;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x;  // debug transform: E complex slots per thread
   const long off = (long)blockIdx.x * N;
   double2 v[E];
   if (tid < T) {
