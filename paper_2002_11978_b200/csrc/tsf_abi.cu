@@ -103,14 +103,17 @@ struct FftF {
   static int call(A... a) { return Dispatch<LOG>::fft(a...); }
 };
 
-// twiddle table W_N^e, e < N, computed in long double
+// two-level twiddle table of W_N (tsf_fft.cuh tw_get): [W^j, j < 64] then
+// [W^(64 i), i < max(1, N/64)], computed in long double
 std::vector<double2> twiddles(int N) {
-  std::vector<double2> t(N);
   const long double two_pi = 6.283185307179586476925286766559005768L;
-  for (int e = 0; e < N; ++e) {
-    long double a = two_pi * (long double)e / (long double)N;
-    t[e] = make_double2((double)cosl(a), (double)-sinl(a));
-  }
+  auto w = [&](long e) {
+    long double a = two_pi * (long double)(e % N) / (long double)N;
+    return make_double2((double)cosl(a), (double)-sinl(a));
+  };
+  std::vector<double2> t(tw_table_elems(N));
+  for (int j = 0; j < 64; ++j) t[j] = w(j);
+  for (int i = 0; i < (int)t.size() - 64; ++i) t[64 + i] = w(64L * i);
   return t;
 }
 

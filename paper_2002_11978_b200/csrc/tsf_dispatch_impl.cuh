@@ -35,9 +35,9 @@ int Dispatch<LOG>::precond(int n, const FilterTables& t, int B, const double* v,
   constexpr int N = 1 << (LOG - 1);
   using S = KShape<N>;
   auto k = k_strang_apply<N>;
-  cudaError_t e = prep_kernel(k, S::FFT_BYTES);
+  cudaError_t e = prep_kernel(k, S::SMEM);
   if (e != cudaSuccess) return launch_error(e);
-  k<<<B, S::BLOCK, S::FFT_BYTES, st>>>(n, v, z, shift, kbar, kbar_dev, t);
+  k<<<B, S::BLOCK, S::SMEM, st>>>(n, v, z, shift, kbar, kbar_dev, t);
   return launch_error(cudaGetLastError());
 }
 
@@ -52,7 +52,7 @@ int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
   constexpr int kChunk = 4;
   cudaError_t e;
   auto kb = k_solve_begin<N, PC, CG>;
-  if ((e = prep_kernel(kb, S::FFT_BYTES)) != cudaSuccess) return launch_error(e);
+  if ((e = prep_kernel(kb, S::SMEM)) != cudaSuccess) return launch_error(e);
   auto kv = k_bicg_v<N, PC>;
   auto kt = k_bicg_t<N, PC>;
   auto kc = k_cg_iter<N, PC>;
@@ -63,7 +63,7 @@ int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
     return launch_error(e);
   }
   k_set_int<<<1, 1, 0, st>>>(a.active, B);
-  kb<<<B, S::BLOCK, S::FFT_BYTES, st>>>(a, a.kst, a.active);
+  kb<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
   if ((e = cudaGetLastError()) != cudaSuccess) return launch_error(e);
   for (int it = 0; it < a.max_iters; it += kChunk) {
     for (int k = 0; k < kChunk && it + k < a.max_iters; ++k) {
@@ -97,7 +97,7 @@ int Dispatch<LOG>::fft(int inverse, int B, const double2* in, double2* out, cons
   constexpr int N = 1 << (LOG - 1);
   using S = KShape<N>;
   constexpr int E = FShape<N>::E;
-  constexpr int smem = 2 * FftPlan<N, E>::SMEM_ELEMS * 16;
+  constexpr int smem = 2 * FftPlan<N, E>::SMEM_ELEMS * 16 + tw_table_elems(N) * 16;
   cudaError_t e;
   if (inverse) {
     auto k = k_fft_debug<N, E, true>;

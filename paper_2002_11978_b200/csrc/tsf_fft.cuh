@@ -139,6 +139,18 @@ TSF_D void dft(double2* a) {
   }
 }
 
+// ------------------------------------------------------------ twiddles
+// Two-level table staged in shared memory by every kernel:
+//   tw[j]        = W^j,       j < 64
+//   tw[64 + i]   = W^(64 i),  i < max(1, NT/64)
+// so W^e = tw[64 + (e >> 6)] * tw[e & 63] (within ~1 ulp; both factors are
+// correctly rounded long-double values).  A full table of NT entries (128 KB
+// at NT = 8192) does not fit the L1 left beside the transform buffers, and
+// streaming it from L2 was the main stall of the first solve kernels
+// (DESIGN.md §3.3).
+TSF_HD constexpr int tw_table_elems(int NT) { return 64 + (NT / 64 > 1 ? NT / 64 : 1); }
+TSF_D double2 tw_get(const double2* tw, int e) { return cmul(tw[64 + (e >> 6)], tw[e & 63]); }
+
 // ------------------------------------------------------------ pass plan
 constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
 constexpr int imin(int a, int b) { return a < b ? a : b; }
@@ -193,7 +205,7 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
       const int sh = tw_log_scale + PL::LOGN - PL::log_ns(P) - PL::log_radix(P);
 #pragma unroll
       for (int m = 1; m < R; ++m) {
-        double2 w = ldt(&tw[(k * m) << sh]);
+        double2 w = tw_get(tw, (k * m) << sh);
         a[m] = INV ? cmulc(a[m], w) : cmul(a[m], w);
       }
     }

@@ -33,7 +33,7 @@
 namespace tsf {
 
 struct FilterTables {
-  const double2* tw;    // W_L^e, e < L  (length-N transforms use stride 2)
+  const double2* tw;    // two-level W_L table (tsf_fft.cuh tw_get); kernels stage it in smem
   const double2* mvS;   // (S_{2k}, S_{2k+1}) / L, even part of the symbol, k < N
   const double2* pclam; // (lam_k, lam_{n-k}), k < n   (pow2 n = N only)
 };
@@ -103,6 +103,18 @@ TSF_D void filt_strang(const double (&x)[kE], double2 (&z)[kE], double2* sm,
 }
 
 // w_j = W_L^j for the owned slots
-TSF_D double2 modulation(const FilterTables& t, int j) { return ldt(&t.tw[j]); }
+TSF_D double2 modulation(const FilterTables& t, int j) { return tw_get(t.tw, j); }
+
+// Copy the two-level twiddle table of the length-L = 2N embedding into
+// shared memory at `dst`; returns the tables with tw redirected there.  The
+// first transform's leading barrier publishes the copy.
+template <int N>
+TSF_D FilterTables stage_tables(const FilterTables& g, double2* dst) {
+  constexpr int NT = tw_table_elems(2 * N);
+  for (int i = threadIdx.x; i < NT; i += blockDim.x) dst[i] = ldt(&g.tw[i]);
+  FilterTables t = g;
+  t.tw = dst;
+  return t;
+}
 
 }  // namespace tsf

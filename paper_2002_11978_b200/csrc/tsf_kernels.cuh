@@ -65,7 +65,10 @@ struct KShape {
   static constexpr int T = FShape<N>::T;         // owning threads
   static constexpr int BLOCK = T < 32 ? 32 : T;  // launched threads
   static constexpr int FFT_BYTES = 2 * FftPlan<N, E>::SMEM_ELEMS * 16;  // ping-pong
-  static constexpr int SMEM = FFT_BYTES + N * 8;  // + one real staging vector
+  static constexpr int TW_BYTES = tw_table_elems(2 * N) * 16;
+  // ping-pong transform buffers | real staging vector | twiddle table
+  static constexpr int SMEM = FFT_BYTES + N * 8 + TW_BYTES;
+  static constexpr int SMEM_PC = FFT_BYTES + N * 8 + TW_BYTES;
   static constexpr int MIN_BLOCKS = BLOCK >= 512 ? 1 : 512 / BLOCK;  // <= 128 regs
 };
 
@@ -115,11 +118,12 @@ k_toeplitz_apply(int n, const double* __restrict__ x, double* __restrict__ y,
                  const double* __restrict__ kappa, double shift, FilterTables tab) {
   extern __shared__ double2 sm[];
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
+  const FilterTables ts = stage_tables<N>(tab, reinterpret_cast<double2*>(aux + N));
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   const long off = (long)blockIdx.x * n;
   double out[kE];
-  apply_level_op<N>(x + off, kappa ? kappa + off : nullptr, shift, n, out, sm, aux, tab);
+  apply_level_op<N>(x + off, kappa ? kappa + off : nullptr, shift, n, out, sm, aux, ts);
   if (tid < T) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) st_real(y + off, n, tid + c * T, out[c]);
@@ -132,6 +136,8 @@ __global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
 k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ zo, double shift,
                double kbar, const double* __restrict__ kbar_dev, FilterTables tab) {
   extern __shared__ double2 sm[];
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
+  const FilterTables ts = stage_tables<N>(tab, reinterpret_cast<double2*>(aux + N));
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   const long off = (long)blockIdx.x * n;
@@ -142,7 +148,7 @@ k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ zo, dou
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) xr[c] = ld_real(v + off, n, tid + c * T);
   }
-  filt_strang<N>(xr, z, sm, tab, shift, kb);
+  filt_strang<N>(xr, z, sm, ts, shift, kb);
   if (tid < T) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) st_real(zo + off, n, tid + c * T, z[c].x);
@@ -217,6 +223,8 @@ __global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
 k_solve_begin(KrylovArgs a, KState* st, int* active) {
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
+  a.tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(
+      reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES + N * 8));
   constexpr int T = KShape<N>::T;
   constexpr int E = KShape<N>::E;
   const int tid = threadIdx.x;
@@ -325,6 +333,7 @@ k_bicg_v(KrylovArgs a, KState* st, int* active) {
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int b = blockIdx.x;
   if (st[b].done) return;
+  a.tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(aux + N));
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
@@ -392,6 +401,7 @@ k_bicg_t(KrylovArgs a, KState* st, int* active) {
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int b = blockIdx.x;
   if (st[b].done) return;
+  a.tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(aux + N));
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
@@ -489,6 +499,7 @@ k_cg_iter(KrylovArgs a, KState* st, int* active) {
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int b = blockIdx.x;
   if (st[b].done) return;
+  a.tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(aux + N));
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
@@ -565,11 +576,14 @@ static __global__ void k_set_int(int* p, int v) { *p = v; }
 // --------------------------------------------------------------- debug FFT
 template <int N, int E, bool INV>
 __global__ void k_fft_debug(const double2* __restrict__ in, double2* __restrict__ out,
-                            const double2* __restrict__ tw, int tw_log_scale) {
+                            const double2* tw, int tw_log_scale) {
   extern __shared__ double2 sm[];
   constexpr int T = N / E;
   const int tid = threadIdx.x;  // debug transform: E complex slots per thread
   const long off = (long)blockIdx.x * N;
+  double2* tws = sm + 2 * FftPlan<N, E>::SMEM_ELEMS;
+  for (int i = tid; i < tw_table_elems(N); i += blockDim.x) tws[i] = ldt(&tw[i]);
+  tw = tws;
   double2 v[E];
   if (tid < T) {
 #pragma unroll
