@@ -50,31 +50,6 @@ def workload(args):
     raise SystemExit(f"unknown workload {args.workload}")
 
 
-def instance_fields(n, b0, B, seed=2002_11978):
-    """Seeded per-instance fields of configs[2]."""
-    N = n + 1
-    x = -1.0 + (2.0 / N) * np.arange(1, N)
-    k = np.arange(1, 9)
-    cos_b = np.cos(np.pi * np.outer(k, x))
-    sin_b = np.sin(np.pi * np.outer(k, x))
-    sin_f = np.sin(np.pi * np.outer(k, (x + 1.0) / 2.0))
-    A = np.empty((B, 8))
-    Bc = np.empty((B, 8))
-    Cc = np.empty((B, 8))
-    U = np.empty(B)
-    for i in range(B):
-        rng = np.random.default_rng([seed, b0 + i])
-        A[i] = rng.normal(0.0, 1.0 / k)
-        Bc[i] = rng.normal(0.0, 1.0 / k)
-        Cc[i] = rng.normal(0.0, 1.0 / k)
-        U[i] = rng.uniform(0.5, 2.0)
-    g = A @ cos_b + Bc @ sin_b
-    kx = np.exp(0.4 * g)
-    fx = Cc @ sin_f
-    u0 = (1.0 - x * x) ** 2 * U[:, None]
-    return x, kx, fx, u0
-
-
 def cfg0_fields(n):
     N = n + 1
     x = -1.0 + (2.0 / N) * np.arange(1, N)
@@ -133,7 +108,8 @@ def _cpu_worker(args):
     import oracle as O
     n = wl["n"]
     if wl.get("cfg2", True):
-        x, kx, fx, u0 = instance_fields(n, b, 1)
+        from paper_2002_11978_b200 import workloads as WL
+        x, kx, fx, u0 = WL.instance_fields(n, b, 1)
         kf = lambda xx, t: kx[0] * (1.0 + 0.2 * t)  # noqa: E731
         sf = lambda xx, t: fx[0] * (1.0 + t)  # noqa: E731
         phi = u0[0]
@@ -236,7 +212,8 @@ def main():
     r = (2.0 - gam) / gam
     N = n + 1
     if cfg2:
-        x, kx, fx, u0 = instance_fields(n, rank * B, B)
+        from paper_2002_11978_b200 import workloads as WL
+        x, kx, fx, u0 = WL.instance_fields(n, rank * B, B)   # weak scaling: B per rank
         kap = P.SeparableField([np.ones(n)], lambda t: [1.0 + 0.2 * t])
         src = P.SeparableField([np.ones(n)], lambda t: [1.0 + t])
         kmodes, fmodes = kx[None], fx[None]
@@ -325,7 +302,8 @@ def main():
     peak_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     k_soe = {"name": "tsf::k_soe_push_rhs", "avg_ms": soe_ms / K,
              "GBps": soe_bytes / (soe_ms / K * 1e-3) / 1e9}
-    k_solve = {"name": "tsf::k_krylov_solve<8192,1,false>", "avg_ms": solve_ms / K,
+    k_solve = {"name": f"tsf level solve: k_solve_begin + k_bicg_v/k_bicg_t<{n},1> (N={n})",
+               "avg_ms": solve_ms / K,
                "GBps": solve_bytes / (solve_ms / K * 1e-3) / 1e9,
                "iterations_per_launch": its_sum / K}
     dom = k_solve if solve_ms >= soe_ms else k_soe
@@ -430,6 +408,9 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
+        # the only collective of the path: gather the final levels (untimed)
+        from paper_2002_11978_b200 import workloads as WL
+        WL.gather_rows(march.u_level(march.next_level - 1))
         dist.destroy_process_group()
 
 
