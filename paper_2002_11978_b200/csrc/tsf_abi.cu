@@ -130,7 +130,7 @@ int ensure_reserved(tsf_plan* p, int B) {
   p->kst = nullptr;
   p->cap = 0;
   CK(cudaSetDevice(p->device));
-  CK(cudaMalloc(&p->ws, sizeof(double) * (size_t)B * p->n * 8));
+  CK(cudaMalloc(&p->ws, sizeof(double) * (size_t)B * p->n * 9));
   CK(cudaMalloc(&p->ist, sizeof(int) * (size_t)B * 2));
   CK(cudaMalloc(&p->dst, sizeof(double) * (size_t)B));
   CK(cudaMalloc(&p->kst, sizeof(KState) * (size_t)B));
@@ -262,6 +262,7 @@ static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cud
   a.s = p->ws + 4 * vn;
   a.sh = p->ws + 5 * vn;
   a.t = p->ws + 6 * vn;
+  a.pspec = p->ws + 8 * vn;
   a.kst = p->kst;
   a.active = p->ist;
   a.h_active = p->h_active;

@@ -102,6 +102,22 @@ TSF_D void filt_strang(const double (&x)[kE], double2 (&z)[kE], double2* sm,
   block_fft<N, E, true>(z, sm, t.tw, 1);
 }
 
+// Strang with a precomputed per-instance spectrum spec[k] = S_k / n (the level
+// solve forms it once per level in k_solve_begin instead of two reciprocals
+// per bin in every application).
+template <int N>
+TSF_D void filt_strang_tab(const double (&x)[kE], double2 (&z)[kE], double2* sm,
+                           const FilterTables& t, const double* __restrict__ spec) {
+  constexpr int T = FShape<N>::T;
+  constexpr int E = FShape<N>::E;
+  block_fft_real<N, E>(x, z, sm, t.tw, 1);
+  if (threadIdx.x < T) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], spec[threadIdx.x + c * T]);
+  }
+  block_fft<N, E, true>(z, sm, t.tw, 1);
+}
+
 // w_j = W_L^j for the owned slots
 TSF_D double2 modulation(const FilterTables& t, int j) { return tw_get(t.tw, j); }
 

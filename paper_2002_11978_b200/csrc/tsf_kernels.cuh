@@ -50,6 +50,7 @@ struct KrylovArgs {
   double* s;
   double* sh;
   double* t;
+  double* pspec;            // [B, n] Strang spectrum S_k / n of the level (PC == 1)
   KState* kst;              // [B] per-instance Krylov scalars (phase kernels)
   int* active;              // device counter of unfinished instances
   int* h_active;            // pinned host mirror of *active (driver polling)
@@ -193,13 +194,13 @@ TSF_D void store_owned(double* g, const double (&u)[kE], int n) {
     for (int c = 0; c < KShape<N>::E; ++c) st_real(g, n, tid + c * T, u[c]);
   }
 }
-// dst = P^{-1} u (u real, owned slots)
+// dst = P^{-1} u (u real, owned slots); spec = the instance's S_k / n
 template <int N>
-TSF_D void precond_store(const double (&u)[kE], double* dst, int n, double d, double kbar,
+TSF_D void precond_store(const double (&u)[kE], double* dst, int n, const double* spec,
                          double2* sm, const FilterTables& t) {
   constexpr int T = KShape<N>::T;
   double2 z[kE];
-  filt_strang<N>(u, z, sm, t, d, kbar);
+  filt_strang_tab<N>(u, z, sm, t, spec);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) st_real(dst, n, threadIdx.x + c * T, z[c].x);
@@ -273,6 +274,15 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
       finish_instance(a, st, active, b, 0, 0.0, TSF_PRECOND_NONPOS);
       return;
     }
+    // the level's Strang filter (even part of 1/total, 1/n folded in), once
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) {
+        const int j = tid + c * T;
+        const double2 lam = ldt(&a.tab.pclam[j]);
+        a.pspec[off + j] = 0.5 * (1.0 / (d + kbar * lam.x) + 1.0 / (d + kbar * lam.y)) / n;
+      }
+    }
   }
   // r = r0 = rhs, x = 0  (krylov.py:107-113 / 64-69)
   double u[kE];
@@ -296,7 +306,7 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
   double rz = ss;
   if constexpr (PC == 1) {
     // BiCGSTAB: p_hat = P^{-1} p ; CG: z = P^{-1} r written to p (p = z)
-    precond_store<N>(u, CG ? a.p + off : a.ph + off, n, d, kbar, sm, a.tab);
+    precond_store<N>(u, CG ? a.p + off : a.ph + off, n, a.pspec + off, sm, a.tab);
     if (CG) {
       double part = 0.0;
       if (own) {
@@ -383,7 +393,7 @@ k_bicg_v(KrylovArgs a, KState* st, int* active) {
     return;
   }
   store_owned<N>(a.s + off, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.sh + off, n, a.shift, s.kbar, sm, a.tab);
+  if constexpr (PC == 1) precond_store<N>(u, a.sh + off, n, a.pspec + off, sm, a.tab);
   if (tid == 0) {
     st[b].alpha = alpha;
     st[b].snorm = snorm;
@@ -478,7 +488,7 @@ k_bicg_t(KrylovArgs a, KState* st, int* active) {
     }
   }
   store_owned<N>(a.p + off, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.ph + off, n, a.shift, s.kbar, sm, a.tab);
+  if constexpr (PC == 1) precond_store<N>(u, a.ph + off, n, a.pspec + off, sm, a.tab);
   if (tid == 0) {
     st[b].rho = s.rho_new;
     st[b].rho_new = rho_new;
@@ -545,7 +555,7 @@ k_cg_iter(KrylovArgs a, KState* st, int* active) {
   }
   // z = P^{-1} r (into s), rz_new = r.z, p = z + beta p
   const double* zg = (PC ? a.s : a.r) + off;
-  if constexpr (PC == 1) precond_store<N>(u, a.s + off, n, a.shift, s.kbar, sm, a.tab);
+  if constexpr (PC == 1) precond_store<N>(u, a.s + off, n, a.pspec + off, sm, a.tab);
   __syncthreads();
   part = 0.0;
   if (own) {
