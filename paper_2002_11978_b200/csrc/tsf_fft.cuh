@@ -203,11 +203,24 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
     if constexpr (NS > 1) {
       // W_{NS R}^{k m} = W_NT^{k m NT/(NS R)}, NT/(NS R) = 2^sh
       const int sh = tw_log_scale + PL::LOGN - PL::log_ns(P) - PL::log_radix(P);
-#pragma unroll
-      for (int m = 1; m < R; ++m) {
-        double2 w = tw_get(tw, (k * m) << sh);
-        a[m] = INV ? cmulc(a[m], w) : cmul(a[m], w);
+      // W^k, W^2k, W^4k from the table; the other powers are one product of
+      // two of them (3 of 7 table reads per butterfly; accuracy measured in
+      // tools/accuracy_probe.py against an exact long-double DFT)
+      double2 w[R];
+      w[1] = tw_get(tw, k << sh);
+      if constexpr (R >= 4) {
+        w[2] = tw_get(tw, (2 * k) << sh);
+        w[3] = cmul(w[2], w[1]);
       }
+      if constexpr (R >= 8) {
+        w[4] = tw_get(tw, (4 * k) << sh);
+        w[5] = cmul(w[4], w[1]);
+        w[6] = cmul(w[4], w[2]);
+        w[7] = cmul(w[4], w[3]);
+      }
+      static_assert(R <= 8, "twiddle product tree covers radix <= 8");
+#pragma unroll
+      for (int m = 1; m < R; ++m) a[m] = INV ? cmulc(a[m], w[m]) : cmul(a[m], w[m]);
     }
     dft<R, INV>(a);
     if constexpr (TO_REGS) {
