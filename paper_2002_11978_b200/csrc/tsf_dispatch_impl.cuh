@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "tsf_dispatch.h"
 
 namespace tsf {
@@ -46,11 +48,29 @@ int Dispatch<LOG>::precond(int n, const FilterTables& t, int B, const double* v,
 // device count of unfinished instances is read back (one small D2H copy and
 // a stream sync per chunk).  Finished instances' CTAs return immediately, so
 // the overshoot costs at most kChunk-1 near-empty launch pairs.
+// TSF_SOLVE_PERSIST=1 selects the persistent per-instance kernel (one launch
+// per level solve) instead of the host-driven phase kernels.
+inline bool persist_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_SOLVE_PERSIST");
+    v = (s && s[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <int N, int PC, bool CG>
 int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
   using S = KShape<N>;
   constexpr int kChunk = 4;
   cudaError_t e;
+  if (persist_mode()) {
+    auto kp = k_krylov_persist<N, PC, CG>;
+    if ((e = prep_kernel(kp, S::SMEM)) != cudaSuccess) return launch_error(e);
+    k_set_int<<<1, 1, 0, st>>>(a.active, B);
+    kp<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
+    return launch_error(cudaGetLastError());
+  }
   auto kb = k_solve_begin<N, PC, CG>;
   if ((e = prep_kernel(kb, S::SMEM)) != cudaSuccess) return launch_error(e);
   auto kv = k_bicg_v<N, PC>;
@@ -97,7 +117,7 @@ int Dispatch<LOG>::fft(int inverse, int B, const double2* in, double2* out, cons
   constexpr int N = 1 << (LOG - 1);
   using S = KShape<N>;
   constexpr int E = FShape<N>::E;
-  constexpr int smem = 2 * FftPlan<N, E>::SMEM_ELEMS * 16 + tw_table_elems(N) * 16;
+  constexpr int smem = (kFftInPlace ? 1 : 2) * FftPlan<N, E>::SMEM_ELEMS * 16 + tw_table_elems(N) * 16;
   cudaError_t e;
   if (inverse) {
     auto k = k_fft_debug<N, E, true>;

@@ -22,6 +22,13 @@
 
 #include "tsf_common.cuh"
 
+#ifndef TSF_FFT_INPLACE
+#define TSF_FFT_INPLACE 0
+#endif
+#ifndef TSF_KE
+#define TSF_KE 8
+#endif
+
 namespace tsf {
 
 // ------------------------------------------------------------ small DFTs
@@ -148,6 +155,11 @@ TSF_D void dft(double2* a) {
 // at NT = 8192) does not fit the L1 left beside the transform buffers, and
 // streaming it from L2 was the main stall of the first solve kernels
 // (DESIGN.md §3.3).
+// In-place passes (one buffer, a barrier between a pass's reads and writes)
+// halve the transform's shared memory; out-of-place (ping-pong) passes need
+// no mid-pass barrier.  See DESIGN.md §3.1.
+constexpr bool kFftInPlace = TSF_FFT_INPLACE;
+
 TSF_HD constexpr int tw_table_elems(int NT) { return 64 + (NT / 64 > 1 ? NT / 64 : 1); }
 TSF_D double2 tw_get(const double2* tw, int e) { return cmul(tw[64 + (e >> 6)], tw[e & 63]); }
 
@@ -187,17 +199,23 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
   constexpr int T = PL::T;
   constexpr int Q = E / R;
   constexpr int NR = N / R;
+  const double2* src = sm + (kFftInPlace ? 0 : ((P + 1) & 1) * PL::SMEM_ELEMS);
+  double2* dst = sm + (kFftInPlace ? 0 : (P & 1) * PL::SMEM_ELEMS);
+  double2 a[Q][R];
+  if (own) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        if constexpr (FROM_REGS) a[q][m] = v[q + m * Q];
+        else a[q][m] = src[PL::pad(tid + q * T + m * NR)];
+      }
+    }
+  }
+  if constexpr (kFftInPlace && !FROM_REGS && !TO_REGS) __syncthreads();  // reads before writes
   if (!own) return;
-  const double2* src = sm + ((P + 1) & 1) * PL::SMEM_ELEMS;
-  double2* dst = sm + (P & 1) * PL::SMEM_ELEMS;
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
-    double2 a[R];
-#pragma unroll
-    for (int m = 0; m < R; ++m) {
-      if constexpr (FROM_REGS) a[m] = v[q + m * Q];
-      else a[m] = src[PL::pad(tid + q * T + m * NR)];
-    }
     const int b = tid + q * T;
     const int k = b & (NS - 1);
     if constexpr (NS > 1) {
@@ -218,18 +236,22 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
         w[6] = cmul(w[4], w[2]);
         w[7] = cmul(w[4], w[3]);
       }
-      static_assert(R <= 8, "twiddle product tree covers radix <= 8");
+      if constexpr (R >= 16) {
+        w[8] = tw_get(tw, (8 * k) << sh);
 #pragma unroll
-      for (int m = 1; m < R; ++m) a[m] = INV ? cmulc(a[m], w[m]) : cmul(a[m], w[m]);
+        for (int m = 9; m < 16; ++m) w[m] = cmul(w[8], w[m - 8]);
+      }
+#pragma unroll
+      for (int m = 1; m < R; ++m) a[q][m] = INV ? cmulc(a[q][m], w[m]) : cmul(a[q][m], w[m]);
     }
-    dft<R, INV>(a);
+    dft<R, INV>(a[q]);
     if constexpr (TO_REGS) {
 #pragma unroll
-      for (int m = 0; m < R; ++m) v[q + m * Q] = a[m];
+      for (int m = 0; m < R; ++m) v[q + m * Q] = a[q][m];
     } else {
       const int base = (b / NS) * NS * R + k;
 #pragma unroll
-      for (int m = 0; m < R; ++m) dst[PL::pad(base + m * NS)] = a[m];
+      for (int m = 0; m < R; ++m) dst[PL::pad(base + m * NS)] = a[q][m];
     }
   }
 }
@@ -293,15 +315,42 @@ TSF_D void dft8_real(const double* x, double2* X) {
   X[3] = cconj(X[5]);
   X[7] = cconj(X[1]);
 }
+TSF_D void dft16_real(const double* x, double2* X) {
+  // X_k = E_k + W16^k O_k over the even/odd halves (both real length 8)
+  double ev[8], od[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    ev[i] = x[2 * i];
+    od[i] = x[2 * i + 1];
+  }
+  double2 E8[8], O8[8];
+  dft8_real(ev, E8);
+  dft8_real(od, O8);
+  X[0] = make_double2(E8[0].x + O8[0].x, 0.0);
+  X[8] = make_double2(E8[0].x - O8[0].x, 0.0);
+  double2 w;
+  w = w16<1, false>(O8[1]); X[1] = cadd(E8[1], w); X[9] = csub(E8[1], w);
+  w = w16<2, false>(O8[2]); X[2] = cadd(E8[2], w); X[10] = csub(E8[2], w);
+  w = w16<3, false>(O8[3]); X[3] = cadd(E8[3], w); X[11] = csub(E8[3], w);
+  X[4] = make_double2(E8[4].x, -O8[4].x);  // W16^4 = -i, O_4 real
+  X[12] = make_double2(E8[4].x, O8[4].x);
+#pragma unroll
+  for (int k = 5; k < 8; ++k) X[k] = cconj(X[16 - k]);
+#pragma unroll
+  for (int k = 13; k < 16; ++k) X[k] = cconj(X[16 - k]);
+}
+
 template <int R>
 TSF_D void dft_real(const double* x, double2* X) {
   if constexpr (R == 2) {
     dft2_real(x, X);
   } else if constexpr (R == 4) {
     dft4_real(x[0], x[1], x[2], x[3], X);
-  } else {
-    static_assert(R == 8, "real first pass supports radix 2, 4, 8");
+  } else if constexpr (R == 8) {
     dft8_real(x, X);
+  } else {
+    static_assert(R == 16, "real first pass supports radix 2, 4, 8, 16");
+    dft16_real(x, X);
   }
 }
 

@@ -45,19 +45,21 @@ TSF_D void st_real(double* __restrict__ base, int n, int j, double v) {
   if (j < n) base[j] = v;
 }
 
-// elements (complex slots) per owning thread: 8 keeps one transform at ~93
-// registers (16 would need ~166)
-constexpr int kE = 8;
+// elements (complex slots) per owning thread
+constexpr int kE = TSF_KE;
 
 template <int N>
 struct FShape {
-  static constexpr int E = kE < N ? kE : N;
+  // 8 slots: one transform needs ~93 registers; 16 slots (radix-16, three
+  // passes at N = 4096) need ~166 and spill under the 128-register cap of
+  // 512-thread CTAs (measured)
+  static constexpr int E = kE;
   static constexpr int T = N / E;
 };
 
 // even output bins: z <- IFFT_N( S_even . FFT_N(x) ) for real x; caller keeps Re(z)
 template <int N>
-TSF_D void filt_even(const double (&x)[kE], double2 (&z)[kE], double2* sm,
+TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E], double2* sm,
                      const FilterTables& t) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
@@ -72,7 +74,7 @@ TSF_D void filt_even(const double (&x)[kE], double2 (&z)[kE], double2* sm,
 // odd output bins: z (already modulated by w_j) <- IFFT_N( S_odd . FFT_N(z) );
 // caller keeps Re(conj(w_j) z_j)
 template <int N>
-TSF_D void filt_odd(double2 (&z)[kE], double2* sm, const FilterTables& t) {
+TSF_D void filt_odd(double2 (&z)[FShape<N>::E], double2* sm, const FilterTables& t) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
   block_fft<N, E, false>(z, sm, t.tw, 1);
@@ -85,7 +87,7 @@ TSF_D void filt_odd(double2 (&z)[kE], double2* sm, const FilterTables& t) {
 
 // Strang: z <- IFFT_n( FFT_n(x) . Ssym / n ) for real x, n = N; caller keeps Re(z)
 template <int N>
-TSF_D void filt_strang(const double (&x)[kE], double2 (&z)[kE], double2* sm,
+TSF_D void filt_strang(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E], double2* sm,
                        const FilterTables& t, double d, double kbar) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
@@ -106,7 +108,7 @@ TSF_D void filt_strang(const double (&x)[kE], double2 (&z)[kE], double2* sm,
 // solve forms it once per level in k_solve_begin instead of two reciprocals
 // per bin in every application).
 template <int N>
-TSF_D void filt_strang_tab(const double (&x)[kE], double2 (&z)[kE], double2* sm,
+TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E], double2* sm,
                            const FilterTables& t, const double* __restrict__ spec) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;

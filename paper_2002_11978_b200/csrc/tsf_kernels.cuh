@@ -65,7 +65,7 @@ struct KShape {
   static constexpr int E = FShape<N>::E;
   static constexpr int T = FShape<N>::T;         // owning threads
   static constexpr int BLOCK = T < 32 ? 32 : T;  // launched threads
-  static constexpr int FFT_BYTES = 2 * FftPlan<N, E>::SMEM_ELEMS * 16;  // ping-pong
+  static constexpr int FFT_BYTES = (kFftInPlace ? 1 : 2) * FftPlan<N, E>::SMEM_ELEMS * 16;
   static constexpr int TW_BYTES = tw_table_elems(2 * N) * 16;
   // ping-pong transform buffers | real staging vector | twiddle table
   static constexpr int SMEM = FFT_BYTES + N * 8 + TW_BYTES;
@@ -77,14 +77,14 @@ struct KShape {
 // x is read from global (twice); result returned in y[].
 template <int N>
 TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restrict__ kg,
-                          double shift, int n, double (&y)[kE], double2* sm, double* aux,
+                          double shift, int n, double (&y)[FShape<N>::E], double2* sm, double* aux,
                           const FilterTables& t) {
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   const bool own = tid < T;
-  double2 z[kE];
+  double2 z[FShape<N>::E];
   {
-    double xr[kE];
+    double xr[FShape<N>::E];
     if (own) {
 #pragma unroll
       for (int c = 0; c < KShape<N>::E; ++c) xr[c] = ld_real(xg, n, tid + c * T);
@@ -123,7 +123,7 @@ k_toeplitz_apply(int n, const double* __restrict__ x, double* __restrict__ y,
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   const long off = (long)blockIdx.x * n;
-  double out[kE];
+  double out[FShape<N>::E];
   apply_level_op<N>(x + off, kappa ? kappa + off : nullptr, shift, n, out, sm, aux, ts);
   if (tid < T) {
 #pragma unroll
@@ -143,8 +143,8 @@ k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ zo, dou
   const int tid = threadIdx.x;
   const long off = (long)blockIdx.x * n;
   const double kb = kbar_dev ? kbar_dev[blockIdx.x] : kbar;
-  double2 z[kE];
-  double xr[kE];
+  double2 z[FShape<N>::E];
+  double xr[FShape<N>::E];
   if (tid < T) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) xr[c] = ld_real(v + off, n, tid + c * T);
@@ -177,7 +177,7 @@ struct KState {
 };
 
 template <int N>
-TSF_D void load_owned(double (&u)[kE], const double* g, int n) {
+TSF_D void load_owned(double (&u)[FShape<N>::E], const double* g, int n) {
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   if (tid < T) {
@@ -186,7 +186,7 @@ TSF_D void load_owned(double (&u)[kE], const double* g, int n) {
   }
 }
 template <int N>
-TSF_D void store_owned(double* g, const double (&u)[kE], int n) {
+TSF_D void store_owned(double* g, const double (&u)[FShape<N>::E], int n) {
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   if (tid < T) {
@@ -196,10 +196,10 @@ TSF_D void store_owned(double* g, const double (&u)[kE], int n) {
 }
 // dst = P^{-1} u (u real, owned slots); spec = the instance's S_k / n
 template <int N>
-TSF_D void precond_store(const double (&u)[kE], double* dst, int n, const double* spec,
+TSF_D void precond_store(const double (&u)[FShape<N>::E], double* dst, int n, const double* spec,
                          double2* sm, const FilterTables& t) {
   constexpr int T = KShape<N>::T;
-  double2 z[kE];
+  double2 z[FShape<N>::E];
   filt_strang_tab<N>(u, z, sm, t, spec);
   if (threadIdx.x < T) {
 #pragma unroll
@@ -219,13 +219,11 @@ TSF_D void finish_instance(const KrylovArgs& a, KState* st, int* active, int b, 
 }
 
 // ---- begin (both methods)
+// Phase bodies are device functions (return true when the instance finished)
+// shared by the phase kernels and the persistent per-instance kernel.
 template <int N, int PC, bool CG>
-__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
-k_solve_begin(KrylovArgs a, KState* st, int* active) {
-  extern __shared__ double2 sm[];
-  __shared__ double red[4 * 32];
-  a.tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(
-      reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES + N * 8));
+TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, int* active, double2* sm,
+                    double* red) {
   constexpr int T = KShape<N>::T;
   constexpr int E = KShape<N>::E;
   const int tid = threadIdx.x;
@@ -260,7 +258,7 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
   kmin = block_min1(kmin, red);
   if (kmin <= 0.0) {
     finish_instance(a, st, active, b, 0, 0.0, TSF_KAPPA_NONPOS);
-    return;
+    return true;
   }
   const double kmean = block_sum1(ksum, red) / n;
   const double kbar = a.kbar > 0.0 ? a.kbar : kmean;
@@ -268,24 +266,24 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
   if constexpr (PC == 1) {
     // total eigenvalues d + kbar*lam > 0  (toeplitz.py:122-124)
     double tmin = 1e308;
-    for (int k = tid; k < n; k += blockDim.x) tmin = fmin(tmin, d + kbar * ldt(&a.tab.pclam[k]).x);
+    for (int k = tid; k < n; k += blockDim.x) tmin = fmin(tmin, d + kbar * ldt(&tab.pclam[k]).x);
     tmin = block_min1(tmin, red);
     if (tmin <= 0.0) {
       finish_instance(a, st, active, b, 0, 0.0, TSF_PRECOND_NONPOS);
-      return;
+      return true;
     }
     // the level's Strang filter (even part of 1/total, 1/n folded in), once
     if (own) {
 #pragma unroll
       for (int c = 0; c < E; ++c) {
         const int j = tid + c * T;
-        const double2 lam = ldt(&a.tab.pclam[j]);
+        const double2 lam = ldt(&tab.pclam[j]);
         a.pspec[off + j] = 0.5 * (1.0 / (d + kbar * lam.x) + 1.0 / (d + kbar * lam.y)) / n;
       }
     }
   }
   // r = r0 = rhs, x = 0  (krylov.py:107-113 / 64-69)
-  double u[kE];
+  double u[FShape<N>::E];
   load_owned<N>(u, a.rhs + off, n);
   double ss = 0.0;
   if (own) {
@@ -299,14 +297,14 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
   ss = block_sum1(ss, red);
   if (sqrt(ss) == 0.0) {
     finish_instance(a, st, active, b, 0, 0.0, TSF_OK);
-    return;
+    return true;
   }
   if (CG) store_owned<N>(a.r + off, u, n);        // r = b
   store_owned<N>(a.p + off, u, n);                // BiCGSTAB: p = r (it 1); CG: p = z (PC=0)
   double rz = ss;
   if constexpr (PC == 1) {
     // BiCGSTAB: p_hat = P^{-1} p ; CG: z = P^{-1} r written to p (p = z)
-    precond_store<N>(u, CG ? a.p + off : a.ph + off, n, a.pspec + off, sm, a.tab);
+    precond_store<N>(u, CG ? a.p + off : a.ph + off, n, a.pspec + off, sm, tab);
     if (CG) {
       double part = 0.0;
       if (own) {
@@ -330,20 +328,18 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
     s.done = 0;
     st[b] = s;
   }
+  return false;
 }
 
 // ---- BiCGSTAB v-phase
 template <int N, int PC>
-__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
-k_bicg_v(KrylovArgs a, KState* st, int* active) {
-  extern __shared__ double2 sm[];
-  __shared__ double red[4 * 32];
+TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, int* active, double2* sm,
+                    double* red) {
   constexpr int T = KShape<N>::T;
   constexpr int E = KShape<N>::E;
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int b = blockIdx.x;
-  if (st[b].done) return;
-  a.tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(aux + N));
+  __syncthreads();  // previous phase's st[b] writes (thread 0) are visible
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
@@ -351,8 +347,8 @@ k_bicg_v(KrylovArgs a, KState* st, int* active) {
   const KState s = st[b];
   const double* phg = (PC ? a.ph : a.p) + off;
   const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
-  double u[kE];
-  apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, a.tab);   // u = v = M p_hat
+  double u[FShape<N>::E];
+  apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, tab);   // u = v = M p_hat
   store_owned<N>(a.v + off, u, n);
   double part = 0.0;
   if (own) {
@@ -365,7 +361,7 @@ k_bicg_v(KrylovArgs a, KState* st, int* active) {
   const double denom = block_sum1(part, red);
   if (denom == 0.0) {
     finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_R0V);
-    return;
+    return true;
   }
   const double alpha = s.rho_new / denom;
   // s = r - alpha v
@@ -390,28 +386,26 @@ k_bicg_v(KrylovArgs a, KState* st, int* active) {
       }
     }
     finish_instance(a, st, active, b, s.it, snorm / s.nrm0, TSF_OK);
-    return;
+    return true;
   }
   store_owned<N>(a.s + off, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.sh + off, n, a.pspec + off, sm, a.tab);
+  if constexpr (PC == 1) precond_store<N>(u, a.sh + off, n, a.pspec + off, sm, tab);
   if (tid == 0) {
     st[b].alpha = alpha;
     st[b].snorm = snorm;
   }
+  return false;
 }
 
 // ---- BiCGSTAB t-phase (+ next p / p_hat)
 template <int N, int PC>
-__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
-k_bicg_t(KrylovArgs a, KState* st, int* active) {
-  extern __shared__ double2 sm[];
-  __shared__ double red[4 * 32];
+TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, int* active, double2* sm,
+                    double* red) {
   constexpr int T = KShape<N>::T;
   constexpr int E = KShape<N>::E;
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int b = blockIdx.x;
-  if (st[b].done) return;
-  a.tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(aux + N));
+  __syncthreads();  // previous phase's st[b] writes (thread 0) are visible
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
@@ -419,8 +413,8 @@ k_bicg_t(KrylovArgs a, KState* st, int* active) {
   const KState s = st[b];
   const double* shg = (PC ? a.sh : a.s) + off;
   const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
-  double u[kE];
-  apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, a.tab);   // u = t = M s_hat
+  double u[FShape<N>::E];
+  apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, tab);   // u = t = M s_hat
   Vals<2> red2;
   red2.v[0] = 0.0;
   red2.v[1] = 0.0;
@@ -437,7 +431,7 @@ k_bicg_t(KrylovArgs a, KState* st, int* active) {
   red2 = block_sum<2>(red2, red);
   if (red2.v[0] == 0.0) {
     finish_instance(a, st, active, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN);
-    return;
+    return true;
   }
   const double omega = red2.v[1] / red2.v[0];
   // x += alpha p_hat + omega s_hat ; r = s - omega t
@@ -463,20 +457,20 @@ k_bicg_t(KrylovArgs a, KState* st, int* active) {
   const double rel = rnorm / s.nrm0;
   if (rel < a.tol) {
     finish_instance(a, st, active, b, s.it, rel, TSF_OK);
-    return;
+    return true;
   }
   if (omega == 0.0) {
     finish_instance(a, st, active, b, s.it, rel, TSF_BD_OMEGA);
-    return;
+    return true;
   }
   if (s.it >= a.max_iters) {
     finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED);
-    return;
+    return true;
   }
   const double rho_new = red2.v[1];
   if (rho_new == 0.0) {  // the next iteration's first test (krylov.py:118-121)
     finish_instance(a, st, active, b, s.it + 1, rel, TSF_BD_RHO);
-    return;
+    return true;
   }
   // next p = r + beta (p - omega v)
   const double beta = (rho_new / s.rho_new) * (s.alpha / omega);
@@ -488,7 +482,7 @@ k_bicg_t(KrylovArgs a, KState* st, int* active) {
     }
   }
   store_owned<N>(a.p + off, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.ph + off, n, a.pspec + off, sm, a.tab);
+  if constexpr (PC == 1) precond_store<N>(u, a.ph + off, n, a.pspec + off, sm, tab);
   if (tid == 0) {
     st[b].rho = s.rho_new;
     st[b].rho_new = rho_new;
@@ -496,28 +490,26 @@ k_bicg_t(KrylovArgs a, KState* st, int* active) {
     st[b].rnorm = rnorm;
     st[b].it = s.it + 1;
   }
+  return false;
 }
 
 // ---- PCG iteration: q = M p, alpha, x, r, ||r||, z = P^{-1} r, beta, p
 template <int N, int PC>
-__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
-k_cg_iter(KrylovArgs a, KState* st, int* active) {
-  extern __shared__ double2 sm[];
-  __shared__ double red[4 * 32];
+TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st, int* active, double2* sm,
+                    double* red) {
   constexpr int T = KShape<N>::T;
   constexpr int E = KShape<N>::E;
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int b = blockIdx.x;
-  if (st[b].done) return;
-  a.tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(aux + N));
+  __syncthreads();  // previous phase's st[b] writes (thread 0) are visible
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
   const long off = (long)b * n;
   const KState s = st[b];
   const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
-  double u[kE];
-  apply_level_op<N>(a.p + off, kg, a.shift, n, u, sm, aux, a.tab);  // u = q = M p
+  double u[FShape<N>::E];
+  apply_level_op<N>(a.p + off, kg, a.shift, n, u, sm, aux, tab);  // u = q = M p
   double part = 0.0;
   if (own) {
 #pragma unroll
@@ -529,7 +521,7 @@ k_cg_iter(KrylovArgs a, KState* st, int* active) {
   const double curv = block_sum1(part, red);
   if (curv <= 0.0) {
     finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_CURVATURE);
-    return;
+    return true;
   }
   const double al = s.rz / curv;
   part = 0.0;
@@ -547,15 +539,15 @@ k_cg_iter(KrylovArgs a, KState* st, int* active) {
   const double rel = rnorm / s.nrm0;
   if (rel < a.tol) {
     finish_instance(a, st, active, b, s.it, rel, TSF_OK);
-    return;
+    return true;
   }
   if (s.it >= a.max_iters) {
     finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED);
-    return;
+    return true;
   }
   // z = P^{-1} r (into s), rz_new = r.z, p = z + beta p
   const double* zg = (PC ? a.s : a.r) + off;
-  if constexpr (PC == 1) precond_store<N>(u, a.s + off, n, a.pspec + off, sm, a.tab);
+  if constexpr (PC == 1) precond_store<N>(u, a.s + off, n, a.pspec + off, sm, tab);
   __syncthreads();
   part = 0.0;
   if (own) {
@@ -579,6 +571,56 @@ k_cg_iter(KrylovArgs a, KState* st, int* active) {
     st[b].rnorm = rnorm;
     st[b].it = s.it + 1;
   }
+  return false;
+}
+
+
+
+template <int N, int PC, bool CG>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
+k_solve_begin(KrylovArgs a, KState* st, int* active) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  const FilterTables tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(
+      reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES + N * 8));
+  dev_begin<N, PC, CG>(a, tab, st, active, sm, red);
+}
+
+#define TSF_PHASE_KERNEL(KNAME, DNAME)                                                  \
+  template <int N, int PC>                                                             \
+  __global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)           \
+  KNAME(KrylovArgs a, KState* st, int* active) {                                       \
+    extern __shared__ double2 sm[];                                                    \
+    __shared__ double red[4 * 32];                                                     \
+    if (st[blockIdx.x].done) return;                                                   \
+    const FilterTables tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(        \
+        reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES + N * 8));                  \
+    DNAME<N, PC>(a, tab, st, active, sm, red);                                         \
+  }
+TSF_PHASE_KERNEL(k_bicg_v, dev_bicg_v)
+TSF_PHASE_KERNEL(k_bicg_t, dev_bicg_t)
+TSF_PHASE_KERNEL(k_cg_iter, dev_cg_iter)
+#undef TSF_PHASE_KERNEL
+
+// Persistent per-instance solve: one CTA runs its instance from begin to
+// convergence (vectors stay L2-resident, no host round trip, and the GPU
+// back-fills SMs as instances finish — no tail of near-empty launches).
+template <int N, int PC, bool CG>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
+k_krylov_persist(KrylovArgs a, KState* st, int* active) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  const FilterTables tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(
+      reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES + N * 8));
+  if (dev_begin<N, PC, CG>(a, tab, st, active, sm, red)) return;
+  for (;;) {
+    if constexpr (!CG) {
+      if (dev_bicg_v<N, PC>(a, tab, st, active, sm, red)) return;
+      if (dev_bicg_t<N, PC>(a, tab, st, active, sm, red)) return;
+    } else {
+      if (dev_cg_iter<N, PC>(a, tab, st, active, sm, red)) return;
+    }
+  }
 }
 
 static __global__ void k_set_int(int* p, int v) { *p = v; }
@@ -591,7 +633,7 @@ __global__ void k_fft_debug(const double2* __restrict__ in, double2* __restrict_
   constexpr int T = N / E;
   const int tid = threadIdx.x;  // debug transform: E complex slots per thread
   const long off = (long)blockIdx.x * N;
-  double2* tws = sm + 2 * FftPlan<N, E>::SMEM_ELEMS;
+  double2* tws = sm + (kFftInPlace ? 1 : 2) * FftPlan<N, E>::SMEM_ELEMS;
   for (int i = tid; i < tw_table_elems(N); i += blockDim.x) tws[i] = ldt(&tw[i]);
   tw = tws;
   double2 v[E];
