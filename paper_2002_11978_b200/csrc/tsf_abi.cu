@@ -103,17 +103,17 @@ struct FftF {
   static int call(A... a) { return Dispatch<LOG>::fft(a...); }
 };
 
-// two-level twiddle table of W_N (tsf_fft.cuh tw_get): [W^j, j < 64] then
-// [W^(64 i), i < max(1, N/64)], computed in long double
+// two-level twiddle table of W_N (tsf_fft.cuh tw_get): padded [W^j, j < 64]
+// then [W^(64 i), i < max(1, N/64)], computed in long double
 std::vector<double2> twiddles(int N) {
   const long double two_pi = 6.283185307179586476925286766559005768L;
   auto w = [&](long e) {
     long double a = two_pi * (long double)(e % N) / (long double)N;
     return make_double2((double)cosl(a), (double)-sinl(a));
   };
-  std::vector<double2> t(tw_table_elems(N));
-  for (int j = 0; j < 64; ++j) t[j] = w(j);
-  for (int i = 0; i < (int)t.size() - 64; ++i) t[64 + i] = w(64L * i);
+  std::vector<double2> t(tw_table_elems(N), make_double2(0.0, 0.0));
+  for (int j = 0; j < 64; ++j) t[tw_lo_slot(j)] = w(j);
+  for (int i = 0; i < (int)t.size() - kTwLo; ++i) t[kTwLo + i] = w(64L * i);
   return t;
 }
 
@@ -357,37 +357,49 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
     if (d->events) CK(cudaEventRecord((cudaEvent_t)d->events[3 * (m - d->m_begin) + k], st));
     return TSF_SUCCESS;
   };
-  for (int m = d->m_begin; m < d->m_end; ++m) {
-    // ---- history term + RHS of level m from W^{m-1} (push of level m-1 fused)
-    if ((rc = rec(m, 0))) return rc;
+  // per-level SOE/RHS arguments: push of level `pm` (pm = 0: none) + history
+  // term and RHS of level `rm` (rm > M: none)
+  auto soe_args = [&](int pm, int rm) {
     SoeArgs s{};
     s.n = n;
     s.nexp = nexp;
     s.W = d->W;
-    s.u = ubuf[(m - 1) & 1];   // u^{m-1}
-    s.uprev = ubuf[m & 1];     // u^{m-2} (buffer about to receive u^m)
-    s.do_push = m > 1;
-    s.w_zero = (m == 1);
-    if (m > 1) {
-      const double* tab = d->soe_tab + (size_t)(m - 2) * 3 * nexp;
-      s.tau_push = d->tau[m - 2];
+    s.u = ubuf[(rm - 1) & 1];  // u^{rm-1} == u^{pm}
+    s.uprev = ubuf[rm & 1];    // u^{rm-2}
+    s.do_push = pm >= 1;
+    s.w_zero = (rm == 1) || (pm == 1);  // W^{0} = 0
+    if (pm >= 1) {
+      const double* tab = d->soe_tab + (size_t)(pm - 1) * 3 * nexp;
+      s.tau_push = d->tau[pm - 1];
       s.decay = tab;
       s.coef = tab + nexp;
     }
-    s.hcoef = d->soe_tab + (size_t)(m - 1) * 3 * nexp + 2 * nexp;
-    s.do_rhs = 1;
-    s.a_next = d->a_mm[m - 1];
+    s.do_rhs = rm <= M;
+    if (s.do_rhs) {
+      s.hcoef = d->soe_tab + (size_t)(rm - 1) * 3 * nexp + 2 * nexp;
+      s.a_next = d->a_mm[rm - 1];
+      s.nf = d->source.nmodes;
+      s.fmodes = d->source.modes ? d->source.modes + (size_t)rm * d->source.t_stride : nullptr;
+      s.fq_stride = d->source.q_stride;
+      s.fb_stride = d->source.b_stride;
+      for (int q = 0; q < s.nf; ++q) s.fcoef[q] = d->source.coef[(size_t)rm * s.nf + q];
+    }
     s.G = d->G;
-    s.nf = d->source.nmodes;
-    s.fmodes = d->source.modes ? d->source.modes + (size_t)m * d->source.t_stride : nullptr;
-    s.fq_stride = d->source.q_stride;
-    s.fb_stride = d->source.b_stride;
-    for (int q = 0; q < s.nf; ++q) s.fcoef[q] = d->source.coef[(size_t)m * s.nf + q];
     s.f = nullptr;
     s.rhs = d->rhs;
-    if ((rc = soe_launch(B, s, st))) return rc;
+    return s;
+  };
+  for (int m = d->m_begin; m < d->m_end; ++m) {
+    if ((rc = rec(m, 0))) return rc;
+    // RHS of level 1 (W = 0); every later RHS is produced by the previous
+    // level's fused epilogue
+    if (m == 1) {
+      SoeArgs s = soe_args(0, 1);
+      if ((rc = soe_launch(B, s, st))) return rc;
+    }
     if ((rc = rec(m, 1))) return rc;
-    // ---- level solve  -> u^m into ubuf[m & 1]
+    // ---- level solve -> u^m into ubuf[m & 1]; each converged instance then
+    // streams its own W rows: push of level m, history term + RHS of level m+1
     KrylovArgs a{};
     a.rhs = d->rhs;
     a.x = ubuf[m & 1];
@@ -404,30 +416,14 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
     a.iters = d->iters + (size_t)(m - 1) * B;
     a.relres = d->relres + (size_t)(m - 1) * B;
     a.status = d->status + (size_t)(m - 1) * B;
+    a.soe = soe_args(m, m + 1);
+    a.soe_epilogue = 1;
     if ((rc = solve_impl(p, B, d->method, d->precond, a, st))) return rc;
     if ((rc = rec(m, 2))) return rc;
     if (d->hist && d->hist_B > 0) {
       CK(cudaMemcpyAsync(d->hist + (size_t)m * d->hist_B * n, ubuf[m & 1],
                          sizeof(double) * (size_t)d->hist_B * n, cudaMemcpyDeviceToDevice, st));
     }
-  }
-  if (d->m_end == M + 1 && d->m_begin <= M) {
-    // final push of level M (scheme.py:290 runs after every level)
-    const double* tab = d->soe_tab + (size_t)(M - 1) * 3 * nexp;
-    SoeArgs s{};
-    s.n = n;
-    s.nexp = nexp;
-    s.W = d->W;
-    s.u = ubuf[M & 1];
-    s.uprev = ubuf[(M - 1) & 1];
-    s.do_push = 1;
-    s.w_zero = (M == 1) ? 1 : 0;
-    s.tau_push = d->tau[M - 1];
-    s.decay = tab;
-    s.coef = tab + nexp;
-    s.hcoef = nullptr;
-    s.do_rhs = 0;
-    if ((rc = soe_launch(B, s, st))) return rc;
   }
   (void)vn;
   return TSF_SUCCESS;

@@ -148,9 +148,9 @@ TSF_D void dft(double2* a) {
 
 // ------------------------------------------------------------ twiddles
 // Two-level table staged in shared memory by every kernel:
-//   tw[j]        = W^j,       j < 64
-//   tw[64 + i]   = W^(64 i),  i < max(1, NT/64)
-// so W^e = tw[64 + (e >> 6)] * tw[e & 63] (within ~1 ulp; both factors are
+//   tw[lo_slot(j)] = W^j,       j < 64
+//   tw[72 + i]     = W^(64 i),  i < max(1, NT/64)
+// so W^e = hi[e >> 6] * lo[e & 63] (within ~1 ulp; both factors are
 // correctly rounded long-double values).  A full table of NT entries (128 KB
 // at NT = 8192) does not fit the L1 left beside the transform buffers, and
 // streaming it from L2 was the main stall of the first solve kernels
@@ -160,8 +160,15 @@ TSF_D void dft(double2* a) {
 // no mid-pass barrier.  See DESIGN.md §3.1.
 constexpr bool kFftInPlace = TSF_FFT_INPLACE;
 
-TSF_HD constexpr int tw_table_elems(int NT) { return 64 + (NT / 64 > 1 ? NT / 64 : 1); }
-TSF_D double2 tw_get(const double2* tw, int e) { return cmul(tw[64 + (e >> 6)], tw[e & 63]); }
+// The 64-entry low table is stored padded, slot i at i + (i >> 3): the
+// W^{2k}, W^{4k}, W^{8k} lookups of a warp then hit distinct banks (unpadded
+// they were 2/4/8-way conflicts, 28% of all shared wavefronts in ncu).
+constexpr int kTwLo = 72;
+TSF_HD constexpr int tw_lo_slot(int j) { return j + (j >> 3); }
+TSF_HD constexpr int tw_table_elems(int NT) { return kTwLo + (NT / 64 > 1 ? NT / 64 : 1); }
+TSF_D double2 tw_get(const double2* tw, int e) {
+  return cmul(tw[kTwLo + (e >> 6)], tw[tw_lo_slot(e & 63)]);
+}
 
 // ------------------------------------------------------------ pass plan
 constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }

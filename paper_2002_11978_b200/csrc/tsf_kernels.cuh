@@ -18,6 +18,7 @@
 #pragma once
 
 #include "tsf_filters.cuh"
+#include "tsf_soe.cuh"
 
 namespace tsf {
 
@@ -52,6 +53,8 @@ struct KrylovArgs {
   double* t;
   double* pspec;            // [B, n] Strang spectrum S_k / n of the level (PC == 1)
   KState* kst;              // [B] per-instance Krylov scalars (phase kernels)
+  SoeArgs soe;              // fused SOE epilogue of converged instances (march)
+  int soe_epilogue;         // 1: run it
   int* active;              // device counter of unfinished instances
   int* h_active;            // pinned host mirror of *active (driver polling)
   int* iters;               // per-instance outputs
@@ -208,7 +211,7 @@ TSF_D void precond_store(const double (&u)[FShape<N>::E], double* dst, int n, co
 }
 
 TSF_D void finish_instance(const KrylovArgs& a, KState* st, int* active, int b, int it,
-                           double rel, int status) {
+                           double rel, int status, double2* sm) {
   if (threadIdx.x == 0) {
     a.iters[b] = it;
     a.relres[b] = rel;
@@ -216,6 +219,8 @@ TSF_D void finish_instance(const KrylovArgs& a, KState* st, int* active, int b, 
     st[b].done = 1;
     atomicSub(active, 1);
   }
+  if (status == TSF_OK && a.soe_epilogue)
+    soe_instance_epilogue(a.soe, reinterpret_cast<double*>(sm), b);
 }
 
 // ---- begin (both methods)
@@ -257,7 +262,7 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
   }
   kmin = block_min1(kmin, red);
   if (kmin <= 0.0) {
-    finish_instance(a, st, active, b, 0, 0.0, TSF_KAPPA_NONPOS);
+    finish_instance(a, st, active, b, 0, 0.0, TSF_KAPPA_NONPOS, sm);
     return true;
   }
   const double kmean = block_sum1(ksum, red) / n;
@@ -269,7 +274,7 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
     for (int k = tid; k < n; k += blockDim.x) tmin = fmin(tmin, d + kbar * ldt(&tab.pclam[k]).x);
     tmin = block_min1(tmin, red);
     if (tmin <= 0.0) {
-      finish_instance(a, st, active, b, 0, 0.0, TSF_PRECOND_NONPOS);
+      finish_instance(a, st, active, b, 0, 0.0, TSF_PRECOND_NONPOS, sm);
       return true;
     }
     // the level's Strang filter (even part of 1/total, 1/n folded in), once
@@ -296,7 +301,7 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
   }
   ss = block_sum1(ss, red);
   if (sqrt(ss) == 0.0) {
-    finish_instance(a, st, active, b, 0, 0.0, TSF_OK);
+    finish_instance(a, st, active, b, 0, 0.0, TSF_OK, sm);
     return true;
   }
   if (CG) store_owned<N>(a.r + off, u, n);        // r = b
@@ -360,7 +365,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   }
   const double denom = block_sum1(part, red);
   if (denom == 0.0) {
-    finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_R0V);
+    finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_R0V, sm);
     return true;
   }
   const double alpha = s.rho_new / denom;
@@ -385,7 +390,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
         st_real(a.x + off, n, j, ld_real(a.x + off, n, j) + alpha * ld_real(phg, n, j));
       }
     }
-    finish_instance(a, st, active, b, s.it, snorm / s.nrm0, TSF_OK);
+    finish_instance(a, st, active, b, s.it, snorm / s.nrm0, TSF_OK, sm);
     return true;
   }
   store_owned<N>(a.s + off, u, n);
@@ -430,7 +435,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   }
   red2 = block_sum<2>(red2, red);
   if (red2.v[0] == 0.0) {
-    finish_instance(a, st, active, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN);
+    finish_instance(a, st, active, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN, sm);
     return true;
   }
   const double omega = red2.v[1] / red2.v[0];
@@ -456,20 +461,20 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   const double rnorm = sqrt(red2.v[0]);
   const double rel = rnorm / s.nrm0;
   if (rel < a.tol) {
-    finish_instance(a, st, active, b, s.it, rel, TSF_OK);
+    finish_instance(a, st, active, b, s.it, rel, TSF_OK, sm);
     return true;
   }
   if (omega == 0.0) {
-    finish_instance(a, st, active, b, s.it, rel, TSF_BD_OMEGA);
+    finish_instance(a, st, active, b, s.it, rel, TSF_BD_OMEGA, sm);
     return true;
   }
   if (s.it >= a.max_iters) {
-    finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED);
+    finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED, sm);
     return true;
   }
   const double rho_new = red2.v[1];
   if (rho_new == 0.0) {  // the next iteration's first test (krylov.py:118-121)
-    finish_instance(a, st, active, b, s.it + 1, rel, TSF_BD_RHO);
+    finish_instance(a, st, active, b, s.it + 1, rel, TSF_BD_RHO, sm);
     return true;
   }
   // next p = r + beta (p - omega v)
@@ -520,7 +525,7 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   }
   const double curv = block_sum1(part, red);
   if (curv <= 0.0) {
-    finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_CURVATURE);
+    finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_CURVATURE, sm);
     return true;
   }
   const double al = s.rz / curv;
@@ -538,11 +543,11 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   const double rnorm = sqrt(block_sum1(part, red));
   const double rel = rnorm / s.nrm0;
   if (rel < a.tol) {
-    finish_instance(a, st, active, b, s.it, rel, TSF_OK);
+    finish_instance(a, st, active, b, s.it, rel, TSF_OK, sm);
     return true;
   }
   if (s.it >= a.max_iters) {
-    finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED);
+    finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED, sm);
     return true;
   }
   // z = P^{-1} r (into s), rz_new = r.z, p = z + beta p

@@ -49,22 +49,21 @@ struct SoeArgs {
   double* rhs;            // [B][n]
 };
 
-template <int UNROLL>
-__global__ void __launch_bounds__(kSoeThreads)
-k_soe_push_rhs(SoeArgs a) {
-  extern __shared__ double tabs[];  // 3*nexp: decay, coef, hcoef
-  const int n = a.n;
+// Per-level coefficient rows into shared memory: decay | coef | hcoef.
+TSF_D void soe_load_tabs(const SoeArgs& a, double* tabs) {
   const int nexp = a.nexp;
   for (int j = threadIdx.x; j < nexp; j += blockDim.x) {
     tabs[j] = a.decay ? a.decay[j] : 0.0;
     tabs[nexp + j] = a.coef ? a.coef[j] : 0.0;
     tabs[2 * nexp + j] = a.hcoef ? a.hcoef[j] : 0.0;
   }
-  __syncthreads();
-  const int chunks = (n + 2 * kSoeThreads - 1) / (2 * kSoeThreads);
-  const int b = blockIdx.x / chunks;
-  const int i0 = 2 * ((blockIdx.x % chunks) * kSoeThreads + threadIdx.x);
-  if (i0 >= n) return;
+}
+
+// The whole update for grid points i0, i0+1 of instance b.
+template <int UNROLL>
+TSF_D void soe_pair(const SoeArgs& a, const double* tabs, int b, int i0) {
+  const int n = a.n;
+  const int nexp = a.nexp;
   const bool pair = (i0 + 1 < n) && ((n & 1) == 0);
   const long vbase = (long)b * n + i0;
   auto ld2 = [&](const double* p) -> double2 {
@@ -157,6 +156,29 @@ k_soe_push_rhs(SoeArgs a) {
       if (i0 + 1 < n) a.rhs[vbase + 1] = r.y;
     }
   }
+}
+
+template <int UNROLL>
+__global__ void __launch_bounds__(kSoeThreads)
+k_soe_push_rhs(SoeArgs a) {
+  extern __shared__ double tabs[];  // 3*nexp: decay, coef, hcoef
+  soe_load_tabs(a, tabs);
+  __syncthreads();
+  const int chunks = (a.n + 2 * kSoeThreads - 1) / (2 * kSoeThreads);
+  const int b = blockIdx.x / chunks;
+  const int i0 = 2 * ((blockIdx.x % chunks) * kSoeThreads + threadIdx.x);
+  if (i0 >= a.n) return;
+  soe_pair<UNROLL>(a, tabs, b, i0);
+}
+
+// Epilogue of a converged instance's level solve (the instance's CTA streams
+// its own W rows: push of this level + history term/RHS of the next one), so
+// the HBM-bound SOE pass overlaps other instances' transform work.
+TSF_D void soe_instance_epilogue(const SoeArgs& a, double* tabs, int b) {
+  __syncthreads();  // the solve's final x writes and last uses of `tabs` memory
+  soe_load_tabs(a, tabs);
+  __syncthreads();
+  for (int i0 = 2 * threadIdx.x; i0 < a.n; i0 += 2 * blockDim.x) soe_pair<4>(a, tabs, b, i0);
 }
 
 }  // namespace tsf
