@@ -1,6 +1,7 @@
 // C ABI of the tsfrac B200 engine: plans, tables, dispatch, native march.
 // Declarations and reference mapping: include/tsfrac_b200.h.
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -389,12 +390,18 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
     s.rhs = d->rhs;
     return s;
   };
+  // TSF_FUSE_SOE=1: each converged instance's CTA streams its own W rows at
+  // the end of its solve (push of level m + RHS of level m+1).  Measured
+  // slower on configs[2] (the 512-thread solve CTA holds the whole register
+  // file, so the streaming cannot overlap transform work on that SM), hence
+  // off by default: one SOE kernel per level.
+  const char* fz = getenv("TSF_FUSE_SOE");
+  const bool fuse = fz && fz[0] == '1';
   for (int m = d->m_begin; m < d->m_end; ++m) {
     if ((rc = rec(m, 0))) return rc;
-    // RHS of level 1 (W = 0); every later RHS is produced by the previous
-    // level's fused epilogue
-    if (m == 1) {
-      SoeArgs s = soe_args(0, 1);
+    if (m == 1 || !fuse) {
+      // push of level m-1 (fused with the history term) + RHS of level m
+      SoeArgs s = soe_args(m - 1, m);
       if ((rc = soe_launch(B, s, st))) return rc;
     }
     if ((rc = rec(m, 1))) return rc;
@@ -417,13 +424,18 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
     a.relres = d->relres + (size_t)(m - 1) * B;
     a.status = d->status + (size_t)(m - 1) * B;
     a.soe = soe_args(m, m + 1);
-    a.soe_epilogue = 1;
+    a.soe_epilogue = fuse ? 1 : 0;
     if ((rc = solve_impl(p, B, d->method, d->precond, a, st))) return rc;
     if ((rc = rec(m, 2))) return rc;
     if (d->hist && d->hist_B > 0) {
       CK(cudaMemcpyAsync(d->hist + (size_t)m * d->hist_B * n, ubuf[m & 1],
                          sizeof(double) * (size_t)d->hist_B * n, cudaMemcpyDeviceToDevice, st));
     }
+  }
+  if (!fuse && d->m_end == M + 1 && d->m_begin <= M) {
+    // final push of level M (scheme.py:290 runs after every level)
+    SoeArgs s = soe_args(M, M + 1);
+    if ((rc = soe_launch(B, s, st))) return rc;
   }
   (void)vn;
   return TSF_SUCCESS;
