@@ -5,7 +5,8 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr
 PKG := paper_2002_11978_b200
 CSRC := $(PKG)/csrc
-SRCS := $(CSRC)/tsf_abi.cu $(wildcard $(CSRC)/gen/inst_L*.cu)
+SRCS := $(CSRC)/tsf_abi.cu $(CSRC)/tsf_large.cu $(wildcard $(CSRC)/gen/inst_L*.cu) \
+        $(wildcard $(CSRC)/gen/large_L*.cu)
 OBJS := $(patsubst $(CSRC)/%.cu,build/obj/%.o,$(SRCS))
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/tsfrac_b200.h
 LIB := $(PKG)/libtsfrac_b200.so

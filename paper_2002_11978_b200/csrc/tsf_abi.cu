@@ -10,6 +10,7 @@
 
 #include "../../include/tsfrac_b200.h"
 #include "tsf_dispatch.h"
+#include "tsf_large_api.h"
 #include "tsf_soe.cuh"
 
 using namespace tsf;
@@ -49,6 +50,21 @@ namespace tsf {
 int report_cuda(cudaError_t e, const char* what) {
   return fail(TSF_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
+int report_error(int code, const char* msg) { return fail(code, "%s", msg); }
+
+// two-level twiddle table of W_N (tsf_fft.cuh tw_get): padded [W^j, j < 64]
+// then [W^(64 i), i < max(1, N/64)], computed in long double
+std::vector<double2> twiddle_table(int N) {
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  auto w = [&](long e) {
+    long double a = two_pi * (long double)(e % N) / (long double)N;
+    return make_double2((double)cosl(a), (double)-sinl(a));
+  };
+  std::vector<double2> t(tw_table_elems(N), make_double2(0.0, 0.0));
+  for (int j = 0; j < 64; ++j) t[tw_lo_slot(j)] = w(j);
+  for (int i = 0; i < (int)t.size() - kTwLo; ++i) t[kTwLo + i] = w(64L * i);
+  return t;
+}
 }  // namespace tsf
 
 struct tsf_plan {
@@ -67,6 +83,7 @@ struct tsf_plan {
   double* dst = nullptr;
   KState* kst = nullptr;    // per-instance Krylov scalars
   int* h_active = nullptr;  // pinned host mirror of the counter
+  LargePlan* large = nullptr;  // n > 4096: four-step engine (tsf_large.cu)
   FilterTables tables() const { return FilterTables{tw, mvS, pclam}; }
 };
 
@@ -104,22 +121,13 @@ struct FftF {
   static int call(A... a) { return Dispatch<LOG>::fft(a...); }
 };
 
-// two-level twiddle table of W_N (tsf_fft.cuh tw_get): padded [W^j, j < 64]
-// then [W^(64 i), i < max(1, N/64)], computed in long double
-std::vector<double2> twiddles(int N) {
-  const long double two_pi = 6.283185307179586476925286766559005768L;
-  auto w = [&](long e) {
-    long double a = two_pi * (long double)(e % N) / (long double)N;
-    return make_double2((double)cosl(a), (double)-sinl(a));
-  };
-  std::vector<double2> t(tw_table_elems(N), make_double2(0.0, 0.0));
-  for (int j = 0; j < 64; ++j) t[tw_lo_slot(j)] = w(j);
-  for (int i = 0; i < (int)t.size() - kTwLo; ++i) t[kTwLo + i] = w(64L * i);
-  return t;
-}
-
 
 int ensure_reserved(tsf_plan* p, int B) {
+  if (p->large) {
+    const int rc = large_reserve(p->large, B);
+    if (rc == TSF_SUCCESS) p->cap = p->large->cap;
+    return rc;
+  }
   if (B <= p->cap) return TSF_SUCCESS;
   if (p->ws) cudaFree(p->ws);
   if (p->ist) cudaFree(p->ist);
@@ -158,8 +166,28 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
     return fail(TSF_E_INVALID, "L=%d must be a power of two >= max(2n-1, 32)", L);
   if (!symbol_re) return fail(TSF_E_INVALID, "symbol is NULL");
   const int lg = ilog2_host(L);
-  if (lg < kMinLogL || lg > kMaxLogL)
-    return fail(TSF_E_UNSUPPORTED, "embedding L=%d outside the single-CTA engine (32..8192, n <= 4096)", L);
+  if (lg > kMaxLogL) {
+    // four-step engine: pow2 n in [2^13, 2^24] with L = 2n
+    if (!(is_pow2(n) && L == 2 * n))
+      return fail(TSF_E_UNSUPPORTED,
+                  "n=%d > 4096 needs a power of two n with L = 2n (got L=%d)", n, L);
+    tsf_plan* p = new tsf_plan();
+    p->n = n;
+    p->L = L;
+    p->log_L = lg;
+    p->device = device;
+    p->has_pc = lam != nullptr;
+    p->large = new LargePlan();
+    const int rc = large_plan_init(p->large, n, symbol_re, lam, device);
+    if (rc) {
+      tsf_plan_destroy(p);
+      return rc;
+    }
+    *out = p;
+    return TSF_SUCCESS;
+  }
+  if (lg < kMinLogL)
+    return fail(TSF_E_UNSUPPORTED, "embedding L=%d below 32", L);
   if (lam && !(is_pow2(n) && n >= 16 && L == 2 * n))
     return fail(TSF_E_UNSUPPORTED, "Strang preconditioner needs pow2 n >= 16 with L = 2n (n=%d, L=%d)", n, L);
   tsf_plan* p = new tsf_plan();
@@ -174,7 +202,7 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
   };
   if (cudaSetDevice(device) != cudaSuccess) return cleanup(fail(TSF_E_CUDA, "cudaSetDevice(%d)", device));
   // twiddles W_L^e: modulation of the odd-bin half; the length-N transforms use stride 2
-  std::vector<double2> tw = twiddles(L);
+  std::vector<double2> tw = twiddle_table(L);
   // The reference keeps Re IFFT(S . FFT(pad x)) (toeplitz.py:62-63): its
   // effective symbol is the even part of S.  1/L of the inverse folded in;
   // stored as (S_{2k}, S_{2k+1}) for the even / odd output-bin halves.
@@ -205,6 +233,10 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
 int tsf_plan_destroy(tsf_plan* p) {
   if (!p) return TSF_SUCCESS;
   cudaSetDevice(p->device);
+  if (p->large) {
+    large_plan_free(p->large);
+    delete p->large;
+  }
   cudaFree(p->tw);
   cudaFree(p->mvS);
   cudaFree(p->pclam);
@@ -236,6 +268,7 @@ int tsf_toeplitz_matvec(tsf_plan* p, int B, const double* x, double* y, const do
                         double shift, void* stream) {
   if (!p || !x || !y || B < 0) return fail(TSF_E_INVALID, "bad argument");
   if (B == 0) return TSF_SUCCESS;
+  if (p->large) return large_matvec(p->large, B, x, y, kappa, shift, (cudaStream_t)stream);
   return ForLog<MatvecF>::run(p->log_L, p->n, p->tables(), B, x, y, kappa, shift,
                               (cudaStream_t)stream);
 }
@@ -245,12 +278,20 @@ int tsf_precond_solve(tsf_plan* p, int B, const double* v, double* z, double shi
   if (!p || !v || !z || B < 0) return fail(TSF_E_INVALID, "bad argument");
   if (!p->has_pc) return fail(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner (non-pow2 n)");
   if (B == 0) return TSF_SUCCESS;
+  if (p->large)
+    return large_precond(p->large, B, v, z, shift, kbar, kbar_dev, (cudaStream_t)stream);
   return ForLog<PrecondF>::run(p->log_L, p->n, p->tables(), B, v, z, shift, kbar, kbar_dev,
                                (cudaStream_t)stream);
 }
 
 static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cudaStream_t st) {
   if (pc && !p->has_pc) return fail(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner");
+  if (p->large) {
+    if (a.soe_epilogue) return fail(TSF_E_UNSUPPORTED, "fused SOE epilogue needs n <= 4096");
+    a.n = p->n;
+    a.B = B;
+    return large_solve(p->large, B, method, pc, a, st);
+  }
   int rc = ensure_reserved(p, B);
   if (rc) return rc;
   const size_t vn = (size_t)p->cap * p->n;
@@ -396,7 +437,7 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
   // file, so the streaming cannot overlap transform work on that SM), hence
   // off by default: one SOE kernel per level.
   const char* fz = getenv("TSF_FUSE_SOE");
-  const bool fuse = fz && fz[0] == '1';
+  const bool fuse = fz && fz[0] == '1' && !p->large;
   for (int m = d->m_begin; m < d->m_end; ++m) {
     if ((rc = rec(m, 0))) return rc;
     if (m == 1 || !fuse) {
@@ -447,7 +488,7 @@ int tsf_fft_debug(int N, int inverse, int B, const double* in, double* out, void
   const int lg = ilog2_host(N) + 1;  // Dispatch<LOG> transforms N = 2^(LOG-1)
   static double2* dtw[kMaxLogL + 2] = {};
   if (!dtw[lg]) {
-    std::vector<double2> t = twiddles(N);
+    std::vector<double2> t = twiddle_table(N);
     CK(cudaMalloc(&dtw[lg], t.size() * sizeof(double2)));
     CK(cudaMemcpy(dtw[lg], t.data(), t.size() * sizeof(double2), cudaMemcpyHostToDevice));
   }

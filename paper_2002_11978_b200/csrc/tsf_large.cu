@@ -1,0 +1,548 @@
+// Large-n engine (n = 2^13 .. 2^24): tables, Krylov scalar / elementwise
+// kernels and the host drivers.  Transform kernels: tsf_large.cuh.
+//
+// One BiCGSTAB iteration (krylov.py:88-153) for B instances is a fixed
+// launch sequence; every kernel returns at once for instances whose LState
+// says they finished, so the host launches whole chunks of iterations and
+// polls the device count of unfinished instances between chunks (as the
+// single-CTA engine does, tsf_dispatch_impl.cuh):
+//   1  p_hat = P^{-1} p      col_fwd(p update) . row(Strang) . col_inv
+//   2  v = M p_hat           even filter (3 kernels) + odd filter/combine (3)
+//   3  alpha                 scalar kernel (r0.v from the combine partials)
+//   4  s_hat = P^{-1} s      col_fwd(s = r - alpha v, ||s||^2) . row . col_inv
+//   5  ||s||, early exit      scalar kernel
+//   6  t = M s_hat           6 kernels (t.t, t.s partials)
+//   7  omega                 scalar kernel
+//   8  x, r update           elementwise (||r||^2, r0.r partials)
+//   9  convergence, rho      scalar kernel
+// Without the preconditioner steps 1/4 are elementwise kernels.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "../../include/tsfrac_b200.h"
+#include "tsf_dispatch.h"
+#include "tsf_large_api.h"
+
+namespace tsf {
+namespace {
+
+constexpr int kLelThreads = 256;
+constexpr int kLelPer = 4;
+constexpr int kLelChunk = kLelThreads * kLelPer;  // elements per elementwise CTA
+constexpr int kLscThreads = 256;
+constexpr int kLargeChunk = 4;  // iterations launched between completion polls
+
+enum LStage : int { LS_BEGIN = 0, LS_ALPHA = 1, LS_SNORM = 2, LS_OMEGA = 3, LS_REL = 4 };
+
+TSF_D double* pslot(const LargeArgs& a, int b, int slot) {
+  return a.part + ((long)b * 4 + slot) * a.np;
+}
+
+TSF_D void lfinish(const LargeArgs& a, int b, int it, double rel, int status) {
+  a.iters[b] = it;
+  a.relres[b] = rel;
+  a.status[b] = status;
+  a.st[b].mode = LM_DONE;
+  atomicSub(a.active, 1);
+}
+
+// ---- elementwise kernels: grid (n / kLelChunk, B)
+
+// kappa on the grid (scheme.py:156-160,280), x = 0, partials: sum kappa,
+// min kappa, ||r0||^2
+__global__ void __launch_bounds__(kLelThreads) k_lel_begin(LargeArgs a, KrylovArgs k) {
+  __shared__ double red[4 * 32];
+  const int b = blockIdx.y, tid = threadIdx.x;
+  const long off = (long)b * a.n;
+  double ksum = 0.0, kmin = 1e308, ss = 0.0;
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long j = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    double kv;
+    if (k.kappa) {
+      kv = k.kappa[off + j];
+    } else {
+      kv = 0.0;
+      for (int q = 0; q < k.nk; ++q) {
+        const double mq = k.kmodes[q * k.kq_stride + (long)b * k.kb_stride + j];
+        kv = __dadd_rn(kv, __dmul_rn(mq, k.kcoef[q]));  // numpy's acc + mode*coef
+      }
+      k.kwork[off + j] = kv;
+    }
+    ksum += kv;
+    kmin = fmin(kmin, kv);
+    a.x[off + j] = 0.0;
+    const double r = a.r0[off + j];
+    ss = fma(r, r, ss);
+  }
+  Vals<2> v;
+  v.v[0] = ksum;
+  v.v[1] = ss;
+  v = block_sum<2>(v, red);
+  kmin = block_min1(kmin, red);
+  if (tid == 0) {
+    pslot(a, b, 0)[blockIdx.x] = v.v[0];
+    pslot(a, b, 1)[blockIdx.x] = kmin;
+    pslot(a, b, 2)[blockIdx.x] = v.v[1];
+  }
+}
+
+// p = r0 (it 1) or r + beta (p - omega v)   (no preconditioner: p_hat = p)
+__global__ void __launch_bounds__(kLelThreads) k_lel_pupd(LargeArgs a) {
+  const int b = blockIdx.y, tid = threadIdx.x;
+  if (inst_skip(a, b)) return;
+  const long off = (long)b * a.n;
+  const LState s = a.st[b];
+  const double beta = s.it == 1 ? 0.0 : (s.rho_new / s.rho) * (s.alpha / s.omega);
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long j = off + (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    a.p[j] = s.it == 1 ? a.r0[j] : a.r[j] + beta * (a.p[j] - s.omega * a.v[j]);
+  }
+}
+
+// s = r - alpha v, ||s||^2 partial (slot 2)
+__global__ void __launch_bounds__(kLelThreads) k_lel_supd(LargeArgs a) {
+  __shared__ double red[4 * 32];
+  const int b = blockIdx.y, tid = threadIdx.x;
+  if (inst_skip(a, b)) return;
+  const long off = (long)b * a.n;
+  const LState s = a.st[b];
+  const double* rc = s.it == 1 ? a.r0 : a.r;
+  double ss = 0.0;
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long j = off + (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const double v = rc[j] - s.alpha * a.v[j];
+    a.s[j] = v;
+    ss = fma(v, v, ss);
+  }
+  ss = block_sum1(ss, red);
+  if (tid == 0) pslot(a, b, 2)[blockIdx.x] = ss;
+}
+
+// x += alpha p_hat + omega s_hat ; r = s - omega t ; partials ||r||^2, r0.r
+// (early-exit instances: x += alpha p_hat only)
+__global__ void __launch_bounds__(kLelThreads) k_lel_xr(LargeArgs a, const double* __restrict__ ph,
+                                                        const double* __restrict__ sh) {
+  __shared__ double red[4 * 32];
+  const int b = blockIdx.y, tid = threadIdx.x;
+  const LState s = a.st[b];
+  if (s.mode == LM_DONE) return;
+  const long off = (long)b * a.n;
+  if (s.mode == LM_EARLY) {
+#pragma unroll
+    for (int c = 0; c < kLelPer; ++c) {
+      const long j = off + (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+      a.x[j] = a.x[j] + s.alpha * ph[j];
+    }
+    return;
+  }
+  Vals<2> v;
+  v.v[0] = v.v[1] = 0.0;
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long j = off + (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    a.x[j] = a.x[j] + (s.alpha * ph[j] + s.omega * sh[j]);
+    const double r = a.s[j] - s.omega * a.t[j];
+    a.r[j] = r;
+    v.v[0] = fma(r, r, v.v[0]);
+    v.v[1] = fma(a.r0[j], r, v.v[1]);
+  }
+  v = block_sum<2>(v, red);
+  if (tid == 0) {
+    pslot(a, b, 0)[blockIdx.x] = v.v[0];
+    pslot(a, b, 1)[blockIdx.x] = v.v[1];
+  }
+}
+
+// The level's Strang filter, permuted like the row spectra:
+// pspec[k1 N2 + k2] = even part of 1/(d + kbar lam_k) / n at k = k1 + N1 k2
+__global__ void __launch_bounds__(kLelThreads) k_lspec(LargeArgs a, double kbar,
+                                                       const double* __restrict__ kbar_dev,
+                                                       int use_state) {
+  const int b = blockIdx.y, tid = threadIdx.x;
+  double kb = kbar;
+  if (use_state) {
+    if (inst_skip(a, b)) return;
+    kb = a.st[b].kbar;
+  } else if (kbar_dev) {
+    kb = kbar_dev[b];
+  }
+  const double d = a.shift;
+  const double inv_n = 1.0 / a.n;
+  const long off = (long)b * a.n;
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long idx = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const double2 lam = ldt(&a.lt.lamP[idx]);
+    a.pspec[off + idx] = 0.5 * (1.0 / (d + kb * lam.x) + 1.0 / (d + kb * lam.y)) * inv_n;
+  }
+}
+
+// ---- scalar kernel: one CTA per instance, partial sums in fixed order
+TSF_D double psum(const LargeArgs& a, int b, int slot, int count, double* red) {
+  const double* p = pslot(a, b, slot);
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += p[i];
+  return block_sum1(s, red);
+}
+
+__global__ void __launch_bounds__(kLscThreads) k_lsc(LargeArgs a, int stage, int count,
+                                                     double kbar_in, double lam_min, int pc) {
+  __shared__ double red[4 * 32];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (stage == LS_BEGIN) {
+    const double* pm = pslot(a, b, 1);
+    double kmin = 1e308;
+    for (int i = tid; i < count; i += blockDim.x) kmin = fmin(kmin, pm[i]);
+    kmin = block_min1(kmin, red);
+    const double ksum = psum(a, b, 0, count, red);
+    const double ss = psum(a, b, 2, count, red);
+    if (tid != 0) return;
+    LState s{};
+    s.mode = LM_ACTIVE;
+    a.st[b] = s;
+    if (kmin <= 0.0) return lfinish(a, b, 0, 0.0, TSF_KAPPA_NONPOS);
+    const double kbar = kbar_in > 0.0 ? kbar_in : ksum / a.n;
+    // total eigenvalues d + kbar lam > 0 (toeplitz.py:122-124); monotone in lam
+    if (pc && a.shift + kbar * lam_min <= 0.0) return lfinish(a, b, 0, 0.0, TSF_PRECOND_NONPOS);
+    if (sqrt(ss) == 0.0) return lfinish(a, b, 0, 0.0, TSF_OK);
+    s.rho = s.alpha = s.omega = 1.0;
+    s.rho_new = ss;
+    s.nrm0 = s.rnorm = s.snorm = sqrt(ss);
+    s.kbar = kbar;
+    s.it = 1;
+    s.mode = LM_ACTIVE;
+    a.st[b] = s;
+    return;
+  }
+  const LState s = a.st[b];
+  if (s.mode == LM_DONE) return;
+  if (stage == LS_ALPHA) {
+    if (s.mode != LM_ACTIVE) return;
+    const double denom = psum(a, b, 1, count, red);
+    if (tid != 0) return;
+    if (denom == 0.0) return lfinish(a, b, s.it, s.rnorm / s.nrm0, TSF_BD_R0V);
+    a.st[b].alpha = s.rho_new / denom;
+  } else if (stage == LS_SNORM) {
+    if (s.mode != LM_ACTIVE) return;
+    const double snorm = sqrt(psum(a, b, 2, count, red));
+    if (tid != 0) return;
+    a.st[b].snorm = snorm;
+    if (snorm / s.nrm0 < a.tol) a.st[b].mode = LM_EARLY;  // krylov.py:135-137
+  } else if (stage == LS_OMEGA) {
+    if (s.mode != LM_ACTIVE) return;
+    const double tt = psum(a, b, 0, count, red);
+    const double ts = psum(a, b, 1, count, red);
+    if (tid != 0) return;
+    if (tt == 0.0) return lfinish(a, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN);
+    a.st[b].omega = ts / tt;
+  } else {  // LS_REL
+    if (s.mode == LM_EARLY) {
+      if (tid == 0) lfinish(a, b, s.it, s.snorm / s.nrm0, TSF_OK);
+      return;
+    }
+    const double rr = psum(a, b, 0, count, red);
+    const double rho_new = psum(a, b, 1, count, red);
+    if (tid != 0) return;
+    const double rnorm = sqrt(rr);
+    const double rel = rnorm / s.nrm0;
+    if (rel < a.tol) return lfinish(a, b, s.it, rel, TSF_OK);
+    if (s.omega == 0.0) return lfinish(a, b, s.it, rel, TSF_BD_OMEGA);
+    if (s.it >= a.max_iters) return lfinish(a, b, a.max_iters, rel, TSF_NOT_CONVERGED);
+    if (rho_new == 0.0) return lfinish(a, b, s.it + 1, rel, TSF_BD_RHO);  // krylov.py:118-121
+    LState u = s;
+    u.rho = s.rho_new;
+    u.rho_new = rho_new;
+    u.rnorm = rnorm;
+    u.it = s.it + 1;
+    a.st[b] = u;
+  }
+}
+
+// ---- per-size dispatch
+template <int LOG = kLargeMinLog>
+int col_fwd_at(int lg, const LargeArgs& a, const double* src, int mode, int real, cudaStream_t st) {
+  if (lg == LOG) return LargeDispatch<LOG>::col_fwd(a, src, mode, real, st);
+  if constexpr (LOG < kLargeMaxLog) return col_fwd_at<LOG + 1>(lg, a, src, mode, real, st);
+  return report_error(TSF_E_UNSUPPORTED, "large-n column length out of range");
+}
+template <int LOG = kLargeMinLog>
+int row_at(int lg, const LargeArgs& a, int spec, cudaStream_t st) {
+  if (lg == LOG) return LargeDispatch<LOG>::row(a, spec, st);
+  if constexpr (LOG < kLargeMaxLog) return row_at<LOG + 1>(lg, a, spec, st);
+  return report_error(TSF_E_UNSUPPORTED, "large-n row length out of range");
+}
+template <int LOG = kLargeMinLog>
+int col_inv_at(int lg, const LargeArgs& a, double* dst, int mode, const double* xin,
+               const double* w1, int slot, cudaStream_t st) {
+  if (lg == LOG) return LargeDispatch<LOG>::col_inv(a, dst, mode, xin, w1, slot, st);
+  if constexpr (LOG < kLargeMaxLog) return col_inv_at<LOG + 1>(lg, a, dst, mode, xin, w1, slot, st);
+  return report_error(TSF_E_UNSUPPORTED, "large-n column length out of range");
+}
+
+int ilog2i(long x) {
+  int r = 0;
+  while ((1L << r) < x) ++r;
+  return r;
+}
+
+int cuda_check(cudaError_t e, const char* what) { return e == cudaSuccess ? 0 : report_cuda(e, what); }
+
+struct Runner {
+  const LargePlan* lp;
+  LargeArgs a;
+  cudaStream_t st;
+  int lg1, lg2;
+
+  // dst = Re IFFT_n(S . FFT_n(src)) with the Strang spectrum (pspec);
+  // in_mode: the column prologue that forms src (p / s update) on the fly
+  int strang(int in_mode, const double* src, double* dst) {
+    int rc;
+    if ((rc = col_fwd_at(lg1, a, src, in_mode, 1, st))) return rc;
+    if ((rc = row_at(lg2, a, RS_STRANG, st))) return rc;
+    return col_inv_at(lg1, a, dst, CO_REAL, nullptr, nullptr, -1, st);
+  }
+  // dst = d src + kappa . (A src)  (kappa null: A src); dot partials
+  // dst.dst (slot) and dst.w1 (slot + 1) per column CTA
+  int apply(const double* src, double* dst, const double* w1, int slot) {
+    int rc;
+    if ((rc = col_fwd_at(lg1, a, src, CI_LOAD, 1, st))) return rc;
+    if ((rc = row_at(lg2, a, RS_EVEN, st))) return rc;
+    if ((rc = col_inv_at(lg1, a, a.ye, CO_REAL, nullptr, nullptr, -1, st))) return rc;
+    if ((rc = col_fwd_at(lg1, a, src, CI_MOD, 0, st))) return rc;
+    if ((rc = row_at(lg2, a, RS_ODD, st))) return rc;
+    return col_inv_at(lg1, a, dst, CO_COMBINE, src, w1, slot, st);
+  }
+  dim3 lel_grid() const { return dim3(a.n / kLelChunk, a.B); }
+  int sc(int stage, int count, int pc) {
+    k_lsc<<<a.B, kLscThreads, 0, st>>>(a, stage, count, 0.0, lp->lam_min, pc);
+    return cuda_check(cudaGetLastError(), "k_lsc");
+  }
+  // one BiCGSTAB iteration for every unfinished instance
+  int bicg_iteration(int pc) {
+    int rc;
+    const int N2 = lp->N2, NR = a.n / kLelChunk;
+    const double* ph = pc ? a.ph : a.p;
+    const double* sh = pc ? a.sh : a.s;
+    if (pc) {
+      if ((rc = strang(CI_PUPD, nullptr, a.ph))) return rc;
+    } else {
+      k_lel_pupd<<<lel_grid(), kLelThreads, 0, st>>>(a);
+      if ((rc = cuda_check(cudaGetLastError(), "k_lel_pupd"))) return rc;
+    }
+    if ((rc = apply(ph, a.v, a.r0, 0))) return rc;
+    if ((rc = sc(LS_ALPHA, N2, pc))) return rc;
+    if (pc) {
+      if ((rc = strang(CI_SUPD, nullptr, a.sh))) return rc;
+    } else {
+      k_lel_supd<<<lel_grid(), kLelThreads, 0, st>>>(a);
+      if ((rc = cuda_check(cudaGetLastError(), "k_lel_supd"))) return rc;
+    }
+    if ((rc = sc(LS_SNORM, pc ? N2 : NR, pc))) return rc;
+    if ((rc = apply(sh, a.t, a.s, 0))) return rc;
+    if ((rc = sc(LS_OMEGA, N2, pc))) return rc;
+    k_lel_xr<<<lel_grid(), kLelThreads, 0, st>>>(a, ph, sh);
+    if ((rc = cuda_check(cudaGetLastError(), "k_lel_xr"))) return rc;
+    return sc(LS_REL, NR, pc);
+  }
+};
+
+Runner make_runner(const LargePlan* lp, int B, cudaStream_t st) {
+  Runner R;
+  R.lp = lp;
+  R.st = st;
+  R.lg1 = ilog2i(lp->N1);
+  R.lg2 = ilog2i(lp->N2);
+  LargeArgs& a = R.a;
+  a = LargeArgs{};
+  a.n = lp->n;
+  a.B = B;
+  a.lt = lp->lt;
+  a.Z = lp->Z;
+  a.part = lp->part;
+  a.np = lp->np;
+  const size_t vn = (size_t)lp->cap * lp->n;
+  double* w = lp->ws;
+  a.r = w;
+  a.p = w + vn;
+  a.v = w + 2 * vn;
+  a.ph = w + 3 * vn;
+  a.s = w + 4 * vn;
+  a.sh = w + 5 * vn;
+  a.t = w + 6 * vn;
+  a.pspec = w + 7 * vn;
+  a.ye = w + 8 * vn;
+  // w + 9 vn: kwork
+  a.active = lp->active;
+  return R;
+}
+
+}  // namespace
+
+// ======================================================================
+int large_plan_init(LargePlan* lp, int n, const double* symbol_re, const double* lam, int device) {
+  const int lg = ilog2i(n);
+  if ((1L << lg) != n || lg < 13 || lg > 2 * kLargeMaxLog)
+    return report_error(TSF_E_UNSUPPORTED, "large-n engine needs a power of two n in [2^13, 2^24]");
+  *lp = LargePlan{};
+  lp->n = n;
+  lp->N1 = 1 << (lg / 2);
+  lp->N2 = n / lp->N1;
+  lp->np = std::max(lp->N2, n / kLelChunk);
+  lp->has_pc = lam != nullptr;
+  lp->device = device;
+  const long L = 2L * n;
+  const int N1 = lp->N1, N2 = lp->N2;
+  std::vector<double2> tw1 = twiddle_table(N1), tw2 = twiddle_table(N2);
+  std::vector<double2> twN = twiddle_table(n), twL = twiddle_table((int)L);
+  // permuted spectra: position k1 N2 + k2 holds bin k = k1 + N1 k2
+  std::vector<double2> sEO((size_t)n), lamP(lam ? (size_t)n : 0);
+  auto Ssym = [&](long k) -> double {
+    return (double)(0.5L * ((long double)symbol_re[k] + (long double)symbol_re[(L - k) % L]) /
+                    (long double)L);
+  };
+  double lam_min = 1e308;
+  for (int k1 = 0; k1 < N1; ++k1) {
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const long k = k1 + (long)N1 * k2;
+      const size_t pos = (size_t)k1 * N2 + k2;
+      sEO[pos] = make_double2(Ssym(2 * k), Ssym(2 * k + 1));
+      if (lam) lamP[pos] = make_double2(lam[k], lam[(n - k) % n]);
+    }
+  }
+  if (lam)
+    for (int k = 0; k < n; ++k) lam_min = std::min(lam_min, lam[k]);
+  lp->lam_min = lam_min;
+  const size_t total = tw1.size() + tw2.size() + twN.size() + twL.size() + sEO.size() + lamP.size();
+  int rc;
+  if ((rc = cuda_check(cudaSetDevice(device), "cudaSetDevice"))) return rc;
+  if ((rc = cuda_check(cudaMalloc(&lp->tables, total * sizeof(double2)), "cudaMalloc(tables)")))
+    return rc;
+  double2* cur = lp->tables;
+  auto put = [&](const std::vector<double2>& h) -> const double2* {
+    if (h.empty()) return nullptr;
+    double2* d = cur;
+    cur += h.size();
+    if (cudaMemcpy(d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = report_cuda(cudaGetLastError(), "cudaMemcpy(tables)");
+    return d;
+  };
+  lp->lt.tw1 = put(tw1);
+  lp->lt.tw2 = put(tw2);
+  lp->lt.twN = put(twN);
+  lp->lt.twL = put(twL);
+  lp->lt.sEO = put(sEO);
+  lp->lt.lamP = put(lamP);
+  return rc;
+}
+
+void large_plan_free(LargePlan* lp) {
+  if (!lp) return;
+  cudaSetDevice(lp->device);
+  cudaFree(lp->tables);
+  cudaFree(lp->ws);
+  cudaFree(lp->Z);
+  cudaFree(lp->part);
+  cudaFree(lp->st);
+  cudaFree(lp->active);
+  if (lp->h_active) cudaFreeHost(lp->h_active);
+  *lp = LargePlan{};
+}
+
+int large_reserve(LargePlan* lp, int B) {
+  if (B <= lp->cap) return TSF_SUCCESS;
+  cudaSetDevice(lp->device);
+  cudaFree(lp->ws);
+  cudaFree(lp->Z);
+  cudaFree(lp->part);
+  cudaFree(lp->st);
+  lp->ws = nullptr;
+  lp->Z = nullptr;
+  lp->part = nullptr;
+  lp->st = nullptr;
+  lp->cap = 0;
+  const size_t vn = (size_t)B * lp->n;
+  int rc;
+  if ((rc = cuda_check(cudaMalloc(&lp->ws, sizeof(double) * vn * 10), "cudaMalloc(large ws)")))
+    return rc;
+  if ((rc = cuda_check(cudaMalloc(&lp->Z, sizeof(double2) * vn), "cudaMalloc(large Z)"))) return rc;
+  if ((rc = cuda_check(cudaMalloc(&lp->part, sizeof(double) * (size_t)B * 4 * lp->np),
+                       "cudaMalloc(partials)")))
+    return rc;
+  if ((rc = cuda_check(cudaMalloc(&lp->st, sizeof(LState) * (size_t)B), "cudaMalloc(state)")))
+    return rc;
+  if (!lp->active && (rc = cuda_check(cudaMalloc(&lp->active, sizeof(int)), "cudaMalloc(active)")))
+    return rc;
+  if (!lp->h_active &&
+      (rc = cuda_check(cudaHostAlloc(&lp->h_active, sizeof(int), cudaHostAllocDefault), "cudaHostAlloc")))
+    return rc;
+  lp->cap = B;
+  return TSF_SUCCESS;
+}
+
+int large_matvec(LargePlan* lp, int B, const double* x, double* y, const double* kappa,
+                 double shift, cudaStream_t st) {
+  int rc = large_reserve(lp, B);
+  if (rc) return rc;
+  Runner R = make_runner(lp, B, st);
+  R.a.kappa = kappa;
+  R.a.shift = shift;
+  return R.apply(x, y, nullptr, -1);
+}
+
+int large_precond(LargePlan* lp, int B, const double* v, double* z, double shift, double kbar,
+                  const double* kbar_dev, cudaStream_t st) {
+  int rc = large_reserve(lp, B);
+  if (rc) return rc;
+  Runner R = make_runner(lp, B, st);
+  R.a.shift = shift;
+  k_lspec<<<R.lel_grid(), kLelThreads, 0, st>>>(R.a, kbar, kbar_dev, 0);
+  if ((rc = cuda_check(cudaGetLastError(), "k_lspec"))) return rc;
+  return R.strang(CI_LOAD, v, z);
+}
+
+int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, cudaStream_t st) {
+  if (method != 0)
+    return report_error(TSF_E_UNSUPPORTED, "large-n engine: only BiCGSTAB (method 0) so far");
+  if (pc && !lp->has_pc) return report_error(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner");
+  int rc = large_reserve(lp, B);
+  if (rc) return rc;
+  Runner R = make_runner(lp, B, st);
+  LargeArgs& a = R.a;
+  KrylovArgs kk = k;
+  if (!kk.kappa && !kk.kwork) kk.kwork = lp->ws + 9 * (size_t)lp->cap * lp->n;
+  a.r0 = k.rhs;
+  a.x = k.x;
+  a.kappa = kk.kappa ? kk.kappa : kk.kwork;
+  a.shift = k.shift;
+  a.tol = k.tol;
+  a.max_iters = k.max_iters > 0 ? k.max_iters : 10 * lp->n;
+  a.iters = k.iters;
+  a.relres = k.relres;
+  a.status = k.status;
+  a.st = lp->st;
+  k_set_int<<<1, 1, 0, st>>>(lp->active, B);
+  k_lel_begin<<<R.lel_grid(), kLelThreads, 0, st>>>(a, kk);
+  if ((rc = cuda_check(cudaGetLastError(), "k_lel_begin"))) return rc;
+  k_lsc<<<B, kLscThreads, 0, st>>>(a, LS_BEGIN, a.n / kLelChunk, k.kbar, lp->lam_min, pc);
+  if ((rc = cuda_check(cudaGetLastError(), "k_lsc(begin)"))) return rc;
+  if (pc) {
+    k_lspec<<<R.lel_grid(), kLelThreads, 0, st>>>(a, 0.0, nullptr, 1);
+    if ((rc = cuda_check(cudaGetLastError(), "k_lspec"))) return rc;
+  }
+  for (int it = 0; it < a.max_iters; it += kLargeChunk) {
+    for (int c = 0; c < kLargeChunk && it + c < a.max_iters; ++c)
+      if ((rc = R.bicg_iteration(pc))) return rc;
+    if ((rc = cuda_check(cudaMemcpyAsync(lp->h_active, lp->active, sizeof(int),
+                                         cudaMemcpyDeviceToHost, st), "poll")))
+      return rc;
+    if ((rc = cuda_check(cudaStreamSynchronize(st), "poll sync"))) return rc;
+    if (*lp->h_active == 0) break;
+  }
+  return TSF_SUCCESS;
+}
+
+}  // namespace tsf

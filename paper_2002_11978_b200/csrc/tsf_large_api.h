@@ -1,0 +1,47 @@
+// Host interface of the large-n engine (tsf_large.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "tsf_large.cuh"
+
+namespace tsf {
+
+// shared with tsf_abi.cu: sets tsf_last_error() and returns `code`
+int report_error(int code, const char* msg);
+// two-level twiddle table of W_N (layout: tsf_fft.cuh tw_get)
+std::vector<double2> twiddle_table(int N);
+
+struct LargePlan {
+  int n = 0, N1 = 0, N2 = 0, np = 0;
+  int has_pc = 0;
+  int device = 0;
+  double lam_min = 0.0;       // min_k lam_k (preconditioner positivity test)
+  LargeTables lt{};
+  double2* tables = nullptr;  // one allocation for every table
+  // workspaces, sized for `cap` instances
+  int cap = 0;
+  double* ws = nullptr;       // 10 vectors [cap][n]
+  double2* Z = nullptr;       // [cap][n]
+  double* part = nullptr;     // [cap][4][np]
+  LState* st = nullptr;       // [cap]
+  int* active = nullptr;
+  int* h_active = nullptr;
+};
+
+// n a power of two in [2^10, 2^24]; symbol_re: L = 2n reals; lam: n reals or null
+int large_plan_init(LargePlan* lp, int n, const double* symbol_re, const double* lam, int device);
+void large_plan_free(LargePlan* lp);
+int large_reserve(LargePlan* lp, int B);
+
+int large_matvec(LargePlan* lp, int B, const double* x, double* y, const double* kappa,
+                 double shift, cudaStream_t st);
+int large_precond(LargePlan* lp, int B, const double* v, double* z, double shift, double kbar,
+                  const double* kbar_dev, cudaStream_t st);
+// Level solve: kappa given [B][n] (kappa != null) or separable modes (KrylovArgs fields);
+// method 0 = BiCGSTAB (CG: TSF_E_UNSUPPORTED for now)
+int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& a, cudaStream_t st);
+
+}  // namespace tsf

@@ -1,0 +1,64 @@
+// Launch bodies of LargeDispatch<LOG> (tsf_large.cuh); explicitly
+// instantiated one size per translation unit (gen/large_L*.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "tsf_dispatch.h"
+#include "tsf_large.cuh"
+
+namespace tsf {
+
+template <int N>
+struct LShape {
+  static constexpr int T = FShape<N>::T;
+  static constexpr int BLOCK = T < 32 ? 32 : T;
+  // ping-pong transform buffers | staged two-level twiddle table of W_N
+  static constexpr int SMEM = 2 * FftPlan<N, FShape<N>::E>::SMEM_ELEMS * 16 + tw_table_elems(N) * 16;
+};
+
+inline int large_launch_error(cudaError_t e) {
+  return e == cudaSuccess ? 0 : report_cuda(e, "large-n kernel launch");
+}
+
+template <typename K>
+inline cudaError_t large_prep(K kernel, int smem) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+template <int LOG>
+int LargeDispatch<LOG>::col_fwd(const LargeArgs& a, const double* src, int in_mode,
+                                int real_input, cudaStream_t st) {
+  constexpr int N1 = 1 << LOG;
+  using S = LShape<N1>;
+  auto k = k_lcol_fwd<N1>;
+  static cudaError_t prep = large_prep(k, S::SMEM);
+  if (prep != cudaSuccess) return large_launch_error(prep);
+  k<<<dim3(a.n / N1, a.B), S::BLOCK, S::SMEM, st>>>(a, src, in_mode, real_input);
+  return large_launch_error(cudaGetLastError());
+}
+
+template <int LOG>
+int LargeDispatch<LOG>::row(const LargeArgs& a, int spec_mode, cudaStream_t st) {
+  constexpr int N2 = 1 << LOG;
+  using S = LShape<N2>;
+  auto k = k_lrow<N2>;
+  static cudaError_t prep = large_prep(k, S::SMEM);
+  if (prep != cudaSuccess) return large_launch_error(prep);
+  k<<<dim3(a.n / N2, a.B), S::BLOCK, S::SMEM, st>>>(a, spec_mode);
+  return large_launch_error(cudaGetLastError());
+}
+
+template <int LOG>
+int LargeDispatch<LOG>::col_inv(const LargeArgs& a, double* dst, int out_mode, const double* xin,
+                                const double* w1, int pslot, cudaStream_t st) {
+  constexpr int N1 = 1 << LOG;
+  using S = LShape<N1>;
+  auto k = k_lcol_inv<N1>;
+  static cudaError_t prep = large_prep(k, S::SMEM);
+  if (prep != cudaSuccess) return large_launch_error(prep);
+  k<<<dim3(a.n / N1, a.B), S::BLOCK, S::SMEM, st>>>(a, dst, out_mode, xin, w1, pslot);
+  return large_launch_error(cudaGetLastError());
+}
+
+}  // namespace tsf
