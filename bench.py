@@ -42,12 +42,24 @@ UNIT = "grid-point solves/s"
 
 def workload(args):
     if args.workload == "cfg2":
-        return dict(name="configs[2] batched FIDS march", n=4096, M=512, gamma=0.5, alpha=1.5,
-                    eps=1e-12, tol=1e-12, B=args.batch or 4096)
-    if args.workload == "cfg0":
-        return dict(name="configs[0] single FIDS march", n=1024, M=256, gamma=0.5, alpha=1.5,
-                    eps=1e-12, tol=1e-12, B=args.batch or 1)
-    raise SystemExit(f"unknown workload {args.workload}")
+        wl = dict(name="configs[2] batched FIDS march", n=4096, M=512, gamma=0.5, alpha=1.5,
+                  eps=1e-12, tol=1e-12, B=args.batch or 4096, cpu_levels=64)
+    elif args.workload == "cfg0":
+        wl = dict(name="configs[0] single FIDS march", n=1024, M=256, gamma=0.5, alpha=1.5,
+                  eps=1e-12, tol=1e-12, B=args.batch or 1, cpu_levels=64)
+    elif args.workload == "cfg1":
+        wl = dict(name="configs[1] single FIDS march at paper-upper scale", n=16384, M=1024,
+                  gamma=0.5, alpha=1.5, eps=1e-12, tol=1e-12, B=args.batch or 1, cpu_levels=64)
+    elif args.workload == "cfg3":
+        wl = dict(name="configs[3] large-N single FIDS march", n=1 << 20, M=256, gamma=0.7,
+                  alpha=1.2, eps=1e-12, tol=1e-12, B=args.batch or 1, cpu_levels=4)
+    else:
+        raise SystemExit(f"unknown workload {args.workload}")
+    if args.gamma:
+        wl["gamma"] = args.gamma
+    if args.alpha:
+        wl["alpha"] = args.alpha
+    return wl
 
 
 def cfg0_fields(n):
@@ -160,7 +172,9 @@ def main():
     ap.add_argument("--steps", type=int, default=509)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg0", "cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--gamma", type=float, default=0.0, help="override the workload's gamma")
+    ap.add_argument("--alpha", type=float, default=0.0, help="override the workload's alpha")
     ap.add_argument("--batch", type=int, default=0, help="instances per rank")
     ap.add_argument("--cpu-workers", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -177,7 +191,8 @@ def main():
         if rank != 0:
             return
         workers = args.cpu_workers or os.cpu_count() or 1
-        value, wall, K, avg_its = cpu_measure(wl, warmup, args.steps, workers, cfg2)
+        value, wall, K, avg_its = cpu_measure(wl, warmup, min(args.steps, wl["cpu_levels"]),
+                                              workers, cfg2)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": K, "warmup": warmup,
@@ -282,20 +297,28 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     iters = march.iters.cpu().numpy()
+    large = n > 4096
+    fused = os.environ.get("TSF_FUSE_SOE") == "1" and not large
     for m0, m1 in levels_done:
         its_sum += int(iters[m0 - 1: m1 - 1].sum())
-        # launches per level: counter init + begin + iteration pairs in chunks
-        # of 4 until every instance finished (+ the level-1 SOE kernel)
+        # launches per level (tsf_abi.cu tsf_fids_march): SOE push + RHS
+        # kernel (level 1 only when fused), counter init, then
+        #   single-CTA engine: begin + (v, t) phase pair per iteration,
+        #   large-n engine: begin, scalar, spectrum + 23 kernels per iteration,
+        # iterations launched in chunks of 4 until every instance finished
         mx = iters[m0 - 1: m1 - 1].max(axis=1)
-        launches += int(np.sum(2 + 2 * 4 * np.ceil(np.maximum(mx, 1) / 4.0)))
-        launches += 1 if m0 == 1 else 0
+        chunks = np.ceil(np.maximum(mx, 1) / 4.0)
+        per_it = 23 if large else 2
+        head = 4 if large else 2
+        launches += int(np.sum(head + per_it * 4 * chunks))
+        launches += (m1 - m0) if not fused else (1 if m0 == 1 else 0)
+        launches += 1 if (m1 == M + 1 and not fused) else 0
     status = march.status.cpu().numpy()
     if np.any(status != 0):
         raise SystemExit(f"solver failure in the timed region: status {np.unique(status)}")
     soe_ms = sum(events[3 * i].elapsed_time(events[3 * i + 1]) for i in range(K))
     solve_ms = sum(events[3 * i + 1].elapsed_time(events[3 * i + 2]) for i in range(K))
     nexp = soe.n_exp
-    fused = os.environ.get("TSF_FUSE_SOE") == "1"
     # algorithmic bytes: BiCGSTAB iteration 216 n per instance (SURVEY.md
     # §8(d)); SOE push + RHS (16 N_exp + 32) n per instance (W read+write;
     # u, u_prev, f-mode read; rhs write)
@@ -309,8 +332,13 @@ def main():
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    sname = (f"tsf level solve: k_solve_begin + k_bicg_v/k_bicg_t<{n},1>"
-             + (" with fused SOE epilogue" if fused else ""))
+    if large:
+        n1 = max(64, n >> 12)   # tsf_large.cu large_plan_init
+        sname = (f"tsf large-n level solve: k_lcol_fwd/k_lcol_inv<{n1}> + k_lrow<{n // n1}> "
+                 "+ k_lsc/k_lel_* (23 kernels per BiCGSTAB iteration)")
+    else:
+        sname = (f"tsf level solve: k_solve_begin + k_bicg_v/k_bicg_t<{n},1>"
+                 + (" with fused SOE epilogue" if fused else ""))
     k_solve = {"name": sname, "avg_ms": solve_ms / K,
                "GBps": solve_bytes / (solve_ms / K * 1e-3) / 1e9,
                "iterations_per_launch": its_sum / K, "algorithmic_bytes": solve_bytes}
@@ -323,8 +351,10 @@ def main():
             "unit": "GB/s", "frac": dom["GBps"] / hbm, "traffic": None,
             "algorithmic_bytes_per_launch": dom["algorithmic_bytes"], "peak_source": peak_src,
             "share_of_step": (solve_ms if dom is k_solve else soe_ms) / ms,
-            "note": "level solve is transform (FP64/shared-memory) bound: ncu FP64 pipe "
-                    "~30% active; the SOE kernel alone runs at ~98% of the HBM peak"}
+            "note": ("large-n level solve: four-step transforms through L2/HBM"
+                     if large else
+                     "level solve is transform (FP64/shared-memory) bound: ncu FP64 pipe "
+                     "~30% active; the SOE kernel alone runs at ~98% of the HBM peak")}
     value = world * B * n * K / (ms * 1e-3)
 
     # ---- end to end through the public API with host buffers
@@ -363,9 +393,9 @@ def main():
                "note": "pinned host u0 + coefficient modes -> device, march levels "
                        f"1..{levels}, final u + per-level iterations/residuals -> host"}
 
-    # ---- standalone Toeplitz matvec throughput (configs[4] point n=4096, B*n=2^26)
+    # ---- standalone Toeplitz matvec throughput (configs[4] point at this n, B*n=2^26)
     mv = None
-    if rank == 0:
+    if rank == 0 and n <= (1 << 20):
         col = P.build_ifl(1.5, 1.75, 1.0, n + 1).first_col
         op = P.build_toeplitz(col)
         Bm = (1 << 26) // n
@@ -391,7 +421,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = args.cpu_workers or min(os.cpu_count() or 1, 8)
-        cw = min(K, 64)
+        cw = min(K, wl["cpu_levels"])
         cval, cwall, cK, cits = cpu_measure(wl, warmup, cw, workers, cfg2)
         cpu = {"value": cval, "unit": UNIT, "cores": workers, "kind": "port",
                "sample": f"{workers} instances (one per process, 1 BLAS thread) x levels "

@@ -292,6 +292,17 @@ TSF_D void block_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ t
   fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, own);
 }
 
+// Several independent transforms per CTA (the large-n column kernels): the
+// caller passes the thread's index inside its transform group and the
+// group's own shared-memory buffers; barriers stay CTA-wide, so every group
+// must run the same transform.
+template <int N, int E, bool INV>
+TSF_D void group_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
+                     int tw_log_scale, int tid) {
+  __syncthreads();
+  fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, true);
+}
+
 // ------------------------------------------------------------ real input
 // Forward DFTs of real data: no imaginary zeros are carried (x + 0.0 cannot
 // be folded under IEEE rules, so a complex first pass on real data wastes
@@ -361,18 +372,15 @@ TSF_D void dft_real(const double* x, double2* X) {
   }
 }
 
-// Forward transform of real owned slots x[c] (j = tid + c*T) into v[c].
+// First pass of a forward transform of real data (owned slots x[c],
+// j = tid + c*T), then the remaining complex passes into v[c].
 template <int N, int E>
-TSF_D void block_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
-                          const double2* __restrict__ tw, int tw_log_scale) {
+TSF_D void real_first_pass(const double (&x)[E], double2 (&v)[E], double2* sm,
+                           const double2* __restrict__ tw, int tw_log_scale, int tid, bool own) {
   using PL = FftPlan<N, E>;
-  static_assert(PL::NPASS >= 2, "real-input transform needs at least two passes");
   constexpr int R = 1 << PL::log_radix(0);
   constexpr int Q = E / R;
   constexpr int T = PL::T;
-  __syncthreads();
-  const int tid = threadIdx.x;
-  const bool own = tid < T;
   if (own) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -388,6 +396,24 @@ TSF_D void block_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
   }
   __syncthreads();
   fft_rec<N, E, 1, false>(v, sm, tw, tw_log_scale, tid, own);
+}
+
+// Forward transform of real owned slots x[c] (j = tid + c*T) into v[c].
+template <int N, int E>
+TSF_D void block_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
+                          const double2* __restrict__ tw, int tw_log_scale) {
+  static_assert(FftPlan<N, E>::NPASS >= 2, "real-input transform needs at least two passes");
+  __syncthreads();
+  const int tid = threadIdx.x;
+  real_first_pass<N, E>(x, v, sm, tw, tw_log_scale, tid, tid < FftPlan<N, E>::T);
+}
+
+template <int N, int E>
+TSF_D void group_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
+                          const double2* __restrict__ tw, int tw_log_scale, int tid) {
+  static_assert(FftPlan<N, E>::NPASS >= 2, "real-input transform needs at least two passes");
+  __syncthreads();
+  real_first_pass<N, E>(x, v, sm, tw, tw_log_scale, tid, true);
 }
 
 }  // namespace tsf

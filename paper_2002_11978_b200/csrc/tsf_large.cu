@@ -7,11 +7,11 @@
 // polls the device count of unfinished instances between chunks (as the
 // single-CTA engine does, tsf_dispatch_impl.cuh):
 //   1  p_hat = P^{-1} p      col_fwd(p update) . row(Strang) . col_inv
-//   2  v = M p_hat           even filter (3 kernels) + odd filter/combine (3)
+//   2  v = M p_hat           col_fwd . row . col_inv, even + odd channels
 //   3  alpha                 scalar kernel (r0.v from the combine partials)
 //   4  s_hat = P^{-1} s      col_fwd(s = r - alpha v, ||s||^2) . row . col_inv
 //   5  ||s||, early exit      scalar kernel
-//   6  t = M s_hat           6 kernels (t.t, t.s partials)
+//   6  t = M s_hat           3 kernels (t.t, t.s partials)
 //   7  omega                 scalar kernel
 //   8  x, r update           elementwise (||r||^2, r0.r partials)
 //   9  convergence, rho      scalar kernel
@@ -264,10 +264,16 @@ __global__ void __launch_bounds__(kLscThreads) k_lsc(LargeArgs a, int stage, int
 
 // ---- per-size dispatch
 template <int LOG = kLargeMinLog>
-int col_fwd_at(int lg, const LargeArgs& a, const double* src, int mode, int real, cudaStream_t st) {
-  if (lg == LOG) return LargeDispatch<LOG>::col_fwd(a, src, mode, real, st);
-  if constexpr (LOG < kLargeMaxLog) return col_fwd_at<LOG + 1>(lg, a, src, mode, real, st);
+int col_fwd_at(int lg, const LargeArgs& a, const double* src, int mode, cudaStream_t st) {
+  if (lg == LOG) return LargeDispatch<LOG>::col_fwd(a, src, mode, st);
+  if constexpr (LOG < kLargeMaxLog) return col_fwd_at<LOG + 1>(lg, a, src, mode, st);
   return report_error(TSF_E_UNSUPPORTED, "large-n column length out of range");
+}
+template <int LOG = kLargeMinLog>
+int col_group_at(int lg) {
+  if (lg == LOG) return LargeDispatch<LOG>::col_group();
+  if constexpr (LOG < kLargeMaxLog) return col_group_at<LOG + 1>(lg);
+  return 1;
 }
 template <int LOG = kLargeMinLog>
 int row_at(int lg, const LargeArgs& a, int spec, cudaStream_t st) {
@@ -301,7 +307,7 @@ struct Runner {
   // in_mode: the column prologue that forms src (p / s update) on the fly
   int strang(int in_mode, const double* src, double* dst) {
     int rc;
-    if ((rc = col_fwd_at(lg1, a, src, in_mode, 1, st))) return rc;
+    if ((rc = col_fwd_at(lg1, a, src, in_mode, st))) return rc;
     if ((rc = row_at(lg2, a, RS_STRANG, st))) return rc;
     return col_inv_at(lg1, a, dst, CO_REAL, nullptr, nullptr, -1, st);
   }
@@ -309,12 +315,9 @@ struct Runner {
   // dst.dst (slot) and dst.w1 (slot + 1) per column CTA
   int apply(const double* src, double* dst, const double* w1, int slot) {
     int rc;
-    if ((rc = col_fwd_at(lg1, a, src, CI_LOAD, 1, st))) return rc;
-    if ((rc = row_at(lg2, a, RS_EVEN, st))) return rc;
-    if ((rc = col_inv_at(lg1, a, a.ye, CO_REAL, nullptr, nullptr, -1, st))) return rc;
-    if ((rc = col_fwd_at(lg1, a, src, CI_MOD, 0, st))) return rc;
-    if ((rc = row_at(lg2, a, RS_ODD, st))) return rc;
-    return col_inv_at(lg1, a, dst, CO_COMBINE, src, w1, slot, st);
+    if ((rc = col_fwd_at(lg1, a, src, CI_APPLY, st))) return rc;
+    if ((rc = row_at(lg2, a, RS_APPLY, st))) return rc;
+    return col_inv_at(lg1, a, dst, CO_APPLY, src, w1, slot, st);
   }
   dim3 lel_grid() const { return dim3(a.n / kLelChunk, a.B); }
   int sc(int stage, int count, int pc) {
@@ -324,7 +327,7 @@ struct Runner {
   // one BiCGSTAB iteration for every unfinished instance
   int bicg_iteration(int pc) {
     int rc;
-    const int N2 = lp->N2, NR = a.n / kLelChunk;
+    const int NC = lp->ncol_cta, NR = a.n / kLelChunk;
     const double* ph = pc ? a.ph : a.p;
     const double* sh = pc ? a.sh : a.s;
     if (pc) {
@@ -334,16 +337,16 @@ struct Runner {
       if ((rc = cuda_check(cudaGetLastError(), "k_lel_pupd"))) return rc;
     }
     if ((rc = apply(ph, a.v, a.r0, 0))) return rc;
-    if ((rc = sc(LS_ALPHA, N2, pc))) return rc;
+    if ((rc = sc(LS_ALPHA, NC, pc))) return rc;
     if (pc) {
       if ((rc = strang(CI_SUPD, nullptr, a.sh))) return rc;
     } else {
       k_lel_supd<<<lel_grid(), kLelThreads, 0, st>>>(a);
       if ((rc = cuda_check(cudaGetLastError(), "k_lel_supd"))) return rc;
     }
-    if ((rc = sc(LS_SNORM, pc ? N2 : NR, pc))) return rc;
+    if ((rc = sc(LS_SNORM, pc ? NC : NR, pc))) return rc;
     if ((rc = apply(sh, a.t, a.s, 0))) return rc;
-    if ((rc = sc(LS_OMEGA, N2, pc))) return rc;
+    if ((rc = sc(LS_OMEGA, NC, pc))) return rc;
     k_lel_xr<<<lel_grid(), kLelThreads, 0, st>>>(a, ph, sh);
     if ((rc = cuda_check(cudaGetLastError(), "k_lel_xr"))) return rc;
     return sc(LS_REL, NR, pc);
@@ -374,8 +377,7 @@ Runner make_runner(const LargePlan* lp, int B, cudaStream_t st) {
   a.sh = w + 5 * vn;
   a.t = w + 6 * vn;
   a.pspec = w + 7 * vn;
-  a.ye = w + 8 * vn;
-  // w + 9 vn: kwork
+  // w + 8 vn: kwork
   a.active = lp->active;
   return R;
 }
@@ -389,9 +391,11 @@ int large_plan_init(LargePlan* lp, int n, const double* symbol_re, const double*
     return report_error(TSF_E_UNSUPPORTED, "large-n engine needs a power of two n in [2^13, 2^24]");
   *lp = LargePlan{};
   lp->n = n;
-  lp->N1 = 1 << (lg / 2);
+  // columns short (cheap, G per CTA), rows up to the single-CTA limit 4096
+  lp->N1 = std::max(64, n >> kLargeMaxLog);
   lp->N2 = n / lp->N1;
-  lp->np = std::max(lp->N2, n / kLelChunk);
+  lp->ncol_cta = lp->N2 / col_group_at(ilog2i(lp->N1));
+  lp->np = std::max(lp->ncol_cta, n / kLelChunk);
   lp->has_pc = lam != nullptr;
   lp->device = device;
   const long L = 2L * n;
@@ -466,9 +470,10 @@ int large_reserve(LargePlan* lp, int B) {
   lp->cap = 0;
   const size_t vn = (size_t)B * lp->n;
   int rc;
-  if ((rc = cuda_check(cudaMalloc(&lp->ws, sizeof(double) * vn * 10), "cudaMalloc(large ws)")))
+  if ((rc = cuda_check(cudaMalloc(&lp->ws, sizeof(double) * vn * 9), "cudaMalloc(large ws)")))
     return rc;
-  if ((rc = cuda_check(cudaMalloc(&lp->Z, sizeof(double2) * vn), "cudaMalloc(large Z)"))) return rc;
+  if ((rc = cuda_check(cudaMalloc(&lp->Z, sizeof(double2) * vn * 2), "cudaMalloc(large Z)")))
+    return rc;
   if ((rc = cuda_check(cudaMalloc(&lp->part, sizeof(double) * (size_t)B * 4 * lp->np),
                        "cudaMalloc(partials)")))
     return rc;
@@ -513,7 +518,7 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
   Runner R = make_runner(lp, B, st);
   LargeArgs& a = R.a;
   KrylovArgs kk = k;
-  if (!kk.kappa && !kk.kwork) kk.kwork = lp->ws + 9 * (size_t)lp->cap * lp->n;
+  if (!kk.kappa && !kk.kwork) kk.kwork = lp->ws + 8 * (size_t)lp->cap * lp->n;
   a.r0 = k.rhs;
   a.x = k.x;
   a.kappa = kk.kappa ? kk.kappa : kk.kwork;

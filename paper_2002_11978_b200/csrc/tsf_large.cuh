@@ -1,20 +1,26 @@
 // Large-n engine (n = N1*N2 > 4096, power of two): four-step transforms
-// through L2/HBM, one CTA per column or row of the N1 x N2 view.
+// through L2/HBM over the N1 x N2 view j = N2 t1 + t2, k = k1 + N1 k2.
 //
-// A length-N filter  y = IFFT_N( S . FFT_N(x) )  is three kernels:
-//   col_fwd : per column t2, x[N2 t1 + t2] (t1 < N1) -> FFT_N1 -> * W_N^{t2 k1}
-//             -> Z[k1][t2]                      (input prologue: load / modulate /
-//                                                 Krylov vector update)
-//   row     : per row k1, FFT_N2 over Z[k1][.] -> * S[k1 + N1 k2] -> IFFT_N2
-//             (S stored permuted as [k1][k2])
-//   col_inv : per column t2, Z[.][t2] * conj(W_N^{t2 k1}) -> IFFT_N1 -> y at
-//             j = N2 t1 + t2                   (epilogue: store / combine /
-//                                                 operator / dot partials)
-// The matvec uses the same even/odd-bin split as the single-CTA engine
-// (tsf_filters.cuh): two length-n filters, the odd one on x_j W_L^j.
-// Reductions are deterministic: per-CTA partials [B][4][N2] reduced in fixed
-// order by one-thread-per-instance scalar kernels, which also hold the
-// reference's BiCGSTAB/PCG control flow (krylov.py:43-153).
+// A length-n filter  y = IFFT_n( S . FFT_n(x) )  is three kernels:
+//   col_fwd : G adjacent columns t2 per CTA, x[N2 t1 + t2] (t1 < N1) -> FFT_N1
+//             -> * W_n^{t2 k1} -> Z[k1][t2]      (prologue: load / Krylov
+//                                                  vector update)
+//   row     : one row k1 per CTA, FFT_N2 over Z[k1][.] -> * S[k1 + N1 k2]
+//             -> IFFT_N2                         (S stored permuted [k1][k2])
+//   col_inv : Z[.][t2] * conj(W_n^{t2 k1}) -> IFFT_N1 -> y at j = N2 t1 + t2
+//                                                 (epilogue: store / combine
+//                                                  with the operator / dot
+//                                                  partials)
+// The Toeplitz product uses the even/odd-bin split of the single-CTA engine
+// (tsf_filters.cuh): two length-n filters, the odd one on x_j W_L^j.  Both
+// run as two CHANNELS of the same three launches (Z holds both), and the
+// column epilogue combines them in registers: y = d x + kappa (ye + Re(conj(w) zo)).
+// Column CTAs run G transforms side by side with the group index in the
+// fast thread bits, so every warp access covers G adjacent columns (full
+// 32-byte sectors from G = 4 on).
+// Reductions are deterministic: per-CTA partials [B][4][np] reduced in fixed
+// order by one-CTA-per-instance scalar kernels (tsf_large.cu), which also
+// hold the reference's BiCGSTAB control flow (krylov.py:88-153).
 #pragma once
 
 #include "tsf_kernels.cuh"
@@ -24,13 +30,13 @@ namespace tsf {
 struct LargeTables {
   const double2* tw1;   // two-level W_N1 table (column transforms)
   const double2* tw2;   // two-level W_N2 table (row transforms)
-  const double2* twN;   // two-level W_N table (N = n): inter-pass twiddles
+  const double2* twN;   // two-level W_n table: inter-pass twiddles
   const double2* twL;   // two-level W_L table (L = 2n), modulation of the odd half
   const double2* sEO;   // [k1][k2] -> (S_{2k}, S_{2k+1}) / L at k = k1 + N1 k2
   const double2* lamP;  // [k1][k2] -> (lam_k, lam_{n-k}) at k = k1 + N1 k2 (Strang)
 };
 
-// BiCGSTAB / PCG per-instance control (scalar kernels)
+// BiCGSTAB per-instance control (scalar kernels)
 enum LMode : int { LM_ACTIVE = 0, LM_EARLY = 1, LM_DONE = 2 };
 
 struct LState {
@@ -40,27 +46,26 @@ struct LState {
 
 // Column prologues
 enum ColIn : int {
-  CI_LOAD = 0,     // z = x
-  CI_MOD = 1,      // z = x_j W_L^j
-  CI_PUPD = 2,     // p = r + beta (p - omega v) (or r0 at it 1); store p; z = p
+  CI_LOAD = 0,     // z = x                                    (1 channel)
+  CI_PUPD = 2,     // p = r + beta (p - omega v) (r0 at it 1); store p; z = p
   CI_SUPD = 3,     // s = r - alpha v; store s; ||s||^2 partial; z = s
+  CI_APPLY = 4,    // channel 0: z = x ; channel 1: z = x_j W_L^j
 };
 // Column epilogues
 enum ColOut : int {
   CO_REAL = 0,     // y_j = Re z   (store)
-  CO_COMBINE = 1,  // y_j = d x_j + kappa_j (ye_j + Re(conj(w_j) z)) ; dot partials
+  CO_APPLY = 1,    // y_j = d x_j + kappa_j (Re z0_j + Re(conj(w_j) z1_j)) ; dot partials
 };
 // Row spectra
-enum RowSpec : int { RS_EVEN = 0, RS_ODD = 1, RS_STRANG = 2 };
+enum RowSpec : int { RS_APPLY = 0, RS_STRANG = 2 };
 
 struct LargeArgs {
   int n, B;
   LargeTables lt;
-  double2* Z;          // [B][N] transform work array
-  double* ye;          // [B][N] even-half result
-  double* part;        // [B][4][NP] partial sums (NP = max(N1, N2))
+  double2* Z;          // [2][B][n] transform work array (channel-major)
+  double* part;        // [B][4][np] partial sums
   int np;
-  LState* st;          // [B]
+  LState* st;          // [B] (null: standalone matvec / preconditioner)
   // Krylov vectors [B][n]
   const double* r0;
   double* x;
@@ -72,7 +77,7 @@ struct LargeArgs {
   double* sh;
   double* t;
   const double* kappa;  // level diffusivity [B][n] (null: plain Toeplitz product)
-  double* pspec;       // [B][N] permuted Strang spectrum S_k / n
+  double* pspec;        // [B][n] permuted Strang spectrum S_k / n
   double shift;
   double tol;
   int max_iters;
@@ -82,12 +87,30 @@ struct LargeArgs {
   int* active;
 };
 
-TSF_D bool inst_skip(const LargeArgs& a, int b) { return a.st[b].mode != LM_ACTIVE; }
+TSF_D bool inst_skip(const LargeArgs& a, int b) { return a.st && a.st[b].mode != LM_ACTIVE; }
 
 // two-level table lookup straight from global memory (L1/L2 resident)
 TSF_D double2 tw_get_g(const double2* tw, long e) {
   return cmul(ldt(&tw[kTwLo + (e >> 6)]), ldt(&tw[tw_lo_slot((int)(e & 63))]));
 }
+
+// Column-kernel geometry: G transforms of length N1 per CTA, T threads each.
+template <int N1>
+struct LCol {
+  static constexpr int E = FShape<N1>::E;
+  static constexpr int T = N1 / E;
+  static constexpr int G = T >= 512 ? 1 : (512 / T > 16 ? 16 : 512 / T);
+  static constexpr int BLOCK = G * T;
+  static constexpr int BUF = 2 * FftPlan<N1, E>::SMEM_ELEMS;  // ping-pong, per group
+  static constexpr int SMEM = (G * BUF + tw_table_elems(N1)) * 16;
+};
+template <int N2>
+struct LRow {
+  static constexpr int E = FShape<N2>::E;
+  static constexpr int T = N2 / E;
+  static constexpr int BLOCK = T < 32 ? 32 : T;
+  static constexpr int SMEM = (2 * FftPlan<N2, E>::SMEM_ELEMS + tw_table_elems(N2)) * 16;
+};
 
 template <int NT>
 TSF_D void stage_tw(double2* dst, const double2* src) {
@@ -96,155 +119,182 @@ TSF_D void stage_tw(double2* dst, const double2* src) {
 
 // ------------------------------------------------------------ col_fwd
 template <int N1>
-__global__ void __launch_bounds__(FShape<N1>::T < 32 ? 32 : FShape<N1>::T)
-k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode, int real_input) {
+__global__ void __launch_bounds__(LCol<N1>::BLOCK, 1)
+k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
+  using C = LCol<N1>;
+  constexpr int E = C::E, T = C::T, G = C::G;
   const int N2 = a.n / N1;
   const long N = a.n;
-  constexpr int E = FShape<N1>::E;
-  constexpr int T = FShape<N1>::T;
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
-  const int t2 = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
-  if (a.st && inst_skip(a, b)) return;
-  double2* tw1 = sm + 2 * FftPlan<N1, E>::SMEM_ELEMS;
+  const int b = blockIdx.y;
+  if (inst_skip(a, b)) return;
+  const int g = threadIdx.x % G, tid = threadIdx.x / G;
+  const int t2 = blockIdx.x * G + g;
+  double2* smg = sm + g * C::BUF;
+  double2* tw1 = sm + G * C::BUF;
   stage_tw<N1>(tw1, a.lt.tw1);
-  const long off = (long)b * a.n;
-  const bool own = tid < T;
+  const long off = (long)b * N;
   double xr[E];
   double2 z[E];
   double part = 0.0;
   const LState stv = a.st ? a.st[b] : LState{};
-  if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) {
-      const int t1 = tid + c * T;
-      const long j = (long)N2 * t1 + t2;
-      double val;
-      if (in_mode == CI_PUPD) {
-        if (stv.it == 1) {
-          val = a.r0[off + j];
-        } else {
-          const double beta = (stv.rho_new / stv.rho) * (stv.alpha / stv.omega);
-          val = a.r[off + j] + beta * (a.p[off + j] - stv.omega * a.v[off + j]);
-        }
-        a.p[off + j] = val;
-      } else if (in_mode == CI_SUPD) {
-        const double* rc = (stv.it == 1) ? a.r0 : a.r;
-        val = rc[off + j] - stv.alpha * a.v[off + j];
-        a.s[off + j] = val;
-        part = fma(val, val, part);
+  for (int c = 0; c < E; ++c) {
+    const long j = (long)N2 * (tid + c * T) + t2;
+    double val;
+    if (in_mode == CI_PUPD) {
+      if (stv.it == 1) {
+        val = a.r0[off + j];
       } else {
-        val = src[off + j];
+        const double beta = (stv.rho_new / stv.rho) * (stv.alpha / stv.omega);
+        val = a.r[off + j] + beta * (a.p[off + j] - stv.omega * a.v[off + j]);
       }
-      xr[c] = val;
-      if (!real_input) z[c] = cscale(tw_get_g(a.lt.twL, j), val);  // x_j W_L^j
+      a.p[off + j] = val;
+    } else if (in_mode == CI_SUPD) {
+      const double* rc = (stv.it == 1) ? a.r0 : a.r;
+      val = rc[off + j] - stv.alpha * a.v[off + j];
+      a.s[off + j] = val;
+      part = fma(val, val, part);
+    } else {
+      val = src[off + j];
     }
+    xr[c] = val;
   }
   if (in_mode == CI_SUPD) {
     part = block_sum1(part, red);
-    if (tid == 0) a.part[((long)b * 4 + 2) * a.np + t2] = part;
+    if (threadIdx.x == 0) a.part[((long)b * 4 + 2) * a.np + blockIdx.x] = part;
   }
-  if (real_input) block_fft_real<N1, E>(xr, z, sm, tw1, 0);
-  else block_fft<N1, E, false>(z, sm, tw1, 0);
-  if (own) {
+  group_fft_real<N1, E>(xr, z, smg, tw1, 0, tid);
+#pragma unroll
+  for (int c = 0; c < E; ++c) {
+    const int k1 = tid + c * T;
+    const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
+    a.Z[off + (long)k1 * N2 + t2] = cmul(z[c], w);
+  }
+  if (in_mode == CI_APPLY) {
+    // odd channel: the modulated input x_j W_L^j
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const long j = (long)N2 * (tid + c * T) + t2;
+      z[c] = cscale(tw_get_g(a.lt.twL, j), xr[c]);
+    }
+    group_fft<N1, E, false>(z, smg, tw1, 0, tid);
+    double2* Zo = a.Z + (long)a.B * N;
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int k1 = tid + c * T;
-      const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) % N);
-      a.Z[(long)b * N + (long)k1 * N2 + t2] = cmul(z[c], w);
+      const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
+      Zo[off + (long)k1 * N2 + t2] = cmul(z[c], w);
     }
   }
 }
 
 // ------------------------------------------------------------ row
 template <int N2>
-__global__ void __launch_bounds__(FShape<N2>::T < 32 ? 32 : FShape<N2>::T)
+__global__ void __launch_bounds__(LRow<N2>::BLOCK, 1)
 k_lrow(LargeArgs a, int spec_mode) {
   const long N = a.n;
-  constexpr int E = FShape<N2>::E;
-  constexpr int T = FShape<N2>::T;
+  constexpr int E = LRow<N2>::E;
+  constexpr int T = LRow<N2>::T;
   extern __shared__ double2 sm[];
   const int k1 = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
-  if (a.st && inst_skip(a, b)) return;
+  if (inst_skip(a, b)) return;
   double2* tw2 = sm + 2 * FftPlan<N2, E>::SMEM_ELEMS;
   stage_tw<N2>(tw2, a.lt.tw2);
   const bool own = tid < T;
-  double2* row = a.Z + (long)b * N + (long)k1 * N2;
-  double2 z[E];
-  if (own) {
+  const int nch = spec_mode == RS_APPLY ? 2 : 1;
+  for (int ch = 0; ch < nch; ++ch) {
+    double2* row = a.Z + (long)ch * a.B * N + (long)b * N + (long)k1 * N2;
+    double2 z[E];
+    if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) z[c] = row[tid + c * T];
-  }
-  block_fft<N2, E, false>(z, sm, tw2, 0);
-  if (own) {
-#pragma unroll
-    for (int c = 0; c < E; ++c) {
-      const long idx = (long)k1 * N2 + tid + c * T;   // bin k1 + N1 k2
-      double s;
-      if (spec_mode == RS_EVEN) s = ldt(&a.lt.sEO[idx]).x;
-      else if (spec_mode == RS_ODD) s = ldt(&a.lt.sEO[idx]).y;
-      else s = a.pspec[(long)b * N + idx];
-      z[c] = cscale(z[c], s);
+      for (int c = 0; c < E; ++c) z[c] = row[tid + c * T];
     }
-  }
-  block_fft<N2, E, true>(z, sm, tw2, 0);
-  if (own) {
+    block_fft<N2, E, false>(z, sm, tw2, 0);
+    if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) row[tid + c * T] = z[c];
+      for (int c = 0; c < E; ++c) {
+        const long idx = (long)k1 * N2 + tid + c * T;   // bin k1 + N1 k2
+        double s;
+        if (spec_mode == RS_APPLY) {
+          const double2 se = ldt(&a.lt.sEO[idx]);
+          s = ch == 0 ? se.x : se.y;
+        } else {
+          s = a.pspec[(long)b * N + idx];
+        }
+        z[c] = cscale(z[c], s);
+      }
+    }
+    block_fft<N2, E, true>(z, sm, tw2, 0);
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) row[tid + c * T] = z[c];
+    }
   }
 }
 
 // ------------------------------------------------------------ col_inv
 template <int N1>
-__global__ void __launch_bounds__(FShape<N1>::T < 32 ? 32 : FShape<N1>::T)
+__global__ void __launch_bounds__(LCol<N1>::BLOCK, 1)
 k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __restrict__ xin,
            const double* __restrict__ w1, int pslot) {
+  using C = LCol<N1>;
+  constexpr int E = C::E, T = C::T, G = C::G;
   const int N2 = a.n / N1;
   const long N = a.n;
-  constexpr int E = FShape<N1>::E;
-  constexpr int T = FShape<N1>::T;
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
-  const int t2 = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
-  if (a.st && inst_skip(a, b)) return;
-  double2* tw1 = sm + 2 * FftPlan<N1, E>::SMEM_ELEMS;
+  const int b = blockIdx.y;
+  if (inst_skip(a, b)) return;
+  const int g = threadIdx.x % G, tid = threadIdx.x / G;
+  const int t2 = blockIdx.x * G + g;
+  double2* smg = sm + g * C::BUF;
+  double2* tw1 = sm + G * C::BUF;
   stage_tw<N1>(tw1, a.lt.tw1);
-  const long off = (long)b * a.n;
-  const bool own = tid < T;
+  const long off = (long)b * N;
   double2 z[E];
-  if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) {
-      const int k1 = tid + c * T;
-      const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) % N);
-      z[c] = cmulc(a.Z[(long)b * N + (long)k1 * N2 + t2], w);
-    }
+  for (int c = 0; c < E; ++c) {
+    const int k1 = tid + c * T;
+    const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
+    z[c] = cmulc(a.Z[off + (long)k1 * N2 + t2], w);
   }
-  block_fft<N1, E, true>(z, sm, tw1, 0);
+  group_fft<N1, E, true>(z, smg, tw1, 0, tid);
+  if (out_mode == CO_REAL) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) dst[off + (long)N2 * (tid + c * T) + t2] = z[c].x;
+    return;
+  }
+  // CO_APPLY: even channel result in registers, then the odd channel
+  double ye[E];
+#pragma unroll
+  for (int c = 0; c < E; ++c) ye[c] = z[c].x;
+  const double2* Zo = a.Z + (long)a.B * N;
+#pragma unroll
+  for (int c = 0; c < E; ++c) {
+    const int k1 = tid + c * T;
+    const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
+    z[c] = cmulc(Zo[off + (long)k1 * N2 + t2], w);
+  }
+  group_fft<N1, E, true>(z, smg, tw1, 0, tid);
   Vals<2> pr;
   pr.v[0] = pr.v[1] = 0.0;
-  if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) {
-      const int t1 = tid + c * T;
-      const long j = (long)N2 * t1 + t2;
-      if (out_mode == CO_REAL) {
-        dst[off + j] = z[c].x;
-      } else {
-        const double2 w = tw_get_g(a.lt.twL, j);
-        const double ax = a.ye[off + j] + fma(z[c].x, w.x, z[c].y * w.y);
-        const double y = a.kappa ? fma(a.shift, xin[off + j], a.kappa[off + j] * ax) : ax;
-        dst[off + j] = y;
-        pr.v[0] = fma(y, y, pr.v[0]);
-        if (w1) pr.v[1] = fma(y, w1[off + j], pr.v[1]);
-      }
-    }
+  for (int c = 0; c < E; ++c) {
+    const long j = (long)N2 * (tid + c * T) + t2;
+    const double2 w = tw_get_g(a.lt.twL, j);
+    const double ax = ye[c] + fma(z[c].x, w.x, z[c].y * w.y);  // + Re(conj(w) z)
+    const double y = a.kappa ? fma(a.shift, xin[off + j], a.kappa[off + j] * ax) : ax;
+    dst[off + j] = y;
+    pr.v[0] = fma(y, y, pr.v[0]);
+    if (w1) pr.v[1] = fma(y, w1[off + j], pr.v[1]);
   }
-  if (out_mode == CO_COMBINE && pslot >= 0) {
+  if (pslot >= 0) {
     pr = block_sum<2>(pr, red);
-    if (tid == 0) {
-      a.part[((long)b * 4 + pslot) * a.np + t2] = pr.v[0];
-      a.part[((long)b * 4 + pslot + 1) * a.np + t2] = pr.v[1];
+    if (threadIdx.x == 0) {
+      a.part[((long)b * 4 + pslot) * a.np + blockIdx.x] = pr.v[0];
+      a.part[((long)b * 4 + pslot + 1) * a.np + blockIdx.x] = pr.v[1];
     }
   }
 }
@@ -256,11 +306,11 @@ constexpr int kLargeMaxLog = 12;  // N1, N2 <= 4096  ->  n <= 2^24
 
 template <int LOG>
 struct LargeDispatch {
-  static int col_fwd(const LargeArgs& a, const double* src, int in_mode, int real_input,
-                     cudaStream_t st);
+  static int col_fwd(const LargeArgs& a, const double* src, int in_mode, cudaStream_t st);
   static int row(const LargeArgs& a, int spec_mode, cudaStream_t st);
   static int col_inv(const LargeArgs& a, double* dst, int out_mode, const double* xin,
                      const double* w1, int pslot, cudaStream_t st);
+  static int col_group();  // G: columns per column CTA
 };
 
 #define TSF_EXTERN_LARGE(L) extern template struct LargeDispatch<L>;

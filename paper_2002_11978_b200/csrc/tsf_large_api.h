@@ -16,6 +16,7 @@ std::vector<double2> twiddle_table(int N);
 
 struct LargePlan {
   int n = 0, N1 = 0, N2 = 0, np = 0;
+  int ncol_cta = 0;            // column CTAs per instance (partial-sum count)
   int has_pc = 0;
   int device = 0;
   double lam_min = 0.0;       // min_k lam_k (preconditioner positivity test)
@@ -23,8 +24,8 @@ struct LargePlan {
   double2* tables = nullptr;  // one allocation for every table
   // workspaces, sized for `cap` instances
   int cap = 0;
-  double* ws = nullptr;       // 10 vectors [cap][n]
-  double2* Z = nullptr;       // [cap][n]
+  double* ws = nullptr;       // 9 vectors [cap][n]
+  double2* Z = nullptr;       // [2][cap][n] (two transform channels)
   double* part = nullptr;     // [cap][4][np]
   LState* st = nullptr;       // [cap]
   int* active = nullptr;

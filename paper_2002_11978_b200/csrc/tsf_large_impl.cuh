@@ -9,14 +9,6 @@
 
 namespace tsf {
 
-template <int N>
-struct LShape {
-  static constexpr int T = FShape<N>::T;
-  static constexpr int BLOCK = T < 32 ? 32 : T;
-  // ping-pong transform buffers | staged two-level twiddle table of W_N
-  static constexpr int SMEM = 2 * FftPlan<N, FShape<N>::E>::SMEM_ELEMS * 16 + tw_table_elems(N) * 16;
-};
-
 inline int large_launch_error(cudaError_t e) {
   return e == cudaSuccess ? 0 : report_cuda(e, "large-n kernel launch");
 }
@@ -28,20 +20,20 @@ inline cudaError_t large_prep(K kernel, int smem) {
 
 template <int LOG>
 int LargeDispatch<LOG>::col_fwd(const LargeArgs& a, const double* src, int in_mode,
-                                int real_input, cudaStream_t st) {
+                                cudaStream_t st) {
   constexpr int N1 = 1 << LOG;
-  using S = LShape<N1>;
+  using S = LCol<N1>;
   auto k = k_lcol_fwd<N1>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  k<<<dim3(a.n / N1, a.B), S::BLOCK, S::SMEM, st>>>(a, src, in_mode, real_input);
+  k<<<dim3(a.n / N1 / S::G, a.B), S::BLOCK, S::SMEM, st>>>(a, src, in_mode);
   return large_launch_error(cudaGetLastError());
 }
 
 template <int LOG>
 int LargeDispatch<LOG>::row(const LargeArgs& a, int spec_mode, cudaStream_t st) {
   constexpr int N2 = 1 << LOG;
-  using S = LShape<N2>;
+  using S = LRow<N2>;
   auto k = k_lrow<N2>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
@@ -53,12 +45,17 @@ template <int LOG>
 int LargeDispatch<LOG>::col_inv(const LargeArgs& a, double* dst, int out_mode, const double* xin,
                                 const double* w1, int pslot, cudaStream_t st) {
   constexpr int N1 = 1 << LOG;
-  using S = LShape<N1>;
+  using S = LCol<N1>;
   auto k = k_lcol_inv<N1>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  k<<<dim3(a.n / N1, a.B), S::BLOCK, S::SMEM, st>>>(a, dst, out_mode, xin, w1, pslot);
+  k<<<dim3(a.n / N1 / S::G, a.B), S::BLOCK, S::SMEM, st>>>(a, dst, out_mode, xin, w1, pslot);
   return large_launch_error(cudaGetLastError());
+}
+
+template <int LOG>
+int LargeDispatch<LOG>::col_group() {
+  return LCol<1 << LOG>::G;
 }
 
 }  // namespace tsf

@@ -3,8 +3,9 @@
 Mirror of tsfrac.toeplitz (toeplitz.py:21-136).  The symbol and the Strang
 eigenvalues are host setup (one numpy FFT each, as in the reference, so
 they are bit-identical to it); `toeplitz_matvec` and `precond_solve` run the
-sm_100a real-packed FFT filter kernels (csrc/tsf_filters.cuh) through the C
-ABI.  Inputs may be numpy arrays (copied) or torch CUDA tensors [n] or
+sm_100a FFT filter kernels through the C ABI (n <= 4096: one CTA per
+instance, csrc/tsf_filters.cuh; larger powers of two: the four-step engine,
+csrc/tsf_large.cuh).  Inputs may be numpy arrays (copied) or torch CUDA tensors [n] or
 [B, n] (zero-copy, batched).
 """
 
@@ -81,9 +82,10 @@ class ToeplitzOperator:
 
     @property
     def plan(self) -> _native.Plan:
-        if self._plan is not None:
-            return self._plan
-        return plan_for(self.first_col, self.device, spectrum=self.spectrum_embed)
+        if self._plan is None:   # built once per operator (hashing + host setup)
+            object.__setattr__(self, "_plan",
+                               plan_for(self.first_col, self.device, spectrum=self.spectrum_embed))
+        return self._plan
 
     def matvec(self, v):
         return toeplitz_matvec(self, v)
@@ -154,15 +156,21 @@ class CirculantPreconditioner:
     first_col: Optional[np.ndarray] = field(default=None, compare=False, repr=False)
     device: int = 0
 
+    _plan: Optional[_native.Plan] = field(default=None, compare=False, repr=False)
+
     def solve(self, v):
         return precond_solve(self, v)
 
     @property
     def plan(self) -> _native.Plan:
-        if self.first_col is not None:
-            return plan_for(self.first_col, self.device, lam=self.lam)
-        # bare spectrum: a plan whose "lam" is the given eigenvalue array
-        return plan_for(np.zeros(self.n), self.device, lam=self.lam)
+        if self._plan is None:   # built once per preconditioner
+            if self.first_col is not None:
+                pl = plan_for(self.first_col, self.device, lam=self.lam)
+            else:
+                # bare spectrum: a plan whose "lam" is the given eigenvalue array
+                pl = plan_for(np.zeros(self.n), self.device, lam=self.lam)
+            object.__setattr__(self, "_plan", pl)
+        return self._plan
 
 
 def build_preconditioner(d, shift: float, kappa_bar: float, device: int = 0
