@@ -7,17 +7,26 @@ PKG := paper_2002_11978_b200
 CSRC := $(PKG)/csrc
 SRCS := $(CSRC)/tsf_abi.cu $(CSRC)/tsf_large.cu $(wildcard $(CSRC)/gen/inst_L*.cu) \
         $(wildcard $(CSRC)/gen/large_L*.cu)
-OBJS := $(patsubst $(CSRC)/%.cu,build/obj/%.o,$(SRCS))
+# Kernel-variant experiments: `make VARIANT=e16 L13_FLAGS="-DTSF_KE=16 -DTSF_MINB=1"`
+# builds build/<variant>/libtsfrac_b200.so (load it with TSF_LIB=...); the
+# product library is the default (no VARIANT).
+VARIANT ?=
+OBJDIR := build/obj$(if $(VARIANT),_$(VARIANT),)
+OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/tsfrac_b200.h
-LIB := $(PKG)/libtsfrac_b200.so
+LIB := $(if $(VARIANT),build/$(VARIANT)/libtsfrac_b200.so,$(PKG)/libtsfrac_b200.so)
+L13_FLAGS ?=
 
 all: $(LIB)
 
-build/obj/%.o: $(CSRC)/%.cu $(HDRS)
+$(OBJDIR)/gen/inst_L13.o: NVFLAGS += $(L13_FLAGS)
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o $@ $< 2> $@.ptxas || (cat $@.ptxas; false)
 
 $(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
 clean:

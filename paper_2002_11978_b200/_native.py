@@ -77,7 +77,8 @@ def load(path: Optional[os.PathLike] = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # TSF_LIB: an alternative build of the same ABI (kernel-variant experiments)
+    p = Path(path) if path else Path(os.environ.get("TSF_LIB", LIB_PATH))
     if not p.exists():
         raise NativeError(
             f"{p.name} is not built ({p}); run `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -53,7 +53,7 @@ int report_cuda(cudaError_t e, const char* what) {
 int report_error(int code, const char* msg) { return fail(code, "%s", msg); }
 
 // two-level twiddle table of W_N (tsf_fft.cuh tw_get): padded [W^j, j < 64]
-// then [W^(64 i), i < max(1, N/64)], computed in long double
+// then padded [W^(64 i), i < max(1, N/64)], computed in long double
 std::vector<double2> twiddle_table(int N) {
   const long double two_pi = 6.283185307179586476925286766559005768L;
   auto w = [&](long e) {
@@ -62,7 +62,7 @@ std::vector<double2> twiddle_table(int N) {
   };
   std::vector<double2> t(tw_table_elems(N), make_double2(0.0, 0.0));
   for (int j = 0; j < 64; ++j) t[tw_lo_slot(j)] = w(j);
-  for (int i = 0; i < (int)t.size() - kTwLo; ++i) t[kTwLo + i] = w(64L * i);
+  for (int i = 0; i < tw_hi_count(N); ++i) t[kTwLo + tw_lo_slot(i)] = w(64L * i);
   return t;
 }
 }  // namespace tsf

@@ -30,6 +30,33 @@ TSF_HD double2 mul_mi(double2 a) {
 // reads are identical in every FFT of a Krylov iteration, so ptxas kept all
 // of them live across the whole loop and spilled.  The
 // re-read hits L1.
+// Asynchronous global -> shared copies (16 bytes, L2 only); completion is
+// awaited with cp_async_wait_all() followed by a barrier.
+TSF_D void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+TSF_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+TSF_D void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Software prefetch of a whole vector (one 128-byte line per thread and
+// step): into L2 at phase start for the vectors an epilogue reads after
+// the transforms, into L1 right before the last transform for the ones read
+// first (ncu: the epilogue loads of kappa / rhs were the top stalls).
+#ifndef TSF_PREFETCH
+#define TSF_PREFETCH 1
+#endif
+TSF_D void prefetch_l2(const double* p, int n) {
+  if (!TSF_PREFETCH) return;
+  for (int i = 16 * threadIdx.x; i < n; i += 16 * blockDim.x)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + i));
+}
+TSF_D void prefetch_l1(const double* p, int n) {
+  if (!TSF_PREFETCH) return;
+  for (int i = 16 * threadIdx.x; i < n; i += 16 * blockDim.x)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p + i));
+}
+
 TSF_D double2 ldt(const double2* p) {
   double2 v;
   asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));

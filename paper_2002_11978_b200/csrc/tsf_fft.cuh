@@ -148,8 +148,8 @@ TSF_D void dft(double2* a) {
 
 // ------------------------------------------------------------ twiddles
 // Two-level table staged in shared memory by every kernel:
-//   tw[lo_slot(j)] = W^j,       j < 64
-//   tw[72 + i]     = W^(64 i),  i < max(1, NT/64)
+//   tw[lo_slot(j)]      = W^j,       j < 64
+//   tw[72 + lo_slot(i)] = W^(64 i),  i < max(1, NT/64)
 // so W^e = hi[e >> 6] * lo[e & 63] (within ~1 ulp; both factors are
 // correctly rounded long-double values).  A full table of NT entries (128 KB
 // at NT = 8192) does not fit the L1 left beside the transform buffers, and
@@ -160,14 +160,19 @@ TSF_D void dft(double2* a) {
 // no mid-pass barrier.  See DESIGN.md §3.1.
 constexpr bool kFftInPlace = TSF_FFT_INPLACE;
 
-// The 64-entry low table is stored padded, slot i at i + (i >> 3): the
-// W^{2k}, W^{4k}, W^{8k} lookups of a warp then hit distinct banks (unpadded
-// they were 2/4/8-way conflicts, 28% of all shared wavefronts in ncu).
+// Both halves are stored padded, entry i at slot i + (i >> 3): the W^{k},
+// W^{2k}, W^{4k} lookups of a warp walk either table with strides 1..8 and
+// then hit distinct banks (unpadded they were 2/4/8-way conflicts: the low
+// table 28% of all shared wavefronts, the high table 8-way on the first
+// twiddled pass, both seen in ncu).
 constexpr int kTwLo = 72;
 TSF_HD constexpr int tw_lo_slot(int j) { return j + (j >> 3); }
-TSF_HD constexpr int tw_table_elems(int NT) { return kTwLo + (NT / 64 > 1 ? NT / 64 : 1); }
+TSF_HD constexpr int tw_hi_count(int NT) { return NT / 64 > 1 ? NT / 64 : 1; }
+TSF_HD constexpr int tw_table_elems(int NT) {
+  return kTwLo + tw_hi_count(NT) + (tw_hi_count(NT) >> 3) + 1;
+}
 TSF_D double2 tw_get(const double2* tw, int e) {
-  return cmul(tw[kTwLo + (e >> 6)], tw[tw_lo_slot(e & 63)]);
+  return cmul(tw[kTwLo + tw_lo_slot(e >> 6)], tw[tw_lo_slot(e & 63)]);
 }
 
 // ------------------------------------------------------------ pass plan
@@ -271,6 +276,7 @@ TSF_D void fft_rec(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
   constexpr bool LAST = (P == PL::NPASS - 1);
   stockham_pass<N, E, P, INV, FIRST, LAST>(v, sm, tw, tw_log_scale, tid, own);
   if constexpr (!LAST) {
+    cp_async_wait_all();  // staged tables (tsf_filters.cuh stage_tables) land here
     __syncthreads();
     fft_rec<N, E, P + 1, INV>(v, sm, tw, tw_log_scale, tid, own);
   }

@@ -36,6 +36,7 @@ struct FilterTables {
   const double2* tw;    // two-level W_L table (tsf_fft.cuh tw_get); kernels stage it in smem
   const double2* mvS;   // (S_{2k}, S_{2k+1}) / L, even part of the symbol, k < N
   const double2* pclam; // (lam_k, lam_{n-k}), k < n   (pow2 n = N only)
+  const double* ps = nullptr;  // the instance's staged Strang spectrum (shared memory) or null
 };
 
 TSF_D double ld_real(const double* __restrict__ base, int n, int j) {
@@ -57,6 +58,39 @@ struct FShape {
   static constexpr int T = N / E;
 };
 
+// Shared-memory plan of the single-CTA kernels:
+//   transform buffer(s) | real staging vector (N doubles) | twiddle table |
+//   [symbol table mvS, N double2] | [instance Strang spectrum, N doubles]
+// With TSF_STAGE_TABLES=1 the two tables are staged (cp.async at kernel
+// start, landing while the first transform runs) when they fit without
+// lowering the CTAs per SM.  Measured slower on configs[2] (35.1 / 36.5 ms
+// per level vs 33.1 ms, ping-pong / in-place): the bigger carve-out costs the
+// L1 the streaming vectors use, so it is off by default.
+#ifndef TSF_STAGE_TABLES
+#define TSF_STAGE_TABLES 0
+#endif
+constexpr int kSmemCap = 227 * 1024;       // dynamic shared memory per CTA
+constexpr int kSmemPerSM = 228 * 1024;
+template <int N>
+struct FStage {
+  static constexpr int FFT_BYTES = (kFftInPlace ? 1 : 2) * FftPlan<N, kE>::SMEM_ELEMS * 16;
+  static constexpr int TW_BYTES = tw_table_elems(2 * N) * 16;
+  static constexpr int BASE = FFT_BYTES + N * 8 + TW_BYTES;
+  static constexpr int BLOCK = (N / kE) < 32 ? 32 : (N / kE);
+  static constexpr int REG_CTAS = (65536 / (BLOCK * 128)) < 1 ? 1 : 65536 / (BLOCK * 128);
+  static constexpr int occ(int bytes) { return kSmemPerSM / (bytes + 1024 + 1024); }
+  static constexpr int OCC0 = occ(BASE) < REG_CTAS ? occ(BASE) : REG_CTAS;
+  static constexpr bool PS = TSF_STAGE_TABLES && BASE + N * 8 <= kSmemCap && occ(BASE + N * 8) >= OCC0;
+  static constexpr bool MV = PS && BASE + N * 24 <= kSmemCap && occ(BASE + N * 24) >= OCC0;
+  static constexpr int SMEM = BASE + (PS ? N * 8 : 0) + (MV ? N * 16 : 0);
+};
+
+template <int N>
+TSF_D double2 mv_spec(const FilterTables& t, int k) {
+  if constexpr (FStage<N>::MV) return t.mvS[k];   // staged in shared memory
+  else return ldt(&t.mvS[k]);
+}
+
 // even output bins: z <- IFFT_N( S_even . FFT_N(x) ) for real x; caller keeps Re(z)
 template <int N>
 TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E], double2* sm,
@@ -66,7 +100,7 @@ TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E]
   block_fft_real<N, E>(x, z, sm, t.tw, 1);
   if (threadIdx.x < T) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], ldt(&t.mvS[threadIdx.x + c * T]).x);
+    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], mv_spec<N>(t, threadIdx.x + c * T).x);
   }
   block_fft<N, E, true>(z, sm, t.tw, 1);
 }
@@ -80,7 +114,7 @@ TSF_D void filt_odd(double2 (&z)[FShape<N>::E], double2* sm, const FilterTables&
   block_fft<N, E, false>(z, sm, t.tw, 1);
   if (threadIdx.x < T) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], ldt(&t.mvS[threadIdx.x + c * T]).y);
+    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], mv_spec<N>(t, threadIdx.x + c * T).y);
   }
   block_fft<N, E, true>(z, sm, t.tw, 1);
 }
@@ -124,14 +158,30 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
 TSF_D double2 modulation(const FilterTables& t, int j) { return tw_get(t.tw, j); }
 
 // Copy the two-level twiddle table of the length-L = 2N embedding into
-// shared memory at `dst`; returns the tables with tw redirected there.  The
-// first transform's leading barrier publishes the copy.
+// shared memory at `dst` (the first transform's leading barrier publishes
+// it) and start the asynchronous copies of the staged tables (FStage; the
+// transforms' inter-pass barriers wait for them, tsf_fft.cuh fft_rec).
+// `ps_src`: the instance's Strang spectrum to stage, or null.
 template <int N>
-TSF_D FilterTables stage_tables(const FilterTables& g, double2* dst) {
+TSF_D FilterTables stage_tables(const FilterTables& g, double2* dst, const double* ps_src = nullptr) {
   constexpr int NT = tw_table_elems(2 * N);
   for (int i = threadIdx.x; i < NT; i += blockDim.x) dst[i] = ldt(&g.tw[i]);
   FilterTables t = g;
   t.tw = dst;
+  double2* next = dst + NT;
+  if constexpr (FStage<N>::MV) {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) cp_async16(&next[i], &g.mvS[i]);
+    t.mvS = next;
+    next += N;
+  }
+  if constexpr (FStage<N>::PS) {
+    if (ps_src) {
+      double* ps = reinterpret_cast<double*>(next);
+      for (int i = 2 * threadIdx.x; i < N; i += 2 * blockDim.x) cp_async16(&ps[i], &ps_src[i]);
+      t.ps = ps;
+    }
+  }
+  cp_async_commit();
   return t;
 }
 

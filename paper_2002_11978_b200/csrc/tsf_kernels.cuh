@@ -68,12 +68,15 @@ struct KShape {
   static constexpr int E = FShape<N>::E;
   static constexpr int T = FShape<N>::T;         // owning threads
   static constexpr int BLOCK = T < 32 ? 32 : T;  // launched threads
-  static constexpr int FFT_BYTES = (kFftInPlace ? 1 : 2) * FftPlan<N, E>::SMEM_ELEMS * 16;
-  static constexpr int TW_BYTES = tw_table_elems(2 * N) * 16;
-  // ping-pong transform buffers | real staging vector | twiddle table
-  static constexpr int SMEM = FFT_BYTES + N * 8 + TW_BYTES;
-  static constexpr int SMEM_PC = FFT_BYTES + N * 8 + TW_BYTES;
+  static constexpr int FFT_BYTES = FStage<N>::FFT_BYTES;
+  static constexpr int TW_BYTES = FStage<N>::TW_BYTES;
+  // transform buffer(s) | real staging vector | twiddle table | staged tables
+  static constexpr int SMEM = FStage<N>::SMEM;
+#ifdef TSF_MINB
+  static constexpr int MIN_BLOCKS = TSF_MINB;
+#else
   static constexpr int MIN_BLOCKS = BLOCK >= 512 ? 1 : 512 / BLOCK;  // <= 128 regs
+#endif
 };
 
 // y = shift*x + kappa .* (A x) on the owned slots (kappa == nullptr: y = A x).
@@ -94,6 +97,9 @@ TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restric
     }
     filt_even<N>(xr, z, sm, t);
   }
+  // the combine below re-reads x and reads kappa: pull them into L1 now
+  prefetch_l1(xg, n);
+  if (kg) prefetch_l1(kg, n);
   if (own) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) aux[tid + c * T] = z[c].x;
@@ -203,7 +209,7 @@ TSF_D void precond_store(const double (&u)[FShape<N>::E], double* dst, int n, co
                          double2* sm, const FilterTables& t) {
   constexpr int T = KShape<N>::T;
   double2 z[FShape<N>::E];
-  filt_strang_tab<N>(u, z, sm, t, spec);
+  filt_strang_tab<N>(u, z, sm, t, t.ps ? t.ps : spec);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) st_real(dst, n, threadIdx.x + c * T, z[c].x);
@@ -352,6 +358,9 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   const KState s = st[b];
   const double* phg = (PC ? a.ph : a.p) + off;
   const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
+  prefetch_l2(kg, n);                  // epilogue operands (x is loaded at once)
+  prefetch_l2(a.rhs + off, n);
+  if (s.it != 1) prefetch_l2(a.r + off, n);
   double u[FShape<N>::E];
   apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, tab);   // u = v = M p_hat
   store_owned<N>(a.v + off, u, n);
@@ -418,6 +427,13 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   const KState s = st[b];
   const double* shg = (PC ? a.sh : a.s) + off;
   const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
+  prefetch_l2(kg, n);                  // epilogue operands (x is loaded at once)
+  prefetch_l2(a.s + off, n);
+  prefetch_l2(a.x + off, n);
+  if (PC) prefetch_l2(a.ph + off, n);
+  prefetch_l2(a.rhs + off, n);
+  prefetch_l2(a.p + off, n);
+  prefetch_l2(a.v + off, n);
   double u[FShape<N>::E];
   apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, tab);   // u = t = M s_hat
   Vals<2> red2;
@@ -599,7 +615,8 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
     __shared__ double red[4 * 32];                                                     \
     if (st[blockIdx.x].done) return;                                                   \
     const FilterTables tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(        \
-        reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES + N * 8));                  \
+        reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES + N * 8),                   \
+        PC ? a.pspec + (long)blockIdx.x * a.n : nullptr);                              \
     DNAME<N, PC>(a, tab, st, active, sm, red);                                         \
   }
 TSF_PHASE_KERNEL(k_bicg_v, dev_bicg_v)

@@ -91,7 +91,7 @@ TSF_D bool inst_skip(const LargeArgs& a, int b) { return a.st && a.st[b].mode !=
 
 // two-level table lookup straight from global memory (L1/L2 resident)
 TSF_D double2 tw_get_g(const double2* tw, long e) {
-  return cmul(ldt(&tw[kTwLo + (e >> 6)]), ldt(&tw[tw_lo_slot((int)(e & 63))]));
+  return cmul(ldt(&tw[kTwLo + (e >> 6) + (e >> 9)]), ldt(&tw[tw_lo_slot((int)(e & 63))]));
 }
 
 // Column-kernel geometry: G transforms of length N1 per CTA, T threads each.
