@@ -299,6 +299,8 @@ def main():
     iters = march.iters.cpu().numpy()
     large = n > 4096
     fused = os.environ.get("TSF_FUSE_SOE") == "1" and not large
+    graph = (os.environ.get("TSF_SOLVE_GRAPH", "1") != "0" and not fused
+             and os.environ.get("TSF_SOLVE_PERSIST") != "1")
     for m0, m1 in levels_done:
         its_sum += int(iters[m0 - 1: m1 - 1].sum())
         # launches per level (tsf_abi.cu tsf_fids_march): SOE push + RHS
@@ -307,10 +309,12 @@ def main():
         #   large-n engine: begin, scalar, spectrum + 23 kernels per iteration,
         # iterations launched in chunks of 4 until every instance finished
         mx = iters[m0 - 1: m1 - 1].max(axis=1)
-        chunks = np.ceil(np.maximum(mx, 1) / 4.0)
-        per_it = 23 if large else 2
-        head = 4 if large else 2
-        launches += int(np.sum(head + per_it * 4 * chunks))
+        if large:      # host-driven chunks of 4 iterations, 17 kernels each
+            launches += int(np.sum(4 + 17 * 4 * np.ceil(np.maximum(mx, 1) / 4.0)))
+        elif graph:    # one graph per level: set, begin, WHILE { v, t, test }
+            launches += int(np.sum(2 + 3 * np.maximum(mx, 1)))
+        else:
+            launches += int(np.sum(2 + 2 * 4 * np.ceil(np.maximum(mx, 1) / 4.0)))
         launches += (m1 - m0) if not fused else (1 if m0 == 1 else 0)
         launches += 1 if (m1 == M + 1 and not fused) else 0
     status = march.status.cpu().numpy()
@@ -338,7 +342,8 @@ def main():
                  "+ k_lsc/k_lel_* (23 kernels per BiCGSTAB iteration)")
     else:
         sname = (f"tsf level solve: k_solve_begin + k_bicg_v/k_bicg_t<{n},1>"
-                 + (" with fused SOE epilogue" if fused else ""))
+                 + (" with fused SOE epilogue" if fused else "")
+                 + (" (one CUDA graph per level, conditional WHILE loop)" if graph else ""))
     k_solve = {"name": sname, "avg_ms": solve_ms / K,
                "GBps": solve_bytes / (solve_ms / K * 1e-3) / 1e9,
                "iterations_per_launch": its_sum / K, "algorithmic_bytes": solve_bytes}

@@ -52,6 +52,24 @@ int report_cuda(cudaError_t e, const char* what) {
 }
 int report_error(int code, const char* msg) { return fail(code, "%s", msg); }
 
+bool graph_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_SOLVE_GRAPH");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+SolveGraphs::~SolveGraphs() {
+  for (auto& a : slot)
+    for (auto& b : a)
+      for (auto& g : b) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+      }
+}
+
 // two-level twiddle table of W_N (tsf_fft.cuh tw_get): padded [W^j, j < 64]
 // then padded [W^(64 i), i < max(1, N/64)], computed in long double
 std::vector<double2> twiddle_table(int N) {
@@ -84,6 +102,7 @@ struct tsf_plan {
   KState* kst = nullptr;    // per-instance Krylov scalars
   int* h_active = nullptr;  // pinned host mirror of the counter
   LargePlan* large = nullptr;  // n > 4096: four-step engine (tsf_large.cu)
+  SolveGraphs* graphs = nullptr;  // graph-mode level solves (tsf_dispatch_impl.cuh)
   FilterTables tables() const { return FilterTables{tw, mvS, pclam}; }
 };
 
@@ -237,6 +256,7 @@ int tsf_plan_destroy(tsf_plan* p) {
     large_plan_free(p->large);
     delete p->large;
   }
+  delete p->graphs;
   cudaFree(p->tw);
   cudaFree(p->mvS);
   cudaFree(p->pclam);
@@ -311,6 +331,11 @@ static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cud
   if (!a.kwork) a.kwork = p->ws + 7 * vn;
   a.tab = p->tables();
   if (a.max_iters <= 0) a.max_iters = 10 * p->n;
+  if (!a.soe_epilogue) {
+    // graph mode (the fused SOE epilogue keeps the host-driven loop)
+    if (!p->graphs) p->graphs = new SolveGraphs();
+    a.graphs = p->graphs;
+  }
   return ForLog<SolveF>::run(p->log_L, B, method, pc, (const KrylovArgs&)a, st);
 }
 

@@ -13,6 +13,22 @@ constexpr int kMaxLogL = 13;  // L = 8192 (n <= 4096 single-CTA engine)
 // sets tsf_last_error() and returns TSF_E_CUDA (defined in tsf_abi.cu)
 int report_cuda(cudaError_t e, const char* what);
 
+// Instantiated level-solve graphs of one plan (graph mode): one slot per
+// (transform size, preconditioner, method).  Built on first use; later
+// solves only rewrite the kernel-node parameters and relaunch.
+struct SolveGraph {
+  bool built = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphConditionalHandle cond{};
+  cudaGraphNode_t n_set = nullptr, n_begin = nullptr, n_a = nullptr, n_b = nullptr;
+};
+struct SolveGraphs {
+  SolveGraph slot[kMaxLogL + 1][2][2];  // [log L][pc][cg]
+  ~SolveGraphs();
+};
+bool graph_mode();  // TSF_SOLVE_GRAPH (default 1)
+
 template <int LOG>
 struct Dispatch {
   static int matvec(int n, const FilterTables& t, int B, const double* x, double* y,

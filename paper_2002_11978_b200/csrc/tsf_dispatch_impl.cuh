@@ -59,11 +59,98 @@ inline bool persist_mode() {
   return v == 1;
 }
 
+// Graph mode: the whole level solve is ONE graph launch —
+//   set(active = B) -> begin -> WHILE(active > 0) { v-phase ; t-phase ; test }
+// (PCG: one iteration kernel in the body).  No host round trip, no chunk
+// overshoot; the graph is instantiated once per plan and size/method, and
+// later solves rewrite the kernel-node parameters in place
+// (cudaGraphExecKernelNodeSetParams, body nodes included).
+template <typename K>
+cudaKernelNodeParams knode(K kernel, dim3 grid, dim3 block, int smem, void** args) {
+  cudaKernelNodeParams p{};
+  p.func = reinterpret_cast<void*>(kernel);
+  p.gridDim = grid;
+  p.blockDim = block;
+  p.sharedMemBytes = smem;
+  p.kernelParams = args;
+  return p;
+}
+
+template <int N, int PC, bool CG>
+int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
+  using S = KShape<N>;
+  constexpr int LOG = ilog2(2 * N);
+  SolveGraphs* cache = static_cast<SolveGraphs*>(a_in.graphs);
+  SolveGraph& G = cache->slot[LOG][PC][CG ? 1 : 0];
+  KrylovArgs a = a_in;
+  KState* kst = a.kst;
+  int* active = a.active;
+  int bval = B;
+  void* set_args[] = {&active, &bval};
+  void* k_args[] = {&a, &kst, &active};
+  auto kb = k_solve_begin<N, PC, CG>;
+  auto kv = k_bicg_v<N, PC>;
+  auto kt = k_bicg_t<N, PC>;
+  auto kc = k_cg_iter<N, PC>;
+  const cudaKernelNodeParams p_set = knode(k_set_int, dim3(1), dim3(1), 0, set_args);
+  const cudaKernelNodeParams p_begin = knode(kb, dim3(B), dim3(S::BLOCK), S::SMEM, k_args);
+  const cudaKernelNodeParams p_a = CG ? knode(kc, dim3(B), dim3(S::BLOCK), S::SMEM, k_args)
+                                      : knode(kv, dim3(B), dim3(S::BLOCK), S::SMEM, k_args);
+  const cudaKernelNodeParams p_b = knode(kt, dim3(B), dim3(S::BLOCK), S::SMEM, k_args);
+  cudaError_t e;
+  if (!G.built) {
+    if ((e = prep_kernel(kb, S::SMEM)) != cudaSuccess) return launch_error(e);
+    if ((e = prep_kernel(CG ? kc : kv, S::SMEM)) != cudaSuccess) return launch_error(e);
+    if (!CG && (e = prep_kernel(kt, S::SMEM)) != cudaSuccess) return launch_error(e);
+    if ((e = cudaGraphCreate(&G.graph, 0)) != cudaSuccess) return launch_error(e);
+    if ((e = cudaGraphConditionalHandleCreate(&G.cond, G.graph, 1, cudaGraphCondAssignDefault)) !=
+        cudaSuccess)
+      return launch_error(e);
+    if ((e = cudaGraphAddKernelNode(&G.n_set, G.graph, nullptr, 0, &p_set)) != cudaSuccess)
+      return launch_error(e);
+    if ((e = cudaGraphAddKernelNode(&G.n_begin, G.graph, &G.n_set, 1, &p_begin)) != cudaSuccess)
+      return launch_error(e);
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = G.cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t n_loop;
+    if ((e = cudaGraphAddNode(&n_loop, G.graph, &G.n_begin, 1, &cp)) != cudaSuccess)
+      return launch_error(e);
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    if ((e = cudaGraphAddKernelNode(&G.n_a, body, nullptr, 0, &p_a)) != cudaSuccess)
+      return launch_error(e);
+    cudaGraphNode_t last = G.n_a;
+    if (!CG) {
+      if ((e = cudaGraphAddKernelNode(&G.n_b, body, &G.n_a, 1, &p_b)) != cudaSuccess)
+        return launch_error(e);
+      last = G.n_b;
+    }
+    cudaGraphConditionalHandle h = G.cond;
+    void* c_args[] = {&h, &active};
+    const cudaKernelNodeParams p_c = knode(k_loop_cond, dim3(1), dim3(1), 0, c_args);
+    cudaGraphNode_t n_c;
+    if ((e = cudaGraphAddKernelNode(&n_c, body, &last, 1, &p_c)) != cudaSuccess)
+      return launch_error(e);
+    if ((e = cudaGraphInstantiate(&G.exec, G.graph, 0)) != cudaSuccess) return launch_error(e);
+    G.built = true;
+  } else {
+    if ((e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_set, &p_set)) != cudaSuccess ||
+        (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_begin, &p_begin)) != cudaSuccess ||
+        (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_a, &p_a)) != cudaSuccess ||
+        (!CG && (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_b, &p_b)) != cudaSuccess))
+      return launch_error(e);
+  }
+  return launch_error(cudaGraphLaunch(G.exec, st));
+}
+
 template <int N, int PC, bool CG>
 int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
   using S = KShape<N>;
   constexpr int kChunk = 4;
   cudaError_t e;
+  if (a.graphs && graph_mode() && !persist_mode()) return solve_graph<N, PC, CG>(B, a, st);
   if (persist_mode()) {
     auto kp = k_krylov_persist<N, PC, CG>;
     if ((e = prep_kernel(kp, S::SMEM)) != cudaSuccess) return launch_error(e);

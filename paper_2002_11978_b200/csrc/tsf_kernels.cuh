@@ -61,6 +61,7 @@ struct KrylovArgs {
   double* relres;
   int* status;
   FilterTables tab;
+  void* graphs;             // host: the plan's SolveGraphs cache (graph mode), kernels ignore it
 };
 
 template <int N>
@@ -646,6 +647,12 @@ k_krylov_persist(KrylovArgs a, KState* st, int* active) {
 }
 
 static __global__ void k_set_int(int* p, int v) { *p = v; }
+
+// Loop test of the graph-mode level solve: keep iterating while any
+// instance is unfinished (conditional WHILE node, tsf_dispatch_impl.cuh).
+static __global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* active) {
+  cudaGraphSetConditional(h, *active > 0 ? 1u : 0u);
+}
 
 // --------------------------------------------------------------- debug FFT
 template <int N, int E, bool INV>
