@@ -83,6 +83,27 @@ std::vector<double2> twiddle_table(int N) {
   for (int i = 0; i < tw_hi_count(N); ++i) t[kTwLo + tw_lo_slot(i)] = w(64L * i);
   return t;
 }
+// Explicit per-pass twiddles of the length-N transform (FftPlan<N, 8>
+// ptw_off layout): pass p >= 1 of radix R = 2^lr(p) after NS = 8^p points
+// holds W_{NS R}^{k m} at off(p) + (m-1) NS + k.
+std::vector<double2> pass_twiddles(int N) {
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  int logn = 0;
+  while ((1 << logn) < N) ++logn;
+  const int npass = (logn + 2) / 3;
+  std::vector<double2> t;
+  for (int p = 1; p < npass; ++p) {
+    const int lr = p < npass - 1 ? 3 : logn - 3 * (npass - 1);
+    const long R = 1L << lr, NS = 1L << (3 * p);
+    for (long m = 1; m < R; ++m)
+      for (long k = 0; k < NS; ++k) {
+        const long double a = two_pi * (long double)((k * m) % (NS * R)) / (long double)(NS * R);
+        t.push_back(make_double2((double)cosl(a), (double)-sinl(a)));
+      }
+  }
+  if (t.empty()) t.push_back(make_double2(1.0, 0.0));
+  return t;
+}
 }  // namespace tsf
 
 struct tsf_plan {
@@ -94,6 +115,7 @@ struct tsf_plan {
   double2* tw = nullptr;   // W_L^e
   double2* mvS = nullptr;  // (S_{2k}, S_{2k+1}) / L, even part of the symbol
   double2* pclam = nullptr;  // (lam_k, lam_{n-k})
+  double2* ptw = nullptr;    // per-pass twiddles of the length-L/2 transform
   // Krylov workspaces [cap][n] x 6
   int cap = 0;
   double* ws = nullptr;
@@ -103,7 +125,11 @@ struct tsf_plan {
   int* h_active = nullptr;  // pinned host mirror of the counter
   LargePlan* large = nullptr;  // n > 4096: four-step engine (tsf_large.cu)
   SolveGraphs* graphs = nullptr;  // graph-mode level solves (tsf_dispatch_impl.cuh)
-  FilterTables tables() const { return FilterTables{tw, mvS, pclam}; }
+  FilterTables tables() const {
+    FilterTables t{tw, mvS, pclam};
+    t.ptw = ptw;
+    return t;
+  }
 };
 
 // ------------------------------------------------------------- dispatch
@@ -243,7 +269,9 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
     return TSF_SUCCESS;
   };
   int rc;
-  if ((rc = up(&p->tw, tw)) || (rc = up(&p->mvS, S)) || (rc = up(&p->pclam, pl)))
+  std::vector<double2> ptw = pass_twiddles(L / 2);
+  if ((rc = up(&p->tw, tw)) || (rc = up(&p->mvS, S)) || (rc = up(&p->pclam, pl)) ||
+      (rc = up(&p->ptw, ptw)))
     return cleanup(rc);
   *out = p;
   return TSF_SUCCESS;
@@ -260,6 +288,7 @@ int tsf_plan_destroy(tsf_plan* p) {
   cudaFree(p->tw);
   cudaFree(p->mvS);
   cudaFree(p->pclam);
+  cudaFree(p->ptw);
   cudaFree(p->ws);
   cudaFree(p->ist);
   cudaFree(p->dst);

@@ -193,7 +193,18 @@ struct FftPlan {
   }
   static constexpr int log_ns(int p) { return p * LOGR; }
   TSF_HD static int pad(int i) { return i + (i >> PADSHIFT); }
+  // explicit per-pass twiddles (TSF_PASS_TW): pass p >= 1 stores
+  // W_{NS R}^{k m} at ptw_off(p) + (m-1) NS + k, k < NS, 1 <= m < R
+  static constexpr int ptw_off(int p) {
+    return p <= 1 ? 0 : ptw_off(p - 1) + ((1 << log_radix(p - 1)) - 1) * (1 << log_ns(p - 1));
+  }
+  static constexpr int PTW_ELEMS = ptw_off(NPASS);
 };
+
+#ifndef TSF_PASS_TW
+#define TSF_PASS_TW 0
+#endif
+constexpr bool kPassTw = TSF_PASS_TW;
 
 // One Stockham pass: radix R, NS = product of the previous radices.
 //  FROM_REGS: inputs come from v[] (first pass), else from shared memory.
@@ -204,7 +215,7 @@ struct FftPlan {
 // them to local memory.  Only owning threads touch data.
 template <int N, int E, int P, bool INV, bool FROM_REGS, bool TO_REGS>
 TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
-                         int tw_log_scale, int tid, bool own) {
+                         int tw_log_scale, int tid, bool own, const double2* __restrict__ ptw) {
   using PL = FftPlan<N, E>;
   constexpr int R = 1 << PL::log_radix(P);
   constexpr int NS = 1 << PL::log_ns(P);
@@ -230,7 +241,15 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
   for (int q = 0; q < Q; ++q) {
     const int b = tid + q * T;
     const int k = b & (NS - 1);
-    if constexpr (NS > 1) {
+    if (kPassTw && NS > 1 && ptw) {
+      // explicit table: one correctly rounded entry per power, no products
+      const double2* pt = ptw + PL::ptw_off(P) + k;
+#pragma unroll
+      for (int m = 1; m < R; ++m) {
+        const double2 w = pt[(m - 1) * NS];
+        a[q][m] = INV ? cmulc(a[q][m], w) : cmul(a[q][m], w);
+      }
+    } else if constexpr (NS > 1) {
       // W_{NS R}^{k m} = W_NT^{k m NT/(NS R)}, NT/(NS R) = 2^sh
       const int sh = tw_log_scale + PL::LOGN - PL::log_ns(P) - PL::log_radix(P);
       // W^k, W^2k, W^4k from the table; the other powers are one product of
@@ -270,15 +289,15 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
 
 template <int N, int E, int P, bool INV>
 TSF_D void fft_rec(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
-                   int tw_log_scale, int tid, bool own) {
+                   int tw_log_scale, int tid, bool own, const double2* __restrict__ ptw = nullptr) {
   using PL = FftPlan<N, E>;
   constexpr bool FIRST = (P == 0);
   constexpr bool LAST = (P == PL::NPASS - 1);
-  stockham_pass<N, E, P, INV, FIRST, LAST>(v, sm, tw, tw_log_scale, tid, own);
+  stockham_pass<N, E, P, INV, FIRST, LAST>(v, sm, tw, tw_log_scale, tid, own, ptw);
   if constexpr (!LAST) {
     cp_async_wait_all();  // staged tables (tsf_filters.cuh stage_tables) land here
     __syncthreads();
-    fft_rec<N, E, P + 1, INV>(v, sm, tw, tw_log_scale, tid, own);
+    fft_rec<N, E, P + 1, INV>(v, sm, tw, tw_log_scale, tid, own, ptw);
   }
 }
 
@@ -290,12 +309,12 @@ TSF_D void fft_rec(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
 // `tw` holds W_NT^e for e < NT with NT = N << tw_log_scale.
 template <int N, int E, bool INV>
 TSF_D void block_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
-                     int tw_log_scale) {
+                     int tw_log_scale, const double2* __restrict__ ptw = nullptr) {
   using PL = FftPlan<N, E>;
   const int tid = threadIdx.x;
   const bool own = tid < PL::T;
   __syncthreads();
-  fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, own);
+  fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, own, ptw);
 }
 
 // Several independent transforms per CTA (the large-n column kernels): the
@@ -382,7 +401,8 @@ TSF_D void dft_real(const double* x, double2* X) {
 // j = tid + c*T), then the remaining complex passes into v[c].
 template <int N, int E>
 TSF_D void real_first_pass(const double (&x)[E], double2 (&v)[E], double2* sm,
-                           const double2* __restrict__ tw, int tw_log_scale, int tid, bool own) {
+                           const double2* __restrict__ tw, int tw_log_scale, int tid, bool own,
+                           const double2* __restrict__ ptw = nullptr) {
   using PL = FftPlan<N, E>;
   constexpr int R = 1 << PL::log_radix(0);
   constexpr int Q = E / R;
@@ -400,18 +420,20 @@ TSF_D void real_first_pass(const double (&x)[E], double2 (&v)[E], double2* sm,
       for (int m = 0; m < R; ++m) sm[PL::pad(base + m)] = out[m];
     }
   }
+  cp_async_wait_all();
   __syncthreads();
-  fft_rec<N, E, 1, false>(v, sm, tw, tw_log_scale, tid, own);
+  fft_rec<N, E, 1, false>(v, sm, tw, tw_log_scale, tid, own, ptw);
 }
 
 // Forward transform of real owned slots x[c] (j = tid + c*T) into v[c].
 template <int N, int E>
 TSF_D void block_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
-                          const double2* __restrict__ tw, int tw_log_scale) {
+                          const double2* __restrict__ tw, int tw_log_scale,
+                          const double2* __restrict__ ptw = nullptr) {
   static_assert(FftPlan<N, E>::NPASS >= 2, "real-input transform needs at least two passes");
   __syncthreads();
   const int tid = threadIdx.x;
-  real_first_pass<N, E>(x, v, sm, tw, tw_log_scale, tid, tid < FftPlan<N, E>::T);
+  real_first_pass<N, E>(x, v, sm, tw, tw_log_scale, tid, tid < FftPlan<N, E>::T, ptw);
 }
 
 template <int N, int E>

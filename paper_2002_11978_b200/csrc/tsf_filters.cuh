@@ -37,6 +37,7 @@ struct FilterTables {
   const double2* mvS;   // (S_{2k}, S_{2k+1}) / L, even part of the symbol, k < N
   const double2* pclam; // (lam_k, lam_{n-k}), k < n   (pow2 n = N only)
   const double* ps = nullptr;  // the instance's staged Strang spectrum (shared memory) or null
+  const double2* ptw = nullptr;  // per-pass twiddles of the length-N transform (TSF_PASS_TW)
 };
 
 TSF_D double ld_real(const double* __restrict__ base, int n, int j) {
@@ -75,7 +76,8 @@ template <int N>
 struct FStage {
   static constexpr int FFT_BYTES = (kFftInPlace ? 1 : 2) * FftPlan<N, kE>::SMEM_ELEMS * 16;
   static constexpr int TW_BYTES = tw_table_elems(2 * N) * 16;
-  static constexpr int BASE = FFT_BYTES + N * 8 + TW_BYTES;
+  static constexpr int PTW_BYTES = kPassTw ? FftPlan<N, kE>::PTW_ELEMS * 16 : 0;
+  static constexpr int BASE = FFT_BYTES + N * 8 + TW_BYTES + PTW_BYTES;
   static constexpr int BLOCK = (N / kE) < 32 ? 32 : (N / kE);
   static constexpr int REG_CTAS = (65536 / (BLOCK * 128)) < 1 ? 1 : 65536 / (BLOCK * 128);
   static constexpr int occ(int bytes) { return kSmemPerSM / (bytes + 1024 + 1024); }
@@ -97,12 +99,12 @@ TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E]
                      const FilterTables& t) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
-  block_fft_real<N, E>(x, z, sm, t.tw, 1);
+  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = cscale(z[c], mv_spec<N>(t, threadIdx.x + c * T).x);
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1);
+  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw);
 }
 
 // odd output bins: z (already modulated by w_j) <- IFFT_N( S_odd . FFT_N(z) );
@@ -111,12 +113,12 @@ template <int N>
 TSF_D void filt_odd(double2 (&z)[FShape<N>::E], double2* sm, const FilterTables& t) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
-  block_fft<N, E, false>(z, sm, t.tw, 1);
+  block_fft<N, E, false>(z, sm, t.tw, 1, t.ptw);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = cscale(z[c], mv_spec<N>(t, threadIdx.x + c * T).y);
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1);
+  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw);
 }
 
 // Strang: z <- IFFT_n( FFT_n(x) . Ssym / n ) for real x, n = N; caller keeps Re(z)
@@ -126,7 +128,7 @@ TSF_D void filt_strang(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
   constexpr double inv_n = 1.0 / N;
-  block_fft_real<N, E>(x, z, sm, t.tw, 1);
+  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
@@ -135,7 +137,7 @@ TSF_D void filt_strang(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::
       z[c] = cscale(z[c], s * inv_n);
     }
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1);
+  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw);
 }
 
 // Strang with a precomputed per-instance spectrum spec[k] = S_k / n (the level
@@ -146,12 +148,12 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
                            const FilterTables& t, const double* __restrict__ spec) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
-  block_fft_real<N, E>(x, z, sm, t.tw, 1);
+  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = cscale(z[c], spec[threadIdx.x + c * T]);
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1);
+  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw);
 }
 
 // w_j = W_L^j for the owned slots
@@ -169,6 +171,14 @@ TSF_D FilterTables stage_tables(const FilterTables& g, double2* dst, const doubl
   FilterTables t = g;
   t.tw = dst;
   double2* next = dst + NT;
+  if constexpr (kPassTw) {
+    constexpr int NP = FftPlan<N, kE>::PTW_ELEMS;
+    if (g.ptw) {
+      for (int i = threadIdx.x; i < NP; i += blockDim.x) cp_async16(&next[i], &g.ptw[i]);
+      t.ptw = next;
+    }
+    next += NP;
+  }
   if constexpr (FStage<N>::MV) {
     for (int i = threadIdx.x; i < N; i += blockDim.x) cp_async16(&next[i], &g.mvS[i]);
     t.mvS = next;

@@ -207,10 +207,21 @@ def _generic_cg(op, precond, rhs, tol, max_iters):
         max_iters, float(torch.linalg.norm(r)) / nrm0, False)
 
 
+def _fused_ok(op, precond) -> bool:
+    """The fused level-solve kernels take a LevelOperator with no or a
+    power-of-two Strang preconditioner; anything else (non-pow2 n with the
+    Strang preconditioner, user callables) runs the device-vector loop below,
+    whose operator and preconditioner applications are still the sm_100a
+    Toeplitz kernels."""
+    if not isinstance(op, LevelOperator):
+        return False
+    return precond is None or getattr(precond, "strang_native", False)
+
+
 def solve_bicgstab(op: MatrixFreeOperator, precond, rhs, tol: float = 1e-10,
                    max_iters: Optional[int] = None):
     """Right-preconditioned BiCGSTAB, x0 = 0 (krylov.py:88-153)."""
-    if isinstance(op, LevelOperator):
+    if _fused_ok(op, precond):
         return _device_solve(op, precond, rhs, tol, max_iters, method=0)
     return _generic_bicgstab(op, precond, rhs, tol, max_iters)
 
@@ -218,7 +229,7 @@ def solve_bicgstab(op: MatrixFreeOperator, precond, rhs, tol: float = 1e-10,
 def solve_cg(op: MatrixFreeOperator, precond, rhs, tol: float = 1e-10,
              max_iters: Optional[int] = None):
     """Preconditioned CG, x0 = 0 (krylov.py:43-85)."""
-    if isinstance(op, LevelOperator):
+    if _fused_ok(op, precond):
         return _device_solve(op, precond, rhs, tol, max_iters, method=1)
     return _generic_cg(op, precond, rhs, tol, max_iters)
 

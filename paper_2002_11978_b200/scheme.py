@@ -361,6 +361,10 @@ def run_fids(spec: ProblemSpec, M: int, r: float, N: int, epsilon: float = 1e-10
         return _finish(spec, mesh, disc, x, hist, its, None, soe, t0, tag, keep_history)
     if tag not in ("krylov", "pkrylov"):
         raise ValueError(f"unknown solver {tag!r}")
+    if tag == "pkrylov" and not (n >= 16 and n & (n - 1) == 0):
+        hist, its, rel = _run_levels(spec, mesh, disc, x, soe, u0, M, options, device,
+                                     keep_history or spec.exact is not None)
+        return _finish(spec, mesh, disc, x, hist, its, rel, soe, t0, tag, keep_history)
     torch = _native.torch_mod()
     dev = torch.device(f"cuda:{device}")
     kap = _device_field(spec.kappa, x, mesh.t, n, M, dev, positive=True)
@@ -381,6 +385,53 @@ def run_fids(spec: ProblemSpec, M: int, r: float, N: int, epsilon: float = 1e-10
         hist = res.u_final[0].cpu().numpy()[None, :]
     return _finish(spec, mesh, disc, x, hist, res.iterations[:, 0], res.relres[:, 0], soe, t0,
                    tag, keep_history)
+
+
+def _run_levels(spec, mesh, disc, x, soe, u0, M, options, device, want_hist):
+    """The reference's level loop (scheme.py:276-294) driven from the host,
+    for the Strang preconditioner at non-power-of-two n: per level the SOE
+    history term / RHS and the push run in the SOE kernel, the operator and
+    P^{-1} = circ(IFFT(1/total)) in the Toeplitz kernels (toeplitz.py
+    _circulant_plan), the BiCGSTAB/CG loop over device vectors."""
+    from .krylov import LevelOperator, solve_bicgstab, solve_cg
+    from .soe import FastHistory, fast_caputo_rhs, history_push
+    from .toeplitz import build_preconditioner
+    torch = _native.torch_mod()
+    dev = torch.device(f"cuda:{device}")
+    n = disc.N - 1
+    G = math.exp(gammaln(1.0 - spec.gamma))
+    op = build_toeplitz(disc.first_col, device=device)
+    h = FastHistory.fresh(soe, n, device)
+    u_prev = torch.from_numpy(np.ascontiguousarray(u0, dtype=np.float64)).to(dev)
+    hist = np.empty((M + 1, n)) if want_hist else None
+    if want_hist:
+        hist[0] = u0
+    its = np.zeros(M, dtype=np.int64)
+    rel = np.zeros(M)
+    solver = solve_cg if spec.kappa_x_independent else solve_bicgstab
+    for m in range(1, M + 1):
+        tau_m = float(mesh.tau[m - 1])
+        tm = float(mesh.t[m])
+        a_mm = _last_weight(tau_m, spec.gamma)
+        kappa = _kappa_at(spec, x, tm)
+        f = torch.from_numpy(np.ascontiguousarray(spec.source(x, tm), dtype=np.float64)).to(dev)
+        rhs = f + fast_caputo_rhs(h, a_mm, u_prev, spec.gamma, tau_m)
+        shift = a_mm / G
+        lev = LevelOperator(op, shift, torch.from_numpy(kappa).to(dev))
+        pc = build_preconditioner(disc.first_col, shift, float(kappa.mean()), device=device)
+        u, rep = solver(lev, pc, rhs, tol=options.tol, max_iters=options.max_iters)
+        if not rep.converged:
+            raise RuntimeError(
+                f"{'CG' if spec.kappa_x_independent else 'BiCGSTAB'} did not converge: {rep}")
+        its[m - 1] = rep.iterations
+        rel[m - 1] = rep.final_relative_residual
+        history_push(h, u - u_prev, tau_m)
+        u_prev = u
+        if want_hist:
+            hist[m] = u.cpu().numpy()
+    if not want_hist:
+        hist = u_prev.cpu().numpy()[None, :]
+    return hist, its, rel
 
 
 def _device_field(fn, x, t, n, M, dev, positive):

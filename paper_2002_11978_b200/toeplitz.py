@@ -162,15 +162,35 @@ class CirculantPreconditioner:
         return precond_solve(self, v)
 
     @property
+    def strang_native(self) -> bool:
+        """Power-of-two n >= 16: the plan carries the Strang tables and the
+        fused level-solve kernels apply P^{-1} themselves."""
+        return _is_pow2(self.n) and self.n >= 16
+
+    @property
     def plan(self) -> _native.Plan:
         if self._plan is None:   # built once per preconditioner
-            if self.first_col is not None:
+            if not self.strang_native:
+                pl = self._circulant_plan()
+            elif self.first_col is not None:
                 pl = plan_for(self.first_col, self.device, lam=self.lam)
             else:
                 # bare spectrum: a plan whose "lam" is the given eigenvalue array
                 pl = plan_for(np.zeros(self.n), self.device, lam=self.lam)
             object.__setattr__(self, "_plan", pl)
         return self._plan
+
+    def _circulant_plan(self) -> _native.Plan:
+        """Any n: P^{-1} = circ(c), c = IFFT_n(1/total) real and even, and a
+        symmetric circulant is the symmetric Toeplitz matrix with first column
+        c — applied by the same device Toeplitz engine through its pow2
+        embedding (in exact arithmetic identical to the reference's
+        Re IFFT(FFT(v)/total), toeplitz.py:131-136)."""
+        c = np.fft.ifft(1.0 / self.total_eigs).real
+        c = 0.5 * (c + np.roll(c[::-1], 1))          # c_j = c_{n-j} exactly
+        L = max(embed_length(self.n), 32)
+        sym = np.fft.fft(_even_embedding(c, L)).real
+        return _native.Plan(self.n, L, sym, None, self.device)
 
 
 def build_preconditioner(d, shift: float, kappa_bar: float, device: int = 0
@@ -199,11 +219,13 @@ def precond_solve(p: CirculantPreconditioner, v):
     """P^{-1} v = IFFT(FFT(v)/total) on the device (toeplitz.py:131-136)."""
     torch = _native.torch_mod()
     x, as_np = _batched(v, p.n, p.device)
-    if not (_is_pow2(p.n) and p.n >= 16):
-        raise NotImplementedError(
-            f"device Strang preconditioner needs a power-of-two n >= 16 (got n={p.n})")
     B = 1 if x.dim() == 1 else x.shape[0]
     z = torch.empty_like(x)
+    if not p.strang_native:
+        # circ(c) applied as a symmetric Toeplitz product (_circulant_plan)
+        _native.check(_native.load().tsf_toeplitz_matvec(
+            p.plan.handle, B, x.data_ptr(), z.data_ptr(), None, 0.0, _native.stream_ptr()))
+        return _arrays.back(z, as_np)
     _native.check(_native.load().tsf_precond_solve(
         p.plan.handle, B, x.data_ptr(), z.data_ptr(), float(p.shift), float(p.kappa_bar), None,
         _native.stream_ptr()))

@@ -25,7 +25,7 @@ import paper_2002_11978_b200 as P  # noqa: E402
 from paper_2002_11978_b200 import _native  # noqa: E402
 
 
-MAX_N = 4096  # single-CTA engine (L <= 8192)
+MAX_N = 1 << 24  # every golden case (single-CTA engine n <= 4096, four-step engine above)
 
 
 def _lin_cases():
@@ -76,18 +76,18 @@ def test_toeplitz_kats():
 
 
 def test_precond_vs_reference():
+    """Every n: power-of-two n >= 16 through the Strang kernels, other n
+    through circ(IFFT(1/total)) as a Toeplitz product (toeplitz.py)."""
     seen = 0
     for i, g in _lin_cases():
         n = g[f"tp{i}_v"].size
-        if n & (n - 1) or n < 16:
-            continue
         p = P.build_preconditioner(g[f"tp{i}_col"], g[f"tp{i}_shift"][0],
                                    float(g[f"tp{i}_kappa"].mean()))
         np.testing.assert_array_equal(p.total_eigs, g[f"tp{i}_total"])
         got = P.precond_solve(p, g[f"tp{i}_v"])
         assert rel_err(got, g[f"tp{i}_Pinv_v"]) <= 1e-13, i
         seen += 1
-    assert seen >= 3
+    assert seen >= 7
 
 
 def test_level_solve_vs_reference():
@@ -99,28 +99,31 @@ def test_level_solve_vs_reference():
         shift = g[f"tp{i}_shift"][0]
         kap = g[f"tp{i}_kappa"]
         lev = P.LevelOperator(op, shift, kap)
-        pow2 = not (n & (n - 1)) and n >= 16
-        if pow2:
-            pc = P.build_preconditioner(col, shift, float(kap.mean()))
-            for tol in (10, 12):
-                key = f"tp{i}_bicg_{tol}"
-                x, rep = P.solve_bicgstab(lev, pc, g[f"{key}_b"], tol=10.0 ** -tol)
-                its = int(g[f"{key}_rep"][0])
-                assert rep.converged
-                # the reference itself moves by 2 (tol 1e-10) and 3 (tol 1e-12)
-                # iterations on these random-kappa/random-rhs solves when only
-                # its FFT engine is swapped (numpy -> scipy.fft; measured with
-                # oracle/, SURVEY.md §7 hard part 1): gate at that floor
-                assert abs(rep.iterations - its) <= (2 if tol == 10 else 3), \
-                    (i, tol, rep.iterations, its)
-                assert rel_l2(x, g[f"{key}_x"]) <= (1e-9 if tol == 10 else 1e-10), (i, tol)
-            seen += 1
-        # unpreconditioned BiCGSTAB works for every n
+        # every n (non-pow2: circulant-as-Toeplitz preconditioner)
+        pc = P.build_preconditioner(col, shift, float(kap.mean()))
+        for tol in (10, 12):
+            key = f"tp{i}_bicg_{tol}"
+            x, rep = P.solve_bicgstab(lev, pc, g[f"{key}_b"], tol=10.0 ** -tol)
+            its = int(g[f"{key}_rep"][0])
+            assert rep.converged
+            # the reference itself moves by 2 (tol 1e-10) and 3 (tol 1e-12)
+            # iterations on these random-kappa/random-rhs solves when only
+            # its FFT engine is swapped (numpy -> scipy.fft; measured with
+            # oracle/, SURVEY.md §7 hard part 1): gate at that floor
+            assert abs(rep.iterations - its) <= (2 if tol == 10 else 3), \
+                (i, tol, rep.iterations, its)
+            assert rel_l2(x, g[f"{key}_x"]) <= (1e-9 if tol == 10 else 1e-10), (i, tol)
+        seen += 1
+        # unpreconditioned BiCGSTAB works for every n.  Its hundreds of
+        # iterations amplify rounding: the reference with only its FFT engine
+        # swapped (numpy -> scipy.fft) takes 283 vs 278 (n=1024), 886 vs 892
+        # (n=4096) but 1966 vs 1236 (n=8192) iterations: gate at that floor
         x, rep = P.solve_bicgstab(lev, None, g[f"tp{i}_bicg_12_b"], tol=1e-10)
         its = int(g[f"tp{i}_plain_rep"][0])
-        assert rep.converged and abs(rep.iterations - its) <= max(2, its // 10), (i, rep, its)
+        gate = max(2, its // 10) if n <= 4096 else int(0.6 * its)
+        assert rep.converged and abs(rep.iterations - its) <= gate, (i, rep, its)
         assert rel_l2(x, g[f"tp{i}_plain_x"]) <= 1e-8
-    assert seen >= 3
+    assert seen >= 7
 
 
 def test_zero_rhs_zero_iterations():
@@ -153,8 +156,10 @@ def test_soe_push_bit_exact():
     np.testing.assert_array_equal(h.W.cpu().numpy(), g["push_W1"])
 
 
-@pytest.mark.parametrize("tag", ["s1", "s3", "s5"])
+@pytest.mark.parametrize("tag", ["s1", "s2", "s3", "s4", "s5"])
 def test_small_march_vs_reference(tag):
+    """s4 is n = 63 (non-power-of-two: host-driven level loop with the
+    circulant-as-Toeplitz preconditioner), s2 alpha = 1.9 at tol 1e-10."""
     g = golden("march")
     gam, a, M, N, tol, r = g[f"{tag}_args"]
     k, f, phi = cfg0_fields()
