@@ -212,10 +212,10 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
   if (!symbol_re) return fail(TSF_E_INVALID, "symbol is NULL");
   const int lg = ilog2_host(L);
   if (lg > kMaxLogL) {
-    // four-step engine: pow2 n in [2^13, 2^24] with L = 2n
-    if (!(is_pow2(n) && L == 2 * n))
+    // four-step engine: transform length L/2 = 2^13..2^24, any n with 2n-1 <= L
+    if (lam && !(is_pow2(n) && L == 2 * n))
       return fail(TSF_E_UNSUPPORTED,
-                  "n=%d > 4096 needs a power of two n with L = 2n (got L=%d)", n, L);
+                  "Strang tables need a power-of-two n with L = 2n (n=%d, L=%d)", n, L);
     tsf_plan* p = new tsf_plan();
     p->n = n;
     p->L = L;
@@ -223,7 +223,7 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
     p->device = device;
     p->has_pc = lam != nullptr;
     p->large = new LargePlan();
-    const int rc = large_plan_init(p->large, n, symbol_re, lam, device);
+    const int rc = large_plan_init(p->large, n, L, symbol_re, lam, device);
     if (rc) {
       tsf_plan_destroy(p);
       return rc;

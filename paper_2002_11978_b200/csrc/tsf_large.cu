@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_begin(LargeArgs a, KrylovAr
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
     const long j = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (j >= a.n) break;
     double kv;
     if (k.kappa) {
       kv = k.kappa[off + j];
@@ -97,7 +98,9 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_pupd(LargeArgs a) {
   const double beta = s.it == 1 ? 0.0 : (s.rho_new / s.rho) * (s.alpha / s.omega);
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
-    const long j = off + (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (jj >= a.n) break;
+    const long j = off + jj;
     a.p[j] = s.it == 1 ? a.r0[j] : a.r[j] + beta * (a.p[j] - s.omega * a.v[j]);
   }
 }
@@ -113,7 +116,9 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_supd(LargeArgs a) {
   double ss = 0.0;
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
-    const long j = off + (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (jj >= a.n) break;
+    const long j = off + jj;
     const double v = rc[j] - s.alpha * a.v[j];
     a.s[j] = v;
     ss = fma(v, v, ss);
@@ -134,7 +139,9 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_xr(LargeArgs a, const doubl
   if (s.mode == LM_EARLY) {
 #pragma unroll
     for (int c = 0; c < kLelPer; ++c) {
-      const long j = off + (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+      const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+      if (jj >= a.n) break;
+      const long j = off + jj;
       a.x[j] = a.x[j] + s.alpha * ph[j];
     }
     return;
@@ -143,7 +150,9 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_xr(LargeArgs a, const doubl
   v.v[0] = v.v[1] = 0.0;
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
-    const long j = off + (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (jj >= a.n) break;
+    const long j = off + jj;
     a.x[j] = a.x[j] + (s.alpha * ph[j] + s.omega * sh[j]);
     const double r = a.s[j] - s.omega * a.t[j];
     a.r[j] = r;
@@ -171,11 +180,12 @@ __global__ void __launch_bounds__(kLelThreads) k_lspec(LargeArgs a, double kbar,
     kb = kbar_dev[b];
   }
   const double d = a.shift;
-  const double inv_n = 1.0 / a.n;
-  const long off = (long)b * a.n;
+  const double inv_n = 1.0 / a.nt;   // the Strang tables exist only for n == nt
+  const long off = (long)b * a.nt;
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
     const long idx = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (idx >= a.nt) break;
     const double2 lam = ldt(&a.lt.lamP[idx]);
     a.pspec[off + idx] = 0.5 * (1.0 / (d + kb * lam.x) + 1.0 / (d + kb * lam.y)) * inv_n;
   }
@@ -319,7 +329,7 @@ struct Runner {
     if ((rc = row_at(lg2, a, RS_APPLY, st))) return rc;
     return col_inv_at(lg1, a, dst, CO_APPLY, src, w1, slot, st);
   }
-  dim3 lel_grid() const { return dim3(a.n / kLelChunk, a.B); }
+  dim3 lel_grid() const { return dim3((a.n + kLelChunk - 1) / kLelChunk, a.B); }
   int sc(int stage, int count, int pc) {
     k_lsc<<<a.B, kLscThreads, 0, st>>>(a, stage, count, 0.0, lp->lam_min, pc);
     return cuda_check(cudaGetLastError(), "k_lsc");
@@ -327,7 +337,7 @@ struct Runner {
   // one BiCGSTAB iteration for every unfinished instance
   int bicg_iteration(int pc) {
     int rc;
-    const int NC = lp->ncol_cta, NR = a.n / kLelChunk;
+    const int NC = lp->ncol_cta, NR = (a.n + kLelChunk - 1) / kLelChunk;
     const double* ph = pc ? a.ph : a.p;
     const double* sh = pc ? a.sh : a.s;
     if (pc) {
@@ -362,6 +372,7 @@ Runner make_runner(const LargePlan* lp, int B, cudaStream_t st) {
   LargeArgs& a = R.a;
   a = LargeArgs{};
   a.n = lp->n;
+  a.nt = lp->nt;
   a.B = B;
   a.lt = lp->lt;
   a.Z = lp->Z;
@@ -376,8 +387,8 @@ Runner make_runner(const LargePlan* lp, int B, cudaStream_t st) {
   a.s = w + 4 * vn;
   a.sh = w + 5 * vn;
   a.t = w + 6 * vn;
-  a.pspec = w + 7 * vn;
-  // w + 8 vn: kwork
+  // w + 7 vn: kwork ; w + 8 vn: the Strang spectrum [cap][nt]
+  a.pspec = w + 8 * vn;
   a.active = lp->active;
   return R;
 }
@@ -385,25 +396,30 @@ Runner make_runner(const LargePlan* lp, int B, cudaStream_t st) {
 }  // namespace
 
 // ======================================================================
-int large_plan_init(LargePlan* lp, int n, const double* symbol_re, const double* lam, int device) {
-  const int lg = ilog2i(n);
-  if ((1L << lg) != n || lg < 13 || lg > 2 * kLargeMaxLog)
-    return report_error(TSF_E_UNSUPPORTED, "large-n engine needs a power of two n in [2^13, 2^24]");
+int large_plan_init(LargePlan* lp, int n, int L, const double* symbol_re, const double* lam,
+                    int device) {
+  const int nt = L / 2;   // transform length (pow2); vectors of n <= nt are zero-padded
+  const int lg = ilog2i(nt);
+  if ((1L << lg) != nt || lg < 13 || lg > 2 * kLargeMaxLog || n > nt || 2L * n - 1 > L)
+    return report_error(TSF_E_UNSUPPORTED,
+                        "large-n engine needs a power-of-two embedding L = 2^14..2^25 >= 2n-1");
+  if (lam && n != nt)
+    return report_error(TSF_E_UNSUPPORTED, "Strang tables need n = L/2 (power-of-two n)");
   *lp = LargePlan{};
   lp->n = n;
+  lp->nt = nt;
   // columns short (cheap, G per CTA), rows up to the single-CTA limit 4096
-  lp->N1 = std::max(64, n >> kLargeMaxLog);
-  lp->N2 = n / lp->N1;
+  lp->N1 = std::max(64, nt >> kLargeMaxLog);
+  lp->N2 = nt / lp->N1;
   lp->ncol_cta = lp->N2 / col_group_at(ilog2i(lp->N1));
-  lp->np = std::max(lp->ncol_cta, n / kLelChunk);
+  lp->np = std::max(lp->ncol_cta, (n + kLelChunk - 1) / kLelChunk);
   lp->has_pc = lam != nullptr;
   lp->device = device;
-  const long L = 2L * n;
   const int N1 = lp->N1, N2 = lp->N2;
   std::vector<double2> tw1 = twiddle_table(N1), tw2 = twiddle_table(N2);
-  std::vector<double2> twN = twiddle_table(n), twL = twiddle_table((int)L);
+  std::vector<double2> twN = twiddle_table(nt), twL = twiddle_table(L);
   // permuted spectra: position k1 N2 + k2 holds bin k = k1 + N1 k2
-  std::vector<double2> sEO((size_t)n), lamP(lam ? (size_t)n : 0);
+  std::vector<double2> sEO((size_t)nt), lamP(lam ? (size_t)nt : 0);
   auto Ssym = [&](long k) -> double {
     return (double)(0.5L * ((long double)symbol_re[k] + (long double)symbol_re[(L - k) % L]) /
                     (long double)L);
@@ -468,11 +484,12 @@ int large_reserve(LargePlan* lp, int B) {
   lp->part = nullptr;
   lp->st = nullptr;
   lp->cap = 0;
-  const size_t vn = (size_t)B * lp->n;
+  const size_t vn = (size_t)B * lp->n, vt = (size_t)B * lp->nt;
   int rc;
-  if ((rc = cuda_check(cudaMalloc(&lp->ws, sizeof(double) * vn * 9), "cudaMalloc(large ws)")))
+  // 8 Krylov vectors [B][n] + the Strang spectrum [B][nt]
+  if ((rc = cuda_check(cudaMalloc(&lp->ws, sizeof(double) * (vn * 8 + vt)), "cudaMalloc(large ws)")))
     return rc;
-  if ((rc = cuda_check(cudaMalloc(&lp->Z, sizeof(double2) * vn * 2), "cudaMalloc(large Z)")))
+  if ((rc = cuda_check(cudaMalloc(&lp->Z, sizeof(double2) * vt * 2), "cudaMalloc(large Z)")))
     return rc;
   if ((rc = cuda_check(cudaMalloc(&lp->part, sizeof(double) * (size_t)B * 4 * lp->np),
                        "cudaMalloc(partials)")))
@@ -518,7 +535,7 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
   Runner R = make_runner(lp, B, st);
   LargeArgs& a = R.a;
   KrylovArgs kk = k;
-  if (!kk.kappa && !kk.kwork) kk.kwork = lp->ws + 8 * (size_t)lp->cap * lp->n;
+  if (!kk.kappa && !kk.kwork) kk.kwork = lp->ws + 7 * (size_t)lp->cap * lp->n;
   a.r0 = k.rhs;
   a.x = k.x;
   a.kappa = kk.kappa ? kk.kappa : kk.kwork;
@@ -532,7 +549,8 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
   k_set_int<<<1, 1, 0, st>>>(lp->active, B);
   k_lel_begin<<<R.lel_grid(), kLelThreads, 0, st>>>(a, kk);
   if ((rc = cuda_check(cudaGetLastError(), "k_lel_begin"))) return rc;
-  k_lsc<<<B, kLscThreads, 0, st>>>(a, LS_BEGIN, a.n / kLelChunk, k.kbar, lp->lam_min, pc);
+  k_lsc<<<B, kLscThreads, 0, st>>>(a, LS_BEGIN, (a.n + kLelChunk - 1) / kLelChunk, k.kbar,
+                                   lp->lam_min, pc);
   if ((rc = cuda_check(cudaGetLastError(), "k_lsc(begin)"))) return rc;
   if (pc) {
     k_lspec<<<R.lel_grid(), kLelThreads, 0, st>>>(a, 0.0, nullptr, 1);

@@ -60,7 +60,8 @@ enum ColOut : int {
 enum RowSpec : int { RS_APPLY = 0, RS_STRANG = 2 };
 
 struct LargeArgs {
-  int n, B;
+  int n, B;            // vector length n <= transform length nt (x is zero beyond n)
+  int nt;
   LargeTables lt;
   double2* Z;          // [2][B][n] transform work array (channel-major)
   double* part;        // [B][4][np] partial sums
@@ -123,8 +124,8 @@ __global__ void __launch_bounds__(LCol<N1>::BLOCK, 1)
 k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
-  const int N2 = a.n / N1;
-  const long N = a.n;
+  const int N2 = a.nt / N1;
+  const long N = a.nt;
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
   const int b = blockIdx.y;
@@ -134,7 +135,8 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   double2* smg = sm + g * C::BUF;
   double2* tw1 = sm + G * C::BUF;
   stage_tw<N1>(tw1, a.lt.tw1);
-  const long off = (long)b * N;
+  const long off = (long)b * a.n;   // vectors [B][n]
+  const long offz = (long)b * N;    // transform work [B][nt]
   double xr[E];
   double2 z[E];
   double part = 0.0;
@@ -142,8 +144,10 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const long j = (long)N2 * (tid + c * T) + t2;
-    double val;
-    if (in_mode == CI_PUPD) {
+    double val = 0.0;
+    if (j >= a.n) {
+      // zero padding up to the transform length
+    } else if (in_mode == CI_PUPD) {
       if (stv.it == 1) {
         val = a.r0[off + j];
       } else {
@@ -170,7 +174,7 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   for (int c = 0; c < E; ++c) {
     const int k1 = tid + c * T;
     const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
-    a.Z[off + (long)k1 * N2 + t2] = cmul(z[c], w);
+    a.Z[offz + (long)k1 * N2 + t2] = cmul(z[c], w);
   }
   if (in_mode == CI_APPLY) {
     // odd channel: the modulated input x_j W_L^j
@@ -185,7 +189,7 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
     for (int c = 0; c < E; ++c) {
       const int k1 = tid + c * T;
       const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
-      Zo[off + (long)k1 * N2 + t2] = cmul(z[c], w);
+      Zo[offz + (long)k1 * N2 + t2] = cmul(z[c], w);
     }
   }
 }
@@ -194,7 +198,7 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
 template <int N2>
 __global__ void __launch_bounds__(LRow<N2>::BLOCK, 1)
 k_lrow(LargeArgs a, int spec_mode) {
-  const long N = a.n;
+  const long N = a.nt;
   constexpr int E = LRow<N2>::E;
   constexpr int T = LRow<N2>::T;
   extern __shared__ double2 sm[];
@@ -241,8 +245,8 @@ k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __
            const double* __restrict__ w1, int pslot) {
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
-  const int N2 = a.n / N1;
-  const long N = a.n;
+  const int N2 = a.nt / N1;
+  const long N = a.nt;
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
   const int b = blockIdx.y;
@@ -252,18 +256,22 @@ k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __
   double2* smg = sm + g * C::BUF;
   double2* tw1 = sm + G * C::BUF;
   stage_tw<N1>(tw1, a.lt.tw1);
-  const long off = (long)b * N;
+  const long off = (long)b * a.n;   // vectors [B][n]
+  const long offz = (long)b * N;    // transform work [B][nt]
   double2 z[E];
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const int k1 = tid + c * T;
     const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
-    z[c] = cmulc(a.Z[off + (long)k1 * N2 + t2], w);
+    z[c] = cmulc(a.Z[offz + (long)k1 * N2 + t2], w);
   }
   group_fft<N1, E, true>(z, smg, tw1, 0, tid);
   if (out_mode == CO_REAL) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) dst[off + (long)N2 * (tid + c * T) + t2] = z[c].x;
+    for (int c = 0; c < E; ++c) {
+      const long j = (long)N2 * (tid + c * T) + t2;
+      if (j < a.n) dst[off + j] = z[c].x;
+    }
     return;
   }
   // CO_APPLY: even channel result in registers, then the odd channel
@@ -275,7 +283,7 @@ k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __
   for (int c = 0; c < E; ++c) {
     const int k1 = tid + c * T;
     const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
-    z[c] = cmulc(Zo[off + (long)k1 * N2 + t2], w);
+    z[c] = cmulc(Zo[offz + (long)k1 * N2 + t2], w);
   }
   group_fft<N1, E, true>(z, smg, tw1, 0, tid);
   Vals<2> pr;
@@ -283,6 +291,7 @@ k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const long j = (long)N2 * (tid + c * T) + t2;
+    if (j >= a.n) continue;
     const double2 w = tw_get_g(a.lt.twL, j);
     const double ax = ye[c] + fma(z[c].x, w.x, z[c].y * w.y);  // + Re(conj(w) z)
     const double y = a.kappa ? fma(a.shift, xin[off + j], a.kappa[off + j] * ax) : ax;

@@ -15,7 +15,7 @@ int report_error(int code, const char* msg);
 std::vector<double2> twiddle_table(int N);
 
 struct LargePlan {
-  int n = 0, N1 = 0, N2 = 0, np = 0;
+  int n = 0, nt = 0, N1 = 0, N2 = 0, np = 0;   // vector length n <= transform length nt
   int ncol_cta = 0;            // column CTAs per instance (partial-sum count)
   int has_pc = 0;
   int device = 0;
@@ -24,7 +24,7 @@ struct LargePlan {
   double2* tables = nullptr;  // one allocation for every table
   // workspaces, sized for `cap` instances
   int cap = 0;
-  double* ws = nullptr;       // 9 vectors [cap][n]
+  double* ws = nullptr;       // 8 vectors [cap][n] + Strang spectrum [cap][nt]
   double2* Z = nullptr;       // [2][cap][n] (two transform channels)
   double* part = nullptr;     // [cap][4][np]
   LState* st = nullptr;       // [cap]
@@ -32,8 +32,10 @@ struct LargePlan {
   int* h_active = nullptr;
 };
 
-// n a power of two in [2^10, 2^24]; symbol_re: L = 2n reals; lam: n reals or null
-int large_plan_init(LargePlan* lp, int n, const double* symbol_re, const double* lam, int device);
+// embedding L a power of two in [2^14, 2^25] with 2n-1 <= L (vectors of length n are
+// zero-padded to the transform length L/2); symbol_re: L reals; lam: n reals (n = L/2) or null
+int large_plan_init(LargePlan* lp, int n, int L, const double* symbol_re, const double* lam,
+                    int device);
 void large_plan_free(LargePlan* lp);
 int large_reserve(LargePlan* lp, int B);
 

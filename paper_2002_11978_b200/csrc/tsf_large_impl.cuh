@@ -26,7 +26,7 @@ int LargeDispatch<LOG>::col_fwd(const LargeArgs& a, const double* src, int in_mo
   auto k = k_lcol_fwd<N1>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  k<<<dim3(a.n / N1 / S::G, a.B), S::BLOCK, S::SMEM, st>>>(a, src, in_mode);
+  k<<<dim3(a.nt / N1 / S::G, a.B), S::BLOCK, S::SMEM, st>>>(a, src, in_mode);
   return large_launch_error(cudaGetLastError());
 }
 
@@ -37,7 +37,7 @@ int LargeDispatch<LOG>::row(const LargeArgs& a, int spec_mode, cudaStream_t st) 
   auto k = k_lrow<N2>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  k<<<dim3(a.n / N2, a.B), S::BLOCK, S::SMEM, st>>>(a, spec_mode);
+  k<<<dim3(a.nt / N2, a.B), S::BLOCK, S::SMEM, st>>>(a, spec_mode);
   return large_launch_error(cudaGetLastError());
 }
 
@@ -49,7 +49,7 @@ int LargeDispatch<LOG>::col_inv(const LargeArgs& a, double* dst, int out_mode, c
   auto k = k_lcol_inv<N1>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  k<<<dim3(a.n / N1 / S::G, a.B), S::BLOCK, S::SMEM, st>>>(a, dst, out_mode, xin, w1, pslot);
+  k<<<dim3(a.nt / N1 / S::G, a.B), S::BLOCK, S::SMEM, st>>>(a, dst, out_mode, xin, w1, pslot);
   return large_launch_error(cudaGetLastError());
 }
 

@@ -218,3 +218,35 @@ def test_cfg1_march_vs_reference(gam, alpha):
     assert abs(d.mean()) <= max(0.1, 3.0 * d.std() / math.sqrt(d.size)), (d.mean(), d.std())
     assert e64 <= max(1e-10, 10 * fl["rel_l2_u64"])
     assert eM <= max(1e-10, 10 * fl["rel_l2_uM"])
+
+
+@pytest.mark.parametrize("n", [5000, 12289, 70001])
+def test_large_nonpow2_matvec_and_precond(n):
+    """n not a power of two: vectors zero-padded to the transform length
+    L/2 of the reference's own embedding (toeplitz.py:39-41)."""
+    rng = np.random.default_rng(n)
+    col = _col(n)
+    v = rng.standard_normal(n)
+    L, sym = O.toeplitz_symbol(col)
+    op = P.build_toeplitz(col)
+    kap = _kappa(n, 3)
+    got = P.toeplitz_matvec(op, v, kappa=kap, shift=11.0)
+    assert rel_err(got, 11.0 * v + kap * O.toeplitz_apply(sym, v)) <= 1e-13
+    p = P.build_preconditioner(col, 41.0, 1.3)
+    total = 41.0 + 1.3 * O.strang_eigs(col)
+    assert rel_err(P.precond_solve(p, v), O.precond_apply(total, v)) <= 1e-13
+
+
+def test_large_nonpow2_level_solves():
+    n = 10000
+    col, kap, shift, b = _level(n, 77)
+    lev = P.LevelOperator(P.build_toeplitz(col), shift, kap)
+    for pc_on in (True, False):
+        tol = 1e-10
+        xo, out = _oracle_solve(col, kap, shift, b, tol, pc=pc_on)
+        pc = P.build_preconditioner(col, shift, float(kap.mean())) if pc_on else None
+        x, rep = P.solve_bicgstab(lev, pc, b, tol=tol)
+        assert rep.converged and out.converged
+        assert abs(rep.iterations - out.iterations) <= max(2, out.iterations // 5), \
+            (pc_on, rep.iterations, out.iterations)
+        assert rel_l2(x, xo) <= 1e-8
