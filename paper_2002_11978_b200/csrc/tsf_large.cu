@@ -33,7 +33,10 @@ constexpr int kLelChunk = kLelThreads * kLelPer;  // elements per elementwise CT
 constexpr int kLscThreads = 256;
 constexpr int kLargeChunk = 4;  // iterations launched between completion polls
 
-enum LStage : int { LS_BEGIN = 0, LS_ALPHA = 1, LS_SNORM = 2, LS_OMEGA = 3, LS_REL = 4 };
+enum LStage : int {
+  LS_BEGIN = 0, LS_ALPHA = 1, LS_SNORM = 2, LS_OMEGA = 3, LS_REL = 4,   // BiCGSTAB
+  LS_CG_RZ0 = 5, LS_CG_ALPHA = 6, LS_CG_REL = 7, LS_CG_BETA = 8,        // PCG
+};
 
 TSF_D double* pslot(const LargeArgs& a, int b, int slot) {
   return a.part + ((long)b * 4 + slot) * a.np;
@@ -191,6 +194,76 @@ __global__ void __launch_bounds__(kLelThreads) k_lspec(LargeArgs a, double kbar,
   }
 }
 
+// ---- PCG elementwise kernels (krylov.py:43-85)
+// dst = src
+__global__ void __launch_bounds__(kLelThreads) k_lel_copy(LargeArgs a, double* __restrict__ dst,
+                                                          const double* __restrict__ src) {
+  const int b = blockIdx.y, tid = threadIdx.x;
+  if (inst_skip(a, b)) return;
+  const long off = (long)b * a.n;
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (jj >= a.n) break;
+    dst[off + jj] = src[off + jj];
+  }
+}
+
+// partial u . w into `slot`
+__global__ void __launch_bounds__(kLelThreads) k_lel_dot(LargeArgs a, const double* __restrict__ u,
+                                                         const double* __restrict__ w, int slot) {
+  __shared__ double red[4 * 32];
+  const int b = blockIdx.y, tid = threadIdx.x;
+  if (inst_skip(a, b)) return;
+  const long off = (long)b * a.n;
+  double d = 0.0;
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (jj >= a.n) break;
+    d = fma(u[off + jj], w[off + jj], d);
+  }
+  d = block_sum1(d, red);
+  if (tid == 0) pslot(a, b, slot)[blockIdx.x] = d;
+}
+
+// x += alpha p ; r -= alpha q (q in v) ; partial ||r||^2 (slot 0)
+__global__ void __launch_bounds__(kLelThreads) k_lel_cgxr(LargeArgs a) {
+  __shared__ double red[4 * 32];
+  const int b = blockIdx.y, tid = threadIdx.x;
+  if (inst_skip(a, b)) return;
+  const long off = (long)b * a.n;
+  const double al = a.st[b].alpha;
+  double rr = 0.0;
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (jj >= a.n) break;
+    const long j = off + jj;
+    a.x[j] = a.x[j] + al * a.p[j];
+    const double r = a.r[j] - al * a.v[j];
+    a.r[j] = r;
+    rr = fma(r, r, rr);
+  }
+  rr = block_sum1(rr, red);
+  if (tid == 0) pslot(a, b, 0)[blockIdx.x] = rr;
+}
+
+// p = z + beta p
+__global__ void __launch_bounds__(kLelThreads) k_lel_cgp(LargeArgs a, const double* __restrict__ z) {
+  const int b = blockIdx.y, tid = threadIdx.x;
+  if (inst_skip(a, b)) return;
+  const long off = (long)b * a.n;
+  const double beta = a.st[b].omega;   // PCG keeps beta in the omega slot
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (jj >= a.n) break;
+    const long j = off + jj;
+    a.p[j] = z[j] + beta * a.p[j];
+  }
+}
+
 // ---- scalar kernel: one CTA per instance, partial sums in fixed order
 TSF_D double psum(const LargeArgs& a, int b, int slot, int count, double* red) {
   const double* p = pslot(a, b, slot);
@@ -249,6 +322,31 @@ __global__ void __launch_bounds__(kLscThreads) k_lsc(LargeArgs a, int stage, int
     if (tid != 0) return;
     if (tt == 0.0) return lfinish(a, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN);
     a.st[b].omega = ts / tt;
+  } else if (stage == LS_CG_RZ0) {         // rz = r . z of the start vector
+    if (s.mode != LM_ACTIVE) return;
+    const double rz = psum(a, b, 0, count, red);
+    if (tid == 0) a.st[b].rz = rz;
+  } else if (stage == LS_CG_ALPHA) {       // curvature p . A p
+    if (s.mode != LM_ACTIVE) return;
+    const double curv = psum(a, b, 1, count, red);
+    if (tid != 0) return;
+    if (curv <= 0.0) return lfinish(a, b, s.it, s.rnorm / s.nrm0, TSF_BD_CURVATURE);
+    a.st[b].alpha = s.rz / curv;
+  } else if (stage == LS_CG_REL) {
+    if (s.mode != LM_ACTIVE) return;
+    const double rnorm = sqrt(psum(a, b, 0, count, red));
+    if (tid != 0) return;
+    const double rel = rnorm / s.nrm0;
+    if (rel < a.tol) return lfinish(a, b, s.it, rel, TSF_OK);
+    if (s.it >= a.max_iters) return lfinish(a, b, a.max_iters, rel, TSF_NOT_CONVERGED);
+    a.st[b].rnorm = rnorm;
+  } else if (stage == LS_CG_BETA) {
+    if (s.mode != LM_ACTIVE) return;
+    const double rz_new = psum(a, b, 0, count, red);
+    if (tid != 0) return;
+    a.st[b].omega = rz_new / s.rz;   // beta
+    a.st[b].rz = rz_new;
+    a.st[b].it = s.it + 1;
   } else {  // LS_REL
     if (s.mode == LM_EARLY) {
       if (tid == 0) lfinish(a, b, s.it, s.snorm / s.nrm0, TSF_OK);
@@ -360,6 +458,44 @@ struct Runner {
     k_lel_xr<<<lel_grid(), kLelThreads, 0, st>>>(a, ph, sh);
     if ((rc = cuda_check(cudaGetLastError(), "k_lel_xr"))) return rc;
     return sc(LS_REL, NR, pc);
+  }
+  int dot(const double* u, const double* w, int slot) {
+    k_lel_dot<<<lel_grid(), kLelThreads, 0, st>>>(a, u, w, slot);
+    return cuda_check(cudaGetLastError(), "k_lel_dot");
+  }
+  // PCG start: r = b, z = P^{-1} r, p = z, rz = r . z
+  int cg_start(int pc) {
+    int rc;
+    const int NR = (a.n + kLelChunk - 1) / kLelChunk;
+    k_lel_copy<<<lel_grid(), kLelThreads, 0, st>>>(a, a.r, a.r0);
+    if ((rc = cuda_check(cudaGetLastError(), "k_lel_copy"))) return rc;
+    if (pc) {
+      if ((rc = strang(CI_LOAD, a.r, a.p))) return rc;
+    } else {
+      k_lel_copy<<<lel_grid(), kLelThreads, 0, st>>>(a, a.p, a.r);
+      if ((rc = cuda_check(cudaGetLastError(), "k_lel_copy"))) return rc;
+    }
+    if ((rc = dot(a.r, a.p, 0))) return rc;
+    return sc(LS_CG_RZ0, NR, pc);
+  }
+  // one PCG iteration: q = M p, alpha, x/r update, test, z = P^{-1} r, beta, p
+  int cg_iteration(int pc) {
+    int rc;
+    const int NC = lp->ncol_cta, NR = (a.n + kLelChunk - 1) / kLelChunk;
+    if ((rc = apply(a.p, a.v, a.p, 0))) return rc;           // q -> v; p.q partials
+    if ((rc = sc(LS_CG_ALPHA, NC, pc))) return rc;
+    k_lel_cgxr<<<lel_grid(), kLelThreads, 0, st>>>(a);
+    if ((rc = cuda_check(cudaGetLastError(), "k_lel_cgxr"))) return rc;
+    if ((rc = sc(LS_CG_REL, NR, pc))) return rc;
+    const double* z = a.r;
+    if (pc) {
+      if ((rc = strang(CI_LOAD, a.r, a.s))) return rc;       // z -> s
+      z = a.s;
+    }
+    if ((rc = dot(a.r, z, 0))) return rc;
+    if ((rc = sc(LS_CG_BETA, NR, pc))) return rc;
+    k_lel_cgp<<<lel_grid(), kLelThreads, 0, st>>>(a, z);
+    return cuda_check(cudaGetLastError(), "k_lel_cgp");
   }
 };
 
@@ -527,8 +663,7 @@ int large_precond(LargePlan* lp, int B, const double* v, double* z, double shift
 }
 
 int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, cudaStream_t st) {
-  if (method != 0)
-    return report_error(TSF_E_UNSUPPORTED, "large-n engine: only BiCGSTAB (method 0) so far");
+  if (method != 0 && method != 1) return report_error(TSF_E_INVALID, "method must be 0 or 1");
   if (pc && !lp->has_pc) return report_error(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner");
   int rc = large_reserve(lp, B);
   if (rc) return rc;
@@ -556,9 +691,10 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
     k_lspec<<<R.lel_grid(), kLelThreads, 0, st>>>(a, 0.0, nullptr, 1);
     if ((rc = cuda_check(cudaGetLastError(), "k_lspec"))) return rc;
   }
+  if (method == 1 && (rc = R.cg_start(pc))) return rc;
   for (int it = 0; it < a.max_iters; it += kLargeChunk) {
     for (int c = 0; c < kLargeChunk && it + c < a.max_iters; ++c)
-      if ((rc = R.bicg_iteration(pc))) return rc;
+      if ((rc = method == 1 ? R.cg_iteration(pc) : R.bicg_iteration(pc))) return rc;
     if ((rc = cuda_check(cudaMemcpyAsync(lp->h_active, lp->active, sizeof(int),
                                          cudaMemcpyDeviceToHost, st), "poll")))
       return rc;

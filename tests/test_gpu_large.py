@@ -250,3 +250,22 @@ def test_large_nonpow2_level_solves():
         assert abs(rep.iterations - out.iterations) <= max(2, out.iterations // 5), \
             (pc_on, rep.iterations, out.iterations)
         assert rel_l2(x, xo) <= 1e-8
+
+
+@pytest.mark.parametrize("n,pc_on", [(16384, True), (16384, False), (65536, True)])
+def test_large_cg_vs_oracle(n, pc_on):
+    """Fused PCG of the four-step engine (krylov.py:43-85) against the oracle."""
+    col, kap, shift, b = _level(n, 5 + n)
+    kc = float(kap.mean())
+    L, sym = O.toeplitz_symbol(col)
+    total = shift + kc * O.strang_eigs(col)
+    apply = lambda q: shift * q + kc * O.toeplitz_apply(sym, q)  # noqa: E731
+    ps = (lambda q: O.precond_apply(total, q)) if pc_on else None
+    xo, out = O.cg(apply, ps, b, tol=1e-10, max_iters=5000)
+    lev = P.LevelOperator(P.build_toeplitz(col), shift, np.full(n, kc))
+    pc = P.build_preconditioner(col, shift, kc) if pc_on else None
+    x, rep = P.solve_cg(lev, pc, b, tol=1e-10, max_iters=5000)
+    assert rep.converged == out.converged
+    assert abs(rep.iterations - out.iterations) <= max(2, out.iterations // 10), \
+        (rep.iterations, out.iterations)
+    assert rel_l2(x, xo) <= 1e-8

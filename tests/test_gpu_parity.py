@@ -126,6 +126,27 @@ def test_level_solve_vs_reference():
     assert seen >= 7
 
 
+def test_cg_vs_reference():
+    """PCG on the x-independent system (kappa constant, the reference's
+    solve_cg branch, scheme.py:138): every golden n, single-CTA and
+    four-step engines, and the circulant path at non-pow2 n."""
+    seen = 0
+    for i, g in _lin_cases():
+        col = g[f"tp{i}_col"]
+        n = col.size
+        shift = g[f"tp{i}_shift"][0]
+        kc = float(g[f"tp{i}_cg_kc"][0])
+        lev = P.LevelOperator(P.build_toeplitz(col), shift, np.full(n, kc))
+        pc = P.build_preconditioner(col, shift, kc)
+        x, rep = P.solve_cg(lev, pc, g[f"tp{i}_bicg_12_b"], tol=1e-12)
+        its = int(g[f"tp{i}_cg_rep"][0])
+        assert rep.converged, (i, rep)
+        assert abs(rep.iterations - its) <= 2, (i, rep.iterations, its)
+        assert rel_l2(x, g[f"tp{i}_cg_x"]) <= 1e-10, i
+        seen += 1
+    assert seen >= 8
+
+
 def test_zero_rhs_zero_iterations():
     col = golden("linalg")["tp0_col"]
     op = P.build_toeplitz(col)
