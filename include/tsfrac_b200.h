@@ -54,11 +54,20 @@ const char* tsf_last_error(void);
  * Plan for one spatial size n (reference: ToeplitzOperator built by
  * build_toeplitz, toeplitz.py:34-48, plus the level-independent part of
  * build_preconditioner, toeplitz.py:101-128).
- *   L          circulant embedding length (power of two >= 2n-1, >= 32)
+ *   L          circulant embedding length (power of two >= 2n-1, >= 32,
+ *              <= 2^25).  L <= 8192: one CTA per instance (single-CTA engine);
+ *              above: the four-step multi-kernel engine.  Any n.
  *   symbol_re  HOST, L reals: Re FFT_L(even embedding of the first column)
- *   lam        HOST, n reals: Re FFT_n(strang_first_column), or NULL when
- *              no preconditioner is needed (n need not be a power of two)
+ *   lam        HOST, n reals: Re FFT_n(strang_first_column) for the fused
+ *              Strang kernels (power-of-two n >= 16 with L = 2n), or NULL.
+ *              Other n apply the Strang preconditioner as circ(IFFT(1/total))
+ *              through a second plan whose symbol is that circulant's
+ *              (toeplitz.py _circulant_plan in the Python layer).
  *   device     CUDA ordinal the plan lives on
+ * All entry points below are stream-ordered.  For L <= 8192 the level solve
+ * is one CUDA graph launch with a conditional WHILE loop and returns without
+ * waiting (TSF_SOLVE_GRAPH=0 selects the host-polled loop); the four-step
+ * engine's solve polls a device counter every 4 iterations (stream sync).
  */
 int tsf_plan_create(tsf_plan** plan, int n, int L, const double* symbol_re,
                     const double* lam, int device);
