@@ -61,6 +61,18 @@ bool graph_mode() {
   return v == 1;
 }
 
+// BiCGSTAB takes the even channel of each Toeplitz product from the Strang
+// solve's stored spectrum (tsf_filters.cuh filt_strang_tab); TSF_SPEC_REUSE=0
+// restores the recomputed forward transform (A/B measurement).
+bool spec_reuse() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_SPEC_REUSE");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 SolveGraphs::~SolveGraphs() {
   for (auto& a : slot)
     for (auto& b : a)
@@ -184,7 +196,8 @@ int ensure_reserved(tsf_plan* p, int B) {
   p->kst = nullptr;
   p->cap = 0;
   CK(cudaSetDevice(p->device));
-  CK(cudaMalloc(&p->ws, sizeof(double) * (size_t)B * p->n * 9));
+  // 9 vectors [B][n] + the Strang half spectra [B][L/4+1] complex (hspec)
+  CK(cudaMalloc(&p->ws, sizeof(double) * ((size_t)B * p->n * 9 + (size_t)B * (p->L / 2 + 2))));
   CK(cudaMalloc(&p->ist, sizeof(int) * (size_t)B * 2));
   CK(cudaMalloc(&p->dst, sizeof(double) * (size_t)B));
   CK(cudaMalloc(&p->kst, sizeof(KState) * (size_t)B));
@@ -354,6 +367,7 @@ static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cud
   a.sh = p->ws + 5 * vn;
   a.t = p->ws + 6 * vn;
   a.pspec = p->ws + 8 * vn;
+  a.hspec = spec_reuse() ? reinterpret_cast<double2*>(p->ws + 9 * vn) : nullptr;
   a.kst = p->kst;
   a.active = p->ist;
   a.h_active = p->h_active;

@@ -28,6 +28,7 @@ struct SolveGraphs {
   ~SolveGraphs();
 };
 bool graph_mode();  // TSF_SOLVE_GRAPH (default 1)
+bool spec_reuse();  // TSF_SPEC_REUSE (default 1)
 
 template <int LOG>
 struct Dispatch {

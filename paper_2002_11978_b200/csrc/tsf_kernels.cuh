@@ -52,6 +52,8 @@ struct KrylovArgs {
   double* sh;
   double* t;
   double* pspec;            // [B, n] Strang spectrum S_k / n of the level (PC == 1)
+  double2* hspec;           // [B, N/2+1] half spectrum of the last Strang output (BiCGSTAB,
+                            // PC == 1), or null: recompute the even channel's transform
   KState* kst;              // [B] per-instance Krylov scalars (phase kernels)
   SoeArgs soe;              // fused SOE epilogue of converged instances (march)
   int soe_epilogue;         // 1: run it
@@ -81,16 +83,19 @@ struct KShape {
 };
 
 // y = shift*x + kappa .* (A x) on the owned slots (kappa == nullptr: y = A x).
-// x is read from global (twice); result returned in y[].
+// x is read from global (twice); result returned in y[].  hs: x's half
+// spectrum from the Strang solve that produced x (filt_strang_tab), or null.
 template <int N>
 TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restrict__ kg,
                           double shift, int n, double (&y)[FShape<N>::E], double2* sm, double* aux,
-                          const FilterTables& t) {
+                          const FilterTables& t, const double2* hs = nullptr) {
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   const bool own = tid < T;
   double2 z[FShape<N>::E];
-  {
+  if (hs) {
+    filt_even_spec<N>(hs, z, sm, t);   // x = Re IFFT(hs): its spectrum is already known
+  } else {
     double xr[FShape<N>::E];
     if (own) {
 #pragma unroll
@@ -181,6 +186,11 @@ k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ zo, dou
 // Krylov scalars live in KState; CTA-local reductions give every dot
 // product of an instance inside its own CTA.
 
+template <int N>
+TSF_D double2* hspec_of(const KrylovArgs& a, int b) {
+  return a.hspec ? a.hspec + (long)b * (N / 2 + 1) : nullptr;
+}
+
 struct KState {
   double rho, rho_new, alpha, omega, nrm0, rnorm, snorm, kbar, rz;
   int it, done;
@@ -207,10 +217,10 @@ TSF_D void store_owned(double* g, const double (&u)[FShape<N>::E], int n) {
 // dst = P^{-1} u (u real, owned slots); spec = the instance's S_k / n
 template <int N>
 TSF_D void precond_store(const double (&u)[FShape<N>::E], double* dst, int n, const double* spec,
-                         double2* sm, const FilterTables& t) {
+                         double2* sm, const FilterTables& t, double2* hs = nullptr) {
   constexpr int T = KShape<N>::T;
   double2 z[FShape<N>::E];
-  filt_strang_tab<N>(u, z, sm, t, t.ps ? t.ps : spec);
+  filt_strang_tab<N>(u, z, sm, t, t.ps ? t.ps : spec, hs);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) st_real(dst, n, threadIdx.x + c * T, z[c].x);
@@ -316,7 +326,8 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
   double rz = ss;
   if constexpr (PC == 1) {
     // BiCGSTAB: p_hat = P^{-1} p ; CG: z = P^{-1} r written to p (p = z)
-    precond_store<N>(u, CG ? a.p + off : a.ph + off, n, a.pspec + off, sm, tab);
+    precond_store<N>(u, CG ? a.p + off : a.ph + off, n, a.pspec + off, sm, tab,
+                     CG ? nullptr : hspec_of<N>(a, b));
     if (CG) {
       double part = 0.0;
       if (own) {
@@ -363,7 +374,8 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   prefetch_l2(a.rhs + off, n);
   if (s.it != 1) prefetch_l2(a.r + off, n);
   double u[FShape<N>::E];
-  apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, tab);   // u = v = M p_hat
+  double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
+  apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, tab, hs);   // u = v = M p_hat
   store_owned<N>(a.v + off, u, n);
   double part = 0.0;
   if (own) {
@@ -404,7 +416,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
     return true;
   }
   store_owned<N>(a.s + off, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.sh + off, n, a.pspec + off, sm, tab);
+  if constexpr (PC == 1) precond_store<N>(u, a.sh + off, n, a.pspec + off, sm, tab, hs);
   if (tid == 0) {
     st[b].alpha = alpha;
     st[b].snorm = snorm;
@@ -436,7 +448,8 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   prefetch_l2(a.p + off, n);
   prefetch_l2(a.v + off, n);
   double u[FShape<N>::E];
-  apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, tab);   // u = t = M s_hat
+  double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
+  apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, tab, hs);   // u = t = M s_hat
   Vals<2> red2;
   red2.v[0] = 0.0;
   red2.v[1] = 0.0;
@@ -504,7 +517,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
     }
   }
   store_owned<N>(a.p + off, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.ph + off, n, a.pspec + off, sm, tab);
+  if constexpr (PC == 1) precond_store<N>(u, a.ph + off, n, a.pspec + off, sm, tab, hs);
   if (tid == 0) {
     st[b].rho = s.rho_new;
     st[b].rho_new = rho_new;
