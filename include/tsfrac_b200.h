@@ -129,6 +129,21 @@ int tsf_soe_push_rhs(int B, int n, int nexp, double* W, const double* u,
                      int do_rhs, double a_next, double G, const double* f, double* rhs,
                      void* stream);
 
+/*
+ * Direct L1 history right-hand side of the DIDS scheme (reference: run_dids,
+ * scheme.py:208-216 — `rhs = f + (a[0]/G) hist[0]; rhs += (diff(a) @ hist[1:m])/G`
+ * with a = l1_weights(mesh, gamma, m).a, mesh.py:53-80):
+ *   rhs_i = (f_i + c0 * hist[0]_i) + (sum_{k=1}^{rows-1} w[k-1] * hist[k]_i) / G
+ *   rows         m (levels 0..m-1 of the history are read)
+ *   hist         [B] x [rows][n] (instance b at hist + b*inst_stride)
+ *   w            device [rows-1]: diff(a)  (unused when rows == 1)
+ *   c0           a[0] / G (host scalar, formed as the reference does)
+ *   f, rhs       [B][n]
+ */
+int tsf_l1_history_rhs(int B, int n, int rows, const double* hist, int64_t inst_stride,
+                       const double* w, double c0, double G, const double* f, double* rhs,
+                       void* stream);
+
 /* Coefficient field  g(x_i, t_m) = sum_q modes_m[q][b][i] * coef[m][q], where
  * modes_m = modes + m*t_stride.  Separable fields use t_stride = 0; a field
  * tabulated per level (arbitrary callables evaluated on the host, as the

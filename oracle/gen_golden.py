@@ -248,6 +248,37 @@ def gen_marches(tsfrac):
     return out
 
 
+def gen_dids(tsfrac):
+    """run_dids (scheme.py:184-233): per-level history + iteration counts for
+    pow2 / non-pow2 n and the dense branch, plus the FIDS march of the same
+    case (the reference's FIDS-DIDS proximity criterion,
+    pkg/tests/test_acceptance.py:141-166)."""
+    from tsfrac.scheme import ProblemSpec, SolverOptions, run_dids
+    kappa, source, initial = cfg0_fields()
+    out = {}
+    cases = {
+        "d1": (0.5, 1.5, 64, 257, 1e-12, "pkrylov"),   # n=256
+        "d2": (0.3, 1.2, 32, 101, 1e-12, "pkrylov"),   # n=100 (non-pow2)
+        "d3": (0.8, 1.9, 24, 129, 1e-10, "krylov"),    # n=128 unpreconditioned
+        "d4": (0.5, 1.5, 16, 65, 1e-12, "auto"),       # n=64 -> dense branch
+    }
+    for tag, (g, a, M, N, tol, solver) in cases.items():
+        spec = ProblemSpec(gamma=g, alpha=a, l=1.0, T=1.0, kappa=kappa,
+                           source=source, initial=initial)
+        r = (2.0 - g) / g
+        with Recorder(tsfrac.scheme) as rec:
+            hist, rep = run_dids(spec, M, r, N, options=SolverOptions(solver=solver, tol=tol))
+        out[f"{tag}_args"] = np.array([g, a, M, N, tol, r])
+        out[f"{tag}_solver"] = np.array(solver)
+        out[f"{tag}_hist"] = hist
+        out[f"{tag}_its"] = np.array(rec.its, dtype=np.int64)
+        out[f"{tag}_avg"] = np.array([rep.avg_iterations])
+        out[f"{tag}_ops"] = rep.history_ops
+        hf, _, _, _ = _march(tsfrac, spec, M, r, N, 1e-12, tol, solver=solver)
+        out[f"{tag}_fids_hist"] = hf
+    return out
+
+
 def gen_big(tsfrac):
     """cfg1 (n=16384, M=1024) for all 12 (gamma, alpha): per-step its + u^M."""
     from concurrent.futures import ProcessPoolExecutor
@@ -274,12 +305,22 @@ def _cfg1_one(ga):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run cfg1 (minutes)")
+    ap.add_argument("--only", default="", help="comma list of fixtures to regenerate "
+                    "(setup,linalg,march,dids,cfg1); default all but cfg1")
     args = ap.parse_args()
     tsfrac = _import_reference()
     OUT.mkdir(parents=True, exist_ok=True)
+    if args.only:
+        gens = {"setup": gen_setup, "linalg": gen_linear_algebra, "march": gen_marches,
+                "dids": gen_dids, "cfg1": gen_big}
+        for name in args.only.split(","):
+            np.savez_compressed(OUT / f"{name}.npz", **gens[name](tsfrac))
+            print(name, (OUT / f"{name}.npz").stat().st_size)
+        return
     np.savez_compressed(OUT / "setup.npz", **gen_setup(tsfrac))
     np.savez_compressed(OUT / "linalg.npz", **gen_linear_algebra(tsfrac))
     np.savez_compressed(OUT / "march.npz", **gen_marches(tsfrac))
+    np.savez_compressed(OUT / "dids.npz", **gen_dids(tsfrac))
     if args.big:
         np.savez_compressed(OUT / "cfg1.npz", **gen_big(tsfrac))
     meta = {"numpy": np.__version__, "seed": SEED,

@@ -30,7 +30,7 @@ __all__ = [
     "normalization_constant", "soe_build", "SoeError", "toeplitz_symbol",
     "toeplitz_apply", "strang_column", "strang_eigs", "precond_apply",
     "bicgstab", "cg", "KrylovOutcome", "soe_push", "soe_history_term",
-    "fids_march", "FidsRecord", "fids_step", "embed_length",
+    "fids_march", "FidsRecord", "fids_step", "embed_length", "dids_march",
 ]
 
 
@@ -433,3 +433,59 @@ def fids_march(gamma, alpha, l, T, M, r, N, kappa_fn, source_fn, initial_fn,
         if keep_history:
             hist[m] = u
     return FidsRecord(hist if keep_history else u_prev, its, rel, s, w)
+
+
+# --------------------------------------------------------------------------
+# scheme.py  (DIDS, Krylov branches)
+# --------------------------------------------------------------------------
+
+def dids_march(gamma, alpha, l, T, M, r, N, kappa_fn, source_fn, initial_fn,
+               mu=None, tol=1e-10, max_iters=None, precondition=True, use_cg=False):
+    """run_dids restated (scheme.py:184-233), Krylov branches only.
+
+    History term at level m (scheme.py:213-216):
+        rhs = f + (a[0]/G) u^0 ;  rhs += (diff(a) @ hist[1:m]) / G   (m > 1)
+    with a = l1_weights(mesh, gamma, m).a (mesh.py:53-80); the level system
+    is the one run_fids solves, with shift = a[-1]/G (scheme.py:218-219).
+    Returns a FidsRecord (nodes/weights empty: DIDS has no SOE).
+    """
+    t, tau = graded_mesh(M, r, T)
+    mu = 1.0 + alpha / 2.0 if mu is None else mu
+    col, h, _ = ifl_column(alpha, mu, l, N)
+    x = -l + h * np.arange(1, N)
+    _, symbol = toeplitz_symbol(col)
+    lam = strang_eigs(col)
+    g1mg = math.exp(gammaln(1.0 - gamma))
+    n = N - 1
+    hist = np.empty((M + 1, n))
+    hist[0] = initial_fn(x)
+    its = np.zeros(M, dtype=np.int64)
+    rel = np.zeros(M)
+    for m in range(1, M + 1):
+        a = l1_weight_row(t, tau, gamma, m)
+        tm = t[m]
+        kappa = np.broadcast_to(np.asarray(kappa_fn(x, tm), dtype=float), x.shape).copy()
+        if np.any(kappa <= 0.0):
+            raise ValueError(f"kappa must be positive on the grid at t={tm}")
+        rhs = np.asarray(source_fn(x, tm), dtype=float) + (a[0] / g1mg) * hist[0]
+        if m > 1:
+            rhs += (np.diff(a) @ hist[1:m]) / g1mg
+        shift = a[-1] / g1mg
+
+        def apply(q, shift=shift, kappa=kappa):
+            return shift * q + kappa * toeplitz_apply(symbol, q)
+
+        psolve = None
+        if precondition:
+            total = shift + float(kappa.mean()) * lam
+            if np.any(total <= 0.0):
+                raise RuntimeError("preconditioner has a non-positive eigenvalue")
+            psolve = lambda q, total=total: precond_apply(total, q)  # noqa: E731
+        solver = cg if use_cg else bicgstab
+        u, out = solver(apply, psolve, rhs, tol=tol, max_iters=max_iters)
+        if not out.converged:
+            raise RuntimeError(f"Krylov solve did not converge: {out}")
+        its[m - 1] = out.iterations
+        rel[m - 1] = out.relres
+        hist[m] = u
+    return FidsRecord(hist, its, rel, np.empty(0), np.empty(0))

@@ -11,7 +11,7 @@ from .krylov import (KrylovReport, LevelOperator, MatrixFreeOperator, solve_bicg
                      solve_cg, solve_dense)
 from .mesh import GradedMesh, L1Weights, build_mesh, l1_weights
 from .scheme import (FidsMarch, ProblemSpec, SeparableField, SolveReport, SolverOptions,
-                     TimeStepSystem, run_fids, run_fids_batched, select_solver)
+                     TimeStepSystem, run_dids, run_fids, run_fids_batched, select_solver)
 from .soe import (FastHistory, SoeApproximation, SoeConstructionError, build_soe,
                   fast_caputo_rhs, fast_coefficients, history_push)
 from .toeplitz import (CirculantPreconditioner, PreconditionerError, ToeplitzOperator,

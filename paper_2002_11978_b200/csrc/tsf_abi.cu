@@ -12,6 +12,7 @@
 #include "tsf_dispatch.h"
 #include "tsf_large_api.h"
 #include "tsf_soe.cuh"
+#include "tsf_dids.cuh"
 
 using namespace tsf;
 
@@ -411,6 +412,22 @@ static int soe_launch(int B, SoeArgs& s, cudaStream_t st) {
     CK(cudaFuncSetAttribute(k_soe_push_rhs<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   }
   k_soe_push_rhs<8><<<(unsigned)B * chunks, kSoeThreads, smem, st>>>(s);
+  CK(cudaGetLastError());
+  return TSF_SUCCESS;
+}
+
+int tsf_l1_history_rhs(int B, int n, int rows, const double* hist, int64_t inst_stride,
+                       const double* w, double c0, double G, const double* f, double* rhs,
+                       void* stream) {
+  if (B < 0 || n < 1 || rows < 1) return fail(TSF_E_INVALID, "bad argument");
+  if (!hist || !f || !rhs || (rows > 1 && !w)) return fail(TSF_E_INVALID, "NULL pointer");
+  if (inst_stride < (int64_t)rows * n && B > 1)
+    return fail(TSF_E_INVALID, "instance stride smaller than rows*n");
+  if (!(G > 0.0)) return fail(TSF_E_INVALID, "G must be > 0");
+  if (B == 0) return TSF_SUCCESS;
+  const dim3 grid((unsigned)((n + kDidsCols - 1) / kDidsCols), (unsigned)B);
+  k_l1_history_rhs<<<grid, dim3(kDidsCols, kDidsGroups), 0, (cudaStream_t)stream>>>(
+      n, rows, hist, (long)inst_stride, w, c0, G, f, rhs);
   CK(cudaGetLastError());
   return TSF_SUCCESS;
 }

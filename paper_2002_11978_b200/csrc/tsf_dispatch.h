@@ -21,7 +21,7 @@ struct SolveGraph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraphConditionalHandle cond{};
-  cudaGraphNode_t n_set = nullptr, n_begin = nullptr, n_a = nullptr, n_b = nullptr;
+  cudaGraphNode_t n_set = nullptr, n_begin = nullptr, n_a = nullptr, n_b = nullptr, n_c = nullptr;
 };
 struct SolveGraphs {
   SolveGraph slot[kMaxLogL + 1][2][2];  // [log L][pc][cg]

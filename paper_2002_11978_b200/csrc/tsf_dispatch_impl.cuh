@@ -97,6 +97,10 @@ int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
   const cudaKernelNodeParams p_a = CG ? knode(kc, dim3(B), dim3(S::BLOCK), S::SMEM, k_args)
                                       : knode(kv, dim3(B), dim3(S::BLOCK), S::SMEM, k_args);
   const cudaKernelNodeParams p_b = knode(kt, dim3(B), dim3(S::BLOCK), S::SMEM, k_args);
+  // the loop test reads the plan's active counter, which moves when the
+  // plan's workspaces grow (ensure_reserved): its node is rewritten too
+  cudaGraphConditionalHandle h = G.cond;
+  void* c_args[] = {&h, &active};
   cudaError_t e;
   if (!G.built) {
     if ((e = prep_kernel(kb, S::SMEM)) != cudaSuccess) return launch_error(e);
@@ -127,11 +131,9 @@ int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
         return launch_error(e);
       last = G.n_b;
     }
-    cudaGraphConditionalHandle h = G.cond;
-    void* c_args[] = {&h, &active};
+    h = G.cond;
     const cudaKernelNodeParams p_c = knode(k_loop_cond, dim3(1), dim3(1), 0, c_args);
-    cudaGraphNode_t n_c;
-    if ((e = cudaGraphAddKernelNode(&n_c, body, &last, 1, &p_c)) != cudaSuccess)
+    if ((e = cudaGraphAddKernelNode(&G.n_c, body, &last, 1, &p_c)) != cudaSuccess)
       return launch_error(e);
     if ((e = cudaGraphInstantiate(&G.exec, G.graph, 0)) != cudaSuccess) return launch_error(e);
     G.built = true;
@@ -140,6 +142,9 @@ int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
         (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_begin, &p_begin)) != cudaSuccess ||
         (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_a, &p_a)) != cudaSuccess ||
         (!CG && (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_b, &p_b)) != cudaSuccess))
+      return launch_error(e);
+    const cudaKernelNodeParams p_c = knode(k_loop_cond, dim3(1), dim3(1), 0, c_args);
+    if ((e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_c, &p_c)) != cudaSuccess)
       return launch_error(e);
   }
   return launch_error(cudaGraphLaunch(G.exec, st));

@@ -287,17 +287,33 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
   }
 }
 
-template <int N, int E, int P, bool INV>
+// Load hook: a transform calls hook() once, at the start of pass
+// max(1, NPASS-2), so the caller's global loads for the step after the
+// transform (spectrum factors, epilogue operands) are in flight during the
+// last two passes instead of stalling every warp at once after the final
+// barrier (ncu: long-scoreboard stalls on those loads were 30% of the level
+// solve's stall cycles).
+struct NoHook {
+  TSF_D void operator()() const {}
+};
+template <int N, int E>
+constexpr int hook_pass() {
+  return FftPlan<N, E>::NPASS - 2 > 1 ? FftPlan<N, E>::NPASS - 2 : 1;
+}
+
+template <int N, int E, int P, bool INV, class Hook = NoHook>
 TSF_D void fft_rec(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
-                   int tw_log_scale, int tid, bool own, const double2* __restrict__ ptw = nullptr) {
+                   int tw_log_scale, int tid, bool own, const double2* __restrict__ ptw = nullptr,
+                   const Hook& hook = Hook{}) {
   using PL = FftPlan<N, E>;
   constexpr bool FIRST = (P == 0);
   constexpr bool LAST = (P == PL::NPASS - 1);
+  if constexpr (P == hook_pass<N, E>()) hook();
   stockham_pass<N, E, P, INV, FIRST, LAST>(v, sm, tw, tw_log_scale, tid, own, ptw);
   if constexpr (!LAST) {
     cp_async_wait_all();  // staged tables (tsf_filters.cuh stage_tables) land here
     __syncthreads();
-    fft_rec<N, E, P + 1, INV>(v, sm, tw, tw_log_scale, tid, own, ptw);
+    fft_rec<N, E, P + 1, INV>(v, sm, tw, tw_log_scale, tid, own, ptw, hook);
   }
 }
 
@@ -307,14 +323,16 @@ TSF_D void fft_rec(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
 // right before; ends with data in registers (sm may be reused after a
 // barrier).
 // `tw` holds W_NT^e for e < NT with NT = N << tw_log_scale.
-template <int N, int E, bool INV>
+template <int N, int E, bool INV, class Hook = NoHook>
 TSF_D void block_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
-                     int tw_log_scale, const double2* __restrict__ ptw = nullptr) {
+                     int tw_log_scale, const double2* __restrict__ ptw = nullptr,
+                     const Hook& hook = Hook{}) {
   using PL = FftPlan<N, E>;
   const int tid = threadIdx.x;
   const bool own = tid < PL::T;
   __syncthreads();
-  fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, own, ptw);
+  if constexpr (PL::NPASS < 2) hook();
+  fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, own, ptw, hook);
 }
 
 // Several independent transforms per CTA (the large-n column kernels): the
@@ -399,10 +417,10 @@ TSF_D void dft_real(const double* x, double2* X) {
 
 // First pass of a forward transform of real data (owned slots x[c],
 // j = tid + c*T), then the remaining complex passes into v[c].
-template <int N, int E>
+template <int N, int E, class Hook = NoHook>
 TSF_D void real_first_pass(const double (&x)[E], double2 (&v)[E], double2* sm,
                            const double2* __restrict__ tw, int tw_log_scale, int tid, bool own,
-                           const double2* __restrict__ ptw = nullptr) {
+                           const double2* __restrict__ ptw = nullptr, const Hook& hook = Hook{}) {
   using PL = FftPlan<N, E>;
   constexpr int R = 1 << PL::log_radix(0);
   constexpr int Q = E / R;
@@ -422,18 +440,18 @@ TSF_D void real_first_pass(const double (&x)[E], double2 (&v)[E], double2* sm,
   }
   cp_async_wait_all();
   __syncthreads();
-  fft_rec<N, E, 1, false>(v, sm, tw, tw_log_scale, tid, own, ptw);
+  fft_rec<N, E, 1, false>(v, sm, tw, tw_log_scale, tid, own, ptw, hook);
 }
 
 // Forward transform of real owned slots x[c] (j = tid + c*T) into v[c].
-template <int N, int E>
+template <int N, int E, class Hook = NoHook>
 TSF_D void block_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
                           const double2* __restrict__ tw, int tw_log_scale,
-                          const double2* __restrict__ ptw = nullptr) {
+                          const double2* __restrict__ ptw = nullptr, const Hook& hook = Hook{}) {
   static_assert(FftPlan<N, E>::NPASS >= 2, "real-input transform needs at least two passes");
   __syncthreads();
   const int tid = threadIdx.x;
-  real_first_pass<N, E>(x, v, sm, tw, tw_log_scale, tid, tid < FftPlan<N, E>::T, ptw);
+  real_first_pass<N, E>(x, v, sm, tw, tw_log_scale, tid, tid < FftPlan<N, E>::T, ptw, hook);
 }
 
 template <int N, int E>

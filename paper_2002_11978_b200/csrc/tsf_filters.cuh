@@ -94,31 +94,48 @@ TSF_D double2 mv_spec(const FilterTables& t, int k) {
 }
 
 // even output bins: z <- IFFT_N( S_even . FFT_N(x) ) for real x; caller keeps Re(z)
-template <int N>
+template <int N, class Hook = NoHook>
 TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E], double2* sm,
-                     const FilterTables& t) {
+                     const FilterTables& t, const Hook& inv_hook = Hook{}) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
-  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw);
-  if (threadIdx.x < T) {
+  const bool own = threadIdx.x < T;
+  double se[E];
+  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw, [&] {
+    if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], mv_spec<N>(t, threadIdx.x + c * T).x);
+      for (int c = 0; c < E; ++c) se[c] = mv_spec<N>(t, threadIdx.x + c * T).x;
+    }
+  });
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], se[c]);
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw);
+  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw, inv_hook);
 }
 
 // odd output bins: z (already modulated by w_j) <- IFFT_N( S_odd . FFT_N(z) );
 // caller keeps Re(conj(w_j) z_j)
-template <int N>
-TSF_D void filt_odd(double2 (&z)[FShape<N>::E], double2* sm, const FilterTables& t) {
+// inv_hook: the caller's loads for after the inverse transform (tsf_fft.cuh
+// NoHook / hook_pass)
+template <int N, class Hook = NoHook>
+TSF_D void filt_odd(double2 (&z)[FShape<N>::E], double2* sm, const FilterTables& t,
+                    const Hook& inv_hook = Hook{}) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
-  block_fft<N, E, false>(z, sm, t.tw, 1, t.ptw);
-  if (threadIdx.x < T) {
+  const bool own = threadIdx.x < T;
+  double so[E];
+  block_fft<N, E, false>(z, sm, t.tw, 1, t.ptw, [&] {
+    if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], mv_spec<N>(t, threadIdx.x + c * T).y);
+      for (int c = 0; c < E; ++c) so[c] = mv_spec<N>(t, threadIdx.x + c * T).y;
+    }
+  });
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], so[c]);
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw);
+  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw, inv_hook);
 }
 
 // Strang: z <- IFFT_n( FFT_n(x) . Ssym / n ) for real x, n = N; caller keeps Re(z)
@@ -159,12 +176,19 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
                            double2* __restrict__ hs = nullptr) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
-  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw);
-  if (threadIdx.x < T) {
+  double sp[E];
+  const bool own = threadIdx.x < T;
+  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw, [&] {
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) sp[c] = spec[threadIdx.x + c * T];
+    }
+  });
+  if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int k = threadIdx.x + c * T;
-      z[c] = cscale(z[c], spec[k]);
+      z[c] = cscale(z[c], sp[c]);
       if (hs && k <= N / 2) hs[k] = z[c];
     }
   }
@@ -174,9 +198,9 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
 // even output bins of the Toeplitz product from a stored half spectrum:
 // z <- IFFT_N( S_even . N Herm(hs) ); caller keeps Re(z).  Equals filt_even
 // of x_hat = Re IFFT_N(hs) without its forward transform.
-template <int N>
+template <int N, class Hook = NoHook>
 TSF_D void filt_even_spec(const double2* hs, double2 (&z)[FShape<N>::E], double2* sm,
-                          const FilterTables& t) {
+                          const FilterTables& t, const Hook& inv_hook = Hook{}) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
   if (threadIdx.x < T) {
@@ -187,7 +211,7 @@ TSF_D void filt_even_spec(const double2* hs, double2 (&z)[FShape<N>::E], double2
       z[c] = cscale(h, mv_spec<N>(t, k).x * N);  // N S/L: exact (N a power of two)
     }
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw);
+  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw, inv_hook);
 }
 
 // w_j = W_L^j for the owned slots

@@ -92,37 +92,48 @@ TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restric
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   const bool own = tid < T;
+  constexpr int E = KShape<N>::E;
   double2 z[FShape<N>::E];
+  // x for the odd channel's modulation and the epilogue: loaded during the
+  // even channel's inverse transform (load hook, tsf_fft.cuh), kept in
+  // registers; kappa loaded during the odd inverse transform
+  double xo[E], ko[E];
+  auto load_x = [&] {
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) xo[c] = ld_real(xg, n, tid + c * T);
+    }
+  };
+  auto load_k = [&] {
+    if (own && kg) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) ko[c] = ld_real(kg, n, tid + c * T);
+    }
+  };
   if (hs) {
-    filt_even_spec<N>(hs, z, sm, t);   // x = Re IFFT(hs): its spectrum is already known
+    filt_even_spec<N>(hs, z, sm, t, load_x);   // x = Re IFFT(hs): its spectrum is known
   } else {
     double xr[FShape<N>::E];
     if (own) {
 #pragma unroll
-      for (int c = 0; c < KShape<N>::E; ++c) xr[c] = ld_real(xg, n, tid + c * T);
+      for (int c = 0; c < E; ++c) xr[c] = ld_real(xg, n, tid + c * T);
     }
-    filt_even<N>(xr, z, sm, t);
+    filt_even<N>(xr, z, sm, t, load_x);
   }
-  // the combine below re-reads x and reads kappa: pull them into L1 now
-  prefetch_l1(xg, n);
-  if (kg) prefetch_l1(kg, n);
   if (own) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) aux[tid + c * T] = z[c].x;
+    for (int c = 0; c < E; ++c) aux[tid + c * T] = z[c].x;
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) {
-      const int j = tid + c * T;
-      z[c] = cscale(modulation(t, j), ld_real(xg, n, j));
-    }
+    for (int c = 0; c < E; ++c) z[c] = cscale(modulation(t, tid + c * T), xo[c]);
   }
-  filt_odd<N>(z, sm, t);
+  filt_odd<N>(z, sm, t, load_k);
   if (own) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) {
+    for (int c = 0; c < E; ++c) {
       const int j = tid + c * T;
       const double2 w = modulation(t, j);
       const double ax = aux[j] + fma(z[c].x, w.x, z[c].y * w.y);  // + Re(conj(w) z)
-      y[c] = kg ? fma(shift, ld_real(xg, n, j), ld_real(kg, n, j) * ax) : ax;
+      y[c] = kg ? fma(shift, xo[c], ko[c] * ax) : ax;
     }
   }
 }
@@ -376,13 +387,24 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   double u[FShape<N>::E];
   double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
   apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, tab, hs);   // u = v = M p_hat
+  // epilogue operands loaded at once (one exposed latency, see the t-phase)
+  const double* rc = (s.it == 1 ? a.rhs : a.r) + off;
+  double r0v[E], rv[E];
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      r0v[c] = ld_real(a.rhs + off, n, j);
+      rv[c] = ld_real(rc, n, j);
+    }
+  }
   store_owned<N>(a.v + off, u, n);
   double part = 0.0;
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int j = tid + c * T;
-      if (j < n) part = fma(a.rhs[off + j], u[c], part);
+      if (j < n) part = fma(r0v[c], u[c], part);
     }
   }
   const double denom = block_sum1(part, red);
@@ -392,13 +414,12 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   }
   const double alpha = s.rho_new / denom;
   // s = r - alpha v
-  const double* rc = (s.it == 1 ? a.rhs : a.r) + off;
   part = 0.0;
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int j = tid + c * T;
-      u[c] = ld_real(rc, n, j) - alpha * u[c];
+      u[c] = rv[c] - alpha * u[c];
       if (j < n) part = fma(u[c], u[c], part);
     }
   }
@@ -450,6 +471,22 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   double u[FShape<N>::E];
   double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
   apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, tab, hs);   // u = t = M s_hat
+  // Every epilogue operand is loaded here at once, while the transform's
+  // registers are dead: one exposed memory latency per phase instead of one
+  // per reduction step (ncu: these loads were 40% of the t-phase's stalls).
+  const double* phg = (PC ? a.ph : a.p) + off;
+  double sv[E], xv[E], pv[E], shv[E], r0v[E], qv[E], vv[E];
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int j = tid + c * T;
+      sv[c] = ld_real(a.s + off, n, j);
+      xv[c] = ld_real(a.x + off, n, j);
+      pv[c] = ld_real(phg, n, j);
+      shv[c] = ld_real(shg, n, j);
+      r0v[c] = ld_real(a.rhs + off, n, j);
+    }
+  }
   Vals<2> red2;
   red2.v[0] = 0.0;
   red2.v[1] = 0.0;
@@ -459,7 +496,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
       const int j = tid + c * T;
       if (j < n) {
         red2.v[0] = fma(u[c], u[c], red2.v[0]);
-        red2.v[1] = fma(u[c], a.s[off + j], red2.v[1]);
+        red2.v[1] = fma(u[c], sv[c], red2.v[1]);
       }
     }
   }
@@ -470,21 +507,26 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   }
   const double omega = red2.v[1] / red2.v[0];
   // x += alpha p_hat + omega s_hat ; r = s - omega t
-  const double* phg = (PC ? a.ph : a.p) + off;
   red2.v[0] = 0.0;
   red2.v[1] = 0.0;
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int j = tid + c * T;
-      st_real(a.x + off, n, j,
-              ld_real(a.x + off, n, j) + (s.alpha * ld_real(phg, n, j) + omega * ld_real(shg, n, j)));
-      u[c] = ld_real(a.s + off, n, j) - omega * u[c];
+      st_real(a.x + off, n, j, xv[c] + (s.alpha * pv[c] + omega * shv[c]));
+      u[c] = sv[c] - omega * u[c];
       st_real(a.r + off, n, j, u[c]);
       if (j < n) {
         red2.v[0] = fma(u[c], u[c], red2.v[0]);
-        red2.v[1] = fma(a.rhs[off + j], u[c], red2.v[1]);
+        red2.v[1] = fma(r0v[c], u[c], red2.v[1]);
       }
+    }
+    // operands of the next p (x, p_hat, s_hat are dead now): in flight
+    // during the reduction
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      qv[c] = ld_real(a.p + off, n, tid + c * T);
+      vv[c] = ld_real(a.v + off, n, tid + c * T);
     }
   }
   red2 = block_sum<2>(red2, red);
@@ -511,10 +553,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   const double beta = (rho_new / s.rho_new) * (s.alpha / omega);
   if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
-      u[c] = u[c] + beta * (ld_real(a.p + off, n, j) - omega * ld_real(a.v + off, n, j));
-    }
+    for (int c = 0; c < E; ++c) u[c] = u[c] + beta * (qv[c] - omega * vv[c]);
   }
   store_owned<N>(a.p + off, u, n);
   if constexpr (PC == 1) precond_store<N>(u, a.ph + off, n, a.pspec + off, sm, tab, hs);

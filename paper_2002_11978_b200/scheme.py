@@ -506,6 +506,111 @@ def _run_direct(spec, mesh, disc, x, soe, u0, M, device):
     return hist, np.zeros(M, dtype=np.int64)
 
 
+# ---------------------------------------------------------------- DIDS
+class _DeviceLevelSolver:
+    """Per-run level solver of scheme.py:105-143 (_LevelSolver) over device
+    vectors: dense LU for the 'direct' tag, else the fused device BiCGSTAB /
+    PCG on the structured operator with the Strang preconditioner
+    ('pkrylov') — the same solves run_fids uses."""
+
+    def __init__(self, spec: ProblemSpec, disc: IflDiscretization, tag: str,
+                 options: SolverOptions, device: int):
+        torch = _native.torch_mod()
+        self.tag = tag
+        self.options = options
+        self.disc = disc
+        self.device = device
+        self.dev = torch.device(f"cuda:{device}")
+        self.n = disc.N - 1
+        self.use_cg = spec.kappa_x_independent
+        if tag == "direct":
+            self.A = torch.from_numpy(disc.dense()).to(self.dev)
+            self.eye = torch.eye(self.n, dtype=torch.float64, device=self.dev)
+        else:
+            self.op = build_toeplitz(disc.first_col, device=device)
+
+    def solve(self, shift: float, kappa: np.ndarray, rhs):
+        torch = _native.torch_mod()
+        from .krylov import LevelOperator, solve_bicgstab, solve_cg
+        from .toeplitz import build_preconditioner
+        kap = torch.from_numpy(kappa).to(self.dev)
+        if self.tag == "direct":
+            mat = shift * self.eye + kap[:, None] * self.A
+            return torch.linalg.solve(mat, rhs), 0, 0.0
+        lev = LevelOperator(self.op, shift, kap)
+        pc = None
+        if self.tag == "pkrylov":
+            pc = build_preconditioner(self.disc.first_col, shift, float(kappa.mean()),
+                                      device=self.device)
+        solver = solve_cg if self.use_cg else solve_bicgstab
+        u, rep = solver(lev, pc, rhs, tol=self.options.tol, max_iters=self.options.max_iters)
+        if not rep.converged:
+            raise RuntimeError(f"{'CG' if self.use_cg else 'BiCGSTAB'} did not converge: {rep}")
+        return u, rep.iterations, rep.final_relative_residual
+
+
+def run_dids(spec: ProblemSpec, M: int, r: float, N: int, mu: Optional[float] = None,
+             options: SolverOptions = SolverOptions(), device: int = 0):
+    """Direct implicit scheme (scheme.py:184-233) on the B200; returns
+    (history [M+1, n], SolveReport).
+
+    The history lives on the device; at level m the L1 history term
+    `(a[0]/G) u^0 + (diff(a) @ hist[1:m]) / G` streams levels 0..m-1 once
+    through k_l1_history_rhs (tsf_l1_history_rhs, csrc/tsf_dids.cuh) with the
+    weights a = l1_weights(mesh, gamma, m).a formed on the host exactly as
+    the reference does (mesh.py:53-80); the level solve is the device solve
+    run_fids uses.  O(m n) work and O((M+1) n) storage per run, like the
+    reference.
+    """
+    t0 = time.perf_counter()
+    mesh, disc, x = _setup(spec, M, r, N, mu)
+    n = N - 1
+    tag = select_solver(N, options)
+    if tag not in ("direct", "krylov", "pkrylov"):
+        raise ValueError(f"unknown solver {tag!r}")
+    torch = _native.torch_mod()
+    dev = torch.device(f"cuda:{device}")
+    lib = _native.load()
+    solver = _DeviceLevelSolver(spec, disc, tag, options, device)
+    G = math.exp(gammaln(1.0 - spec.gamma))
+    hist = torch.empty((M + 1, n), dtype=torch.float64, device=dev)
+    hist[0] = torch.from_numpy(np.ascontiguousarray(spec.initial(x), dtype=np.float64)).to(dev)
+    rhs = torch.empty(n, dtype=torch.float64, device=dev)
+    its = np.zeros(M, dtype=np.int64)
+    rel = np.zeros(M)
+    ops = np.empty(M, dtype=np.int64)
+    for m in range(1, M + 1):
+        a = l1_weights(mesh, spec.gamma, m).a
+        tm = float(mesh.t[m])
+        kappa = _kappa_at(spec, x, tm)
+        f = torch.from_numpy(np.ascontiguousarray(spec.source(x, tm), dtype=np.float64)).to(dev)
+        w = torch.from_numpy(np.diff(a)).to(dev) if m > 1 else None
+        _native.check(lib.tsf_l1_history_rhs(1, n, m, hist.data_ptr(), m * n,
+                                             None if w is None else w.data_ptr(),
+                                             a[0] / G, G, f.data_ptr(), rhs.data_ptr(),
+                                             _native.stream_ptr()))
+        ops[m - 1] = m * n
+        u, it, rr = solver.solve(a[-1] / G, kappa, rhs)
+        its[m - 1] = it
+        rel[m - 1] = rr
+        hist[m] = u
+    hist_np = hist.cpu().numpy()
+    err_inf = err_2 = None
+    if spec.exact is not None:
+        sh = math.sqrt(disc.h)
+        err_inf = err_2 = 0.0
+        for m in range(M + 1):
+            e = hist_np[m] - spec.exact(x, mesh.t[m])
+            err_inf = max(err_inf, float(np.max(np.abs(e))))
+            err_2 = max(err_2, sh * float(np.linalg.norm(e)))
+    rep = SolveReport(
+        err_inf=err_inf, err_2=err_2, avg_iterations=float(its.sum()) / M,
+        wall_time=time.perf_counter() - t0, scheme_tag="DIDS", solver_tag=tag,
+        history_ops=ops, history_memory_values=hist_np.size, iterations=its,
+        relres=None if tag == "direct" else rel)
+    return hist_np, rep
+
+
 # ---------------------------------------------------------------- batched
 def run_fids_batched(gamma: float, alpha: float, M: int, r: float, N: int,
                      kappa: SeparableField, source: SeparableField, initial,

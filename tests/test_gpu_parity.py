@@ -258,3 +258,31 @@ def test_batched_march_matches_single_instances():
                            lambda xx, b=b: u0[b], epsilon=1e-12, tol=1e-12)
         assert rel_l2(uB[b], rec.hist[-1]) <= 1e-10
         assert np.mean(np.abs(rep["iterations"][:, b] - rec.iterations) <= 1) >= 0.95
+
+
+@pytest.mark.parametrize("n", [256, 4096])
+def test_plan_growth_keeps_graph_solves_correct(n):
+    """A plan first used with B = 1 and then with a larger batch reallocates
+    its workspaces and active-instance counter; the cached level-solve graph
+    must follow (every node's parameters rewritten, the loop test included).
+    Each batched solution equals the oracle solve of the same system."""
+    d = P.build_ifl(1.5, 1.75, 1.0, n + 1)
+    col = d.first_col
+    op = P.build_toeplitz(col)
+    rng = np.random.default_rng(n)
+    shift = 3.5
+    _, sym = O.toeplitz_symbol(col)
+    lam = O.strang_eigs(col)
+    for B in (1, 6, 2, 9):
+        kap = rng.uniform(0.5, 2.0, (B, n))
+        b = rng.standard_normal((B, n))
+        kb = float(kap.mean())     # one preconditioner for the batch (the ABI's kappa_bar)
+        lev = P.LevelOperator(op, shift, kap)
+        pc = P.build_preconditioner(col, shift, kb)
+        x, reps = P.solve_bicgstab(lev, pc, b, tol=1e-12)
+        x = np.asarray(x)
+        for i in range(B):
+            ref, out = O.bicgstab(lambda q: shift * q + kap[i] * O.toeplitz_apply(sym, q),
+                                  lambda q: O.precond_apply(shift + kb * lam, q), b[i], tol=1e-12)
+            assert reps[i].converged and abs(reps[i].iterations - out.iterations) <= 3, (B, i)
+            assert rel_l2(x[i], ref) <= 1e-10, (B, i)

@@ -160,3 +160,26 @@ class TestMarchPins:
                            epsilon=1e-12, tol=1e-12, use_cg=True)
         np.testing.assert_array_equal(rec.iterations, g["cg_its"])
         assert _rel(rec.hist, g["cg_hist"]) <= 1e-13
+
+
+class TestDidsPins:
+    """run_dids (scheme.py:184-233) restated by oracle.dids_march."""
+
+    @pytest.mark.parametrize("tag", ["d1", "d2", "d3"])
+    def test_dids_marches(self, tag):
+        g = golden("dids")
+        gam, a, M, N, tol, r = g[f"{tag}_args"]
+        solver = str(g[f"{tag}_solver"])
+        rec = O.dids_march(gam, a, 1.0, 1.0, int(M), r, int(N), *_cfg0_fields(), tol=tol,
+                           precondition=solver == "pkrylov")
+        np.testing.assert_array_equal(rec.iterations, g[f"{tag}_its"])
+        assert _rel(rec.hist, g[f"{tag}_hist"]) <= 1e-13
+        assert rec.iterations.sum() / M == g[f"{tag}_avg"][0]
+        np.testing.assert_array_equal(g[f"{tag}_ops"], np.arange(1, int(M) + 1) * (int(N) - 1))
+
+    @pytest.mark.parametrize("tag", ["d1", "d2", "d3", "d4"])
+    def test_fids_dids_proximity_in_the_goldens(self, tag):
+        # the reference's criterion 7 (pkg/tests/test_acceptance.py:141-166),
+        # here at SOE eps 1e-12: |DIDS - FIDS| <= 100 eps
+        g = golden("dids")
+        assert np.max(np.abs(g[f"{tag}_hist"] - g[f"{tag}_fids_hist"])) <= 100 * 1e-12
