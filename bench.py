@@ -359,7 +359,31 @@ def main():
             "note": ("large-n level solve: four-step transforms through L2/HBM"
                      if large else
                      "level solve is transform (FP64/shared-memory) bound: ncu FP64 pipe "
-                     "~30% active; the SOE kernel alone runs at ~98% of the HBM peak")}
+                     "~35% active (see fp64); the SOE kernel alone runs at ~98% of the "
+                     "HBM peak")}
+    # FP64 view of the same launch: algorithmic flops per BiCGSTAB iteration
+    # (SURVEY.md §8(d)): 2 Toeplitz products (5 L log2 L + L + 3n each: two
+    # real length-L transforms), 2 Strang solves (5 n log2 n + 3n), ~20n
+    # vector flops; against the measured FP64 FMA peak (profiles/
+    # r01_fp64_peak.json, tools/probes/fp64_peak.cu)
+    Lemb = 1 << max(5, (2 * n - 1 - 1).bit_length())
+    it_flops = (2 * (5 * Lemb * math.log2(Lemb) + Lemb + 3 * n)
+                + 2 * (5 * n * math.log2(n) + 3 * n) + 20 * n)
+    fp64_peak = 36.8
+    try:
+        fp64_peak = float(json.loads((ROOT / "profiles" / "r01_fp64_peak.json").read_text())
+                          ["fp64_fma_tflops"])
+    except Exception:
+        pass
+    solve_flops = it_flops * its_sum / K
+    roof["fp64"] = {"algorithmic_flops_per_launch": solve_flops,
+                    "achieved_tflops": solve_flops / (solve_ms / K * 1e-3) / 1e12,
+                    "peak_tflops": fp64_peak,
+                    "frac": solve_flops / (solve_ms / K * 1e-3) / 1e12 / fp64_peak,
+                    "peak_source": "measured DFMA peak, profiles/r01_fp64_peak.json",
+                    "note": "algorithmic flops count real-input transforms; the engine runs "
+                            "full complex transforms of the real data (parity with the "
+                            "reference's numpy path, DESIGN.md §3.2), ~2x these flops"}
     value = world * B * n * K / (ms * 1e-3)
 
     # ---- end to end through the public API with host buffers

@@ -205,6 +205,16 @@ struct FftPlan {
 #define TSF_PASS_TW 0
 #endif
 constexpr bool kPassTw = TSF_PASS_TW;
+#ifndef TSF_STAGE_TABLES
+#define TSF_STAGE_TABLES 0
+#endif
+// cp.async staging in flight during transforms (tsf_filters.cuh
+// stage_tables): only then do the inter-pass barriers wait for it.  The
+// unconditional wait compiled to DEPBAR.LE SB0 before every barrier.
+#ifndef TSF_FORCE_WAIT
+#define TSF_FORCE_WAIT 0
+#endif
+constexpr bool kAsyncStaging = TSF_STAGE_TABLES || TSF_PASS_TW || TSF_FORCE_WAIT;
 
 // One Stockham pass: radix R, NS = product of the previous radices.
 //  FROM_REGS: inputs come from v[] (first pass), else from shared memory.
@@ -311,7 +321,7 @@ TSF_D void fft_rec(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
   if constexpr (P == hook_pass<N, E>()) hook();
   stockham_pass<N, E, P, INV, FIRST, LAST>(v, sm, tw, tw_log_scale, tid, own, ptw);
   if constexpr (!LAST) {
-    cp_async_wait_all();  // staged tables (tsf_filters.cuh stage_tables) land here
+    if constexpr (kAsyncStaging) cp_async_wait_all();  // staged tables land here
     __syncthreads();
     fft_rec<N, E, P + 1, INV>(v, sm, tw, tw_log_scale, tid, own, ptw, hook);
   }
@@ -438,7 +448,7 @@ TSF_D void real_first_pass(const double (&x)[E], double2 (&v)[E], double2* sm,
       for (int m = 0; m < R; ++m) sm[PL::pad(base + m)] = out[m];
     }
   }
-  cp_async_wait_all();
+  if constexpr (kAsyncStaging) cp_async_wait_all();
   __syncthreads();
   fft_rec<N, E, 1, false>(v, sm, tw, tw_log_scale, tid, own, ptw, hook);
 }

@@ -198,9 +198,8 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
 // even output bins of the Toeplitz product from a stored half spectrum:
 // z <- IFFT_N( S_even . N Herm(hs) ); caller keeps Re(z).  Equals filt_even
 // of x_hat = Re IFFT_N(hs) without its forward transform.
-template <int N, class Hook = NoHook>
-TSF_D void filt_even_spec(const double2* hs, double2 (&z)[FShape<N>::E], double2* sm,
-                          const FilterTables& t, const Hook& inv_hook = Hook{}) {
+template <int N>
+TSF_D void load_even_spec(const double2* hs, const FilterTables& t, double2 (&z)[FShape<N>::E]) {
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
   if (threadIdx.x < T) {
@@ -211,7 +210,12 @@ TSF_D void filt_even_spec(const double2* hs, double2 (&z)[FShape<N>::E], double2
       z[c] = cscale(h, mv_spec<N>(t, k).x * N);  // N S/L: exact (N a power of two)
     }
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw, inv_hook);
+}
+template <int N, class Hook = NoHook>
+TSF_D void filt_even_spec(const double2* hs, double2 (&z)[FShape<N>::E], double2* sm,
+                          const FilterTables& t, const Hook& inv_hook = Hook{}) {
+  load_even_spec<N>(hs, t, z);
+  block_fft<N, FShape<N>::E, true>(z, sm, t.tw, 1, t.ptw, inv_hook);
 }
 
 // w_j = W_L^j for the owned slots
@@ -249,7 +253,7 @@ TSF_D FilterTables stage_tables(const FilterTables& g, double2* dst, const doubl
       t.ps = ps;
     }
   }
-  cp_async_commit();
+  if constexpr (kAsyncStaging) cp_async_commit();
   return t;
 }
 

@@ -84,11 +84,13 @@ struct KShape {
 
 // y = shift*x + kappa .* (A x) on the owned slots (kappa == nullptr: y = A x).
 // x is read from global (twice); result returned in y[].  hs: x's half
-// spectrum from the Strang solve that produced x (filt_strang_tab), or null.
+// spectrum from the Strang solve that produced x (filt_strang_tab), or null;
+// hz: that spectrum already loaded into the owned slots (load_even_spec).
 template <int N>
 TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restrict__ kg,
                           double shift, int n, double (&y)[FShape<N>::E], double2* sm, double* aux,
-                          const FilterTables& t, const double2* hs = nullptr) {
+                          const FilterTables& t, const double2* hs = nullptr,
+                          const double2* hz = nullptr) {
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   const bool own = tid < T;
@@ -110,7 +112,12 @@ TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restric
       for (int c = 0; c < E; ++c) ko[c] = ld_real(kg, n, tid + c * T);
     }
   };
-  if (hs) {
+  if (hz) {
+    // even-channel spectrum preloaded by the phase kernel (k_bicg_phase)
+#pragma unroll
+    for (int c = 0; c < E; ++c) z[c] = hz[c];
+    block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw, load_x);
+  } else if (hs) {
     filt_even_spec<N>(hs, z, sm, t, load_x);   // x = Re IFFT(hs): its spectrum is known
   } else {
     double xr[FShape<N>::E];
@@ -368,17 +375,17 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
 // ---- BiCGSTAB v-phase
 template <int N, int PC>
 TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, int* active, double2* sm,
-                    double* red) {
+                    double* red, const KState* pre = nullptr, const double2* hz = nullptr) {
   constexpr int T = KShape<N>::T;
   constexpr int E = KShape<N>::E;
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int b = blockIdx.x;
-  __syncthreads();  // previous phase's st[b] writes (thread 0) are visible
+  if (!pre) __syncthreads();  // previous phase's st[b] writes (thread 0) are visible
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
   const long off = (long)b * n;
-  const KState s = st[b];
+  const KState s = pre ? *pre : st[b];
   const double* phg = (PC ? a.ph : a.p) + off;
   const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
   prefetch_l2(kg, n);                  // epilogue operands (x is loaded at once)
@@ -386,7 +393,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   if (s.it != 1) prefetch_l2(a.r + off, n);
   double u[FShape<N>::E];
   double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
-  apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, tab, hs);   // u = v = M p_hat
+  apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, tab, hs, hz);   // u = v = M p_hat
   // epilogue operands loaded at once (one exposed latency, see the t-phase)
   const double* rc = (s.it == 1 ? a.rhs : a.r) + off;
   double r0v[E], rv[E];
@@ -448,17 +455,17 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
 // ---- BiCGSTAB t-phase (+ next p / p_hat)
 template <int N, int PC>
 TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, int* active, double2* sm,
-                    double* red) {
+                    double* red, const KState* pre = nullptr, const double2* hz = nullptr) {
   constexpr int T = KShape<N>::T;
   constexpr int E = KShape<N>::E;
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
   const int b = blockIdx.x;
-  __syncthreads();  // previous phase's st[b] writes (thread 0) are visible
+  if (!pre) __syncthreads();  // previous phase's st[b] writes (thread 0) are visible
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
   const long off = (long)b * n;
-  const KState s = st[b];
+  const KState s = pre ? *pre : st[b];
   const double* shg = (PC ? a.sh : a.s) + off;
   const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
   prefetch_l2(kg, n);                  // epilogue operands (x is loaded at once)
@@ -470,7 +477,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   prefetch_l2(a.v + off, n);
   double u[FShape<N>::E];
   double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
-  apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, tab, hs);   // u = t = M s_hat
+  apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, tab, hs, hz);   // u = t = M s_hat
   // Every epilogue operand is loaded here at once, while the transform's
   // registers are dead: one exposed memory latency per phase instead of one
   // per reduction step (ncu: these loads were 40% of the t-phase's stalls).
@@ -672,10 +679,67 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
         PC ? a.pspec + (long)blockIdx.x * a.n : nullptr);                              \
     DNAME<N, PC>(a, tab, st, active, sm, red);                                         \
   }
-TSF_PHASE_KERNEL(k_bicg_v, dev_bicg_v)
-TSF_PHASE_KERNEL(k_bicg_t, dev_bicg_t)
 TSF_PHASE_KERNEL(k_cg_iter, dev_cg_iter)
 #undef TSF_PHASE_KERNEL
+
+// BiCGSTAB phase kernels.  Their entry loads are issued together — the
+// instance's Krylov state, this thread's twiddle-table entries and (Strang
+// preconditioner) the even-channel spectrum of the vector the phase
+// multiplies — so a CTA waits for one memory latency at entry instead of
+// three in a row (ncu: state check, table staging and spectrum loads each
+// stalled every warp of the SM).
+#ifndef TSF_ENTRY_PRELOAD
+#define TSF_ENTRY_PRELOAD 0
+#endif
+template <int N, int PC, bool TPHASE>
+TSF_D void bicg_phase(const KrylovArgs& a, KState* st, int* active) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  constexpr int E = KShape<N>::E;
+  double2* tws = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES +
+                                            N * 8);
+  if constexpr (!TSF_ENTRY_PRELOAD || kAsyncStaging || FStage<N>::MV || FStage<N>::PS) {
+    // table-staging variants: the plain entry sequence
+    if (st[blockIdx.x].done) return;
+    const FilterTables tab = stage_tables<N>(a.tab, tws, PC ? a.pspec + (long)blockIdx.x * a.n : nullptr);
+    if constexpr (TPHASE) dev_bicg_t<N, PC>(a, tab, st, active, sm, red);
+    else dev_bicg_v<N, PC>(a, tab, st, active, sm, red);
+  } else {
+    constexpr int NT = tw_table_elems(2 * N);
+    constexpr int BL = KShape<N>::BLOCK;
+    constexpr int KT = (NT + BL - 1) / BL;
+    double2 twv[KT];
+#pragma unroll
+    for (int q = 0; q < KT; ++q) {
+      const int i = threadIdx.x + q * BL;
+      if (i < NT) twv[q] = ldt(&a.tab.tw[i]);
+    }
+    const KState s = st[blockIdx.x];
+    double2 hz[E];
+    const bool pre_spec = PC && a.hspec;
+    FilterTables tab = a.tab;
+    if (pre_spec) load_even_spec<N>(hspec_of<N>(a, blockIdx.x), tab, hz);
+    if (s.done) return;
+#pragma unroll
+    for (int q = 0; q < KT; ++q) {
+      const int i = threadIdx.x + q * BL;
+      if (i < NT) tws[i] = twv[q];
+    }
+    tab.tw = tws;   // published by the first transform's leading barrier
+    if constexpr (TPHASE) dev_bicg_t<N, PC>(a, tab, st, active, sm, red, &s, pre_spec ? hz : nullptr);
+    else dev_bicg_v<N, PC>(a, tab, st, active, sm, red, &s, pre_spec ? hz : nullptr);
+  }
+}
+template <int N, int PC>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
+k_bicg_v(KrylovArgs a, KState* st, int* active) {
+  bicg_phase<N, PC, false>(a, st, active);
+}
+template <int N, int PC>
+__global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
+k_bicg_t(KrylovArgs a, KState* st, int* active) {
+  bicg_phase<N, PC, true>(a, st, active);
+}
 
 // Persistent per-instance solve: one CTA runs its instance from begin to
 // convergence (vectors stay L2-resident, no host round trip, and the GPU

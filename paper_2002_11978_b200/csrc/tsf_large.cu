@@ -499,6 +499,33 @@ struct Runner {
   }
 };
 
+// ---- graph-mode loop (TSF_SOLVE_GRAPH, default on)
+__global__ void k_lloop_cond(cudaGraphConditionalHandle h, const int* active) {
+  cudaGraphSetConditional(h, *active > 0 ? 1u : 0u);
+}
+
+// kernel nodes of a captured launch chain, in chain order
+int chain_nodes(cudaGraph_t g, std::vector<cudaGraphNode_t>& out) {
+  out.clear();
+  size_t nr = 0;
+  if (cudaGraphGetRootNodes(g, nullptr, &nr) != cudaSuccess || nr != 1)
+    return report_error(TSF_E_CUDA, "captured iteration is not a single chain");
+  cudaGraphNode_t cur;
+  if (cudaGraphGetRootNodes(g, &cur, &nr) != cudaSuccess)
+    return report_error(TSF_E_CUDA, "cudaGraphGetRootNodes");
+  for (;;) {
+    out.push_back(cur);
+    size_t nd = 0;
+    if (cudaGraphNodeGetDependentNodes(cur, nullptr, &nd) != cudaSuccess)
+      return report_error(TSF_E_CUDA, "cudaGraphNodeGetDependentNodes");
+    if (nd == 0) break;
+    if (nd != 1) return report_error(TSF_E_CUDA, "captured iteration is not a single chain");
+    if (cudaGraphNodeGetDependentNodes(cur, &cur, &nd) != cudaSuccess)
+      return report_error(TSF_E_CUDA, "cudaGraphNodeGetDependentNodes");
+  }
+  return 0;
+}
+
 Runner make_runner(const LargePlan* lp, int B, cudaStream_t st) {
   Runner R;
   R.lp = lp;
@@ -598,6 +625,12 @@ int large_plan_init(LargePlan* lp, int n, int L, const double* symbol_re, const 
 void large_plan_free(LargePlan* lp) {
   if (!lp) return;
   cudaSetDevice(lp->device);
+  for (auto& row : lp->loops)
+    for (auto& g : row) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      if (g.graph) cudaGraphDestroy(g.graph);
+    }
+  if (lp->cap_stream) cudaStreamDestroy(lp->cap_stream);
   cudaFree(lp->tables);
   cudaFree(lp->ws);
   cudaFree(lp->Z);
@@ -662,6 +695,79 @@ int large_precond(LargePlan* lp, int B, const double* v, double* z, double shift
   return R.strang(CI_LOAD, v, z);
 }
 
+// One graph launch runs every remaining iteration: WHILE(active > 0) { one
+// iteration's launch chain ; loop test }.  No host polling, no chunk
+// overshoot (the scalar kernels hold max_iters, krylov.py:100).
+static int loop_graph(LargePlan* lp, const Runner& R0, int method, int pc, cudaStream_t st) {
+  LargeLoopGraph& G = lp->loops[method][pc];
+  int rc;
+  if (!lp->cap_stream &&
+      (rc = cuda_check(cudaStreamCreateWithFlags(&lp->cap_stream, cudaStreamNonBlocking),
+                       "cudaStreamCreate(capture)")))
+    return rc;
+  Runner R = R0;
+  R.st = lp->cap_stream;
+  auto record = [&](cudaGraphConditionalHandle h) -> int {
+    const int r = method == 1 ? R.cg_iteration(pc) : R.bicg_iteration(pc);
+    if (r) return r;
+    k_lloop_cond<<<1, 1, 0, R.st>>>(h, lp->active);
+    return cuda_check(cudaGetLastError(), "k_lloop_cond");
+  };
+  if (!G.built) {
+    if ((rc = cuda_check(cudaGraphCreate(&G.graph, 0), "cudaGraphCreate"))) return rc;
+    if ((rc = cuda_check(cudaGraphConditionalHandleCreate(&G.cond, G.graph, 1,
+                                                          cudaGraphCondAssignDefault),
+                         "cudaGraphConditionalHandleCreate")))
+      return rc;
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = G.cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t loop;
+    if ((rc = cuda_check(cudaGraphAddNode(&loop, G.graph, nullptr, 0, &cp), "cudaGraphAddNode")))
+      return rc;
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    if ((rc = cuda_check(cudaStreamBeginCaptureToGraph(R.st, body, nullptr, nullptr, 0,
+                                                       cudaStreamCaptureModeRelaxed),
+                         "cudaStreamBeginCaptureToGraph")))
+      return rc;
+    const int r1 = record(G.cond);
+    cudaGraph_t out = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(R.st, &out);
+    if (r1) return r1;
+    if ((rc = cuda_check(e, "cudaStreamEndCapture"))) return rc;
+    if ((rc = chain_nodes(body, G.body))) return rc;
+    if ((rc = cuda_check(cudaGraphInstantiate(&G.exec, G.graph, 0), "cudaGraphInstantiate")))
+      return rc;
+    G.built = true;
+  } else {
+    // re-capture this solve's chain and copy its kernel parameters in
+    cudaGraph_t tmp = nullptr;
+    if ((rc = cuda_check(cudaStreamBeginCapture(R.st, cudaStreamCaptureModeRelaxed),
+                         "cudaStreamBeginCapture")))
+      return rc;
+    const int r1 = record(G.cond);
+    const cudaError_t e = cudaStreamEndCapture(R.st, &tmp);
+    if (r1) return r1;
+    if ((rc = cuda_check(e, "cudaStreamEndCapture"))) return rc;
+    std::vector<cudaGraphNode_t> nodes;
+    rc = chain_nodes(tmp, nodes);
+    if (!rc && nodes.size() != G.body.size())
+      rc = report_error(TSF_E_CUDA, "iteration chain changed shape");
+    for (size_t i = 0; !rc && i < nodes.size(); ++i) {
+      cudaKernelNodeParams kp{};
+      rc = cuda_check(cudaGraphKernelNodeGetParams(nodes[i], &kp), "cudaGraphKernelNodeGetParams");
+      if (!rc)
+        rc = cuda_check(cudaGraphExecKernelNodeSetParams(G.exec, G.body[i], &kp),
+                        "cudaGraphExecKernelNodeSetParams");
+    }
+    cudaGraphDestroy(tmp);
+    if (rc) return rc;
+  }
+  return cuda_check(cudaGraphLaunch(G.exec, st), "cudaGraphLaunch");
+}
+
 int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, cudaStream_t st) {
   if (method != 0 && method != 1) return report_error(TSF_E_INVALID, "method must be 0 or 1");
   if (pc && !lp->has_pc) return report_error(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner");
@@ -692,6 +798,7 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
     if ((rc = cuda_check(cudaGetLastError(), "k_lspec"))) return rc;
   }
   if (method == 1 && (rc = R.cg_start(pc))) return rc;
+  if (graph_mode()) return loop_graph(lp, R, method, pc, st);
   for (int it = 0; it < a.max_iters; it += kLargeChunk) {
     for (int c = 0; c < kLargeChunk && it + c < a.max_iters; ++c)
       if ((rc = method == 1 ? R.cg_iteration(pc) : R.bicg_iteration(pc))) return rc;

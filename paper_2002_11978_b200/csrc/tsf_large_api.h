@@ -14,6 +14,19 @@ int report_error(int code, const char* msg);
 // two-level twiddle table of W_N (layout: tsf_fft.cuh tw_get)
 std::vector<double2> twiddle_table(int N);
 
+// Graph-mode iteration loop of one (method, preconditioner): a conditional
+// WHILE node whose body is one captured Krylov iteration (the launch chain of
+// Runner::bicg_iteration / cg_iteration) plus the loop test.  Later solves
+// re-capture the chain into a scratch graph and copy its kernel parameters
+// into the instantiated body node by node (the chain's shape never changes).
+struct LargeLoopGraph {
+  bool built = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphConditionalHandle cond{};
+  std::vector<cudaGraphNode_t> body;   // body kernel nodes in chain order
+};
+
 struct LargePlan {
   int n = 0, nt = 0, N1 = 0, N2 = 0, np = 0;   // vector length n <= transform length nt
   int ncol_cta = 0;            // column CTAs per instance (partial-sum count)
@@ -30,6 +43,8 @@ struct LargePlan {
   LState* st = nullptr;       // [cap]
   int* active = nullptr;
   int* h_active = nullptr;
+  cudaStream_t cap_stream = nullptr;   // graph capture (non-blocking)
+  LargeLoopGraph loops[2][2];          // [method][pc]
 };
 
 // embedding L a power of two in [2^14, 2^25] with 2n-1 <= L (vectors of length n are
