@@ -209,7 +209,7 @@ class FidsMarch:
     def __init__(self, gamma, alpha, l, T, M, r, N, soe: SoeApproximation, method: int,
                  precond: int, tol: float, max_iters: Optional[int], B: int,
                  kappa: _FieldDev, source: _FieldDev, u0, hist_B: int = 0, device: int = 0,
-                 mu: Optional[float] = None):
+                 mu: Optional[float] = None, private_plan: bool = False):
         torch = _native.torch_mod()
         self.dev = torch.device(f"cuda:{device}")
         self.mesh = build_mesh(M, r, T)
@@ -224,7 +224,8 @@ class FidsMarch:
         self.max_iters = int(max_iters) if max_iters is not None else 10 * self.n
         self.G = math.exp(gammaln(1.0 - gamma))
         op = build_toeplitz(self.disc.first_col, device=device)
-        self.plan = plan_for(self.disc.first_col, device, spectrum=op.spectrum_embed)
+        self.plan = plan_for(self.disc.first_col, device, spectrum=op.spectrum_embed,
+                             private=private_plan)
         if self.precond and not self.plan.has_precond:
             raise NotImplementedError(
                 f"device Strang preconditioner needs a power-of-two n >= 16 (got n={self.n})")

@@ -45,8 +45,12 @@ _plans: dict = {}
 
 
 def plan_for(first_col: np.ndarray, device: int = 0, lam: Optional[np.ndarray] = None,
-             spectrum: Optional[np.ndarray] = None) -> _native.Plan:
-    """Cached device plan for a Toeplitz first column (symbol + Strang tables)."""
+             spectrum: Optional[np.ndarray] = None, private: bool = False) -> _native.Plan:
+    """Cached device plan for a Toeplitz first column (symbol + Strang tables).
+
+    private=True returns a fresh, uncached plan: its workspaces, solve
+    graphs and instance counters are not shared, so marches holding private
+    plans can run concurrently on different streams."""
     col = np.ascontiguousarray(first_col, dtype=np.float64)
     n = col.size
     L_ref = embed_length(n)
@@ -58,14 +62,15 @@ def plan_for(first_col: np.ndarray, device: int = 0, lam: Optional[np.ndarray] =
         lam = None
     key = (n, device, hashlib.sha1(col.tobytes()).hexdigest(),
            None if lam is None else hashlib.sha1(np.ascontiguousarray(lam).tobytes()).hexdigest())
-    pl = _plans.get(key)
+    pl = None if private else _plans.get(key)
     if pl is None:
         if spectrum is not None and L == L_ref:
             sym = np.ascontiguousarray(np.real(spectrum))
         else:
             sym = np.fft.fft(_even_embedding(col, L)).real
         pl = _native.Plan(n, L, sym, lam, device)
-        _plans[key] = pl
+        if not private:
+            _plans[key] = pl
     return pl
 
 
