@@ -28,6 +28,9 @@
 #ifndef TSF_KE
 #define TSF_KE 8
 #endif
+#ifndef TSF_PTW_SMALL
+#define TSF_PTW_SMALL 0
+#endif
 
 namespace tsf {
 
@@ -199,12 +202,25 @@ struct FftPlan {
     return p <= 1 ? 0 : ptw_off(p - 1) + ((1 << log_radix(p - 1)) - 1) * (1 << log_ns(p - 1));
   }
   static constexpr int PTW_ELEMS = ptw_off(NPASS);
+  // passes whose twiddles come from the small explicit table (kPassTwSmall):
+  // NS R <= kPtwSmall; their entries are a prefix of the full ptw layout
+  static constexpr int small_passes(int p = 1) {
+    return (p < NPASS && (1 << (log_ns(p) + log_radix(p))) <= TSF_PTW_SMALL) ? small_passes(p + 1)
+                                                                            : p;
+  }
+  static constexpr int PTWS_ELEMS = ptw_off(small_passes());
 };
 
 #ifndef TSF_PASS_TW
 #define TSF_PASS_TW 0
 #endif
 constexpr bool kPassTw = TSF_PASS_TW;
+// Explicit twiddles for the early passes (NS R <= TSF_PTW_SMALL, e.g. 512: 504 entries
+// = 8 KB at N = 4096), staged in shared memory: one correctly rounded table
+// read per factor instead of three two-level lookups and four products per
+// radix-8 butterfly; the last pass keeps the two-level table.  Off (0) by
+// default: measured slower on configs[2] (27.5 vs 26.8 ms per level solve).
+constexpr bool kPassTwSmall = TSF_PTW_SMALL > 0 && !TSF_PASS_TW;
 #ifndef TSF_STAGE_TABLES
 #define TSF_STAGE_TABLES 0
 #endif
@@ -223,9 +239,23 @@ constexpr bool kAsyncStaging = TSF_STAGE_TABLES || TSF_PASS_TW || TSF_FORCE_WAIT
 // transform buffers), so loaded values never have to survive a barrier —
 // with an in-place pass they did, and inside the Krylov loop ptxas spilled
 // them to local memory.  Only owning threads touch data.
-template <int N, int E, int P, bool INV, bool FROM_REGS, bool TO_REGS>
+// Explicit-twiddle table pointer of the early passes (kPassTwSmall): a
+// distinct type, so transforms given one compile only the table path for
+// those passes and transforms given a plain pointer (or none) only the
+// two-level path — no runtime branch, no dead path inflating registers.
+struct SmallTw {
+  const double2* p;
+};
+template <class PT>
+constexpr bool is_small_tw() { return false; }
+template <>
+constexpr bool is_small_tw<SmallTw>() { return true; }
+TSF_D const double2* tw_ptr(const double2* p) { return p; }
+TSF_D const double2* tw_ptr(SmallTw p) { return p.p; }
+
+template <int N, int E, int P, bool INV, bool FROM_REGS, bool TO_REGS, class PT>
 TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
-                         int tw_log_scale, int tid, bool own, const double2* __restrict__ ptw) {
+                         int tw_log_scale, int tid, bool own, PT ptw_in) {
   using PL = FftPlan<N, E>;
   constexpr int R = 1 << PL::log_radix(P);
   constexpr int NS = 1 << PL::log_ns(P);
@@ -251,7 +281,9 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
   for (int q = 0; q < Q; ++q) {
     const int b = tid + q * T;
     const int k = b & (NS - 1);
-    if (kPassTw && NS > 1 && ptw) {
+    constexpr bool XS = is_small_tw<PT>() && NS * R <= TSF_PTW_SMALL;
+    const double2* ptw = tw_ptr(ptw_in);
+    if ((XS || kPassTw) && NS > 1 && (XS || ptw)) {
       // explicit table: one correctly rounded entry per power, no products
       const double2* pt = ptw + PL::ptw_off(P) + k;
 #pragma unroll
@@ -311,9 +343,9 @@ constexpr int hook_pass() {
   return FftPlan<N, E>::NPASS - 2 > 1 ? FftPlan<N, E>::NPASS - 2 : 1;
 }
 
-template <int N, int E, int P, bool INV, class Hook = NoHook>
+template <int N, int E, int P, bool INV, class Hook = NoHook, class PT = const double2*>
 TSF_D void fft_rec(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
-                   int tw_log_scale, int tid, bool own, const double2* __restrict__ ptw = nullptr,
+                   int tw_log_scale, int tid, bool own, PT ptw = nullptr,
                    const Hook& hook = Hook{}) {
   using PL = FftPlan<N, E>;
   constexpr bool FIRST = (P == 0);
@@ -333,10 +365,9 @@ TSF_D void fft_rec(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
 // right before; ends with data in registers (sm may be reused after a
 // barrier).
 // `tw` holds W_NT^e for e < NT with NT = N << tw_log_scale.
-template <int N, int E, bool INV, class Hook = NoHook>
+template <int N, int E, bool INV, class Hook = NoHook, class PT = const double2*>
 TSF_D void block_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
-                     int tw_log_scale, const double2* __restrict__ ptw = nullptr,
-                     const Hook& hook = Hook{}) {
+                     int tw_log_scale, PT ptw = nullptr, const Hook& hook = Hook{}) {
   using PL = FftPlan<N, E>;
   const int tid = threadIdx.x;
   const bool own = tid < PL::T;
@@ -427,10 +458,10 @@ TSF_D void dft_real(const double* x, double2* X) {
 
 // First pass of a forward transform of real data (owned slots x[c],
 // j = tid + c*T), then the remaining complex passes into v[c].
-template <int N, int E, class Hook = NoHook>
+template <int N, int E, class Hook = NoHook, class PT = const double2*>
 TSF_D void real_first_pass(const double (&x)[E], double2 (&v)[E], double2* sm,
                            const double2* __restrict__ tw, int tw_log_scale, int tid, bool own,
-                           const double2* __restrict__ ptw = nullptr, const Hook& hook = Hook{}) {
+                           PT ptw = nullptr, const Hook& hook = Hook{}) {
   using PL = FftPlan<N, E>;
   constexpr int R = 1 << PL::log_radix(0);
   constexpr int Q = E / R;
@@ -454,10 +485,10 @@ TSF_D void real_first_pass(const double (&x)[E], double2 (&v)[E], double2* sm,
 }
 
 // Forward transform of real owned slots x[c] (j = tid + c*T) into v[c].
-template <int N, int E, class Hook = NoHook>
+template <int N, int E, class Hook = NoHook, class PT = const double2*>
 TSF_D void block_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
                           const double2* __restrict__ tw, int tw_log_scale,
-                          const double2* __restrict__ ptw = nullptr, const Hook& hook = Hook{}) {
+                          PT ptw = nullptr, const Hook& hook = Hook{}) {
   static_assert(FftPlan<N, E>::NPASS >= 2, "real-input transform needs at least two passes");
   __syncthreads();
   const int tid = threadIdx.x;

@@ -76,7 +76,9 @@ template <int N>
 struct FStage {
   static constexpr int FFT_BYTES = (kFftInPlace ? 1 : 2) * FftPlan<N, kE>::SMEM_ELEMS * 16;
   static constexpr int TW_BYTES = tw_table_elems(2 * N) * 16;
-  static constexpr int PTW_BYTES = kPassTw ? FftPlan<N, kE>::PTW_ELEMS * 16 : 0;
+  static constexpr int PTW_BYTES = kPassTw        ? FftPlan<N, kE>::PTW_ELEMS * 16
+                                   : kPassTwSmall ? FftPlan<N, kE>::PTWS_ELEMS * 16
+                                                  : 0;
   static constexpr int BASE = FFT_BYTES + N * 8 + TW_BYTES + PTW_BYTES;
   static constexpr int BLOCK = (N / kE) < 32 ? 32 : (N / kE);
   static constexpr int REG_CTAS = (65536 / (BLOCK * 128)) < 1 ? 1 : 65536 / (BLOCK * 128);
@@ -86,6 +88,12 @@ struct FStage {
   static constexpr bool MV = PS && BASE + N * 24 <= kSmemCap && occ(BASE + N * 24) >= OCC0;
   static constexpr int SMEM = BASE + (PS ? N * 8 : 0) + (MV ? N * 16 : 0);
 };
+
+// twiddle-table argument of the filters' transforms (tsf_fft.cuh SmallTw)
+TSF_D auto xtw(const FilterTables& t) {
+  if constexpr (kPassTwSmall) return SmallTw{t.ptw};
+  else return t.ptw;
+}
 
 template <int N>
 TSF_D double2 mv_spec(const FilterTables& t, int k) {
@@ -101,7 +109,7 @@ TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E]
   constexpr int E = FShape<N>::E;
   const bool own = threadIdx.x < T;
   double se[E];
-  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw, [&] {
+  block_fft_real<N, E>(x, z, sm, t.tw, 1, xtw(t), [&] {
     if (own) {
 #pragma unroll
       for (int c = 0; c < E; ++c) se[c] = mv_spec<N>(t, threadIdx.x + c * T).x;
@@ -111,7 +119,7 @@ TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E]
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = cscale(z[c], se[c]);
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw, inv_hook);
+  block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t), inv_hook);
 }
 
 // odd output bins: z (already modulated by w_j) <- IFFT_N( S_odd . FFT_N(z) );
@@ -125,7 +133,7 @@ TSF_D void filt_odd(double2 (&z)[FShape<N>::E], double2* sm, const FilterTables&
   constexpr int E = FShape<N>::E;
   const bool own = threadIdx.x < T;
   double so[E];
-  block_fft<N, E, false>(z, sm, t.tw, 1, t.ptw, [&] {
+  block_fft<N, E, false>(z, sm, t.tw, 1, xtw(t), [&] {
     if (own) {
 #pragma unroll
       for (int c = 0; c < E; ++c) so[c] = mv_spec<N>(t, threadIdx.x + c * T).y;
@@ -135,7 +143,7 @@ TSF_D void filt_odd(double2 (&z)[FShape<N>::E], double2* sm, const FilterTables&
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = cscale(z[c], so[c]);
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw, inv_hook);
+  block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t), inv_hook);
 }
 
 // Strang: z <- IFFT_n( FFT_n(x) . Ssym / n ) for real x, n = N; caller keeps Re(z)
@@ -145,7 +153,7 @@ TSF_D void filt_strang(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
   constexpr double inv_n = 1.0 / N;
-  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw);
+  block_fft_real<N, E>(x, z, sm, t.tw, 1, xtw(t));
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
@@ -154,7 +162,7 @@ TSF_D void filt_strang(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::
       z[c] = cscale(z[c], s * inv_n);
     }
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw);
+  block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t));
 }
 
 // Strang with a precomputed per-instance spectrum spec[k] = S_k / n (the level
@@ -178,7 +186,7 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
   constexpr int E = FShape<N>::E;
   double sp[E];
   const bool own = threadIdx.x < T;
-  block_fft_real<N, E>(x, z, sm, t.tw, 1, t.ptw, [&] {
+  block_fft_real<N, E>(x, z, sm, t.tw, 1, xtw(t), [&] {
     if (own) {
 #pragma unroll
       for (int c = 0; c < E; ++c) sp[c] = spec[threadIdx.x + c * T];
@@ -192,7 +200,7 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
       if (hs && k <= N / 2) hs[k] = z[c];
     }
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw);
+  block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t));
 }
 
 // even output bins of the Toeplitz product from a stored half spectrum:
@@ -215,7 +223,7 @@ template <int N, class Hook = NoHook>
 TSF_D void filt_even_spec(const double2* hs, double2 (&z)[FShape<N>::E], double2* sm,
                           const FilterTables& t, const Hook& inv_hook = Hook{}) {
   load_even_spec<N>(hs, t, z);
-  block_fft<N, FShape<N>::E, true>(z, sm, t.tw, 1, t.ptw, inv_hook);
+  block_fft<N, FShape<N>::E, true>(z, sm, t.tw, 1, xtw(t), inv_hook);
 }
 
 // w_j = W_L^j for the owned slots
@@ -233,6 +241,12 @@ TSF_D FilterTables stage_tables(const FilterTables& g, double2* dst, const doubl
   FilterTables t = g;
   t.tw = dst;
   double2* next = dst + NT;
+  if constexpr (kPassTwSmall) {
+    constexpr int NP = FftPlan<N, kE>::PTWS_ELEMS;
+    for (int i = threadIdx.x; i < NP; i += blockDim.x) next[i] = ldt(&g.ptw[i]);
+    t.ptw = next;   // the plan always builds the table (tsf_abi.cu pass_twiddles)
+    next += NP;
+  }
   if constexpr (kPassTw) {
     constexpr int NP = FftPlan<N, kE>::PTW_ELEMS;
     if (g.ptw) {

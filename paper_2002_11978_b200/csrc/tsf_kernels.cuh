@@ -116,7 +116,7 @@ TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restric
     // even-channel spectrum preloaded by the phase kernel (k_bicg_phase)
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = hz[c];
-    block_fft<N, E, true>(z, sm, t.tw, 1, t.ptw, load_x);
+    block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t), load_x);
   } else if (hs) {
     filt_even_spec<N>(hs, z, sm, t, load_x);   // x = Re IFFT(hs): its spectrum is known
   } else {
