@@ -380,11 +380,13 @@ TSF_D void block_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ t
 // caller passes the thread's index inside its transform group and the
 // group's own shared-memory buffers; barriers stay CTA-wide, so every group
 // must run the same transform.
-template <int N, int E, bool INV>
+template <int N, int E, bool INV, class Hook = NoHook>
 TSF_D void group_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ tw,
-                     int tw_log_scale, int tid) {
+                     int tw_log_scale, int tid, const Hook& hook = Hook{}) {
   __syncthreads();
-  fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, true);
+  if constexpr (FftPlan<N, E>::NPASS < 2) hook();
+  fft_rec<N, E, 0, INV>(v, sm, tw, tw_log_scale, tid, true,
+                         static_cast<const double2*>(nullptr), hook);
 }
 
 // ------------------------------------------------------------ real input
@@ -495,12 +497,14 @@ TSF_D void block_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
   real_first_pass<N, E>(x, v, sm, tw, tw_log_scale, tid, tid < FftPlan<N, E>::T, ptw, hook);
 }
 
-template <int N, int E>
+template <int N, int E, class Hook = NoHook>
 TSF_D void group_fft_real(const double (&x)[E], double2 (&v)[E], double2* sm,
-                          const double2* __restrict__ tw, int tw_log_scale, int tid) {
+                          const double2* __restrict__ tw, int tw_log_scale, int tid,
+                          const Hook& hook = Hook{}) {
   static_assert(FftPlan<N, E>::NPASS >= 2, "real-input transform needs at least two passes");
   __syncthreads();
-  real_first_pass<N, E>(x, v, sm, tw, tw_log_scale, tid, true);
+  real_first_pass<N, E>(x, v, sm, tw, tw_log_scale, tid, true,
+                        static_cast<const double2*>(nullptr), hook);
 }
 
 }  // namespace tsf

@@ -96,11 +96,20 @@ TSF_D double2 tw_get_g(const double2* tw, long e) {
 }
 
 // Column-kernel geometry: G transforms of length N1 per CTA, T threads each.
+// TSF_LCOL_THREADS: threads per column CTA.  256 (default) leaves room for
+// two CTAs per SM (128 registers, <= 113 KB shared memory each), so one CTA's
+// exposed global loads overlap the other's transforms (ncu: the column
+// kernels were 30-50% long-scoreboard stalls at one 512-thread CTA per SM).
+#ifndef TSF_LCOL_THREADS
+#define TSF_LCOL_THREADS 256
+#endif
 template <int N1>
 struct LCol {
   static constexpr int E = FShape<N1>::E;
   static constexpr int T = N1 / E;
-  static constexpr int G = T >= 512 ? 1 : (512 / T > 16 ? 16 : 512 / T);
+  static constexpr int TH = TSF_LCOL_THREADS;
+  static constexpr int G = T >= TH ? 1 : (TH / T > 16 ? 16 : TH / T);
+  static constexpr int MINB = (G * T <= 256) ? 2 : 1;
   static constexpr int BLOCK = G * T;
   static constexpr int BUF = 2 * FftPlan<N1, E>::SMEM_ELEMS;  // ping-pong, per group
   static constexpr int SMEM = (G * BUF + tw_table_elems(N1)) * 16;
@@ -120,7 +129,7 @@ TSF_D void stage_tw(double2* dst, const double2* src) {
 
 // ------------------------------------------------------------ col_fwd
 template <int N1>
-__global__ void __launch_bounds__(LCol<N1>::BLOCK, 1)
+__global__ void __launch_bounds__(LCol<N1>::BLOCK, LCol<N1>::MINB)
 k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
@@ -204,43 +213,62 @@ k_lrow(LargeArgs a, int spec_mode) {
   extern __shared__ double2 sm[];
   const int k1 = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   if (inst_skip(a, b)) return;
-  double2* tw2 = sm + 2 * FftPlan<N2, E>::SMEM_ELEMS;
-  stage_tw<N2>(tw2, a.lt.tw2);
   const bool own = tid < T;
   const int nch = spec_mode == RS_APPLY ? 2 : 1;
+  // the row is loaded before the twiddle staging (both in flight at once);
+  // spectrum factors and the next channel's row are loaded by the
+  // transforms' load hooks (tsf_fft.cuh), two passes before they are used
+  double2 z[E];
+  double2* row = a.Z + (long)b * N + (long)k1 * N2;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) z[c] = row[tid + c * T];
+  }
+  double2* tw2 = sm + 2 * FftPlan<N2, E>::SMEM_ELEMS;
+  stage_tw<N2>(tw2, a.lt.tw2);
   for (int ch = 0; ch < nch; ++ch) {
-    double2* row = a.Z + (long)ch * a.B * N + (long)b * N + (long)k1 * N2;
-    double2 z[E];
-    if (own) {
+    double sp[E];
+    block_fft<N2, E, false>(z, sm, tw2, 0, static_cast<const double2*>(nullptr), [&] {
+      if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) z[c] = row[tid + c * T];
-    }
-    block_fft<N2, E, false>(z, sm, tw2, 0);
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < E; ++c) {
-        const long idx = (long)k1 * N2 + tid + c * T;   // bin k1 + N1 k2
-        double s;
-        if (spec_mode == RS_APPLY) {
-          const double2 se = ldt(&a.lt.sEO[idx]);
-          s = ch == 0 ? se.x : se.y;
-        } else {
-          s = a.pspec[(long)b * N + idx];
+        for (int c = 0; c < E; ++c) {
+          const long idx = (long)k1 * N2 + tid + c * T;   // bin k1 + N1 k2
+          if (spec_mode == RS_APPLY) {
+            const double2 se = ldt(&a.lt.sEO[idx]);
+            sp[c] = ch == 0 ? se.x : se.y;
+          } else {
+            sp[c] = a.pspec[(long)b * N + idx];
+          }
         }
-        z[c] = cscale(z[c], s);
       }
+    });
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) z[c] = cscale(z[c], sp[c]);
     }
-    block_fft<N2, E, true>(z, sm, tw2, 0);
+    double2 zn[E];
+    double2* nrow = row + (long)a.B * N;   // next channel's row
+    block_fft<N2, E, true>(z, sm, tw2, 0, static_cast<const double2*>(nullptr), [&] {
+      if (own && ch + 1 < nch) {
+#pragma unroll
+        for (int c = 0; c < E; ++c) zn[c] = nrow[tid + c * T];
+      }
+    });
     if (own) {
 #pragma unroll
       for (int c = 0; c < E; ++c) row[tid + c * T] = z[c];
+    }
+    if (ch + 1 < nch) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) z[c] = zn[c];
+      row = nrow;
     }
   }
 }
 
 // ------------------------------------------------------------ col_inv
 template <int N1>
-__global__ void __launch_bounds__(LCol<N1>::BLOCK, 1)
+__global__ void __launch_bounds__(LCol<N1>::BLOCK, LCol<N1>::MINB)
 k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __restrict__ xin,
            const double* __restrict__ w1, int pslot) {
   using C = LCol<N1>;

@@ -49,6 +49,11 @@ def main():
         hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
     except Exception:
         hbm = 6650.0
+    try:   # measured DFMA peak (tools/probes/fp64_peak.cu)
+        fp64 = float(json.loads((ROOT / "profiles" / "r01_fp64_peak.json").read_text())
+                     ["fp64_fma_tflops"])
+    except Exception:
+        fp64 = 36.8
     lib = _native.load()
     st = _native.stream_ptr()
     dev = torch.device("cuda:0")
@@ -76,6 +81,17 @@ def main():
         q = {"kernel": "precond_solve", "n": n, "B": B, "ms": t_pc * 1e3,
              "GBps": 16.0 * n * B / t_pc / 1e9}
         q["frac_hbm"] = q["GBps"] / hbm
+        # FP64 roofline (SURVEY.md §8(d) algorithmic flops: two real length-L
+        # transforms per product, two real length-n transforms per Strang
+        # solve) and the binding roof t_roof = max(bytes/HBM, flops/FP64)
+        L = 2 * n
+        for row, flops, byts, t in ((r, 5 * L * np.log2(L) + L + 3 * n, 24.0 * n, t_mv),
+                                    (q, 5 * n * np.log2(n) + 3 * n, 16.0 * n, t_pc)):
+            row["TFLOPs"] = flops * B / t / 1e12
+            row["frac_fp64"] = row["TFLOPs"] / fp64
+            t_roof = max(byts * B / (hbm * 1e9), flops * B / (fp64 * 1e12))
+            row["bound"] = "fp64" if flops * B / (fp64 * 1e12) > byts * B / (hbm * 1e9) else "hbm"
+            row["frac_roof"] = t_roof / t
         rows += [r, q]
         print(json.dumps(r), flush=True)
         print(json.dumps(q), flush=True)
@@ -103,7 +119,8 @@ def main():
         del W
         torch.cuda.empty_cache()
     if args.out:
-        Path(args.out).write_text(json.dumps({"hbm_peak_gbs": hbm, "rows": rows}, indent=1) + "\n")
+        Path(args.out).write_text(json.dumps({"hbm_peak_gbs": hbm, "fp64_peak_tflops": fp64,
+                                              "rows": rows}, indent=1) + "\n")
 
 
 if __name__ == "__main__":
