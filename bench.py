@@ -190,7 +190,10 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        workers = args.cpu_workers or os.cpu_count() or 1
+        # batched configs[2]: one instance per host core; the single-instance
+        # configs are one march (the reference cannot split a march over
+        # processes; numpy/OpenBLAS threads are left at their default)
+        workers = args.cpu_workers or (os.cpu_count() or 1) if cfg2 else 1
         value, wall, K, avg_its = cpu_measure(wl, warmup, min(args.steps, wl["cpu_levels"]),
                                               workers, cfg2)
         line = {
@@ -449,13 +452,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        workers = args.cpu_workers or min(os.cpu_count() or 1, 8)
+        workers = (args.cpu_workers or min(os.cpu_count() or 1, 8)) if cfg2 else 1
         cw = min(K, wl["cpu_levels"])
         cval, cwall, cK, cits = cpu_measure(wl, warmup, cw, workers, cfg2)
         cpu = {"value": cval, "unit": UNIT, "cores": workers, "kind": "port",
-               "sample": f"{workers} instances (one per process, 1 BLAS thread) x levels "
-                         f"{warmup + 1}..{warmup + cK} via oracle/ (numpy restatement of "
-                         f"tsfrac.run_fids); avg its {cits:.2f}"}
+               "sample": (f"{workers} instances (one per process, 1 BLAS thread)" if cfg2 else
+                          "the single instance (one process)")
+                         + f" x levels {warmup + 1}..{warmup + cK} via oracle/ (numpy "
+                         f"restatement of tsfrac.run_fids); avg its {cits:.2f}"}
 
     if rank == 0:
         line = {
