@@ -355,8 +355,20 @@ def main():
              "GBps": (soe_bytes / (soe_ms / K * 1e-3) / 1e9) if not fused else None,
              "algorithmic_bytes": soe_bytes}
     dom = k_solve if solve_ms >= soe_ms else k_soe
+    # ncu DRAM bytes of the same kernels (one capture, profiles/r01b_ncu_traffic.json),
+    # scaled to this launch's instance-iterations / SOE level
+    traffic = None
+    try:
+        tr = json.loads((ROOT / "profiles" / "r01b_ncu_traffic.json").read_text())
+        if cfg2 and not large:
+            traffic = (tr["dram_bytes_per_instance_iteration"] * its_sum / K
+                       if dom is k_solve else tr["soe_dram_bytes_per_level_cfg2"] * B / 4096)
+    except Exception:
+        traffic = None
     roof = {"kernel": dom["name"], "bound": "hbm", "achieved": dom["GBps"], "peak": hbm,
-            "unit": "GB/s", "frac": dom["GBps"] / hbm, "traffic": None,
+            "unit": "GB/s", "frac": dom["GBps"] / hbm, "traffic": traffic,
+            "traffic_source": "ncu dram__bytes_read+write of the same kernels "
+                              "(profiles/r01b_ncu_traffic.json) x this launch's work",
             "algorithmic_bytes_per_launch": dom["algorithmic_bytes"], "peak_source": peak_src,
             "share_of_step": (solve_ms if dom is k_solve else soe_ms) / ms,
             "note": ("large-n level solve: four-step transforms through L2/HBM"

@@ -744,6 +744,9 @@ k_bicg_t(KrylovArgs a, KState* st, int* active) {
 // Persistent per-instance solve: one CTA runs its instance from begin to
 // convergence (vectors stay L2-resident, no host round trip, and the GPU
 // back-fills SMs as instances finish — no tail of near-empty launches).
+// (Measured slower than the graph-mode phase kernels even for one instance:
+// configs[0] 0.396 vs 0.318 ms per level solve — the loop spills ~1.3 KB per
+// thread at any register cap.)
 template <int N, int PC, bool CG>
 __global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
 k_krylov_persist(KrylovArgs a, KState* st, int* active) {

@@ -1,0 +1,65 @@
+"""The engine's measurement switches compute the same solves: spectrum reuse
+on/off (TSF_SPEC_REUSE), graph-mode vs host-driven iteration loops
+(TSF_SOLVE_GRAPH) for both engines.  Each mode runs in its own process (the
+switches are read once per process) on the same seeded systems; solutions
+agree to 1e-10 and iteration counts to +-1 (the modes differ only in
+rounding: the reused spectrum skips one forward transform)."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = Path(__file__).resolve().parent.parent
+
+_PROG = r"""
+import sys, json
+import numpy as np
+sys.path.insert(0, %r)
+import paper_2002_11978_b200 as P
+n, B = %d, %d
+d = P.build_ifl(1.5, 1.75, 1.0, n + 1)
+op = P.build_toeplitz(d.first_col)
+rng = np.random.default_rng(11)
+kap = rng.uniform(0.5, 2.0, (B, n))
+b = rng.standard_normal((B, n))
+pc = P.build_preconditioner(d.first_col, 2.5, float(kap.mean()))
+x, reps = P.solve_bicgstab(P.LevelOperator(op, 2.5, kap), pc, b, tol=1e-12)
+np.save(%r, np.asarray(x))
+print(json.dumps([r.iterations for r in reps]))
+"""
+
+
+def _run(n, B, env, tmp_path, tag):
+    out = tmp_path / f"x_{tag}.npy"
+    prog = _PROG % (str(ROOT), n, B, str(out))
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([sys.executable, "-c", prog], env=e, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(out), np.array(json.loads(r.stdout.strip().splitlines()[-1]))
+
+
+@pytest.mark.parametrize("n,B,env", [
+    (4096, 6, {"TSF_SPEC_REUSE": "0"}),
+    (1024, 5, {"TSF_SPEC_REUSE": "0"}),
+    (4096, 6, {"TSF_SOLVE_GRAPH": "0"}),
+    (16384, 2, {"TSF_SOLVE_GRAPH": "0"}),
+])
+def test_mode_switch_computes_the_same_solves(n, B, env, tmp_path):
+    x0, it0 = _run(n, B, {}, tmp_path, "default")
+    x1, it1 = _run(n, B, env, tmp_path, "switched")
+    assert np.all(np.abs(it0 - it1) <= 1), (it0, it1)
+    for i in range(B):
+        assert np.linalg.norm(x0[i] - x1[i]) <= 1e-10 * np.linalg.norm(x0[i])
