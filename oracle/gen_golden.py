@@ -279,6 +279,29 @@ def gen_dids(tsfrac):
     return out
 
 
+def gen_cfg2(tsfrac):
+    """Two configs[2] instances (global indices 37 and 200 of the seeded
+    batch, paper_2002_11978_b200/workloads.py) at full size: n = 4096,
+    M = 512, gamma = 0.5, alpha = 1.5, SOE eps 1e-12, tol 1e-12 — per-level
+    iterations and u^M from the reference's own run_fids."""
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    from paper_2002_11978_b200 import workloads as WL
+    from tsfrac.scheme import ProblemSpec
+    out = {}
+    n, M = 4096, 512
+    for b in (37, 200):
+        x, kx, fx, u0 = WL.instance_fields(n, b, 1)
+        spec = ProblemSpec(gamma=0.5, alpha=1.5, l=1.0, T=1.0,
+                           kappa=lambda xx, t, k=kx[0]: k * (1.0 + 0.2 * t),
+                           source=lambda xx, t, f=fx[0]: f * (1.0 + t),
+                           initial=lambda xx, u=u0[0]: u.copy())
+        hist, rep, its, rel = _march(tsfrac, spec, M, 3.0, n + 1, 1e-12, 1e-12)
+        out[f"b{b}_its"] = its
+        out[f"b{b}_uM"] = hist[-1]
+        out[f"b{b}_u64"] = hist[64]
+    return out
+
+
 def gen_big(tsfrac):
     """cfg1 (n=16384, M=1024) for all 12 (gamma, alpha): per-step its + u^M."""
     from concurrent.futures import ProcessPoolExecutor
@@ -306,13 +329,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run cfg1 (minutes)")
     ap.add_argument("--only", default="", help="comma list of fixtures to regenerate "
-                    "(setup,linalg,march,dids,cfg1); default all but cfg1")
+                    "(setup,linalg,march,dids,cfg1,cfg2); default all but cfg1/cfg2")
     args = ap.parse_args()
     tsfrac = _import_reference()
     OUT.mkdir(parents=True, exist_ok=True)
     if args.only:
         gens = {"setup": gen_setup, "linalg": gen_linear_algebra, "march": gen_marches,
-                "dids": gen_dids, "cfg1": gen_big}
+                "dids": gen_dids, "cfg1": gen_big, "cfg2": gen_cfg2}
         for name in args.only.split(","):
             np.savez_compressed(OUT / f"{name}.npz", **gens[name](tsfrac))
             print(name, (OUT / f"{name}.npz").stat().st_size)

@@ -183,3 +183,17 @@ class TestDidsPins:
         # here at SOE eps 1e-12: |DIDS - FIDS| <= 100 eps
         g = golden("dids")
         assert np.max(np.abs(g[f"{tag}_hist"] - g[f"{tag}_fids_hist"])) <= 100 * 1e-12
+
+
+def test_cfg2_full_size_instances_pin_the_oracle():
+    """Two configs[2] instances at full size (n = 4096, M = 512): the oracle
+    reproduces the reference's per-level iterations and u^M bit for bit."""
+    from paper_2002_11978_b200 import workloads as WL
+    g = golden("cfg2")
+    b = 37
+    x, kx, fx, u0 = WL.instance_fields(4096, b, 1)
+    rec = O.fids_march(0.5, 1.5, 1.0, 1.0, 512, 3.0, 4097,
+                       lambda xx, t: kx[0] * (1.0 + 0.2 * t), lambda xx, t: fx[0] * (1.0 + t),
+                       lambda xx: u0[0], epsilon=1e-12, tol=1e-12, keep_history=False)
+    np.testing.assert_array_equal(rec.iterations, g[f"b{b}_its"])
+    np.testing.assert_array_equal(rec.hist, g[f"b{b}_uM"])
