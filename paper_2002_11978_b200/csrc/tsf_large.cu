@@ -626,10 +626,11 @@ void large_plan_free(LargePlan* lp) {
   if (!lp) return;
   cudaSetDevice(lp->device);
   for (auto& row : lp->loops)
-    for (auto& g : row) {
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-      if (g.graph) cudaGraphDestroy(g.graph);
-    }
+    for (auto& pcs : row)
+      for (auto& g : pcs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+      }
   if (lp->cap_stream) cudaStreamDestroy(lp->cap_stream);
   cudaFree(lp->tables);
   cudaFree(lp->ws);
@@ -699,7 +700,11 @@ int large_precond(LargePlan* lp, int B, const double* v, double* z, double shift
 // iteration's launch chain ; loop test }.  No host polling, no chunk
 // overshoot (the scalar kernels hold max_iters, krylov.py:100).
 static int loop_graph(LargePlan* lp, const Runner& R0, int method, int pc, cudaStream_t st) {
-  LargeLoopGraph& G = lp->loops[method][pc];
+  // the column kernels' instantiation depends on the launch size
+  // (tsf_large_impl.cuh few_ctas): one cached chain per choice, so a cached
+  // node never changes its kernel function
+  const int few = few_ctas((long)lp->ncol_cta * R0.a.B) ? 1 : 0;
+  LargeLoopGraph& G = lp->loops[method][pc][few];
   int rc;
   if (!lp->cap_stream &&
       (rc = cuda_check(cudaStreamCreateWithFlags(&lp->cap_stream, cudaStreamNonBlocking),

@@ -96,20 +96,28 @@ TSF_D double2 tw_get_g(const double2* tw, long e) {
 }
 
 // Column-kernel geometry: G transforms of length N1 per CTA, T threads each.
-// TSF_LCOL_THREADS: threads per column CTA.  256 (default) leaves room for
-// two CTAs per SM (128 registers, <= 113 KB shared memory each), so one CTA's
-// exposed global loads overlap the other's transforms (ncu: the column
-// kernels were 30-50% long-scoreboard stalls at one 512-thread CTA per SM).
-#ifndef TSF_LCOL_THREADS
-#define TSF_LCOL_THREADS 256
+// Threads per column CTA.  Small CTAs let several run per SM (128 registers
+// each), so one CTA's exposed global loads overlap the others' transforms
+// (ncu: the column kernels were 30-50% long-scoreboard stalls at one
+// 512-thread CTA per SM); measured per column length on the configs[4]
+// sweep: 128 threads (4 CTAs/SM) up to N1 = 256 (n = 2^20: 4.69 -> 4.29 ms
+// per matvec; n = 2^14: 4.05 -> 3.13 ms), 256 at N1 = 512, 512 above (fewer
+// columns per CTA cost coalescing there).  TSF_LCOL_THREADS overrides.
+template <int N1>
+constexpr int lcol_threads() {
+#ifdef TSF_LCOL_THREADS
+  return TSF_LCOL_THREADS;
+#else
+  return N1 <= 256 ? 128 : N1 == 512 ? 256 : 512;
 #endif
+}
 template <int N1>
 struct LCol {
   static constexpr int E = FShape<N1>::E;
   static constexpr int T = N1 / E;
-  static constexpr int TH = TSF_LCOL_THREADS;
+  static constexpr int TH = lcol_threads<N1>();
   static constexpr int G = T >= TH ? 1 : (TH / T > 16 ? 16 : TH / T);
-  static constexpr int MINB = (G * T <= 256) ? 2 : 1;
+  static constexpr int MINB = (G * T <= 128) ? 4 : (G * T <= 256) ? 2 : 1;
   static constexpr int BLOCK = G * T;
   static constexpr int BUF = 2 * FftPlan<N1, E>::SMEM_ELEMS;  // ping-pong, per group
   static constexpr int SMEM = (G * BUF + tw_table_elems(N1)) * 16;
@@ -128,8 +136,11 @@ TSF_D void stage_tw(double2* dst, const double2* src) {
 }
 
 // ------------------------------------------------------------ col_fwd
-template <int N1>
-__global__ void __launch_bounds__(LCol<N1>::BLOCK, LCol<N1>::MINB)
+// MB: CTAs per SM the register allocation is sized for — LCol::MINB for
+// launches that fill the GPU, 1 (no register cap below 255) for the few-CTA
+// launches of single large instances, which are latency-bound (configs[1]).
+template <int N1, int MB = LCol<N1>::MINB>
+__global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)
 k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
@@ -267,8 +278,8 @@ k_lrow(LargeArgs a, int spec_mode) {
 }
 
 // ------------------------------------------------------------ col_inv
-template <int N1>
-__global__ void __launch_bounds__(LCol<N1>::BLOCK, LCol<N1>::MINB)
+template <int N1, int MB = LCol<N1>::MINB>
+__global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)
 k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __restrict__ xin,
            const double* __restrict__ w1, int pslot) {
   using C = LCol<N1>;
@@ -334,6 +345,15 @@ k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __
       a.part[((long)b * 4 + pslot + 1) * a.np + blockIdx.x] = pr.v[1];
     }
   }
+}
+
+// Column launches smaller than two waves of one CTA per SM take the
+// uncapped-register instantiation (latency-bound single instances).
+inline bool few_ctas(long ctas) {
+  static int sms = 0;
+  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess)
+    sms = 148;
+  return ctas < 2L * sms;
 }
 
 // Per-size launchers (bodies in tsf_large_impl.cuh, one TU per size:

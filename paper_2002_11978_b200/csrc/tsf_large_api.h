@@ -44,7 +44,7 @@ struct LargePlan {
   int* active = nullptr;
   int* h_active = nullptr;
   cudaStream_t cap_stream = nullptr;   // graph capture (non-blocking)
-  LargeLoopGraph loops[2][2];          // [method][pc]
+  LargeLoopGraph loops[2][2][2];       // [method][pc][few-CTA column kernels]
 };
 
 // embedding L a power of two in [2^14, 2^25] with 2n-1 <= L (vectors of length n are

@@ -23,10 +23,13 @@ int LargeDispatch<LOG>::col_fwd(const LargeArgs& a, const double* src, int in_mo
                                 cudaStream_t st) {
   constexpr int N1 = 1 << LOG;
   using S = LCol<N1>;
-  auto k = k_lcol_fwd<N1>;
-  static cudaError_t prep = large_prep(k, S::SMEM);
+  const dim3 grid(a.nt / N1 / S::G, a.B);
+  auto k = few_ctas((long)grid.x * grid.y) ? k_lcol_fwd<N1, 1> : k_lcol_fwd<N1>;
+  static cudaError_t prep = large_prep(k_lcol_fwd<N1>, S::SMEM);
+  static cudaError_t prep1 = large_prep(k_lcol_fwd<N1, 1>, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  k<<<dim3(a.nt / N1 / S::G, a.B), S::BLOCK, S::SMEM, st>>>(a, src, in_mode);
+  if (prep1 != cudaSuccess) return large_launch_error(prep1);
+  k<<<grid, S::BLOCK, S::SMEM, st>>>(a, src, in_mode);
   return large_launch_error(cudaGetLastError());
 }
 
@@ -46,10 +49,13 @@ int LargeDispatch<LOG>::col_inv(const LargeArgs& a, double* dst, int out_mode, c
                                 const double* w1, int pslot, cudaStream_t st) {
   constexpr int N1 = 1 << LOG;
   using S = LCol<N1>;
-  auto k = k_lcol_inv<N1>;
-  static cudaError_t prep = large_prep(k, S::SMEM);
+  const dim3 grid(a.nt / N1 / S::G, a.B);
+  auto k = few_ctas((long)grid.x * grid.y) ? k_lcol_inv<N1, 1> : k_lcol_inv<N1>;
+  static cudaError_t prep = large_prep(k_lcol_inv<N1>, S::SMEM);
+  static cudaError_t prep1 = large_prep(k_lcol_inv<N1, 1>, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  k<<<dim3(a.nt / N1 / S::G, a.B), S::BLOCK, S::SMEM, st>>>(a, dst, out_mode, xin, w1, pslot);
+  if (prep1 != cudaSuccess) return large_launch_error(prep1);
+  k<<<grid, S::BLOCK, S::SMEM, st>>>(a, dst, out_mode, xin, w1, pslot);
   return large_launch_error(cudaGetLastError());
 }
 
