@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--cpu-workers", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tol", type=float, default=0.0,
+                    help="experiments only: override the Krylov tolerance (not a bench number)")
     args = ap.parse_args()
     wl = workload(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -246,6 +248,8 @@ def main():
     kdev = _field_separable(kap, x, mesh.t, B, kmodes, dev)
     fdev = _field_separable(src, x, mesh.t, B, fmodes, dev)
     u0_d = torch.from_numpy(np.ascontiguousarray(u0)).to(dev)
+    if args.tol > 0:
+        wl["tol"] = args.tol
     march = FidsMarch(gam, alpha, 1.0, 1.0, M, r, N, soe, method=0, precond=1, tol=wl["tol"],
                       max_iters=None, B=B, kappa=kdev, source=fdev, u0=u0_d, device=local)
     K = args.steps
