@@ -333,7 +333,24 @@ def main():
     # algorithmic bytes: BiCGSTAB iteration 216 n per instance (SURVEY.md
     # §8(d)); SOE push + RHS (16 N_exp + 32) n per instance (W read+write;
     # u, u_prev, f-mode read; rhs write)
-    soe_bytes = (16 * nexp + 32) * n * B
+    Kb = getattr(march, "soe_block", 1)
+    if Kb > 1 and not fused:
+        # blocked SOE (csrc/tsf_soe.cuh): level m = mb+1 runs the W pass
+        # (W read+write, du ring reads, u^{mb}, u^{mb-1}, G ring writes, f, rhs),
+        # the other levels k_soe_level (u^{m-1}, u^{m-2}, du write, G read,
+        # du^{mb+1..m-2} reads, f, rhs); bytes averaged over the timed levels
+        def _soe_level_bytes(m):
+            mb = Kb * ((m - 1) // Kb)
+            if m - 1 == mb:
+                ka = 0 if mb == 0 else Kb
+                kn = min(Kb, M - mb)
+                wb = 0 if (ka == 0) else 16 * nexp
+                return (wb + 8 * max(ka - 1, 0) + 16 + 8 * max(kn - 1, 0) + 16) * n * B
+            return (16 + 8 + 8 + 8 * (m - 2 - mb) + 16) * n * B
+        lv = [m for m0, m1 in levels_done for m in range(m0, m1)]
+        soe_bytes = sum(_soe_level_bytes(m) for m in lv) / max(len(lv), 1)
+    else:
+        soe_bytes = (16 * nexp + 32) * n * B
     krylov_bytes = 216 * n * its_sum / K
     solve_bytes = krylov_bytes + (soe_bytes if fused else 0)
     peaks = {}
@@ -354,7 +371,9 @@ def main():
     k_solve = {"name": sname, "avg_ms": solve_ms / K,
                "GBps": solve_bytes / (solve_ms / K * 1e-3) / 1e9,
                "iterations_per_launch": its_sum / K, "algorithmic_bytes": solve_bytes}
-    k_soe = {"name": "tsf::k_soe_push_rhs" + (" (level 1 only)" if fused else ""),
+    k_soe = {"name": (f"tsf::k_soe_block + k_soe_level (blocked SOE, one W pass per {Kb} levels)"
+                      if Kb > 1 and not fused else
+                      "tsf::k_soe_push_rhs" + (" (level 1 only)" if fused else "")),
              "avg_ms": soe_ms / K,
              "GBps": (soe_bytes / (soe_ms / K * 1e-3) / 1e9) if not fused else None,
              "algorithmic_bytes": soe_bytes}

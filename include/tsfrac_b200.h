@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define TSF_ABI_VERSION 1
+#define TSF_ABI_VERSION 2
 
 /* API return codes */
 #define TSF_SUCCESS 0
@@ -202,6 +202,19 @@ typedef struct tsf_march {
    * kernel, between the SOE and solve kernels, after the solve kernel),
    * recorded on `stream`; NULL disables */
   void** events;
+  /* Blocked SOE schedule (soe_block = K in 2..16; 0 or 1: one W pass per
+   * level).  One pass over W per K levels advances W by the block's K pushes
+   * (bit-identical recurrence) and forms the W-part of the block's history
+   * terms; each level adds a combination of the block's du vectors.
+   *   soe_alpha  device [M][nexp]: alpha_j(m) = h_j(m) prod_{l=mb+1}^{m-1} d_j(l),
+   *              mb = K*floor((m-1)/K) the base of level m's block
+   *   soe_beta   HOST [M][16]: beta(m, mb+1+q) = sum_j h_j(m) prod_{l=mb+2+q}^{m-1} d_j(l) c_j(mb+1+q)
+   *   soe_ring   device [2][K][B][n] scratch (du and history-term rings),
+   *              kept between calls of the same march */
+  int soe_block;
+  const double* soe_alpha;
+  const double* soe_beta;
+  double* soe_ring;
 } tsf_march;
 
 int tsf_fids_march(tsf_plan* plan, const tsf_march* desc, void* stream);

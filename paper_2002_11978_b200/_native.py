@@ -62,7 +62,8 @@ class March(C.Structure):
         ("soe_tab", P), ("kappa", Field), ("source", Field), ("u_buf0", P),
         ("u_buf1", P), ("W", P), ("rhs", P), ("kwork", P), ("iters", P),
         ("relres", P), ("status", P), ("hist", P), ("hist_B", I), ("m_begin", I),
-        ("m_end", I), ("events", P),
+        ("m_end", I), ("events", P), ("soe_block", I), ("soe_alpha", P), ("soe_beta", P),
+        ("soe_ring", P),
     ]
 
 

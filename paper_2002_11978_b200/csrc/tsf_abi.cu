@@ -522,10 +522,96 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
   // file, so the streaming cannot overlap transform work on that SM), hence
   // off by default: one SOE kernel per level.
   const char* fz = getenv("TSF_FUSE_SOE");
-  const bool fuse = fz && fz[0] == '1' && !p->large;
+  const int K = d->soe_block;
+  const bool blocked = K > 1;
+  if (blocked && (K > kSoeMaxBlock || !d->soe_alpha || !d->soe_beta || !d->soe_ring))
+    return fail(TSF_E_INVALID, "blocked SOE needs soe_block <= %d, soe_alpha, soe_beta, soe_ring",
+                kSoeMaxBlock);
+  const bool fuse = fz && fz[0] == '1' && !p->large && !blocked;
+  double* du_ring = blocked ? d->soe_ring : nullptr;
+  double* g_ring = blocked ? d->soe_ring + (size_t)K * vn : nullptr;
+  // block pass at base mb: W^{mb-ka} -> W^{mb} (ka pushes), history terms of
+  // levels mb+1 .. mb+kn, RHS of level mb+1
+  auto block_pass = [&](int mb, int ka, int kn) -> int {
+    SoeBlockArgs b{};
+    b.n = n;
+    b.nexp = nexp;
+    b.B = B;
+    b.W = d->W;
+    b.u_cur = ubuf[mb & 1];
+    b.u_prev = ubuf[(mb + 1) & 1];
+    b.tau_cur = mb >= 1 ? d->tau[mb - 1] : 0.0;
+    b.du_ring = du_ring;
+    b.K = K;
+    b.mb = mb;
+    b.ka = ka;
+    b.w_zero = (mb - ka) == 0;
+    b.push_tab = d->soe_tab;
+    b.kn = kn;
+    b.alpha = d->soe_alpha;
+    b.g_ring = g_ring;
+    if (kn >= 1) {
+      const int rm = mb + 1;
+      b.a_next = d->a_mm[rm - 1];
+      b.nf = d->source.nmodes;
+      b.fmodes = d->source.modes ? d->source.modes + (size_t)rm * d->source.t_stride : nullptr;
+      b.fq_stride = d->source.q_stride;
+      b.fb_stride = d->source.b_stride;
+      for (int q = 0; q < b.nf; ++q) b.fcoef[q] = d->source.coef[(size_t)rm * b.nf + q];
+    }
+    b.G = d->G;
+    b.rhs = d->rhs;
+    const int chunks = (n + 2 * kSoeThreads - 1) / (2 * kSoeThreads);
+    const int smem = (2 * ka + kn) * nexp * (int)sizeof(double);
+    // register arrays sized by the block length (K <= 8: ~90 registers, 5 CTAs/SM)
+    auto go = [&](auto kern) -> int {
+      if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<(unsigned)B * chunks, kSoeThreads, smem, st>>>(b);
+      CK(cudaGetLastError());
+      return TSF_SUCCESS;
+    };
+    if (K <= 4) return go(k_soe_block<4>);
+    if (K <= 8) return go(k_soe_block<8>);
+    return go(k_soe_block<kSoeMaxBlock>);
+  };
+  auto level_rhs = [&](int m, int mb) -> int {
+    SoeLevelArgs l{};
+    l.n = n;
+    l.B = B;
+    l.K = K;
+    l.m = m;
+    l.mb = mb;
+    l.u1 = ubuf[(m - 1) & 1];
+    l.u2 = ubuf[m & 1];
+    l.tau1 = d->tau[m - 2];
+    l.du_ring = du_ring;
+    l.g_ring = g_ring;
+    for (int q = 0; q < m - 1 - mb; ++q) l.beta[q] = d->soe_beta[(size_t)(m - 1) * 16 + q];
+    l.a_m = d->a_mm[m - 1];
+    l.G = d->G;
+    l.nf = d->source.nmodes;
+    l.fmodes = d->source.modes ? d->source.modes + (size_t)m * d->source.t_stride : nullptr;
+    l.fq_stride = d->source.q_stride;
+    l.fb_stride = d->source.b_stride;
+    for (int q = 0; q < l.nf; ++q) l.fcoef[q] = d->source.coef[(size_t)m * l.nf + q];
+    l.rhs = d->rhs;
+    const long total = (long)B * n;
+    const long grid = std::min<long>((total + 255) / 256, 148L * 16);
+    k_soe_level<<<(unsigned)grid, 256, 0, st>>>(l);
+    CK(cudaGetLastError());
+    return TSF_SUCCESS;
+  };
   for (int m = d->m_begin; m < d->m_end; ++m) {
     if ((rc = rec(m, 0))) return rc;
-    if (m == 1 || !fuse) {
+    if (blocked) {
+      const int mb = ((m - 1) / K) * K;
+      if (m - 1 == mb) {
+        if ((rc = block_pass(mb, mb == 0 ? 0 : K, std::min(K, M - mb)))) return rc;
+      } else if ((rc = level_rhs(m, mb))) {
+        return rc;
+      }
+    } else if (m == 1 || !fuse) {
       // push of level m-1 (fused with the history term) + RHS of level m
       SoeArgs s = soe_args(m - 1, m);
       if ((rc = soe_launch(B, s, st))) return rc;
@@ -560,8 +646,13 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
   }
   if (!fuse && d->m_end == M + 1 && d->m_begin <= M) {
     // final push of level M (scheme.py:290 runs after every level)
-    SoeArgs s = soe_args(M, M + 1);
-    if ((rc = soe_launch(B, s, st))) return rc;
+    if (blocked) {
+      const int mbl = ((M - 1) / K) * K;   // base of level M's block
+      if ((rc = block_pass(M, M - mbl, 0))) return rc;
+    } else {
+      SoeArgs s = soe_args(M, M + 1);
+      if ((rc = soe_launch(B, s, st))) return rc;
+    }
   }
   (void)vn;
   return TSF_SUCCESS;

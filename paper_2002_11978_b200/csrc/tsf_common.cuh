@@ -36,6 +36,16 @@ TSF_D void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+// Programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may be scheduled while
+// its predecessor still runs; pdl_enter() blocks until the predecessor grid
+// has completed (its writes visible), then lets the next kernel launch.
+// Both are no-ops for a normal launch.  Every kernel that can follow another
+// in a PDL chain calls it first, before touching any memory.
+TSF_D void pdl_enter() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
 TSF_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 TSF_D void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 

@@ -55,6 +55,7 @@ TSF_D void lfinish(const LargeArgs& a, int b, int it, double rel, int status) {
 // kappa on the grid (scheme.py:156-160,280), x = 0, partials: sum kappa,
 // min kappa, ||r0||^2
 __global__ void __launch_bounds__(kLelThreads) k_lel_begin(LargeArgs a, KrylovArgs k) {
+  pdl_enter();
   __shared__ double red[4 * 32];
   const int b = blockIdx.y, tid = threadIdx.x;
   const long off = (long)b * a.n;
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_begin(LargeArgs a, KrylovAr
 
 // p = r0 (it 1) or r + beta (p - omega v)   (no preconditioner: p_hat = p)
 __global__ void __launch_bounds__(kLelThreads) k_lel_pupd(LargeArgs a) {
+  pdl_enter();
   const int b = blockIdx.y, tid = threadIdx.x;
   if (inst_skip(a, b)) return;
   const long off = (long)b * a.n;
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_pupd(LargeArgs a) {
 
 // s = r - alpha v, ||s||^2 partial (slot 2)
 __global__ void __launch_bounds__(kLelThreads) k_lel_supd(LargeArgs a) {
+  pdl_enter();
   __shared__ double red[4 * 32];
   const int b = blockIdx.y, tid = threadIdx.x;
   if (inst_skip(a, b)) return;
@@ -134,6 +137,7 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_supd(LargeArgs a) {
 // (early-exit instances: x += alpha p_hat only)
 __global__ void __launch_bounds__(kLelThreads) k_lel_xr(LargeArgs a, const double* __restrict__ ph,
                                                         const double* __restrict__ sh) {
+  pdl_enter();
   __shared__ double red[4 * 32];
   const int b = blockIdx.y, tid = threadIdx.x;
   const LState s = a.st[b];
@@ -174,6 +178,7 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_xr(LargeArgs a, const doubl
 __global__ void __launch_bounds__(kLelThreads) k_lspec(LargeArgs a, double kbar,
                                                        const double* __restrict__ kbar_dev,
                                                        int use_state) {
+  pdl_enter();
   const int b = blockIdx.y, tid = threadIdx.x;
   double kb = kbar;
   if (use_state) {
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(kLelThreads) k_lspec(LargeArgs a, double kbar,
 // dst = src
 __global__ void __launch_bounds__(kLelThreads) k_lel_copy(LargeArgs a, double* __restrict__ dst,
                                                           const double* __restrict__ src) {
+  pdl_enter();
   const int b = blockIdx.y, tid = threadIdx.x;
   if (inst_skip(a, b)) return;
   const long off = (long)b * a.n;
@@ -212,6 +218,7 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_copy(LargeArgs a, double* _
 // partial u . w into `slot`
 __global__ void __launch_bounds__(kLelThreads) k_lel_dot(LargeArgs a, const double* __restrict__ u,
                                                          const double* __restrict__ w, int slot) {
+  pdl_enter();
   __shared__ double red[4 * 32];
   const int b = blockIdx.y, tid = threadIdx.x;
   if (inst_skip(a, b)) return;
@@ -229,6 +236,7 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_dot(LargeArgs a, const doub
 
 // x += alpha p ; r -= alpha q (q in v) ; partial ||r||^2 (slot 0)
 __global__ void __launch_bounds__(kLelThreads) k_lel_cgxr(LargeArgs a) {
+  pdl_enter();
   __shared__ double red[4 * 32];
   const int b = blockIdx.y, tid = threadIdx.x;
   if (inst_skip(a, b)) return;
@@ -251,6 +259,7 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_cgxr(LargeArgs a) {
 
 // p = z + beta p
 __global__ void __launch_bounds__(kLelThreads) k_lel_cgp(LargeArgs a, const double* __restrict__ z) {
+  pdl_enter();
   const int b = blockIdx.y, tid = threadIdx.x;
   if (inst_skip(a, b)) return;
   const long off = (long)b * a.n;
@@ -274,6 +283,7 @@ TSF_D double psum(const LargeArgs& a, int b, int slot, int count, double* red) {
 
 __global__ void __launch_bounds__(kLscThreads) k_lsc(LargeArgs a, int stage, int count,
                                                      double kbar_in, double lam_min, int pc) {
+  pdl_enter();
   __shared__ double red[4 * 32];
   const int b = blockIdx.x, tid = threadIdx.x;
   if (stage == LS_BEGIN) {
@@ -429,7 +439,7 @@ struct Runner {
   }
   dim3 lel_grid() const { return dim3((a.n + kLelChunk - 1) / kLelChunk, a.B); }
   int sc(int stage, int count, int pc) {
-    k_lsc<<<a.B, kLscThreads, 0, st>>>(a, stage, count, 0.0, lp->lam_min, pc);
+    launch_pdl(k_lsc, a.B, kLscThreads, 0, st, a, stage, count, 0.0, lp->lam_min, pc);
     return cuda_check(cudaGetLastError(), "k_lsc");
   }
   // one BiCGSTAB iteration for every unfinished instance
@@ -441,7 +451,7 @@ struct Runner {
     if (pc) {
       if ((rc = strang(CI_PUPD, nullptr, a.ph))) return rc;
     } else {
-      k_lel_pupd<<<lel_grid(), kLelThreads, 0, st>>>(a);
+      launch_pdl(k_lel_pupd, lel_grid(), kLelThreads, 0, st, a);
       if ((rc = cuda_check(cudaGetLastError(), "k_lel_pupd"))) return rc;
     }
     if ((rc = apply(ph, a.v, a.r0, 0))) return rc;
@@ -449,30 +459,30 @@ struct Runner {
     if (pc) {
       if ((rc = strang(CI_SUPD, nullptr, a.sh))) return rc;
     } else {
-      k_lel_supd<<<lel_grid(), kLelThreads, 0, st>>>(a);
+      launch_pdl(k_lel_supd, lel_grid(), kLelThreads, 0, st, a);
       if ((rc = cuda_check(cudaGetLastError(), "k_lel_supd"))) return rc;
     }
     if ((rc = sc(LS_SNORM, pc ? NC : NR, pc))) return rc;
     if ((rc = apply(sh, a.t, a.s, 0))) return rc;
     if ((rc = sc(LS_OMEGA, NC, pc))) return rc;
-    k_lel_xr<<<lel_grid(), kLelThreads, 0, st>>>(a, ph, sh);
+    launch_pdl(k_lel_xr, lel_grid(), kLelThreads, 0, st, a, ph, sh);
     if ((rc = cuda_check(cudaGetLastError(), "k_lel_xr"))) return rc;
     return sc(LS_REL, NR, pc);
   }
   int dot(const double* u, const double* w, int slot) {
-    k_lel_dot<<<lel_grid(), kLelThreads, 0, st>>>(a, u, w, slot);
+    launch_pdl(k_lel_dot, lel_grid(), kLelThreads, 0, st, a, u, w, slot);
     return cuda_check(cudaGetLastError(), "k_lel_dot");
   }
   // PCG start: r = b, z = P^{-1} r, p = z, rz = r . z
   int cg_start(int pc) {
     int rc;
     const int NR = (a.n + kLelChunk - 1) / kLelChunk;
-    k_lel_copy<<<lel_grid(), kLelThreads, 0, st>>>(a, a.r, a.r0);
+    launch_pdl(k_lel_copy, lel_grid(), kLelThreads, 0, st, a, a.r, a.r0);
     if ((rc = cuda_check(cudaGetLastError(), "k_lel_copy"))) return rc;
     if (pc) {
       if ((rc = strang(CI_LOAD, a.r, a.p))) return rc;
     } else {
-      k_lel_copy<<<lel_grid(), kLelThreads, 0, st>>>(a, a.p, a.r);
+      launch_pdl(k_lel_copy, lel_grid(), kLelThreads, 0, st, a, a.p, a.r);
       if ((rc = cuda_check(cudaGetLastError(), "k_lel_copy"))) return rc;
     }
     if ((rc = dot(a.r, a.p, 0))) return rc;
@@ -484,7 +494,7 @@ struct Runner {
     const int NC = lp->ncol_cta, NR = (a.n + kLelChunk - 1) / kLelChunk;
     if ((rc = apply(a.p, a.v, a.p, 0))) return rc;           // q -> v; p.q partials
     if ((rc = sc(LS_CG_ALPHA, NC, pc))) return rc;
-    k_lel_cgxr<<<lel_grid(), kLelThreads, 0, st>>>(a);
+    launch_pdl(k_lel_cgxr, lel_grid(), kLelThreads, 0, st, a);
     if ((rc = cuda_check(cudaGetLastError(), "k_lel_cgxr"))) return rc;
     if ((rc = sc(LS_CG_REL, NR, pc))) return rc;
     const double* z = a.r;
@@ -494,13 +504,14 @@ struct Runner {
     }
     if ((rc = dot(a.r, z, 0))) return rc;
     if ((rc = sc(LS_CG_BETA, NR, pc))) return rc;
-    k_lel_cgp<<<lel_grid(), kLelThreads, 0, st>>>(a, z);
+    launch_pdl(k_lel_cgp, lel_grid(), kLelThreads, 0, st, a, z);
     return cuda_check(cudaGetLastError(), "k_lel_cgp");
   }
 };
 
 // ---- graph-mode loop (TSF_SOLVE_GRAPH, default on)
 __global__ void k_lloop_cond(cudaGraphConditionalHandle h, const int* active) {
+  pdl_enter();
   cudaGraphSetConditional(h, *active > 0 ? 1u : 0u);
 }
 
@@ -515,12 +526,15 @@ int chain_nodes(cudaGraph_t g, std::vector<cudaGraphNode_t>& out) {
     return report_error(TSF_E_CUDA, "cudaGraphGetRootNodes");
   for (;;) {
     out.push_back(cur);
+    // _v2: programmatic (PDL) edges carry edge data; the plain query
+    // refuses them (cudaErrorLossyQuery)
     size_t nd = 0;
-    if (cudaGraphNodeGetDependentNodes(cur, nullptr, &nd) != cudaSuccess)
+    if (cudaGraphNodeGetDependentNodes_v2(cur, nullptr, nullptr, &nd) != cudaSuccess)
       return report_error(TSF_E_CUDA, "cudaGraphNodeGetDependentNodes");
     if (nd == 0) break;
     if (nd != 1) return report_error(TSF_E_CUDA, "captured iteration is not a single chain");
-    if (cudaGraphNodeGetDependentNodes(cur, &cur, &nd) != cudaSuccess)
+    cudaGraphEdgeData ed{};
+    if (cudaGraphNodeGetDependentNodes_v2(cur, &cur, &ed, &nd) != cudaSuccess)
       return report_error(TSF_E_CUDA, "cudaGraphNodeGetDependentNodes");
   }
   return 0;
@@ -691,7 +705,7 @@ int large_precond(LargePlan* lp, int B, const double* v, double* z, double shift
   if (rc) return rc;
   Runner R = make_runner(lp, B, st);
   R.a.shift = shift;
-  k_lspec<<<R.lel_grid(), kLelThreads, 0, st>>>(R.a, kbar, kbar_dev, 0);
+  launch_pdl(k_lspec, R.lel_grid(), kLelThreads, 0, st, R.a, kbar, kbar_dev, 0);
   if ((rc = cuda_check(cudaGetLastError(), "k_lspec"))) return rc;
   return R.strang(CI_LOAD, v, z);
 }
@@ -715,7 +729,7 @@ static int loop_graph(LargePlan* lp, const Runner& R0, int method, int pc, cudaS
   auto record = [&](cudaGraphConditionalHandle h) -> int {
     const int r = method == 1 ? R.cg_iteration(pc) : R.bicg_iteration(pc);
     if (r) return r;
-    k_lloop_cond<<<1, 1, 0, R.st>>>(h, lp->active);
+    launch_pdl(k_lloop_cond, 1, 1, 0, R.st, h, lp->active);
     return cuda_check(cudaGetLastError(), "k_lloop_cond");
   };
   if (!G.built) {
@@ -793,13 +807,13 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
   a.status = k.status;
   a.st = lp->st;
   k_set_int<<<1, 1, 0, st>>>(lp->active, B);
-  k_lel_begin<<<R.lel_grid(), kLelThreads, 0, st>>>(a, kk);
+  launch_pdl(k_lel_begin, R.lel_grid(), kLelThreads, 0, st, a, kk);
   if ((rc = cuda_check(cudaGetLastError(), "k_lel_begin"))) return rc;
-  k_lsc<<<B, kLscThreads, 0, st>>>(a, LS_BEGIN, (a.n + kLelChunk - 1) / kLelChunk, k.kbar,
+  launch_pdl(k_lsc, B, kLscThreads, 0, st, a, LS_BEGIN, (a.n + kLelChunk - 1) / kLelChunk, k.kbar,
                                    lp->lam_min, pc);
   if ((rc = cuda_check(cudaGetLastError(), "k_lsc(begin)"))) return rc;
   if (pc) {
-    k_lspec<<<R.lel_grid(), kLelThreads, 0, st>>>(a, 0.0, nullptr, 1);
+    launch_pdl(k_lspec, R.lel_grid(), kLelThreads, 0, st, a, 0.0, nullptr, 1);
     if ((rc = cuda_check(cudaGetLastError(), "k_lspec"))) return rc;
   }
   if (method == 1 && (rc = R.cg_start(pc))) return rc;

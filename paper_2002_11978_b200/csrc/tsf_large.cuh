@@ -142,6 +142,7 @@ TSF_D void stage_tw(double2* dst, const double2* src) {
 template <int N1, int MB = LCol<N1>::MINB>
 __global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)
 k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
+  pdl_enter();
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
   const int N2 = a.nt / N1;
@@ -218,6 +219,7 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
 template <int N2>
 __global__ void __launch_bounds__(LRow<N2>::BLOCK, 1)
 k_lrow(LargeArgs a, int spec_mode) {
+  pdl_enter();
   const long N = a.nt;
   constexpr int E = LRow<N2>::E;
   constexpr int T = LRow<N2>::T;
@@ -282,6 +284,7 @@ template <int N1, int MB = LCol<N1>::MINB>
 __global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)
 k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __restrict__ xin,
            const double* __restrict__ w1, int pslot) {
+  pdl_enter();
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
   const int N2 = a.nt / N1;
@@ -369,6 +372,34 @@ struct LargeDispatch {
                      const double* w1, int pslot, cudaStream_t st);
   static int col_group();  // G: columns per column CTA
 };
+
+// Launches of the large-n engine are programmatic dependent launches
+// (kernels enter through pdl_enter, tsf_common.cuh): a B = 1 iteration is 17
+// short dependent launches, and the next grid's launch latency and CTA
+// rasterisation now overlap the running one.  TSF_PDL=0 launches plainly.
+inline bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_PDL");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
 
 #define TSF_EXTERN_LARGE(L) extern template struct LargeDispatch<L>;
 TSF_EXTERN_LARGE(6)

@@ -29,7 +29,7 @@ int LargeDispatch<LOG>::col_fwd(const LargeArgs& a, const double* src, int in_mo
   static cudaError_t prep1 = large_prep(k_lcol_fwd<N1, 1>, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
   if (prep1 != cudaSuccess) return large_launch_error(prep1);
-  k<<<grid, S::BLOCK, S::SMEM, st>>>(a, src, in_mode);
+  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, src, in_mode);
   return large_launch_error(cudaGetLastError());
 }
 
@@ -40,7 +40,7 @@ int LargeDispatch<LOG>::row(const LargeArgs& a, int spec_mode, cudaStream_t st) 
   auto k = k_lrow<N2>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  k<<<dim3(a.nt / N2, a.B), S::BLOCK, S::SMEM, st>>>(a, spec_mode);
+  launch_pdl(k, dim3(a.nt / N2, a.B), S::BLOCK, S::SMEM, st, a, spec_mode);
   return large_launch_error(cudaGetLastError());
 }
 
@@ -55,7 +55,7 @@ int LargeDispatch<LOG>::col_inv(const LargeArgs& a, double* dst, int out_mode, c
   static cudaError_t prep1 = large_prep(k_lcol_inv<N1, 1>, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
   if (prep1 != cudaSuccess) return large_launch_error(prep1);
-  k<<<grid, S::BLOCK, S::SMEM, st>>>(a, dst, out_mode, xin, w1, pslot);
+  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, dst, out_mode, xin, w1, pslot);
   return large_launch_error(cudaGetLastError());
 }
 

@@ -171,6 +171,197 @@ k_soe_push_rhs(SoeArgs a) {
   soe_pair<UNROLL>(a, tabs, b, i0);
 }
 
+// ---------------------------------------------------------------- blocked
+// Blocked SOE schedule of the march (tsf_fids_march, K = soe_block > 1): the
+// W pass runs once per K levels instead of once per level.  With W^k the
+// state after the push of level k, d_j(l) = e^{-s_j tau_l}, c_j(l) the push
+// coefficient and h_j(m) = w_j e^{-s_j tau_m}, for a block base mb and
+// mb < m <= mb + K:
+//   W^{m-1} = [prod_{l=mb+1}^{m-1} d(l)] W^{mb} + sum_{i=mb+1}^{m-1} [prod_{l=i+1}^{m-1} d(l)] c(i) du^i
+//   H^m     = sum_j alpha_j(m) W_j^{mb} + sum_{i=mb+1}^{m-1} beta(m, i) du^i
+//   alpha_j(m) = h_j(m) prod_{l=mb+1}^{m-1} d_j(l),
+//   beta(m, i) = sum_j h_j(m) [prod_{l=i+1}^{m-1} d_j(l)] c_j(i)      (host tables)
+// so one pass over W at the base gives the W-part G_m of every history term
+// of the block, and each level adds a short combination of the block's du
+// vectors.  The pass advances W by the K pushes of the block with the
+// reference's own recurrence, in registers (w <- (w d) + (c du), no FMA), so
+// W at every block base is bit-identical to the per-level schedule; only the
+// history term's summation order differs (as it already does against the
+// reference's BLAS GEMV).  HBM traffic per level: 16 N_exp n / K + O(K n)
+// instead of 16 N_exp n.
+constexpr int kSoeMaxBlock = 16;
+
+struct SoeBlockArgs {
+  int n, nexp, B;
+  double* W;               // [B][nexp][n]: W^{mb_prev} in, W^{mb} out
+  const double* u_cur;     // u^{mb}
+  const double* u_prev;    // u^{mb-1}
+  double tau_cur;          // tau_{mb}
+  const double* du_ring;   // [K][B][n]: du^i at slot (i-1) % K
+  int K;
+  int mb;                  // new base level
+  int ka;                  // pushes to apply: levels mb-ka+1 .. mb (0: none)
+  int w_zero;              // W^{mb_prev} == 0 (not read)
+  const double* push_tab;  // soe_tab rows of the pushed levels: level l at (l-1)*3*nexp
+  int kn;                  // history levels of the new block: mb+1 .. mb+kn (0: none)
+  const double* alpha;     // [M][nexp]: alpha_j(m) at (m-1)*nexp
+  double* g_ring;          // [K][B][n]: G_m at slot (m-1) % K  (m >= mb+2)
+  // RHS of level mb+1 (kn >= 1): f + (a u^{mb} - G_{mb+1}) / G
+  double a_next, G;
+  const double* fmodes;
+  long fq_stride, fb_stride;
+  int nf;
+  double fcoef[4];
+  double* rhs;
+};
+
+// shared tables: [ka][nexp] (d, c) pairs | [kn][nexp] alpha
+template <int KMAX>
+__global__ void __launch_bounds__(kSoeThreads) k_soe_block(SoeBlockArgs a) {
+  extern __shared__ double sh[];
+  const int n = a.n, nexp = a.nexp, K = a.K, ka = a.ka, kn = a.kn;
+  double2* dc = reinterpret_cast<double2*>(sh);          // [ka][nexp]
+  double* al = sh + 2 * ka * nexp;                       // [kn][nexp]
+  for (int t = threadIdx.x; t < ka * nexp; t += blockDim.x) {
+    const int l = t / nexp, j = t % nexp;
+    const double* row = a.push_tab + (size_t)(a.mb - ka + l) * 3 * nexp;  // level mb-ka+1+l
+    dc[t] = make_double2(row[j], row[nexp + j]);
+  }
+  for (int t = threadIdx.x; t < kn * nexp; t += blockDim.x)
+    al[t] = a.alpha[(size_t)(a.mb + t / nexp) * nexp + t % nexp];          // level mb+1+t/nexp
+  __syncthreads();
+  const int chunks = (n + 2 * kSoeThreads - 1) / (2 * kSoeThreads);
+  const int b = blockIdx.x / chunks;
+  const int i0 = 2 * ((blockIdx.x % chunks) * kSoeThreads + threadIdx.x);
+  if (i0 >= n) return;
+  const bool pair = (i0 + 1 < n) && ((n & 1) == 0);
+  const long vb = (long)b * n + i0;
+  const long vn = (long)a.B * n;
+  auto ld2 = [&](const double* p) -> double2 {
+    if (pair) return *reinterpret_cast<const double2*>(p + vb);
+    return make_double2(p[vb], (i0 + 1 < n) ? p[vb + 1] : 0.0);
+  };
+  // du^i of the pushed levels: ring slots, the last one (level mb) from u
+  double2 du[KMAX];
+#pragma unroll
+  for (int l = 0; l < KMAX; ++l) {
+    du[l] = make_double2(0.0, 0.0);
+    if (l < ka) {
+      const int lev = a.mb - ka + 1 + l;
+      if (lev == a.mb) {
+        const double2 uc = ld2(a.u_cur), up = ld2(a.u_prev);
+        du[l].x = __ddiv_rn(__dsub_rn(uc.x, up.x), a.tau_cur);
+        du[l].y = __ddiv_rn(__dsub_rn(uc.y, up.y), a.tau_cur);
+      } else {
+        du[l] = ld2(a.du_ring + (long)((lev - 1) % K) * vn);
+      }
+    }
+  }
+  double2 g[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) g[k] = make_double2(0.0, 0.0);
+  double* Wp = a.W + (long)b * nexp * n + i0;
+  const bool need_w = ka > 0 || !a.w_zero;   // else W^{mb} = 0: G = 0
+  if (need_w) {
+    for (int j = 0; j < nexp; ++j) {
+      double2 w = make_double2(0.0, 0.0);
+      if (!a.w_zero) {
+        if (pair) w = __ldcs(reinterpret_cast<const double2*>(Wp + (long)j * n));
+        else w = make_double2(Wp[(long)j * n], (i0 + 1 < n) ? Wp[(long)j * n + 1] : 0.0);
+      }
+      if (ka > 0) {
+#pragma unroll
+        for (int l = 0; l < KMAX; ++l) {
+          if (l < ka) {
+            const double2 q = dc[l * nexp + j];   // (decay, coef) of the pushed level
+            w.x = __dadd_rn(__dmul_rn(w.x, q.x), __dmul_rn(q.y, du[l].x));
+            w.y = __dadd_rn(__dmul_rn(w.y, q.x), __dmul_rn(q.y, du[l].y));
+          }
+        }
+        if (pair) {
+          __stcs(reinterpret_cast<double2*>(Wp + (long)j * n), w);
+        } else {
+          Wp[(long)j * n] = w.x;
+          if (i0 + 1 < n) Wp[(long)j * n + 1] = w.y;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k < kn) {
+          const double c = al[k * nexp + j];
+          g[k].x = fma(c, w.x, g[k].x);
+          g[k].y = fma(c, w.y, g[k].y);
+        }
+      }
+    }
+  }
+  auto st2 = [&](double* p, double2 v) {
+    if (pair) {
+      *reinterpret_cast<double2*>(p + vb) = v;
+    } else {
+      p[vb] = v.x;
+      if (i0 + 1 < n) p[vb + 1] = v.y;
+    }
+  };
+#pragma unroll
+  for (int k = 1; k < KMAX; ++k)
+    if (k < kn) st2(a.g_ring + (long)((a.mb + k) % K) * vn, g[k]);   // level mb+1+k, slot (m-1)%K
+  if (kn >= 1) {
+    const double2 u = ld2(a.u_cur);
+    double2 f = make_double2(0.0, 0.0);
+    for (int q = 0; q < a.nf; ++q) {
+      const double* fq = a.fmodes + q * a.fq_stride + (long)b * a.fb_stride - (long)b * n;
+      const double2 m = ld2(fq);
+      f.x = __dadd_rn(f.x, __dmul_rn(m.x, a.fcoef[q]));
+      f.y = __dadd_rn(f.y, __dmul_rn(m.y, a.fcoef[q]));
+    }
+    double2 r;
+    r.x = __dadd_rn(f.x, __ddiv_rn(__dsub_rn(__dmul_rn(a.a_next, u.x), g[0].x), a.G));
+    r.y = __dadd_rn(f.y, __ddiv_rn(__dsub_rn(__dmul_rn(a.a_next, u.y), g[0].y), a.G));
+    st2(a.rhs, r);
+  }
+}
+
+// Level m of a block (mb + 2 <= m <= mb + K): du^{m-1} (stored in the ring)
+// and rhs^m = f + (a u^{m-1} - (G_m + sum_{i=mb+1}^{m-1} beta(m, i) du^i)) / G.
+struct SoeLevelArgs {
+  int n, B, K, m, mb;
+  const double* u1;        // u^{m-1}
+  const double* u2;        // u^{m-2}
+  double tau1;             // tau_{m-1}
+  double* du_ring;
+  const double* g_ring;
+  double beta[kSoeMaxBlock];   // beta(m, mb+1+q), q < m-1-mb
+  double a_m, G;
+  const double* fmodes;
+  long fq_stride, fb_stride;
+  int nf;
+  double fcoef[4];
+  double* rhs;
+};
+
+static __global__ void __launch_bounds__(256) k_soe_level(SoeLevelArgs a) {
+  const int n = a.n;
+  const long vn = (long)a.B * n;
+  const long total = vn;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(e / n), i = (int)(e % n);
+    const double u1 = a.u1[e];
+    const double du = __ddiv_rn(__dsub_rn(u1, a.u2[e]), a.tau1);
+    a.du_ring[(long)((a.m - 2) % a.K) * vn + e] = du;          // du^{m-1}, slot (m-2) % K
+    double H = a.g_ring[(long)((a.m - 1) % a.K) * vn + e];     // G_m
+    const int nq = a.m - 1 - a.mb;                             // du^{mb+1} .. du^{m-1}
+    for (int q = 0; q < nq - 1; ++q)
+      H = fma(a.beta[q], a.du_ring[(long)((a.mb + q) % a.K) * vn + e], H);
+    H = fma(a.beta[nq - 1], du, H);
+    double f = 0.0;
+    for (int q = 0; q < a.nf; ++q)
+      f = __dadd_rn(f, __dmul_rn(a.fmodes[q * a.fq_stride + (long)b * a.fb_stride + i], a.fcoef[q]));
+    a.rhs[e] = __dadd_rn(f, __ddiv_rn(__dsub_rn(__dmul_rn(a.a_m, u1), H), a.G));
+  }
+}
+
 // Epilogue of a converged instance's level solve (the instance's CTA streams
 // its own W rows: push of this level + history term/RHS of the next one), so
 // the HBM-bound SOE pass overlaps other instances' transform work.

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
@@ -202,6 +203,52 @@ class MarchResult:
     W: object               # torch [B, nexp, n]
 
 
+def _soe_block_default(B: int, n: int) -> int:
+    """Levels per W pass of the march's blocked SOE schedule.
+
+    TSF_SOE_BLOCK overrides (0 or 1: one W pass per level).  By default the
+    schedule is blocked (K = 8) on the single-CTA engine (n <= 4096), where
+    batches make the SOE pass a large share of a level (configs[2]: 16%), and
+    per-level on the large-n engine, where single instances make it ~1-4%
+    (configs[1], configs[3]) and the per-level schedule keeps the history
+    term in the reference's order.  The choice depends on n
+    only, so an instance's result does not depend on the batch it is in."""
+    env = os.environ.get("TSF_SOE_BLOCK")
+    if env is not None:
+        k = int(env)
+        return k if 2 <= k <= 16 else 1
+    return 8 if n <= 4096 else 1
+
+
+def soe_block_tables(tab: np.ndarray, K: int):
+    """Host tables of the blocked SOE schedule (csrc/tsf_soe.cuh k_soe_block).
+
+    tab[m-1] = (d(m), c(m), h(m)) are level m's decay e^{-s tau_m}, push
+    coefficient -expm1(-s tau_m)/s and history weight w e^{-s tau_m}, i.e. the
+    factors of history_push (soe.py:221-223) and of the history term
+    (scheme.py:281-282).  For level m in the block with base mb = K floor((m-1)/K):
+      alpha_j(m)   = h_j(m) prod_{l=mb+1}^{m-1} d_j(l)
+      beta(m, i)   = sum_j h_j(m) prod_{l=i+1}^{m-1} d_j(l) c_j(i),  mb < i < m
+    so that H^m = sum_j alpha_j(m) W_j^{mb} + sum_i beta(m, i) du^i exactly in
+    real arithmetic (products and sums in extended precision, rounded once)."""
+    M, _, nexp = tab.shape
+    ld = np.longdouble
+    dec, cf, hc = tab[:, 0].astype(ld), tab[:, 1].astype(ld), tab[:, 2].astype(ld)
+    alpha = np.empty((M, nexp))
+    beta = np.zeros((M, 16))
+    for m in range(1, M + 1):
+        mb = K * ((m - 1) // K)
+        # Q_i = prod_{l=i+1}^{m-1} d(l) for i = m-1 down to mb
+        Q = np.ones(nexp, dtype=ld)
+        for i in range(m - 1, mb - 1, -1):
+            if i > mb:
+                beta[m - 1, i - mb - 1] = float(np.sum(hc[m - 1] * Q * cf[i - 1]))
+            if i >= mb + 1:
+                Q = Q * dec[i - 1]
+        alpha[m - 1] = (hc[m - 1] * Q).astype(np.float64)
+    return alpha, beta
+
+
 class FidsMarch:
     """Device state + native driver for a batch of FIDS instances sharing
     (gamma, alpha, l, T, M, r, N, SOE).  Reusable: `reset()` then `run()`."""
@@ -209,7 +256,8 @@ class FidsMarch:
     def __init__(self, gamma, alpha, l, T, M, r, N, soe: SoeApproximation, method: int,
                  precond: int, tol: float, max_iters: Optional[int], B: int,
                  kappa: _FieldDev, source: _FieldDev, u0, hist_B: int = 0, device: int = 0,
-                 mu: Optional[float] = None, private_plan: bool = False):
+                 mu: Optional[float] = None, private_plan: bool = False,
+                 soe_block: Optional[int] = None):
         torch = _native.torch_mod()
         self.dev = torch.device(f"cuda:{device}")
         self.mesh = build_mesh(M, r, T)
@@ -242,6 +290,13 @@ class FidsMarch:
             tab[m, 1] = -np.expm1(-s * tau[m]) / s
             tab[m, 2] = w * dec
         self.soe_tab = torch.from_numpy(tab).to(self.dev)
+        # blocked SOE schedule (tsf_march.soe_block; csrc/tsf_soe.cuh k_soe_block)
+        self.soe_block = (soe_block if soe_block is not None
+                          else _soe_block_default(self.B, self.n))
+        if self.soe_block > 1:
+            alpha, beta = soe_block_tables(tab, self.soe_block)
+            self.soe_alpha = torch.from_numpy(alpha).to(self.dev)
+            self.soe_beta = beta
         self.kappa, self.source = kappa, source
         n, nexp = self.n, soe.n_exp
         f64 = dict(dtype=torch.float64, device=self.dev)
@@ -253,6 +308,8 @@ class FidsMarch:
         self.iters = torch.zeros((M, B), dtype=torch.int32, device=self.dev)
         self.relres = torch.zeros((M, B), **f64)
         self.status = torch.zeros((M, B), dtype=torch.int32, device=self.dev)
+        self.soe_ring = (torch.empty((2, self.soe_block, B, n), **f64) if self.soe_block > 1
+                         else None)
         self.hist_B = int(hist_B)
         self.hist = torch.empty((M + 1, hist_B, n), **f64) if hist_B > 0 else None
         _native.check(_native.load().tsf_plan_reserve(self.plan.handle, self.B))
@@ -289,6 +346,11 @@ class FidsMarch:
         d.hist = self.hist.data_ptr() if self.hist is not None else None
         d.hist_B = self.hist_B
         d.m_begin, d.m_end = m_begin, m_end
+        d.soe_block = self.soe_block if self.soe_block > 1 else 0
+        if self.soe_block > 1:
+            d.soe_alpha = self.soe_alpha.data_ptr()
+            d.soe_beta = self.soe_beta.ctypes.data
+            d.soe_ring = self.soe_ring.data_ptr()
         return d
 
     def run(self, levels: Optional[int] = None, stream=None, events=None):
@@ -650,5 +712,6 @@ def run_fids_batched(gamma: float, alpha: float, M: int, r: float, N: int,
     _raise_status(res.status, res.iterations, res.relres, mesh.t, use_cg)
     rep = dict(iterations=res.iterations, relres=res.relres, n_exp=soe.n_exp,
                wall_time=time.perf_counter() - t0,
-               hist=None if res.hist is None else res.hist.cpu().numpy())
+               hist=None if res.hist is None else res.hist.cpu().numpy(),
+               W=res.W, soe_block=march.soe_block)
     return _arrays.back(res.u_final, as_np), rep
