@@ -571,6 +571,24 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
       CK(cudaGetLastError());
       return TSF_SUCCESS;
     };
+    if (ka == K && kn == K && (n & 1) == 0 && (K == 4 || K == 8 || K == 16)) {
+      const int fsm = ((K + K / 2) * nexp + kSoeRing * kSoeThreads) * (int)sizeof(double2);
+      auto gof = [&](auto kern) -> int {
+        if (fsm > 48 * 1024)
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+        kern<<<(unsigned)B * chunks, kSoeThreads, fsm, st>>>(b);
+        CK(cudaGetLastError());
+        return TSF_SUCCESS;
+      };
+      const bool wz = b.w_zero != 0;
+      if (K == 4) return wz ? gof(k_soe_block_full<4, true>) : gof(k_soe_block_full<4, false>);
+      if (K == 8) {
+        static const int pd = getenv("TSF_SOE_PD") ? atoi(getenv("TSF_SOE_PD")) : 0;
+        if (!wz && pd == 0) return gof(k_soe_block_full<8, false, 0>);
+        return wz ? gof(k_soe_block_full<8, true>) : gof(k_soe_block_full<8, false>);
+      }
+      return wz ? gof(k_soe_block_full<16, true>) : gof(k_soe_block_full<16, false>);
+    }
     if (K <= 4) return go(k_soe_block<4>);
     if (K <= 8) return go(k_soe_block<8>);
     return go(k_soe_block<kSoeMaxBlock>);
@@ -596,9 +614,8 @@ int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
     l.fb_stride = d->source.b_stride;
     for (int q = 0; q < l.nf; ++q) l.fcoef[q] = d->source.coef[(size_t)m * l.nf + q];
     l.rhs = d->rhs;
-    const long total = (long)B * n;
-    const long grid = std::min<long>((total + 255) / 256, 148L * 16);
-    k_soe_level<<<(unsigned)grid, 256, 0, st>>>(l);
+    const dim3 grid((unsigned)((n + 511) / 512), (unsigned)B);
+    k_soe_level<<<grid, 256, 0, st>>>(l);
     CK(cudaGetLastError());
     return TSF_SUCCESS;
   };

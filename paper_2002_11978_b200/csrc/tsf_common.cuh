@@ -47,6 +47,8 @@ TSF_D void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 TSF_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+TSF_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 TSF_D void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Software prefetch of a whole vector (one 128-byte line per thread and

@@ -322,6 +322,123 @@ __global__ void __launch_bounds__(kSoeThreads) k_soe_block(SoeBlockArgs a) {
   }
 }
 
+// Full passes (ka = kn = K, n even): K a template parameter, no predicates,
+// the per-exponential coefficients interleaved in shared memory so one
+// broadcast LDS.128 feeds a (decay, coef) pair or two alphas.  The generic
+// kernel above issued ~190 instructions per exponential and point pair
+// (ncu: issue-bound at 61%, 10-16 ms per pass); this one ~80.
+constexpr int kSoeRing = 12;   // cp.async W-row slots per thread (k_soe_block_full, PD = 0)
+template <int K, bool WZERO, int PD = 4>
+__global__ void __launch_bounds__(kSoeThreads) k_soe_block_full(SoeBlockArgs a) {
+  static_assert(K % 2 == 0, "K even");
+  extern __shared__ double2 shc[];
+  const int n = a.n, nexp = a.nexp;
+  double2* dc = shc;                 // [nexp][K]   (d_l, c_l), level mb-K+1+l
+  double2* al = shc + nexp * K;      // [nexp][K/2] (alpha_{2q}, alpha_{2q+1}), level mb+1+k
+  for (int t = threadIdx.x; t < nexp * K; t += blockDim.x) {
+    const int j = t / K, l = t % K;
+    const double* row = a.push_tab + (size_t)(a.mb - K + l) * 3 * nexp;
+    dc[t] = make_double2(row[j], row[nexp + j]);
+  }
+  for (int t = threadIdx.x; t < nexp * (K / 2); t += blockDim.x) {
+    const int j = t / (K / 2), q = t % (K / 2);
+    al[t] = make_double2(a.alpha[(size_t)(a.mb + 2 * q) * nexp + j],
+                         a.alpha[(size_t)(a.mb + 2 * q + 1) * nexp + j]);
+  }
+  __syncthreads();
+  const int chunks = (n + 2 * kSoeThreads - 1) / (2 * kSoeThreads);
+  const int b = blockIdx.x / chunks;
+  const int i0 = 2 * ((blockIdx.x % chunks) * kSoeThreads + threadIdx.x);
+  if (i0 >= n) return;
+  const long vb = (long)b * n + i0;
+  const long vn = (long)a.B * n;
+  auto ld2 = [&](const double* p) { return *reinterpret_cast<const double2*>(p + vb); };
+  double2 du[K];
+#pragma unroll
+  for (int l = 0; l < K - 1; ++l) du[l] = ld2(a.du_ring + (long)((a.mb - K + l) % a.K) * vn);
+  {
+    const double2 uc = ld2(a.u_cur), up = ld2(a.u_prev);
+    du[K - 1].x = __ddiv_rn(__dsub_rn(uc.x, up.x), a.tau_cur);
+    du[K - 1].y = __ddiv_rn(__dsub_rn(uc.y, up.y), a.tau_cur);
+  }
+  double2 g[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) g[k] = make_double2(0.0, 0.0);
+  double2* Wp = reinterpret_cast<double2*>(a.W + (long)b * nexp * n + i0);
+  const long rs = n / 2;   // row stride in double2
+  // W rows are loaded PD rows ahead: at 4 CTAs x 128 threads per SM (the
+  // register budget of 2K accumulators + K du pairs) one row in flight per
+  // thread kept ~16 KB per SM in flight — half the HBM rate (ncu, 12.6 ms
+  // per pass); PD = 4 keeps ~64 KB per SM in flight.
+  // PD == 0: the rows go through a per-thread cp.async ring of kSoeRing
+  // slots in shared memory instead (no registers held; ~12 rows ahead).
+  constexpr bool RING = (PD == 0) && !WZERO;
+  constexpr int PR = PD > 0 ? PD : 1;
+  double2* ring = al + nexp * (K / 2) + threadIdx.x;   // slot s at ring[s * kSoeThreads]
+  double2 wb[PR];
+  if constexpr (RING) {
+#pragma unroll
+    for (int p = 0; p < kSoeRing - 1; ++p) {
+      if (p < nexp) cp_async16(ring + p * kSoeThreads, Wp + p * rs);
+      cp_async_commit();
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < PR; ++p)
+      wb[p] = (!WZERO && p < nexp) ? __ldcs(Wp + p * rs) : make_double2(0.0, 0.0);
+  }
+  for (int j0 = 0; j0 < nexp; j0 += PR) {
+#pragma unroll
+  for (int p = 0; p < PR; ++p) {
+    const int j = j0 + p;
+    if (j >= nexp) break;
+    double2 w;
+    if constexpr (RING) {
+      const int jn = j + kSoeRing - 1;
+      if (jn < nexp) cp_async16(ring + (jn % kSoeRing) * kSoeThreads, Wp + jn * rs);
+      cp_async_commit();
+      cp_async_wait<kSoeRing - 1>();   // this thread's row j has landed
+      w = ring[(j % kSoeRing) * kSoeThreads];
+    } else {
+      w = wb[p];
+      if (!WZERO && j + PR < nexp) wb[p] = __ldcs(Wp + (j + PR) * rs);
+    }
+    const double2* q = dc + j * K;
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+      const double2 c = q[l];
+      w.x = __dadd_rn(__dmul_rn(w.x, c.x), __dmul_rn(c.y, du[l].x));
+      w.y = __dadd_rn(__dmul_rn(w.y, c.x), __dmul_rn(c.y, du[l].y));
+    }
+    __stcs(Wp + j * rs, w);
+    const double2* h = al + j * (K / 2);
+#pragma unroll
+    for (int k2 = 0; k2 < K / 2; ++k2) {
+      const double2 c = h[k2];
+      g[2 * k2].x = fma(c.x, w.x, g[2 * k2].x);
+      g[2 * k2].y = fma(c.x, w.y, g[2 * k2].y);
+      g[2 * k2 + 1].x = fma(c.y, w.x, g[2 * k2 + 1].x);
+      g[2 * k2 + 1].y = fma(c.y, w.y, g[2 * k2 + 1].y);
+    }
+  }
+  }
+#pragma unroll
+  for (int k = 1; k < K; ++k)
+    *reinterpret_cast<double2*>(a.g_ring + (long)((a.mb + k) % a.K) * vn + vb) = g[k];
+  const double2 u = ld2(a.u_cur);
+  double2 f = make_double2(0.0, 0.0);
+  for (int qq = 0; qq < a.nf; ++qq) {
+    const double* fq = a.fmodes + qq * a.fq_stride + (long)b * a.fb_stride - (long)b * n;
+    const double2 m = ld2(fq);
+    f.x = __dadd_rn(f.x, __dmul_rn(m.x, a.fcoef[qq]));
+    f.y = __dadd_rn(f.y, __dmul_rn(m.y, a.fcoef[qq]));
+  }
+  double2 r;
+  r.x = __dadd_rn(f.x, __ddiv_rn(__dsub_rn(__dmul_rn(a.a_next, u.x), g[0].x), a.G));
+  r.y = __dadd_rn(f.y, __ddiv_rn(__dsub_rn(__dmul_rn(a.a_next, u.y), g[0].y), a.G));
+  *reinterpret_cast<double2*>(a.rhs + vb) = r;
+}
+
 // Level m of a block (mb + 2 <= m <= mb + K): du^{m-1} (stored in the ring)
 // and rhs^m = f + (a u^{m-1} - (G_m + sum_{i=mb+1}^{m-1} beta(m, i) du^i)) / G.
 struct SoeLevelArgs {
@@ -340,25 +457,43 @@ struct SoeLevelArgs {
   double* rhs;
 };
 
+// Two adjacent points per thread (16-byte accesses), grid (chunks, B); every
+// load is issued before the du^{m-1} store (the ring is read and written in
+// the same kernel, so the store would otherwise order the later loads).
 static __global__ void __launch_bounds__(256) k_soe_level(SoeLevelArgs a) {
-  const int n = a.n;
+  const int n = a.n, b = blockIdx.y;
+  const int i0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (i0 >= n) return;
   const long vn = (long)a.B * n;
-  const long total = vn;
-  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long)gridDim.x * blockDim.x) {
-    const int b = (int)(e / n), i = (int)(e % n);
-    const double u1 = a.u1[e];
-    const double du = __ddiv_rn(__dsub_rn(u1, a.u2[e]), a.tau1);
-    a.du_ring[(long)((a.m - 2) % a.K) * vn + e] = du;          // du^{m-1}, slot (m-2) % K
-    double H = a.g_ring[(long)((a.m - 1) % a.K) * vn + e];     // G_m
-    const int nq = a.m - 1 - a.mb;                             // du^{mb+1} .. du^{m-1}
-    for (int q = 0; q < nq - 1; ++q)
-      H = fma(a.beta[q], a.du_ring[(long)((a.mb + q) % a.K) * vn + e], H);
-    H = fma(a.beta[nq - 1], du, H);
-    double f = 0.0;
-    for (int q = 0; q < a.nf; ++q)
-      f = __dadd_rn(f, __dmul_rn(a.fmodes[q * a.fq_stride + (long)b * a.fb_stride + i], a.fcoef[q]));
-    a.rhs[e] = __dadd_rn(f, __ddiv_rn(__dsub_rn(__dmul_rn(a.a_m, u1), H), a.G));
+  const long e = (long)b * n + i0;
+  const bool pair = (n & 1) == 0;   // else one point per thread-slot pair, scalar path
+  const int np = pair ? 2 : ((i0 + 1 < n) ? 2 : 1);
+  double u1[2], u2[2], H[2], f[2];
+  const int nq = a.m - 1 - a.mb;    // du^{mb+1} .. du^{m-1}
+  double dq[kSoeMaxBlock - 1][2];
+  for (int c = 0; c < np; ++c) {
+    u1[c] = a.u1[e + c];
+    u2[c] = a.u2[e + c];
+    H[c] = a.g_ring[(long)((a.m - 1) % a.K) * vn + e + c];   // G_m
+    f[c] = 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < kSoeMaxBlock - 1; ++q)
+    if (q < nq - 1)
+      for (int c = 0; c < np; ++c) dq[q][c] = a.du_ring[(long)((a.mb + q) % a.K) * vn + e + c];
+  for (int qq = 0; qq < a.nf; ++qq)
+    for (int c = 0; c < np; ++c)
+      f[c] = __dadd_rn(f[c], __dmul_rn(a.fmodes[qq * a.fq_stride + (long)b * a.fb_stride + i0 + c],
+                                       a.fcoef[qq]));
+  for (int c = 0; c < np; ++c) {
+    const double du = __ddiv_rn(__dsub_rn(u1[c], u2[c]), a.tau1);
+    double h = H[c];
+#pragma unroll
+    for (int q = 0; q < kSoeMaxBlock - 1; ++q)
+      if (q < nq - 1) h = fma(a.beta[q], dq[q][c], h);
+    h = fma(a.beta[nq - 1], du, h);
+    a.rhs[e + c] = __dadd_rn(f[c], __ddiv_rn(__dsub_rn(__dmul_rn(a.a_m, u1[c]), h), a.G));
+    a.du_ring[(long)((a.m - 2) % a.K) * vn + e + c] = du;     // du^{m-1}, slot (m-2) % K
   }
 }
 
