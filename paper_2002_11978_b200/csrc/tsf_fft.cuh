@@ -297,20 +297,26 @@ TSF_D void stockham_pass(double2 (&v)[E], double2* sm, const double2* __restrict
       // W^k, W^2k, W^4k from the table; the other powers are one product of
       // two of them (3 of 7 table reads per butterfly; accuracy measured in
       // tools/accuracy_probe.py against an exact long-double DFT)
+      // exponents that are multiples of 64 (sh >= 6: the first twiddled pass)
+      // need only the high table: lo[0] = 1 exactly, so the product it saves
+      // was exact — same values, 3 loads and 3 complex products fewer
+      auto twx = [&](int e) {
+        return sh >= 6 ? tw[kTwLo + tw_lo_slot(e >> 6)] : tw_get(tw, e);
+      };
       double2 w[R];
-      w[1] = tw_get(tw, k << sh);
+      w[1] = twx(k << sh);
       if constexpr (R >= 4) {
-        w[2] = tw_get(tw, (2 * k) << sh);
+        w[2] = twx((2 * k) << sh);
         w[3] = cmul(w[2], w[1]);
       }
       if constexpr (R >= 8) {
-        w[4] = tw_get(tw, (4 * k) << sh);
+        w[4] = twx((4 * k) << sh);
         w[5] = cmul(w[4], w[1]);
         w[6] = cmul(w[4], w[2]);
         w[7] = cmul(w[4], w[3]);
       }
       if constexpr (R >= 16) {
-        w[8] = tw_get(tw, (8 * k) << sh);
+        w[8] = twx((8 * k) << sh);
 #pragma unroll
         for (int m = 9; m < 16; ++m) w[m] = cmul(w[8], w[m - 8]);
       }
