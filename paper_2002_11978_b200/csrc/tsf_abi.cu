@@ -74,6 +74,18 @@ bool spec_reuse() {
   return v == 1;
 }
 
+int solve_groups(int B) {
+  static int env = -2;
+  if (env == -2) {
+    const char* s = getenv("TSF_SOLVE_GROUPS");
+    env = s ? atoi(s) : -1;
+  }
+  int g = env > 0 ? env : (B >= 1024 ? 4 : 1);
+  if (g > kMaxSolveGroups) g = kMaxSolveGroups;
+  if (g > B) g = B > 0 ? B : 1;
+  return g;
+}
+
 SolveGraphs::~SolveGraphs() {
   for (auto& a : slot)
     for (auto& b : a)

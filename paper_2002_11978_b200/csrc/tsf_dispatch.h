@@ -16,13 +16,19 @@ int report_cuda(cudaError_t e, const char* what);
 // Instantiated level-solve graphs of one plan (graph mode): one slot per
 // (transform size, preconditioner, method).  Built on first use; later
 // solves only rewrite the kernel-node parameters and relaunch.
+// A level-solve graph: `groups` independent branches (contiguous instance
+// groups), each  set -> begin -> WHILE(active_g > 0) { a ; b ; test }.
+constexpr int kMaxSolveGroups = 8;
 struct SolveGraph {
   bool built = false;
+  int groups = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  cudaGraphConditionalHandle cond{};
-  cudaGraphNode_t n_set = nullptr, n_begin = nullptr, n_a = nullptr, n_b = nullptr, n_c = nullptr;
+  cudaGraphConditionalHandle cond[kMaxSolveGroups]{};
+  cudaGraphNode_t n_set[kMaxSolveGroups]{}, n_begin[kMaxSolveGroups]{}, n_a[kMaxSolveGroups]{},
+      n_b[kMaxSolveGroups]{}, n_c[kMaxSolveGroups]{};
 };
+int solve_groups(int B);  // TSF_SOLVE_GROUPS (default: 4 for B >= 1024, else 1)
 struct SolveGraphs {
   SolveGraph slot[kMaxLogL + 1][2][2];  // [log L][pc][cg]
   ~SolveGraphs();

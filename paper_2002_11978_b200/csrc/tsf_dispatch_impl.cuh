@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "tsf_dispatch.h"
@@ -76,76 +77,128 @@ cudaKernelNodeParams knode(K kernel, dim3 grid, dim3 block, int smem, void** arg
   return p;
 }
 
+// Instance group [o, o + Bg) of a level solve: every per-instance pointer
+// offset, its own active counter (a.active + g).
+inline KrylovArgs group_args(const KrylovArgs& a, int N, int o, int Bg, int g) {
+  KrylovArgs r = a;
+  const long vo = (long)o * a.n;
+  r.B = Bg;
+  r.rhs = a.rhs + vo;
+  r.x = a.x + vo;
+  if (a.kappa) r.kappa = a.kappa + vo;
+  if (a.kmodes) r.kmodes = a.kmodes + (long)o * a.kb_stride;
+  if (a.kwork) r.kwork = a.kwork + vo;
+  r.r = a.r + vo;
+  r.p = a.p + vo;
+  r.v = a.v + vo;
+  r.ph = a.ph + vo;
+  r.s = a.s + vo;
+  r.sh = a.sh + vo;
+  r.t = a.t + vo;
+  if (a.pspec) r.pspec = a.pspec + vo;
+  if (a.hspec) r.hspec = a.hspec + (long)o * (N / 2 + 1);
+  r.kst = a.kst + o;
+  r.active = a.active + g;
+  r.iters = a.iters + o;
+  r.relres = a.relres + o;
+  r.status = a.status + o;
+  return r;
+}
+
+// The level solve as one graph launch of G independent branches over
+// contiguous instance groups.  With one branch, the level's tail (a few
+// slow instances, ~30-40 us per phase launch) leaves the GPU nearly idle;
+// with G branches the other groups' full launches fill it (measured on
+// configs[2] with G separate marches on G streams: 3.7% faster at G = 4,
+// tools/group_probe.py).  Each group's instances are computed exactly as
+// with one branch (per-instance CTAs), so results do not depend on G.
 template <int N, int PC, bool CG>
 int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
   using S = KShape<N>;
   constexpr int LOG = ilog2(2 * N);
   SolveGraphs* cache = static_cast<SolveGraphs*>(a_in.graphs);
   SolveGraph& G = cache->slot[LOG][PC][CG ? 1 : 0];
-  KrylovArgs a = a_in;
-  KState* kst = a.kst;
-  int* active = a.active;
-  int bval = B;
-  void* set_args[] = {&active, &bval};
-  void* k_args[] = {&a, &kst, &active};
+  const int ng = solve_groups(B);
+  const int bg = (B + ng - 1) / ng;
+  cudaError_t e;
+  if (G.built && G.groups != ng) {
+    cudaGraphExecDestroy(G.exec);
+    cudaGraphDestroy(G.graph);
+    G = SolveGraph{};
+  }
   auto kb = k_solve_begin<N, PC, CG>;
   auto kv = k_bicg_v<N, PC>;
   auto kt = k_bicg_t<N, PC>;
   auto kc = k_cg_iter<N, PC>;
-  const cudaKernelNodeParams p_set = knode(k_set_int, dim3(1), dim3(1), 0, set_args);
-  const cudaKernelNodeParams p_begin = knode(kb, dim3(B), dim3(S::BLOCK), S::SMEM, k_args);
-  const cudaKernelNodeParams p_a = CG ? knode(kc, dim3(B), dim3(S::BLOCK), S::SMEM, k_args)
-                                      : knode(kv, dim3(B), dim3(S::BLOCK), S::SMEM, k_args);
-  const cudaKernelNodeParams p_b = knode(kt, dim3(B), dim3(S::BLOCK), S::SMEM, k_args);
-  // the loop test reads the plan's active counter, which moves when the
-  // plan's workspaces grow (ensure_reserved): its node is rewritten too
-  cudaGraphConditionalHandle h = G.cond;
-  void* c_args[] = {&h, &active};
-  cudaError_t e;
   if (!G.built) {
     if ((e = prep_kernel(kb, S::SMEM)) != cudaSuccess) return launch_error(e);
     if ((e = prep_kernel(CG ? kc : kv, S::SMEM)) != cudaSuccess) return launch_error(e);
     if (!CG && (e = prep_kernel(kt, S::SMEM)) != cudaSuccess) return launch_error(e);
     if ((e = cudaGraphCreate(&G.graph, 0)) != cudaSuccess) return launch_error(e);
-    if ((e = cudaGraphConditionalHandleCreate(&G.cond, G.graph, 1, cudaGraphCondAssignDefault)) !=
-        cudaSuccess)
-      return launch_error(e);
-    if ((e = cudaGraphAddKernelNode(&G.n_set, G.graph, nullptr, 0, &p_set)) != cudaSuccess)
-      return launch_error(e);
-    if ((e = cudaGraphAddKernelNode(&G.n_begin, G.graph, &G.n_set, 1, &p_begin)) != cudaSuccess)
-      return launch_error(e);
-    cudaGraphNodeParams cp{};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = G.cond;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t n_loop;
-    if ((e = cudaGraphAddNode(&n_loop, G.graph, &G.n_begin, 1, &cp)) != cudaSuccess)
-      return launch_error(e);
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    if ((e = cudaGraphAddKernelNode(&G.n_a, body, nullptr, 0, &p_a)) != cudaSuccess)
-      return launch_error(e);
-    cudaGraphNode_t last = G.n_a;
-    if (!CG) {
-      if ((e = cudaGraphAddKernelNode(&G.n_b, body, &G.n_a, 1, &p_b)) != cudaSuccess)
+    G.groups = ng;
+  }
+  for (int g = 0; g < ng; ++g) {
+    const int o = g * bg;
+    const int Bg = std::min(bg, B - o);
+    KrylovArgs a = group_args(a_in, N, o, Bg, g);
+    KState* kst = a.kst;
+    int* active = a.active;
+    int bval = Bg;
+    void* set_args[] = {&active, &bval};
+    void* k_args[] = {&a, &kst, &active};
+    const cudaKernelNodeParams p_set = knode(k_set_int, dim3(1), dim3(1), 0, set_args);
+    const cudaKernelNodeParams p_begin = knode(kb, dim3(Bg), dim3(S::BLOCK), S::SMEM, k_args);
+    const cudaKernelNodeParams p_a = CG ? knode(kc, dim3(Bg), dim3(S::BLOCK), S::SMEM, k_args)
+                                        : knode(kv, dim3(Bg), dim3(S::BLOCK), S::SMEM, k_args);
+    const cudaKernelNodeParams p_b = knode(kt, dim3(Bg), dim3(S::BLOCK), S::SMEM, k_args);
+    // the loop test reads the group's active counter, which moves when the
+    // plan's workspaces grow (ensure_reserved): its node is rewritten too
+    cudaGraphConditionalHandle h = G.cond[g];
+    void* c_args[] = {&h, &active};
+    if (!G.built) {
+      if ((e = cudaGraphConditionalHandleCreate(&G.cond[g], G.graph, 1,
+                                                cudaGraphCondAssignDefault)) != cudaSuccess)
         return launch_error(e);
-      last = G.n_b;
+      if ((e = cudaGraphAddKernelNode(&G.n_set[g], G.graph, nullptr, 0, &p_set)) != cudaSuccess)
+        return launch_error(e);
+      if ((e = cudaGraphAddKernelNode(&G.n_begin[g], G.graph, &G.n_set[g], 1, &p_begin)) !=
+          cudaSuccess)
+        return launch_error(e);
+      cudaGraphNodeParams cp{};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = G.cond[g];
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t n_loop;
+      if ((e = cudaGraphAddNode(&n_loop, G.graph, &G.n_begin[g], 1, &cp)) != cudaSuccess)
+        return launch_error(e);
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      if ((e = cudaGraphAddKernelNode(&G.n_a[g], body, nullptr, 0, &p_a)) != cudaSuccess)
+        return launch_error(e);
+      cudaGraphNode_t last = G.n_a[g];
+      if (!CG) {
+        if ((e = cudaGraphAddKernelNode(&G.n_b[g], body, &G.n_a[g], 1, &p_b)) != cudaSuccess)
+          return launch_error(e);
+        last = G.n_b[g];
+      }
+      h = G.cond[g];
+      const cudaKernelNodeParams p_c = knode(k_loop_cond, dim3(1), dim3(1), 0, c_args);
+      if ((e = cudaGraphAddKernelNode(&G.n_c[g], body, &last, 1, &p_c)) != cudaSuccess)
+        return launch_error(e);
+    } else {
+      if ((e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_set[g], &p_set)) != cudaSuccess ||
+          (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_begin[g], &p_begin)) != cudaSuccess ||
+          (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_a[g], &p_a)) != cudaSuccess ||
+          (!CG && (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_b[g], &p_b)) != cudaSuccess))
+        return launch_error(e);
+      const cudaKernelNodeParams p_c = knode(k_loop_cond, dim3(1), dim3(1), 0, c_args);
+      if ((e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_c[g], &p_c)) != cudaSuccess)
+        return launch_error(e);
     }
-    h = G.cond;
-    const cudaKernelNodeParams p_c = knode(k_loop_cond, dim3(1), dim3(1), 0, c_args);
-    if ((e = cudaGraphAddKernelNode(&G.n_c, body, &last, 1, &p_c)) != cudaSuccess)
-      return launch_error(e);
+  }
+  if (!G.built) {
     if ((e = cudaGraphInstantiate(&G.exec, G.graph, 0)) != cudaSuccess) return launch_error(e);
     G.built = true;
-  } else {
-    if ((e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_set, &p_set)) != cudaSuccess ||
-        (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_begin, &p_begin)) != cudaSuccess ||
-        (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_a, &p_a)) != cudaSuccess ||
-        (!CG && (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_b, &p_b)) != cudaSuccess))
-      return launch_error(e);
-    const cudaKernelNodeParams p_c = knode(k_loop_cond, dim3(1), dim3(1), 0, c_args);
-    if ((e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_c, &p_c)) != cudaSuccess)
-      return launch_error(e);
   }
   return launch_error(cudaGraphLaunch(G.exec, st));
 }
