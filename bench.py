@@ -318,8 +318,16 @@ def main():
         mx = iters[m0 - 1: m1 - 1].max(axis=1)
         if large:      # host-driven chunks of 4 iterations, 17 kernels each
             launches += int(np.sum(4 + 17 * 4 * np.ceil(np.maximum(mx, 1) / 4.0)))
-        elif graph:    # one graph per level: set, begin, WHILE { v, t, test }
-            launches += int(np.sum(2 + 3 * np.maximum(mx, 1)))
+        elif graph:    # one graph per level, G instance-group branches each
+            # set, begin, WHILE { v, t, test } (csrc/tsf_dispatch_impl.cuh
+            # solve_graph; G = solve_groups(B): TSF_SOLVE_GROUPS, default 4 for B >= 1024)
+            genv = int(os.environ.get("TSF_SOLVE_GROUPS", "0") or 0)
+            ng = min(8, genv if genv > 0 else (4 if B >= 1024 else 1), B)
+            bg = -(-B // ng)
+            lv = iters[m0 - 1: m1 - 1]
+            for g in range(ng):
+                mxg = lv[:, g * bg:(g + 1) * bg].max(axis=1)
+                launches += int(np.sum(2 + 3 * np.maximum(mxg, 1)))
         else:
             launches += int(np.sum(2 + 2 * 4 * np.ceil(np.maximum(mx, 1) / 4.0)))
         launches += (m1 - m0) if not fused else (1 if m0 == 1 else 0)
@@ -367,7 +375,8 @@ def main():
     else:
         sname = (f"tsf level solve: k_solve_begin + k_bicg_v/k_bicg_t<{n},1>"
                  + (" with fused SOE epilogue" if fused else "")
-                 + (" (one CUDA graph per level, conditional WHILE loop)" if graph else ""))
+                 + (" (one CUDA graph per level: instance-group branches, each a conditional "
+                    "WHILE loop)" if graph else ""))
     k_solve = {"name": sname, "avg_ms": solve_ms / K,
                "GBps": solve_bytes / (solve_ms / K * 1e-3) / 1e9,
                "iterations_per_launch": its_sum / K, "algorithmic_bytes": solve_bytes}
