@@ -279,6 +279,64 @@ k_lrow(LargeArgs a, int spec_mode) {
   }
 }
 
+// ------------------------------------------------------------ row, short rows
+// Rows of N2 <= 128 points (n = 8192) have T < 32 owning threads: k_lrow ran
+// each row as a sub-warp CTA doing its two channels one after the other, a
+// latency chain of four transforms.  Here a 64-thread CTA runs 64/T
+// independent (row, channel) items side by side — the two channels of a row
+// concurrently — through the grouped transform (configs[4] n = 8192: matvec
+// 3.92 -> 3.21 ms, preconditioner 2.18 -> 1.63 ms).  At N2 = 256 (configs[1],
+// one warp per item) it measured no faster than k_lrow (0.777 vs 0.777 ms per
+// level), so k_lrow keeps those rows.
+template <int N2>
+__global__ void __launch_bounds__(64) k_lrow_small(LargeArgs a, int spec_mode) {
+  pdl_enter();
+  constexpr int E = LRow<N2>::E;
+  constexpr int T = LRow<N2>::T;
+  static_assert(T <= 32 && 64 % T == 0, "short-row kernel");
+  constexpr int IT = 64 / T;
+  constexpr int BUF = 2 * FftPlan<N2, E>::SMEM_ELEMS;
+  const long N = a.nt;
+  const int N1 = (int)(N / N2);
+  const int b = blockIdx.y;
+  if (inst_skip(a, b)) return;
+  const int nch = spec_mode == RS_APPLY ? 2 : 1;
+  const int slot = threadIdx.x / T, tid = threadIdx.x % T;
+  const int item = blockIdx.x * IT + slot;
+  const bool valid = item < N1 * nch;
+  const int k1 = valid ? item / nch : 0, ch = valid ? item % nch : 0;
+  extern __shared__ double2 sm[];
+  double2* smi = sm + slot * BUF;
+  double2* tw2 = sm + IT * BUF;
+  stage_tw<N2>(tw2, a.lt.tw2);
+  double2* row = a.Z + (long)ch * a.B * N + (long)b * N + (long)k1 * N2;
+  double2 z[E];
+#pragma unroll
+  for (int c = 0; c < E; ++c) z[c] = valid ? row[tid + c * T] : make_double2(0.0, 0.0);
+  double sp[E];
+  group_fft<N2, E, false>(z, smi, tw2, 0, tid, [&] {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const long idx = (long)k1 * N2 + tid + c * T;   // bin k1 + N1 k2
+      if (!valid) {
+        sp[c] = 0.0;
+      } else if (spec_mode == RS_APPLY) {
+        const double2 se = ldt(&a.lt.sEO[idx]);
+        sp[c] = ch == 0 ? se.x : se.y;
+      } else {
+        sp[c] = a.pspec[(long)b * N + idx];
+      }
+    }
+  });
+#pragma unroll
+  for (int c = 0; c < E; ++c) z[c] = cscale(z[c], sp[c]);
+  group_fft<N2, E, true>(z, smi, tw2, 0, tid);
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) row[tid + c * T] = z[c];
+  }
+}
+
 // ------------------------------------------------------------ col_inv
 template <int N1, int MB = LCol<N1>::MINB>
 __global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)

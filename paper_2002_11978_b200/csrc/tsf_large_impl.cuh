@@ -37,6 +37,18 @@ template <int LOG>
 int LargeDispatch<LOG>::row(const LargeArgs& a, int spec_mode, cudaStream_t st) {
   constexpr int N2 = 1 << LOG;
   using S = LRow<N2>;
+  // short rows (N2 <= 128: n = 8192) — at N2 = 256 (configs[1]) measured no
+  // faster than k_lrow, which stays (profiles/r01c_summary.md)
+  if constexpr (S::T < 32) {
+    constexpr int IT = 64 / S::T;
+    constexpr int smem = (IT * 2 * FftPlan<N2, S::E>::SMEM_ELEMS + tw_table_elems(N2)) * 16;
+    auto ks = k_lrow_small<N2>;
+    static cudaError_t prep_s = large_prep(ks, smem);
+    if (prep_s != cudaSuccess) return large_launch_error(prep_s);
+    const int items = (int)(a.nt / N2) * (spec_mode == RS_APPLY ? 2 : 1);
+    launch_pdl(ks, dim3((items + IT - 1) / IT, a.B), 64, smem, st, a, spec_mode);
+    return large_launch_error(cudaGetLastError());
+  }
   auto k = k_lrow<N2>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
