@@ -325,17 +325,98 @@ def _cfg1_one(ga):
     return its, hist[-1], hist[64]
 
 
+# Acceptance-gate runs (pkg/tests/test_acceptance.py:38-166): every scheme
+# configuration of criteria 1-7 with the reference's own err_inf / average
+# iterations / final level, plus the manufactured-problem functions
+# (pkg/src/tsfrac/problems.py) tabulated for tests/test_problems.py.
+ACCEPTANCE_RUNS = [
+    # label, scheme, case, alpha, gamma, r, mu, M or None, N or None, q, eps, solver, tol
+    ("c1_M128", "both", "example1", 1.5, 0.5, 2, None, 2 ** 7, None, 2, 1e-10, "auto", 1e-10),
+    ("c1_M256", "both", "example1", 1.5, 0.5, 2, None, 2 ** 8, None, 2, 1e-10, "auto", 1e-10),
+    ("c1_M512", "both", "example1", 1.5, 0.5, 2, None, 2 ** 9, None, 2, 1e-10, "auto", 1e-10),
+    ("c1_M1024", "both", "example1", 1.5, 0.5, 2, None, 2 ** 10, None, 2, 1e-10, "auto", 1e-10),
+    ("c2_M512", "dids", "example1", 1.6, 0.8, 3, 2.0, 2 ** 9, None, 2, 1e-10, "auto", 1e-10),
+    ("c2_M1024", "dids", "example1", 1.6, 0.8, 3, 2.0, 2 ** 10, None, 2, 1e-10, "auto", 1e-10),
+    ("c3_N8", "dids", "example1", 1.5, 0.8, 1, None, None, 8, 2, 1e-10, "auto", 1e-10),
+    ("c3_N16", "dids", "example1", 1.5, 0.8, 1, None, None, 16, 2, 1e-10, "auto", 1e-10),
+    ("c3_N32", "dids", "example1", 1.5, 0.8, 1, None, None, 32, 2, 1e-10, "auto", 1e-10),
+    ("c3_N64", "dids", "example1", 1.5, 0.8, 1, None, None, 64, 2, 1e-10, "auto", 1e-10),
+    ("c4_N9", "dids", "example2", 1.9, 0.8, 3, None, None, 9, 1.95, 1e-10, "auto", 1e-10),
+    ("c4_N18", "dids", "example2", 1.9, 0.8, 3, None, None, 18, 1.95, 1e-10, "auto", 1e-10),
+    ("c4_N36", "dids", "example2", 1.9, 0.8, 3, None, None, 36, 1.95, 1e-10, "auto", 1e-10),
+    ("c4_N72", "dids", "example2", 1.9, 0.8, 3, None, None, 72, 1.95, 1e-10, "auto", 1e-10),
+    ("c5_N256", "fids", "example2", 0.5, 0.5, 2, None, None, 2 ** 8, 1.25, 1e-9, "auto", 1e-10),
+    ("c5_N512", "fids", "example2", 0.5, 0.5, 2, None, None, 2 ** 9, 1.25, 1e-9, "auto", 1e-10),
+    ("c6_plain_N256", "fids", "example2", 1.9, 0.5, 2, None, None, 2 ** 8, 1.95, 1e-9, "krylov", 1e-10),
+    ("c6_prec_N64", "fids", "example2", 1.9, 0.5, 2, None, None, 2 ** 6, 1.95, 1e-9, "pkrylov", 1e-10),
+    ("c6_prec_N128", "fids", "example2", 1.9, 0.5, 2, None, None, 2 ** 7, 1.95, 1e-9, "pkrylov", 1e-10),
+    ("c6_prec_N256", "fids", "example2", 1.9, 0.5, 2, None, None, 2 ** 8, 1.95, 1e-9, "pkrylov", 1e-10),
+]
+
+
+def gen_acceptance(tsfrac):
+    import time
+
+    from tsfrac.couplings import m_from_n, n_from_m
+    from tsfrac.problems import make_case
+    from tsfrac.scheme import SolverOptions, run_dids, run_fids
+
+    out = {}
+    xs = np.concatenate([np.linspace(-1.0, 1.0, 41), [-0.999, 0.3333, 0.999]])
+    for i, (name, a, g) in enumerate([("example1", 1.5, 0.5), ("example1", 1.6, 0.8),
+                                      ("example2", 1.9, 0.8), ("example2", 0.5, 0.5),
+                                      ("example1", 1.5, 0.8), ("example2", 1.9, 0.5)]):
+        case = make_case(name, a, g)
+        out[f"fn{i}_args"] = np.array([a, g, case.s])
+        out[f"fn{i}_name"] = np.array(name)
+        out[f"fn{i}_x"] = xs
+        out[f"fn{i}_initial"] = case.spec.initial(xs)
+        for j, t in enumerate((0.0, 0.37, 1.0)):
+            out[f"fn{i}_source_t{j}"] = case.spec.source(xs, t)
+            out[f"fn{i}_exact_t{j}"] = case.spec.exact(xs, t)
+            out[f"fn{i}_kappa_t{j}"] = case.spec.kappa(xs, t)
+    labels = []
+    for (label, scheme, name, a, g, r, mu, M, N, q, eps, solver, tol) in ACCEPTANCE_RUNS:
+        if N is None:
+            N = n_from_m(M, r, g, q)
+        else:
+            M = m_from_n(N, r, g, q)
+        case = make_case(name, a, g)
+        opts = SolverOptions(solver=solver, tol=tol)
+        t0 = time.perf_counter()
+        row = [M, N, np.nan, np.nan, np.nan, np.nan]
+        if scheme in ("dids", "both"):
+            h, rep = run_dids(case.spec, M, r, N, mu=mu, options=opts)
+            row[2] = rep.err_inf
+            out[f"acc_{label}_dids_uM"] = h[-1]
+        if scheme in ("fids", "both"):
+            with Recorder(tsfrac.scheme) as rec:
+                h, rep = run_fids(case.spec, M, r, N, epsilon=eps, mu=mu, options=opts)
+            row[3] = rep.err_inf
+            row[4] = rep.avg_iterations
+            out[f"acc_{label}_fids_uM"] = h[-1]
+            if rec.its:
+                out[f"acc_{label}_fids_its"] = np.array(rec.its, dtype=np.int64)
+        row[5] = time.perf_counter() - t0
+        out[f"acc_{label}"] = np.array(row, dtype=float)
+        labels.append(label)
+        print(label, row, flush=True)
+    out["acc_labels"] = np.array(labels)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run cfg1 (minutes)")
     ap.add_argument("--only", default="", help="comma list of fixtures to regenerate "
-                    "(setup,linalg,march,dids,cfg1,cfg2); default all but cfg1/cfg2")
+                    "(setup,linalg,march,dids,cfg1,cfg2,acceptance); default all but cfg1/cfg2")
     args = ap.parse_args()
     tsfrac = _import_reference()
     OUT.mkdir(parents=True, exist_ok=True)
     if args.only:
         gens = {"setup": gen_setup, "linalg": gen_linear_algebra, "march": gen_marches,
-                "dids": gen_dids, "cfg1": gen_big, "cfg2": gen_cfg2}
+                "dids": gen_dids, "cfg1": gen_big, "cfg2": gen_cfg2,
+                "acceptance": gen_acceptance}
         for name in args.only.split(","):
             np.savez_compressed(OUT / f"{name}.npz", **gens[name](tsfrac))
             print(name, (OUT / f"{name}.npz").stat().st_size)
