@@ -16,11 +16,13 @@ OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/tsfrac_b200.h
 LIB := $(if $(VARIANT),build/$(VARIANT)/libtsfrac_b200.so,$(PKG)/libtsfrac_b200.so)
 L13_FLAGS ?=
+INST_FLAGS ?=
 LARGE_FLAGS ?=
 
 all: $(LIB)
 
 $(OBJDIR)/gen/inst_L13.o: NVFLAGS += $(L13_FLAGS)
+$(OBJDIR)/gen/inst_%.o: NVFLAGS += $(INST_FLAGS)
 $(OBJDIR)/gen/large_%.o $(OBJDIR)/tsf_large.o: NVFLAGS += $(LARGE_FLAGS)
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
