@@ -242,6 +242,10 @@ def main():
         kap = P.SeparableField([np.ones(n), 0.5 * np.sin(np.pi * x)], lambda t: [1.0, math.exp(-t)])
         src = P.SeparableField([np.sin(np.pi * x)], lambda t: [1.0 + t])
         u0 = np.repeat(((1.0 - x * x) ** 2)[None, :], B, axis=0)
+        if args.workload == "cfg3" and (world > 1 or B > 1):
+            # configs[3] as seeded copies: phi * U_b per global copy (workloads.copy_scales)
+            from paper_2002_11978_b200 import workloads as WL
+            u0 = u0 * WL.copy_scales(rank * B, B)[:, None]
         kmodes = fmodes = None
     mesh = P.build_mesh(M, r, 1.0)
     soe = P.build_soe(gam, wl["eps"], (1.0 / M) ** r, 1.0)
@@ -517,7 +521,9 @@ def main():
                        "levels_timed": [list(v) for v in levels_done],
                        "avg_iterations": its_sum / (K * B),
                        "l2": "inputs larger than L2: W is %.1f GB per GPU" % (B * nexp * n * 8 / 1e9),
-                       "parallelism": f"instances sharded over {world} GPU(s), no collectives"},
+                       "parallelism": f"instances sharded over {world} GPU(s), no collectives"}
+            | ({"copies": "phi * U_b, U_b ~ U[0.5, 2] per global copy (workloads.copy_scales)"}
+               if args.workload == "cfg3" and (world > 1 or B > 1) else {}),
             "roofline": roof,
             "kernels": {"soe_push_rhs": k_soe, "level_solve": k_solve},
             "toeplitz_matvec": mv,

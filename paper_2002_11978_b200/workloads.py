@@ -7,6 +7,11 @@ index b,
     kappa  = exp(0.4 g(x)) * (1 + 0.2 t)
     f      = (sum_{k=1..8} c_k sin(k pi (x+1)/2)) * (1 + t),    c_k ~ N(0, 1/k^2)
     phi    = (1 - x^2)^2 * U,                                   U ~ U[0.5, 2]
+configs[3] copies: when configs[3] runs as several
+instances (8 seeded copies over 8 GPUs, or a batch on one), copy b is the
+configs[0]-style problem with phi scaled by U_b ~ U[0.5, 2] drawn from
+default_rng([seed, 3, b]) (`copy_scales`); the single-instance config keeps
+U = 1.
 Instances are sharded across ranks in contiguous blocks; the fields of an
 instance depend only on its global index, so any sharding reproduces the
 same per-instance problems (checked by tests/test_shard_gloo.py).  The time
@@ -61,6 +66,12 @@ def instance_fields(n: int, b0: int, B: int, seed: int = SEED):
     fx = Cc @ sin_f
     u0 = (1.0 - x * x) ** 2 * U[:, None]
     return x, kx, fx, u0
+
+
+def copy_scales(b0: int, B: int, seed: int = SEED) -> np.ndarray:
+    """U_b ~ U[0.5, 2] of the configs[3] seeded copies b0 .. b0+B-1 (global indices)."""
+    return np.array([np.random.default_rng([seed, 3, b0 + i]).uniform(0.5, 2.0)
+                     for i in range(B)])
 
 
 def kappa_t(t: float) -> float:

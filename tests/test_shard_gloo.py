@@ -70,6 +70,13 @@ def test_instance_fields_independent_of_sharding():
     np.testing.assert_array_equal(u_all[3:], u_b)
 
 
+def test_cfg3_copy_scales_independent_of_sharding():
+    all8 = WL.copy_scales(0, 8)
+    assert np.all((all8 >= 0.5) & (all8 <= 2.0)) and np.unique(all8).size == 8
+    for r in range(8):   # one copy per rank over 8 GPUs == the batched 8 copies
+        np.testing.assert_array_equal(WL.copy_scales(r, 1), all8[r:r + 1])
+
+
 def test_two_rank_gloo_shard_and_gather_matches_single_process():
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
