@@ -178,3 +178,24 @@ def test_criterion_07_fids_dids_proximity():
         h_f, _ = run_fids(case.spec, M, r, N, epsilon=eps, mu=mu)
         diff = float(np.max(np.abs(np.asarray(h_d) - np.asarray(h_f))))
         assert diff <= 100.0 * eps, f"{name} M={M} N={N}: {diff:.2e}"
+
+
+def test_foreign_problem_spec_is_accepted():
+    """A spec object of another package (the reference's own ProblemSpec) works:
+    the drivers read its fields by name (CLI backend switch)."""
+    from types import SimpleNamespace
+
+    case = make_case("example1", 1.5, 0.5)
+    sp = case.spec
+    foreign = SimpleNamespace(gamma=sp.gamma, alpha=sp.alpha, l=sp.l, T=sp.T, kappa=sp.kappa,
+                              source=sp.source, initial=sp.initial, exact=sp.exact,
+                              kappa_x_independent=False)
+    M = 2 ** 7
+    N = n_from_m(M, 2, 0.5, 2)
+    h0, r0 = run_fids(sp, M, 2, N, epsilon=1e-10)
+    h1, r1 = run_fids(foreign, M, 2, N, epsilon=1e-10)
+    np.testing.assert_array_equal(np.asarray(h0), np.asarray(h1))
+    assert r0.err_inf == r1.err_inf
+    _, d0 = run_dids(sp, M, 2, N)
+    _, d1 = run_dids(foreign, M, 2, N)
+    assert d0.err_inf == d1.err_inf
