@@ -155,16 +155,30 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_xr(LargeArgs a, const doubl
   }
   Vals<2> v;
   v.v[0] = v.v[1] = 0.0;
+  // all operands loaded before the first store (the vectors may alias, so a
+  // store would otherwise hold back the next element's loads)
+  double xv[kLelPer], pv[kLelPer], sv[kLelPer], ssv[kLelPer], tv[kLelPer], r0v[kLelPer];
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const long j = off + (jj < a.n ? jj : 0);
+    xv[c] = a.x[j];
+    pv[c] = ph[j];
+    sv[c] = sh[j];
+    ssv[c] = a.s[j];
+    tv[c] = a.t[j];
+    r0v[c] = a.r0[j];
+  }
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
     const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
     if (jj >= a.n) break;
     const long j = off + jj;
-    a.x[j] = a.x[j] + (s.alpha * ph[j] + s.omega * sh[j]);
-    const double r = a.s[j] - s.omega * a.t[j];
+    a.x[j] = xv[c] + (s.alpha * pv[c] + s.omega * sv[c]);
+    const double r = ssv[c] - s.omega * tv[c];
     a.r[j] = r;
     v.v[0] = fma(r, r, v.v[0]);
-    v.v[1] = fma(a.r0[j], r, v.v[1]);
+    v.v[1] = fma(r0v[c], r, v.v[1]);
   }
   v = block_sum<2>(v, red);
   if (tid == 0) {

@@ -162,6 +162,24 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   double2 z[E];
   double part = 0.0;
   const LState stv = a.st ? a.st[b] : LState{};
+  // Every operand is loaded before the first store: the vectors are plain
+  // pointers that may alias, so a store between two elements' loads kept
+  // the compiler from issuing the next element's loads early and serialised
+  // E memory latencies per thread (ncu, configs[3]: 65% of this kernel's
+  // stall samples were long-scoreboard waits on these loads).
+  const bool pupd_it1 = in_mode == CI_PUPD && stv.it == 1;
+  const double* l0p = in_mode == CI_PUPD ? (pupd_it1 ? a.r0 : a.r)
+                      : in_mode == CI_SUPD ? (stv.it == 1 ? a.r0 : a.r) : src;
+  double l0[E], l1[E], l2[E];
+#pragma unroll
+  for (int c = 0; c < E; ++c) {
+    const long j = (long)N2 * (tid + c * T) + t2;
+    const bool in = j < a.n;   // zero padding up to the transform length
+    l0[c] = in ? l0p[off + j] : 0.0;
+    l1[c] = (in && ((in_mode == CI_PUPD && !pupd_it1) || in_mode == CI_SUPD))
+                ? (in_mode == CI_PUPD ? a.p[off + j] : a.v[off + j]) : 0.0;
+    l2[c] = (in && in_mode == CI_PUPD && !pupd_it1) ? a.v[off + j] : 0.0;
+  }
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const long j = (long)N2 * (tid + c * T) + t2;
@@ -169,20 +187,19 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
     if (j >= a.n) {
       // zero padding up to the transform length
     } else if (in_mode == CI_PUPD) {
-      if (stv.it == 1) {
-        val = a.r0[off + j];
+      if (pupd_it1) {
+        val = l0[c];
       } else {
         const double beta = (stv.rho_new / stv.rho) * (stv.alpha / stv.omega);
-        val = a.r[off + j] + beta * (a.p[off + j] - stv.omega * a.v[off + j]);
+        val = l0[c] + beta * (l1[c] - stv.omega * l2[c]);
       }
       a.p[off + j] = val;
     } else if (in_mode == CI_SUPD) {
-      const double* rc = (stv.it == 1) ? a.r0 : a.r;
-      val = rc[off + j] - stv.alpha * a.v[off + j];
+      val = l0[c] - stv.alpha * l1[c];
       a.s[off + j] = val;
       part = fma(val, val, part);
     } else {
-      val = src[off + j];
+      val = l0[c];
     }
     xr[c] = val;
   }
@@ -191,11 +208,14 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
     if (threadIdx.x == 0) a.part[((long)b * 4 + 2) * a.np + blockIdx.x] = part;
   }
   group_fft_real<N1, E>(xr, z, smg, tw1, 0, tid);
+  // inter-pass twiddles loaded before the stores (aliasing, see above)
+  double2 wt[E];
+#pragma unroll
+  for (int c = 0; c < E; ++c) wt[c] = tw_get_g(a.lt.twN, ((long)t2 * (tid + c * T)) & (N - 1));
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const int k1 = tid + c * T;
-    const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
-    a.Z[offz + (long)k1 * N2 + t2] = cmul(z[c], w);
+    a.Z[offz + (long)k1 * N2 + t2] = cmul(z[c], wt[c]);
   }
   if (in_mode == CI_APPLY) {
     // odd channel: the modulated input x_j W_L^j
@@ -209,8 +229,7 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int k1 = tid + c * T;
-      const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
-      Zo[offz + (long)k1 * N2 + t2] = cmul(z[c], w);
+      Zo[offz + (long)k1 * N2 + t2] = cmul(z[c], wt[c]);   // same k1 -> same twiddle
     }
   }
 }
@@ -388,16 +407,34 @@ k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __
   group_fft<N1, E, true>(z, smg, tw1, 0, tid);
   Vals<2> pr;
   pr.v[0] = pr.v[1] = 0.0;
+  // epilogue operands loaded before the stores, half the slots at a time
+  // (aliasing, see k_lcol_fwd; all at once would exceed the register cap)
+  constexpr int H = E > 1 ? E / 2 : 1;
 #pragma unroll
-  for (int c = 0; c < E; ++c) {
-    const long j = (long)N2 * (tid + c * T) + t2;
-    if (j >= a.n) continue;
-    const double2 w = tw_get_g(a.lt.twL, j);
-    const double ax = ye[c] + fma(z[c].x, w.x, z[c].y * w.y);  // + Re(conj(w) z)
-    const double y = a.kappa ? fma(a.shift, xin[off + j], a.kappa[off + j] * ax) : ax;
-    dst[off + j] = y;
-    pr.v[0] = fma(y, y, pr.v[0]);
-    if (w1) pr.v[1] = fma(y, w1[off + j], pr.v[1]);
+  for (int c0 = 0; c0 < E; c0 += H) {
+    double2 wm[H];
+    double xv[H], kv[H], w1v[H];
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+      const long j = (long)N2 * (tid + (c0 + q) * T) + t2;
+      const bool in = j < a.n;
+      wm[q] = in ? tw_get_g(a.lt.twL, j) : make_double2(0.0, 0.0);
+      xv[q] = (in && a.kappa) ? xin[off + j] : 0.0;
+      kv[q] = (in && a.kappa) ? a.kappa[off + j] : 0.0;
+      w1v[q] = (in && w1) ? w1[off + j] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+      const int c = c0 + q;
+      const long j = (long)N2 * (tid + c * T) + t2;
+      if (j >= a.n) continue;
+      const double2 w = wm[q];
+      const double ax = ye[c] + fma(z[c].x, w.x, z[c].y * w.y);  // + Re(conj(w) z)
+      const double y = a.kappa ? fma(a.shift, xv[q], kv[q] * ax) : ax;
+      dst[off + j] = y;
+      pr.v[0] = fma(y, y, pr.v[0]);
+      if (w1) pr.v[1] = fma(y, w1v[q], pr.v[1]);
+    }
   }
   if (pslot >= 0) {
     pr = block_sum<2>(pr, red);
