@@ -101,12 +101,21 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_pupd(LargeArgs a) {
   const long off = (long)b * a.n;
   const LState s = a.st[b];
   const double beta = s.it == 1 ? 0.0 : (s.rho_new / s.rho) * (s.alpha / s.omega);
+  // operands loaded before the stores (aliasing pointers, see k_lcol_fwd)
+  double rv[kLelPer], pv[kLelPer], vv[kLelPer];
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const long j = off + (jj < a.n ? jj : 0);
+    rv[c] = s.it == 1 ? a.r0[j] : a.r[j];
+    pv[c] = s.it == 1 ? 0.0 : a.p[j];
+    vv[c] = s.it == 1 ? 0.0 : a.v[j];
+  }
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
     const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
     if (jj >= a.n) break;
-    const long j = off + jj;
-    a.p[j] = s.it == 1 ? a.r0[j] : a.r[j] + beta * (a.p[j] - s.omega * a.v[j]);
+    a.p[off + jj] = s.it == 1 ? rv[c] : rv[c] + beta * (pv[c] - s.omega * vv[c]);
   }
 }
 
@@ -120,13 +129,20 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_supd(LargeArgs a) {
   const LState s = a.st[b];
   const double* rc = s.it == 1 ? a.r0 : a.r;
   double ss = 0.0;
+  double rv[kLelPer], vv[kLelPer];   // loads before the stores (see k_lel_pupd)
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const long j = off + (jj < a.n ? jj : 0);
+    rv[c] = rc[j];
+    vv[c] = a.v[j];
+  }
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
     const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
     if (jj >= a.n) break;
-    const long j = off + jj;
-    const double v = rc[j] - s.alpha * a.v[j];
-    a.s[j] = v;
+    const double v = rv[c] - s.alpha * vv[c];
+    a.s[off + jj] = v;
     ss = fma(v, v, ss);
   }
   ss = block_sum1(ss, red);
@@ -257,13 +273,23 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_cgxr(LargeArgs a) {
   const long off = (long)b * a.n;
   const double al = a.st[b].alpha;
   double rr = 0.0;
+  double xv[kLelPer], pv[kLelPer], rv[kLelPer], vv[kLelPer];   // loads before the stores
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const long j = off + (jj < a.n ? jj : 0);
+    xv[c] = a.x[j];
+    pv[c] = a.p[j];
+    rv[c] = a.r[j];
+    vv[c] = a.v[j];
+  }
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
     const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
     if (jj >= a.n) break;
     const long j = off + jj;
-    a.x[j] = a.x[j] + al * a.p[j];
-    const double r = a.r[j] - al * a.v[j];
+    a.x[j] = xv[c] + al * pv[c];
+    const double r = rv[c] - al * vv[c];
     a.r[j] = r;
     rr = fma(r, r, rr);
   }
@@ -278,12 +304,19 @@ __global__ void __launch_bounds__(kLelThreads) k_lel_cgp(LargeArgs a, const doub
   if (inst_skip(a, b)) return;
   const long off = (long)b * a.n;
   const double beta = a.st[b].omega;   // PCG keeps beta in the omega slot
+  double zv[kLelPer], pv[kLelPer];     // loads before the stores (see k_lel_pupd)
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    const long j = off + (jj < a.n ? jj : 0);
+    zv[c] = z[j];
+    pv[c] = a.p[j];
+  }
 #pragma unroll
   for (int c = 0; c < kLelPer; ++c) {
     const long jj = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
     if (jj >= a.n) break;
-    const long j = off + jj;
-    a.p[j] = z[j] + beta * a.p[j];
+    a.p[off + jj] = zv[c] + beta * pv[c];
   }
 }
 
