@@ -150,36 +150,45 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
   const int b = blockIdx.y;
-  if (inst_skip(a, b)) return;
   const int g = threadIdx.x % G, tid = threadIdx.x / G;
   const int t2 = blockIdx.x * G + g;
   double2* smg = sm + g * C::BUF;
   double2* tw1 = sm + G * C::BUF;
-  stage_tw<N1>(tw1, a.lt.tw1);
   const long off = (long)b * a.n;   // vectors [B][n]
   const long offz = (long)b * N;    // transform work [B][nt]
   double xr[E];
   double2 z[E];
   double part = 0.0;
-  const LState stv = a.st ? a.st[b] : LState{};
   // Every operand is loaded before the first store: the vectors are plain
   // pointers that may alias, so a store between two elements' loads kept
   // the compiler from issuing the next element's loads early and serialised
   // E memory latencies per thread (ncu, configs[3]: 65% of this kernel's
   // stall samples were long-scoreboard waits on these loads).
-  const bool pupd_it1 = in_mode == CI_PUPD && stv.it == 1;
-  const double* l0p = in_mode == CI_PUPD ? (pupd_it1 ? a.r0 : a.r)
-                      : in_mode == CI_SUPD ? (stv.it == 1 ? a.r0 : a.r) : src;
+  // The loads are also issued before the instance state arrives: they
+  // assume iteration > 1 (r, p, v) and the first iteration re-reads r0; a
+  // finished instance's CTA loads its (valid, unused) vectors and returns.
+  const bool upd = in_mode == CI_PUPD || in_mode == CI_SUPD;
+  const double* l0p = upd ? a.r : src;
   double l0[E], l1[E], l2[E];
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const long j = (long)N2 * (tid + c * T) + t2;
     const bool in = j < a.n;   // zero padding up to the transform length
     l0[c] = in ? l0p[off + j] : 0.0;
-    l1[c] = (in && ((in_mode == CI_PUPD && !pupd_it1) || in_mode == CI_SUPD))
-                ? (in_mode == CI_PUPD ? a.p[off + j] : a.v[off + j]) : 0.0;
-    l2[c] = (in && in_mode == CI_PUPD && !pupd_it1) ? a.v[off + j] : 0.0;
+    l1[c] = (in && upd) ? (in_mode == CI_PUPD ? a.p[off + j] : a.v[off + j]) : 0.0;
+    l2[c] = (in && in_mode == CI_PUPD) ? a.v[off + j] : 0.0;
   }
+  if (inst_skip(a, b)) return;
+  const LState stv = a.st ? a.st[b] : LState{};
+  const bool pupd_it1 = in_mode == CI_PUPD && stv.it == 1;
+  if (upd && stv.it == 1) {   // krylov.py:114-116: the first p (and s) start from r0
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const long j = (long)N2 * (tid + c * T) + t2;
+      l0[c] = j < a.n ? a.r0[off + j] : 0.0;
+    }
+  }
+  stage_tw<N1>(tw1, a.lt.tw1);
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const long j = (long)N2 * (tid + c * T) + t2;
