@@ -113,22 +113,19 @@ class ClockSampler:
 
 # --------------------------------------------------------------------- CPU
 def _cpu_worker(args):
-    """One instance of the workload through the oracle port; returns the
-    wall time of levels (warmup, warmup+K]."""
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    wl, b, warmup, K = args
+    """Instances of the workload through the oracle port, one after another
+    in this process; returns (wall seconds of levels (warmup, warmup+K] summed
+    over the instances, iterations).  Runs in a SPAWNED process whose
+    environment pins OpenBLAS/OpenMP to one thread before numpy loads
+    (cpu_measure); threadpoolctl re-asserts it."""
+    wl, bs, warmup, K = args
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
     import oracle as O
     n = wl["n"]
-    if wl.get("cfg2", True):
-        from paper_2002_11978_b200 import workloads as WL
-        x, kx, fx, u0 = WL.instance_fields(n, b, 1)
-        kf = lambda xx, t: kx[0] * (1.0 + 0.2 * t)  # noqa: E731
-        sf = lambda xx, t: fx[0] * (1.0 + t)  # noqa: E731
-        phi = u0[0]
-    else:
-        kf = lambda xx, t: 1.0 + 0.5 * np.sin(np.pi * xx) * np.exp(-t)  # noqa: E731
-        sf = lambda xx, t: (1.0 + t) * np.sin(np.pi * xx)  # noqa: E731
-        phi = (1.0 - cfg0_fields(n) ** 2) ** 2
     gam, alpha, M = wl["gamma"], wl["alpha"], wl["M"]
     r = (2.0 - gam) / gam
     N = n + 1
@@ -139,30 +136,132 @@ def _cpu_worker(args):
     lam = O.strang_eigs(col)
     G = math.exp(math.lgamma(1.0 - gam))
     s, w = O.soe_build(gam, wl["eps"], (1.0 / M) ** r, 1.0)
-    u = np.asarray(phi, dtype=float)
-    W = np.zeros((s.size, n))
-    t0 = None
+    wall = 0.0
     its = 0
-    for m in range(1, min(M, warmup + K) + 1):
-        if m == warmup + 1:
-            t0 = time.perf_counter()
-        kap = kf(xx, t[m])
-        f = sf(xx, t[m])
-        u, _, out = O.fids_step(u, W, s, w, tau[m - 1], gam, G, kap, f, symbol, lam, wl["tol"])
-        if m > warmup:
-            its += out.iterations
-    return time.perf_counter() - t0, its
+    for b in bs:
+        if wl.get("cfg2", True):
+            from paper_2002_11978_b200 import workloads as WL
+            x, kx, fx, u0 = WL.instance_fields(n, b, 1)
+            kf = lambda xx, t, k=kx[0]: k * (1.0 + 0.2 * t)  # noqa: E731
+            sf = lambda xx, t, f=fx[0]: f * (1.0 + t)  # noqa: E731
+            phi = u0[0]
+        else:
+            kf = lambda xx, t: 1.0 + 0.5 * np.sin(np.pi * xx) * np.exp(-t)  # noqa: E731
+            sf = lambda xx, t: (1.0 + t) * np.sin(np.pi * xx)  # noqa: E731
+            phi = (1.0 - cfg0_fields(n) ** 2) ** 2
+        u = np.asarray(phi, dtype=float)
+        W = np.zeros((s.size, n))
+        t0 = None
+        for m in range(1, min(M, warmup + K) + 1):
+            if m == warmup + 1:
+                t0 = time.perf_counter()
+            kap = kf(xx, t[m])
+            f = sf(xx, t[m])
+            u, _, out = O.fids_step(u, W, s, w, tau[m - 1], gam, G, kap, f, symbol, lam,
+                                    wl["tol"])
+            if m > warmup:
+                its += out.iterations
+        wall += time.perf_counter() - t0
+    return wall, its
 
 
-def cpu_measure(wl, warmup, K, workers, cfg2=True):
+def host_info():
+    """CPU model, core count and the numpy/scipy/BLAS versions of this host."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    info["numpy"] = np.__version__
+    try:
+        import scipy
+        info["scipy"] = scipy.__version__
+    except Exception:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [d for d in threadpool_info() if d.get("user_api") == "blas"]
+        if blas:
+            info["blas"] = f"{blas[0].get('internal_api')} {blas[0].get('version')}"
+    except Exception:
+        pass
+    return info
+
+
+def cpu_measure(wl, warmup, K, workers, instances, cfg2=True):
+    """Time `instances` instances (cfg2) or the single instance over `workers`
+    spawned processes, each at ONE BLAS/OpenMP thread (set in the environment
+    the children start with, so OpenBLAS sizes its pool to 1 before numpy
+    loads).  value = instances * n * K / wall of the whole pool."""
+    import multiprocessing as mp
     from concurrent.futures import ProcessPoolExecutor
     wl = dict(wl, cfg2=cfg2)
     K = min(K, wl["M"] - warmup)
-    with ProcessPoolExecutor(max_workers=workers) as ex:
-        res = list(ex.map(_cpu_worker, [(wl, b, warmup, K) for b in range(workers)]))
-    wall = max(r[0] for r in res)
-    value = workers * wl["n"] * K / wall
-    return value, wall, K, sum(r[1] for r in res) / (workers * K)
+    if not cfg2:
+        instances, workers = 1, 1
+    workers = max(1, min(workers, instances))
+    chunks = [list(range(i, instances, workers)) for i in range(workers)]
+    saved = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS",
+                                            "MKL_NUM_THREADS")}
+    for k in saved:
+        os.environ[k] = "1"
+    try:
+        with ProcessPoolExecutor(max_workers=workers,
+                                 mp_context=mp.get_context("spawn")) as ex:
+            list(ex.map(_cpu_worker, [(wl, [], 0, 1)] * workers))   # start-up, imports
+            t0 = time.perf_counter()
+            res = list(ex.map(_cpu_worker, [(wl, c, warmup, K) for c in chunks]))
+            wall = time.perf_counter() - t0
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    # wall of the pool includes each worker's untimed warm-up levels: use the
+    # sum of the timed level walls of the busiest worker instead
+    busiest = max(r[0] for r in res)
+    value = instances * wl["n"] * K / busiest
+    return value, busiest, K, sum(r[1] for r in res) / (instances * K), wall
+
+
+def cpu_sample_text(instances, workers, warmup, K, avg_its, cfg2):
+    who = (f"{instances} configs[2] instances (global indices 0..{instances - 1}) over "
+           f"{workers} spawned processes" if cfg2 else "the single instance (one process)")
+    return (who + f", each process at 1 OpenBLAS/OpenMP thread, levels {warmup + 1}.."
+            f"{warmup + K} via oracle/ (numpy pocketfft/OpenBLAS restatement of "
+            f"tsfrac.run_fids, same arithmetic); avg iterations {avg_its:.2f}")
+
+
+# ------------------------------------------------------------- launcher
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n: int, argv=None, executable=None) -> int:
+    """Run this script as `n` ranks, one process per GPU, with the environment
+    torchrun would give them (RANK, LOCAL_RANK, WORLD_SIZE, MASTER_ADDR =
+    127.0.0.1, MASTER_PORT); NCCL's INFO log (communicator / NVLS lines) goes
+    to each rank's stderr.  Only rank 0 prints the JSON line.  Returns the
+    largest exit code."""
+    argv = sys.argv[1:] if argv is None else argv
+    port = str(free_port())
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        procs.append(subprocess.Popen([executable or sys.executable, str(Path(__file__).resolve())]
+                                      + list(argv), env=env))
+    rcs = [p.wait() for p in procs]
+    return max(rcs)
 
 
 # --------------------------------------------------------------------- GPU
@@ -177,6 +276,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=0.0, help="override the workload's alpha")
     ap.add_argument("--batch", type=int, default=0, help="instances per rank")
     ap.add_argument("--cpu-workers", type=int, default=0)
+    ap.add_argument("--cpu-instances", type=int, default=0,
+                    help="configs[2] instances timed by the CPU legs (default max(64, cores))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tol", type=float, default=0.0,
@@ -192,30 +293,39 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        # batched configs[2]: one instance per host core; the single-instance
-        # configs are one march (the reference cannot split a march over
-        # processes; numpy/OpenBLAS threads are left at their default)
-        workers = args.cpu_workers or (os.cpu_count() or 1) if cfg2 else 1
-        value, wall, K, avg_its = cpu_measure(wl, warmup, min(args.steps, wl["cpu_levels"]),
-                                              workers, cfg2)
+        # batched configs[2]: >= 64 instances over every host core (one
+        # process per core, 1 BLAS thread each); the single-instance configs
+        # are one march in one process (the reference cannot split a march)
+        ncpu = os.cpu_count() or 1
+        workers = (args.cpu_workers or ncpu) if cfg2 else 1
+        inst = max(64, workers) if cfg2 else 1
+        if args.cpu_instances:
+            inst = args.cpu_instances
+        K = min(args.steps, wl["cpu_levels"])
+        value, busiest, K, avg_its, pool_wall = cpu_measure(wl, warmup, K, workers, inst, cfg2)
+        workers = min(workers, inst)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": K, "warmup": warmup,
-            "ms_per_step": wall / K * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": busiest / K * 1e3 / max(1, inst // workers),
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-            "config": {"workload": wl["name"], "instances_sampled": workers, "n": wl["n"],
+            "config": {"workload": wl["name"], "instances_sampled": inst, "n": wl["n"],
                        "M": wl["M"], "gamma": wl["gamma"], "alpha": wl["alpha"],
                        "tol": wl["tol"], "avg_iterations": avg_its},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                             "sample": f"{workers} instances (one per worker process, "
-                                       f"OPENBLAS_NUM_THREADS=1) x levels {warmup + 1}.."
-                                       f"{warmup + K} of the configs march via oracle/ "
-                                       "(numpy pocketfft/OpenBLAS restatement of tsfrac.run_fids)"},
+                             "sample": cpu_sample_text(inst, workers, warmup, K, avg_its, cfg2),
+                             "host": host_info(), "pool_wall_s": pool_wall},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line), flush=True)
         return
+
+    if world == 1 and args.gpus > 1:
+        # the driver may call `bench.py --gpus N` without torchrun: launch the
+        # N ranks here (one process per GPU, torchrun's environment)
+        raise SystemExit(spawn_ranks(args.gpus))
 
     import torch
     import paper_2002_11978_b200 as P
@@ -226,6 +336,8 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if args.gpus > 1 and dist.get_world_size() != args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {dist.get_world_size()}")
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     n, M, gam, alpha, B = wl["n"], wl["M"], wl["gamma"], wl["alpha"], wl["B"]
@@ -320,7 +432,11 @@ def main():
         #   large-n engine: begin, scalar, spectrum + 23 kernels per iteration,
         # iterations launched in chunks of 4 until every instance finished
         mx = iters[m0 - 1: m1 - 1].max(axis=1)
-        if large:      # host-driven chunks of 4 iterations, 17 kernels each
+        if large and graph:
+            # tsf_large.cu large_solve: set, begin, scalar, spectrum, then one
+            # graph whose WHILE body is the 17-kernel iteration chain + loop test
+            launches += int(np.sum(4 + 18 * np.maximum(mx, 1)))
+        elif large:    # host-driven chunks of 4 iterations, 17 kernels each
             launches += int(np.sum(4 + 17 * 4 * np.ceil(np.maximum(mx, 1) / 4.0)))
         elif graph:    # one graph per level, G instance-group branches each
             # set, begin, WHILE { v, t, test } (csrc/tsf_dispatch_impl.cuh
@@ -328,6 +444,7 @@ def main():
             genv = int(os.environ.get("TSF_SOLVE_GROUPS", "0") or 0)
             ng = min(8, genv if genv > 0 else (4 if B >= 1024 else 1), B)
             bg = -(-B // ng)
+            ng = -(-B // bg)
             lv = iters[m0 - 1: m1 - 1]
             for g in range(ng):
                 mxg = lv[:, g * bg:(g + 1) * bg].max(axis=1)
@@ -391,20 +508,22 @@ def main():
              "GBps": (soe_bytes / (soe_ms / K * 1e-3) / 1e9) if not fused else None,
              "algorithmic_bytes": soe_bytes}
     dom = k_solve if solve_ms >= soe_ms else k_soe
-    # ncu DRAM bytes of the same kernels (one capture, profiles/r01b_ncu_traffic.json),
-    # scaled to this launch's instance-iterations / SOE level
-    traffic = None
+    # ncu DRAM bytes of the same kernels, from a capture of THIS build only
+    # (profiles/ncu_traffic.json, keyed by workload and the library's sha256;
+    # tools/ncu_traffic.py writes it): per instance-iteration of the level solve
+    traffic, traffic_src = None, "no ncu capture of this build for this workload"
     try:
-        tr = json.loads((ROOT / "profiles" / "r01b_ncu_traffic.json").read_text())
-        if cfg2 and not large:
+        tr = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())[args.workload]
+        if tr.get("lib_sha256") == _native.lib_sha256():
             traffic = (tr["dram_bytes_per_instance_iteration"] * its_sum / K
-                       if dom is k_solve else tr["soe_dram_bytes_per_level_cfg2"] * B / 4096)
+                       if dom is k_solve else tr["soe_dram_bytes_per_level"] * B / tr["B"])
+            traffic_src = (f"ncu dram__bytes_read+write of the same kernels ({tr['capture']}) "
+                           "x this launch's instance-iterations")
     except Exception:
         traffic = None
     roof = {"kernel": dom["name"], "bound": "hbm", "achieved": dom["GBps"], "peak": hbm,
             "unit": "GB/s", "frac": dom["GBps"] / hbm, "traffic": traffic,
-            "traffic_source": "ncu dram__bytes_read+write of the same kernels "
-                              "(profiles/r01b_ncu_traffic.json) x this launch's work",
+            "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": dom["algorithmic_bytes"], "peak_source": peak_src,
             "share_of_step": (solve_ms if dom is k_solve else soe_ms) / ms,
             "note": ("large-n level solve: four-step transforms through L2/HBM"
@@ -500,14 +619,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        workers = (args.cpu_workers or min(os.cpu_count() or 1, 8)) if cfg2 else 1
+        ncpu = os.cpu_count() or 1
+        workers = (args.cpu_workers or ncpu) if cfg2 else 1
+        inst = (args.cpu_instances or max(64, workers)) if cfg2 else 1
         cw = min(K, wl["cpu_levels"])
-        cval, cwall, cK, cits = cpu_measure(wl, warmup, cw, workers, cfg2)
-        cpu = {"value": cval, "unit": UNIT, "cores": workers, "kind": "port",
-               "sample": (f"{workers} instances (one per process, 1 BLAS thread)" if cfg2 else
-                          "the single instance (one process)")
-                         + f" x levels {warmup + 1}..{warmup + cK} via oracle/ (numpy "
-                         f"restatement of tsfrac.run_fids); avg its {cits:.2f}"}
+        cval, cbusy, cK, cits, _ = cpu_measure(wl, warmup, cw, workers, inst, cfg2)
+        cpu = {"value": cval, "unit": UNIT, "cores": min(workers, inst), "kind": "port",
+               "sample": cpu_sample_text(inst, min(workers, inst), warmup, cK, cits, cfg2),
+               "host": host_info()}
 
     if rank == 0:
         line = {

@@ -1,0 +1,209 @@
+"""Full-size goldens for BASELINE configs[2] and configs[3] (TEST INFRASTRUCTURE).
+
+Runs only in the build container (imports the read-only reference `tsfrac`
+from /root/reference/pkg/src).  For each case it runs the UNMODIFIED
+reference `run_fids` twice: once stock (numpy pocketfft) and once with only
+its FFT engine swapped to scipy.fft (tsfrac.fourier.fft/ifft) — the
+reference's own noise floor, exactly as oracle/engine_swap_floor.py does for
+configs[1].  Per-level BiCGSTAB iterations are recorded by rebinding
+`tsfrac.scheme.solve_bicgstab` (scheme.py:31, :136-138).
+
+Outputs (tests/golden/):
+  cfg2_many.npz     48 configs[2] instances (n = 4096, M = 512): per-level
+                    iterations, u^64 and u^M (stock run)
+  cfg2_floor.json   per instance and pooled: stock vs swapped within-±1
+                    fraction, mean Δ, max |Δ|, rel-l2 of u^M
+  cfg3.npz          configs[3] (n = 2^20, M = 256, γ = 0.7, α = 1.2): all
+                    256 per-level iteration counts, u at levels 1/64/128/256
+                    sub-sampled every 16th point plus its full l2 norm, and
+                    projections of u^M onto 4 seeded N(0,1) vectors
+  cfg3_floor.json   the same comparison for configs[3]
+
+    OPENBLAS_NUM_THREADS=1 python oracle/gen_fullsize.py [--only cfg2|cfg3]
+"""
+from __future__ import annotations
+
+import os
+
+os.environ["OPENBLAS_NUM_THREADS"] = "1"
+os.environ["OMP_NUM_THREADS"] = "1"
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import multiprocessing as mp  # noqa: E402
+import sys  # noqa: E402
+import time  # noqa: E402
+from pathlib import Path  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ROOT = Path(__file__).resolve().parent.parent
+OUT = ROOT / "tests" / "golden"
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+# 48 configs[2] global instance indices: the two of cfg2.npz plus 46 drawn
+# from a fixed seed over the whole batch of 4096
+CFG2_INSTANCES = sorted({37, 200} | set(
+    np.random.default_rng(2002_11978 + 2).choice(4096, 46, replace=False).tolist()))
+CFG3_LEVELS = (1, 64, 128, 256)
+CFG3_SUB = 16          # sub-sampling stride of the stored configs[3] levels
+CFG3_PROJ_SEED = 33
+
+
+def _reference(swap: bool):
+    from gen_golden import _import_reference
+    tsfrac = _import_reference()
+    if swap:
+        import scipy.fft as sf
+        import tsfrac.fourier as fourier
+        import tsfrac.toeplitz as tz
+        fourier.fft = lambda x: sf.fft(x)
+        fourier.ifft = lambda x: sf.ifft(x)
+        tz.fourier = fourier
+    return tsfrac
+
+
+def _cfg2_one(args):
+    b, swap = args
+    tsfrac = _reference(swap)
+    from gen_golden import _march
+    from paper_2002_11978_b200 import workloads as WL
+    from tsfrac.scheme import ProblemSpec
+    n, M = 4096, 512
+    x, kx, fx, u0 = WL.instance_fields(n, b, 1)
+    spec = ProblemSpec(gamma=0.5, alpha=1.5, l=1.0, T=1.0,
+                       kappa=lambda xx, t, k=kx[0]: k * (1.0 + 0.2 * t),
+                       source=lambda xx, t, f=fx[0]: f * (1.0 + t),
+                       initial=lambda xx, u=u0[0]: u.copy())
+    t0 = time.time()
+    hist, rep, its, rel = _march(tsfrac, spec, M, 3.0, n + 1, 1e-12, 1e-12)
+    print(f"cfg2 b{b} swap={swap} avg {its.mean():.2f} {time.time() - t0:.0f}s", flush=True)
+    return b, swap, its, hist[64].copy(), hist[-1].copy()
+
+
+def cfg3_fields():
+    kappa = lambda x, t: 1.0 + 0.5 * np.sin(np.pi * x) * np.exp(-t)  # noqa: E731
+    source = lambda x, t: (1.0 + t) * np.sin(np.pi * x)  # noqa: E731
+    initial = lambda x: (1.0 - x * x) ** 2  # noqa: E731
+    return kappa, source, initial
+
+
+def cfg3_projectors(n: int) -> np.ndarray:
+    return np.random.default_rng(CFG3_PROJ_SEED).standard_normal((4, n))
+
+
+def _cfg3_one(swap):
+    tsfrac = _reference(swap)
+    from tsfrac.scheme import ProblemSpec, SolverOptions, run_fids
+    n, M, g, a = 1 << 20, 256, 0.7, 1.2
+    kappa, source, initial = cfg3_fields()
+    spec = ProblemSpec(gamma=g, alpha=a, l=1.0, T=1.0, kappa=kappa, source=source,
+                       initial=initial)
+    # keep_history would hold (M+1) x 2^20 doubles (2.2 GB): keep the wanted
+    # levels from the solver's own return value (scheme.py:288 u = solve(...))
+    import tsfrac.scheme as sch
+    keep = {}
+    its_l = []
+    orig = sch.solve_bicgstab
+
+    def rec(*a, **k):
+        x, rep = orig(*a, **k)
+        its_l.append(rep.iterations)
+        if len(its_l) in CFG3_LEVELS:
+            keep[len(its_l)] = np.array(x, copy=True)
+        return x, rep
+
+    sch.solve_bicgstab = rec
+    t0 = time.time()
+    try:
+        uM, rep = run_fids(spec, M, (2.0 - g) / g, n + 1, epsilon=1e-12,
+                           options=SolverOptions(solver="pkrylov", tol=1e-12),
+                           keep_history=False)
+    finally:
+        sch.solve_bicgstab = orig
+    assert np.array_equal(keep[M], uM)
+    its = np.array(its_l)
+    print(f"cfg3 swap={swap} avg {its.mean():.2f} {time.time() - t0:.0f}s", flush=True)
+    return swap, its, keep
+
+
+def _rl2(x, y):
+    return float(np.linalg.norm(x - y) / np.linalg.norm(y))
+
+
+def _stats(d):
+    return {"within1": float(np.mean(np.abs(d) <= 1)), "within2": float(np.mean(np.abs(d) <= 2)),
+            "mean_d": float(d.mean()), "max_abs_d": int(np.abs(d).max())}
+
+
+def run_cfg2(pool):
+    res = pool.map(_cfg2_one, [(b, s) for b in CFG2_INSTANCES for s in (False, True)])
+    stock = {b: r for b, s, *r in res if not s}
+    swap = {b: r for b, s, *r in res if s}
+    out = {"instances": np.array(CFG2_INSTANCES)}
+    floor = {}
+    all_d = []
+    for b in CFG2_INSTANCES:
+        its, u64, uM = stock[b]
+        out[f"b{b}_its"] = its
+        out[f"b{b}_uM"] = uM
+        out[f"b{b}_u64"] = u64
+        d = swap[b][0] - its
+        all_d.append(d)
+        floor[f"b{b}"] = dict(_stats(d), rel_l2_uM=_rl2(swap[b][2], uM),
+                              rel_l2_u64=_rl2(swap[b][1], u64))
+    allD = np.concatenate(all_d)
+    floor["pooled"] = dict(_stats(allD),
+                           min_within1=min(v["within1"] for k, v in floor.items()),
+                           max_rel_l2_uM=max(v["rel_l2_uM"] for k, v in floor.items()))
+    np.savez_compressed(OUT / "cfg2_many.npz", **out)
+    (OUT / "cfg2_floor.json").write_text(json.dumps(floor, indent=1) + "\n")
+    print("cfg2 floor pooled", floor["pooled"], flush=True)
+
+
+def run_cfg3(pool):
+    res = dict((s, (its, keep)) for s, its, keep in pool.map(_cfg3_one, [False, True]))
+    its, keep = res[False]
+    its_s, keep_s = res[True]
+    n = 1 << 20
+    P = cfg3_projectors(n)
+    out = {"its": its, "levels": np.array(CFG3_LEVELS), "sub": np.array([CFG3_SUB]),
+           "proj_seed": np.array([CFG3_PROJ_SEED])}
+    floor = dict(_stats(its_s - its))
+    for m in CFG3_LEVELS:
+        u = keep[m]
+        out[f"u{m}_sub"] = u[::CFG3_SUB].copy()
+        out[f"u{m}_norm"] = np.array([np.linalg.norm(u)])
+        out[f"u{m}_proj"] = P @ u
+        floor[f"rel_l2_u{m}"] = _rl2(keep_s[m], u)
+        floor[f"rel_l2_u{m}_sub"] = _rl2(keep_s[m][::CFG3_SUB], u[::CFG3_SUB])
+    np.savez_compressed(OUT / "cfg3.npz", **out)
+    (OUT / "cfg3_floor.json").write_text(json.dumps(floor, indent=1) + "\n")
+    print("cfg3 floor", floor, flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="cfg2,cfg3")
+    ap.add_argument("--workers", type=int, default=os.cpu_count())
+    args = ap.parse_args()
+    ctx = mp.get_context("spawn")
+    which = args.only.split(",")
+    with ctx.Pool(args.workers) as pool:
+        if "cfg3" in which:
+            a3 = pool.map_async(_cfg3_one, [False, True])
+        if "cfg2" in which:
+            run_cfg2(pool)
+        if "cfg3" in which:
+            res = a3.get()
+
+            class _P:
+                @staticmethod
+                def map(fn, xs):
+                    return res
+            run_cfg3(_P)
+
+
+if __name__ == "__main__":
+    main()

@@ -127,9 +127,11 @@ def torch_mod():
     return torch
 
 
-def stream_ptr(stream=None) -> int:
+def stream_ptr(stream=None, device=None) -> int:
+    """The launch stream: `stream`, else torch's current stream OF `device`
+    (the tensors' device — not whichever device happens to be current)."""
     torch = torch_mod()
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)
 
 
@@ -176,3 +178,14 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def lib_sha256(path: Optional[os.PathLike] = None) -> str:
+    """sha256 of the loaded library file (ties profiles to the build they measured)."""
+    import hashlib
+    p = Path(path) if path else Path(os.environ.get("TSF_LIB", LIB_PATH))
+    h = hashlib.sha256()
+    with open(p, "rb") as f:
+        for chunk in iter(lambda: f.read(1 << 20), b""):
+            h.update(chunk)
+    return h.hexdigest()

@@ -83,6 +83,12 @@ int solve_groups(int B) {
   int g = env > 0 ? env : (B >= 1024 ? 4 : 1);
   if (g > kMaxSolveGroups) g = kMaxSolveGroups;
   if (g > B) g = B > 0 ? B : 1;
+  // groups of ceil(B/g) instances: drop the empty trailing groups (B = 5,
+  // g = 4 -> 2 per group -> 3 groups; B = 9, g = 4 -> 3 groups of 3)
+  if (B > 0) {
+    const int bg = (B + g - 1) / g;
+    g = (B + bg - 1) / bg;
+  }
   return g;
 }
 
@@ -221,6 +227,21 @@ int ensure_reserved(tsf_plan* p, int B) {
 
 }  // namespace
 
+// Every plan entry point runs on the plan's device and restores the caller's
+// current device on return (ctypes callers and Plan.__del__ may run with
+// any device current).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 // ======================================================================
 extern "C" {
 
@@ -237,6 +258,7 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
     return fail(TSF_E_INVALID, "L=%d must be a power of two >= max(2n-1, 32)", L);
   if (!symbol_re) return fail(TSF_E_INVALID, "symbol is NULL");
   const int lg = ilog2_host(L);
+  DeviceGuard dg(device);
   if (lg > kMaxLogL) {
     // four-step engine: transform length L/2 = 2^13..2^24, any n with 2n-1 <= L
     if (lam && !(is_pow2(n) && L == 2 * n))
@@ -305,7 +327,7 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
 
 int tsf_plan_destroy(tsf_plan* p) {
   if (!p) return TSF_SUCCESS;
-  cudaSetDevice(p->device);
+  DeviceGuard dg(p->device);
   if (p->large) {
     large_plan_free(p->large);
     delete p->large;
@@ -336,6 +358,7 @@ int tsf_plan_info(const tsf_plan* p, int64_t* o) {
 
 int tsf_plan_reserve(tsf_plan* p, int B) {
   if (!p || B < 1) return fail(TSF_E_INVALID, "bad plan or batch");
+  DeviceGuard dg(p->device);
   return ensure_reserved(p, B);
 }
 
@@ -343,6 +366,7 @@ int tsf_toeplitz_matvec(tsf_plan* p, int B, const double* x, double* y, const do
                         double shift, void* stream) {
   if (!p || !x || !y || B < 0) return fail(TSF_E_INVALID, "bad argument");
   if (B == 0) return TSF_SUCCESS;
+  DeviceGuard dg(p->device);
   if (p->large) return large_matvec(p->large, B, x, y, kappa, shift, (cudaStream_t)stream);
   return ForLog<MatvecF>::run(p->log_L, p->n, p->tables(), B, x, y, kappa, shift,
                               (cudaStream_t)stream);
@@ -353,6 +377,7 @@ int tsf_precond_solve(tsf_plan* p, int B, const double* v, double* z, double shi
   if (!p || !v || !z || B < 0) return fail(TSF_E_INVALID, "bad argument");
   if (!p->has_pc) return fail(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner (non-pow2 n)");
   if (B == 0) return TSF_SUCCESS;
+  DeviceGuard dg(p->device);
   if (p->large)
     return large_precond(p->large, B, v, z, shift, kbar, kbar_dev, (cudaStream_t)stream);
   return ForLog<PrecondF>::run(p->log_L, p->n, p->tables(), B, v, z, shift, kbar, kbar_dev,
@@ -361,6 +386,7 @@ int tsf_precond_solve(tsf_plan* p, int B, const double* v, double* z, double shi
 
 static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cudaStream_t st) {
   if (pc && !p->has_pc) return fail(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner");
+  DeviceGuard dg(p->device);
   if (p->large) {
     if (a.soe_epilogue) return fail(TSF_E_UNSUPPORTED, "fused SOE epilogue needs n <= 4096");
     a.n = p->n;
@@ -477,6 +503,7 @@ int tsf_soe_push_rhs(int B, int n, int nexp, double* W, const double* u,
 
 int tsf_fids_march(tsf_plan* p, const tsf_march* d, void* stream) {
   if (!p || !d) return fail(TSF_E_INVALID, "NULL argument");
+  DeviceGuard dg(p->device);
   const int B = d->B, M = d->M, nexp = d->nexp, n = p->n;
   if (B < 1 || M < 1 || nexp < 1) return fail(TSF_E_INVALID, "bad B/M/nexp");
   if (d->m_begin < 1 || d->m_end < d->m_begin || d->m_end > M + 1)

@@ -95,7 +95,7 @@ def _device_solve(op: LevelOperator, precond, rhs, tol, max_iters, method):
     _native.check(_native.load().tsf_krylov_solve(
         plan.handle, B, method, pc, b.data_ptr(), x.data_ptr(), kap.data_ptr(), op.shift,
         kbar, float(tol), int(max_iters) if max_iters is not None else 0, iters.data_ptr(),
-        relres.data_ptr(), status.data_ptr(), _native.stream_ptr()))
+        relres.data_ptr(), status.data_ptr(), _native.stream_ptr(device=b.device)))
     reps = _reports(iters.cpu(), relres.cpu(), status.cpu())
     xs = _arrays.back(x, as_np)
     return (xs, reps[0]) if b.dim() == 1 else (xs, reps)
@@ -209,18 +209,61 @@ def _generic_cg(op, precond, rhs, tol, max_iters):
 
 def _fused_ok(op, precond) -> bool:
     """The fused level-solve kernels take a LevelOperator with no or a
-    power-of-two Strang preconditioner; anything else (non-pow2 n with the
-    Strang preconditioner, user callables) runs the device-vector loop below,
-    whose operator and preconditioner applications are still the sm_100a
-    Toeplitz kernels."""
+    power-of-two Strang preconditioner BUILT FOR THIS OPERATOR: the kernels
+    form P from the operator's own shift, the plan's Strang eigenvalues and
+    the preconditioner's kappa_bar, so a preconditioner with another shift
+    or another eigenvalue array (a hand-made CirculantPreconditioner, as in
+    pkg/tests/test_toeplitz.py:163-164) takes the device-vector loop below,
+    whose P^{-1} is exactly that preconditioner's.  Anything else (non-pow2 n
+    with the Strang preconditioner, user callables) runs that loop too; its
+    operator and preconditioner applications are still the sm_100a Toeplitz
+    kernels."""
     if not isinstance(op, LevelOperator):
         return False
-    return precond is None or getattr(precond, "strang_native", False)
+    if precond is None:
+        return True
+    if not getattr(precond, "strang_native", False):
+        return False
+    if float(precond.shift) != float(op.shift):
+        return False
+    return precond.plan is op.toeplitz.plan or _same_strang(precond, op)
+
+
+def _same_strang(precond, op) -> bool:
+    """The preconditioner's eigenvalues are the operator plan's (same Strang
+    column), so the fused kernels' P equals the preconditioner."""
+    from .toeplitz import strang_first_column
+    col = getattr(op.toeplitz, "first_col", None)
+    if col is None or getattr(precond, "first_col", None) is None:
+        return False
+    if not np.array_equal(np.asarray(precond.first_col), np.asarray(col)):
+        return False
+    lam = np.fft.fft(strang_first_column(np.asarray(col, dtype=float))).real
+    return np.array_equal(np.asarray(precond.lam), lam)
+
+
+def _zero_iteration_report(rhs, max_iters):
+    """max_iters <= 0 (krylov.py:105-116 with an empty loop): zero RHS ->
+    (0, 0.0, converged); otherwise (max_iters, ||r0||/||r0|| = 1, not converged)."""
+    torch = _native.torch_mod()
+    b, as_np = _arrays.to_device(rhs)
+    x = torch.zeros_like(b)
+    if b.dim() == 1:
+        nrm = float(torch.linalg.norm(b))
+        rep = (KrylovReport(0, 0.0, True) if nrm == 0.0
+               else KrylovReport(int(max_iters), 1.0, False))
+        return _arrays.back(x, as_np), rep
+    nrms = torch.linalg.norm(b, dim=1).cpu().tolist()
+    reps = [KrylovReport(0, 0.0, True) if v == 0.0 else KrylovReport(int(max_iters), 1.0, False)
+            for v in nrms]
+    return _arrays.back(x, as_np), reps
 
 
 def solve_bicgstab(op: MatrixFreeOperator, precond, rhs, tol: float = 1e-10,
                    max_iters: Optional[int] = None):
     """Right-preconditioned BiCGSTAB, x0 = 0 (krylov.py:88-153)."""
+    if max_iters is not None and max_iters <= 0:
+        return _zero_iteration_report(rhs, max_iters)
     if _fused_ok(op, precond):
         return _device_solve(op, precond, rhs, tol, max_iters, method=0)
     return _generic_bicgstab(op, precond, rhs, tol, max_iters)
@@ -229,6 +272,8 @@ def solve_bicgstab(op: MatrixFreeOperator, precond, rhs, tol: float = 1e-10,
 def solve_cg(op: MatrixFreeOperator, precond, rhs, tol: float = 1e-10,
              max_iters: Optional[int] = None):
     """Preconditioned CG, x0 = 0 (krylov.py:43-85)."""
+    if max_iters is not None and max_iters <= 0:
+        return _zero_iteration_report(rhs, max_iters)
     if _fused_ok(op, precond):
         return _device_solve(op, precond, rhs, tol, max_iters, method=1)
     return _generic_cg(op, precond, rhs, tol, max_iters)

@@ -373,8 +373,13 @@ class FidsMarch:
             torch.cuda.synchronize(self.dev)
             self._ev = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
             d.events = C.cast(self._ev, C.c_void_p)
+        if stream is not None:
+            # reset() and the constructor's uploads ran on torch's current
+            # stream of this device: order them before the march
+            torch = _native.torch_mod()
+            stream.wait_stream(torch.cuda.current_stream(self.dev))
         _native.check(_native.load().tsf_fids_march(self.plan.handle, C.byref(d),
-                                                    _native.stream_ptr(stream)))
+                                                    _native.stream_ptr(stream, self.dev)))
         self.next_level = m1
 
     def u_level(self, m: int):
@@ -430,18 +435,31 @@ def run_fids(spec: ProblemSpec, M: int, r: float, N: int, epsilon: float = 1e-10
         return _finish(spec, mesh, disc, x, hist, its, rel, soe, t0, tag, keep_history)
     torch = _native.torch_mod()
     dev = torch.device(f"cuda:{device}")
-    kap = _device_field(spec.kappa, x, mesh.t, n, M, dev, positive=True)
-    src = _device_field(spec.source, x, mesh.t, n, M, dev, positive=False)
+    kap = _device_field(spec.kappa, x, mesh.t, n, M, dev, positive=True, chunk=MARCH_CHUNK)
+    src = _device_field(spec.source, x, mesh.t, n, M, dev, positive=False, chunk=MARCH_CHUNK)
     u0_t = torch.from_numpy(np.ascontiguousarray(u0)[None, :]).to(dev)
     want_hist = keep_history or spec.exact is not None
+    chunked = [f for f in (kap, src) if isinstance(f, _ChunkField)]
+    if chunked:
+        for f in chunked:
+            f.fill(1, min(M + 1, 1 + MARCH_CHUNK))
     march = FidsMarch(spec.gamma, spec.alpha, spec.l, spec.T, M, r, N, soe,
                       method=1 if spec.kappa_x_independent else 0,
                       precond=1 if tag == "pkrylov" else 0, tol=options.tol,
                       max_iters=options.max_iters, B=1, kappa=kap, source=src, u0=u0_t,
                       hist_B=1 if want_hist else 0, device=device, mu=mu)
-    march.run()
+    for m0 in range(1, M + 1, MARCH_CHUNK):
+        m1 = min(M + 1, m0 + MARCH_CHUNK)
+        if m0 > 1:
+            for f in chunked:
+                f.fill(m0, m1)   # after the previous chunk (stream order + status sync)
+        march.run(m1 - m0)
+        st = march.status[m0 - 1: m1 - 1].cpu().numpy()
+        if np.any(st != 0):
+            _raise_status(st, march.iters[m0 - 1: m1 - 1].cpu().numpy(),
+                          march.relres[m0 - 1: m1 - 1].cpu().numpy(), mesh.t[m0 - 1:],
+                          spec.kappa_x_independent)
     res = march.result()
-    _raise_status(res.status, res.iterations, res.relres, mesh.t, spec.kappa_x_independent)
     if want_hist:
         hist = res.hist[:, 0, :].cpu().numpy()
     else:
@@ -497,9 +515,48 @@ def _run_levels(spec, mesh, disc, x, soe, u0, M, options, device, want_hist):
     return hist, its, rel
 
 
-def _device_field(fn, x, t, n, M, dev, positive):
+class _ChunkField(_FieldDev):
+    """An arbitrary callable field tabulated CHUNK levels at a time: the
+    device holds [CHUNK, n] instead of [M+1, n] (2.15 GB per field at
+    configs[3] for the whole march).  `fill(m0, m1)` evaluates levels
+    m0..m1-1 on the host as the reference does per level (scheme.py:280,283);
+    the march descriptor's base pointer is offset so level m reads row m - m0
+    (the march only touches levels inside the range it runs)."""
+
+    def __init__(self, fn, x, t, n, dev, positive, chunk):
+        torch = _native.torch_mod()
+        buf = torch.empty((chunk, 1, n), dtype=torch.float64, device=dev)
+        super().__init__(1, buf, 0, n, n, np.ones((t.size, 1)))
+        self.fn, self.x, self.t, self.positive, self.m0 = fn, x, t, positive, 0
+
+    def fill(self, m0: int, m1: int):
+        torch = _native.torch_mod()
+        tab = np.empty((m1 - m0, 1, self.x.size))
+        for m in range(m0, m1):
+            if self.positive:
+                tab[m - m0, 0] = _kappa_at_fn(self.fn, self.x, self.t[m])
+            else:
+                tab[m - m0, 0] = np.asarray(self.fn(self.x, self.t[m]), dtype=float)
+        self.modes[: m1 - m0].copy_(torch.from_numpy(tab))
+        self.m0 = m0
+
+    def as_c(self) -> _native.Field:
+        base = self.modes.data_ptr() - self.m0 * self.t_stride * 8
+        return _native.Field(1, base, 0, self.b_stride, self.t_stride, self.coef.ctypes.data)
+
+
+# levels per native-march launch in run_fids: the status of a chunk is read
+# back before the next one runs, so a failing level raises (as the
+# reference does at that level, scheme.py:139-142) without the whole march
+# running first, and callable fields are tabulated per chunk
+MARCH_CHUNK = 32
+
+
+def _device_field(fn, x, t, n, M, dev, positive, chunk=None):
     if isinstance(fn, SeparableField):
         return _field_separable(fn, x, t, 1, None, dev)
+    if chunk:
+        return _ChunkField(fn, x, t, n, dev, positive, min(chunk, M))
     tab = np.empty((M + 1, 1, n))
     tab[0] = 0.0
     for m in range(1, M + 1):
@@ -648,10 +705,11 @@ def run_dids(spec: ProblemSpec, M: int, r: float, N: int, mu: Optional[float] = 
         kappa = _kappa_at(spec, x, tm)
         f = torch.from_numpy(np.ascontiguousarray(spec.source(x, tm), dtype=np.float64)).to(dev)
         w = torch.from_numpy(np.diff(a)).to(dev) if m > 1 else None
-        _native.check(lib.tsf_l1_history_rhs(1, n, m, hist.data_ptr(), m * n,
-                                             None if w is None else w.data_ptr(),
-                                             a[0] / G, G, f.data_ptr(), rhs.data_ptr(),
-                                             _native.stream_ptr()))
+        with torch.cuda.device(dev):
+            _native.check(lib.tsf_l1_history_rhs(1, n, m, hist.data_ptr(), m * n,
+                                                 None if w is None else w.data_ptr(),
+                                                 a[0] / G, G, f.data_ptr(), rhs.data_ptr(),
+                                                 _native.stream_ptr(device=dev)))
         ops[m - 1] = m * n
         u, it, rr = solver.solve(a[-1] / G, kappa, rhs)
         its[m - 1] = it

@@ -175,10 +175,11 @@ def history_push(h: FastHistory, delta_u, tau_m: float) -> FastHistory:
     tab = _coef_tables(h.soe, tau_m, None, dev)
     zero = torch.zeros(n, dtype=torch.float64, device=dev)
     # push with u = delta_u, uprev = 0 reproduces (u - 0)/tau == delta_u/tau exactly
-    _native.check(_native.load().tsf_soe_push_rhs(
-        1, n, h.soe.n_exp, h.W.data_ptr(), du.data_ptr(), zero.data_ptr(),
-        float(tau_m), tab[0].data_ptr(), tab[1].data_ptr(), tab[2].data_ptr(), 1, 0, 0,
-        0.0, 1.0, None, None, _native.stream_ptr()))
+    with torch.cuda.device(dev):
+        _native.check(_native.load().tsf_soe_push_rhs(
+            1, n, h.soe.n_exp, h.W.data_ptr(), du.data_ptr(), zero.data_ptr(),
+            float(tau_m), tab[0].data_ptr(), tab[1].data_ptr(), tab[2].data_ptr(), 1, 0, 0,
+            0.0, 1.0, None, None, _native.stream_ptr(device=dev)))
     h.level += 1
     return h
 
@@ -195,8 +196,9 @@ def fast_caputo_rhs(h: FastHistory, a_mm: float, u_prev, gamma: float, tau_m: fl
     out = torch.empty(n, dtype=torch.float64, device=dev)
     zero_f = torch.zeros(n, dtype=torch.float64, device=dev)
     G = math.exp(gammaln(1.0 - gamma))
-    _native.check(_native.load().tsf_soe_push_rhs(
-        1, n, h.soe.n_exp, h.W.data_ptr(), up.data_ptr(), None, 0.0,
-        None, None, tab[2].data_ptr(), 0, 0, 1, float(a_mm), G, zero_f.data_ptr(),
-        out.data_ptr(), _native.stream_ptr()))
+    with torch.cuda.device(dev):
+        _native.check(_native.load().tsf_soe_push_rhs(
+            1, n, h.soe.n_exp, h.W.data_ptr(), up.data_ptr(), None, 0.0,
+            None, None, tab[2].data_ptr(), 0, 0, 1, float(a_mm), G, zero_f.data_ptr(),
+            out.data_ptr(), _native.stream_ptr(device=dev)))
     return _arrays.back(out, as_np)

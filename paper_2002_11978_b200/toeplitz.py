@@ -12,6 +12,8 @@ csrc/tsf_large.cuh).  Inputs may be numpy arrays (copied) or torch CUDA tensors 
 from __future__ import annotations
 
 import hashlib
+import os
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -41,7 +43,16 @@ def _is_pow2(n: int) -> bool:
     return n > 0 and (n & (n - 1)) == 0
 
 
-_plans: dict = {}
+# Plan cache, least recently used first.  A plan keeps its Krylov workspaces
+# (sized to the largest batch it ran) and cached graphs, so the cache is
+# bounded: evicted plans are freed once no operator holds them.
+_plans: "OrderedDict[tuple, _native.Plan]" = OrderedDict()
+PLAN_CACHE_SIZE = int(os.environ.get("TSF_PLAN_CACHE", "8"))
+
+
+def clear_plans() -> None:
+    """Drop every cached plan (device memory is released with the last reference)."""
+    _plans.clear()
 
 
 def plan_for(first_col: np.ndarray, device: int = 0, lam: Optional[np.ndarray] = None,
@@ -63,6 +74,8 @@ def plan_for(first_col: np.ndarray, device: int = 0, lam: Optional[np.ndarray] =
     key = (n, device, hashlib.sha1(col.tobytes()).hexdigest(),
            None if lam is None else hashlib.sha1(np.ascontiguousarray(lam).tobytes()).hexdigest())
     pl = None if private else _plans.get(key)
+    if pl is not None:
+        _plans.move_to_end(key)
     if pl is None:
         if spectrum is not None and L == L_ref:
             sym = np.ascontiguousarray(np.real(spectrum))
@@ -71,6 +84,8 @@ def plan_for(first_col: np.ndarray, device: int = 0, lam: Optional[np.ndarray] =
         pl = _native.Plan(n, L, sym, lam, device)
         if not private:
             _plans[key] = pl
+            while len(_plans) > max(1, PLAN_CACHE_SIZE):
+                _plans.popitem(last=False)
     return pl
 
 
@@ -131,7 +146,7 @@ def toeplitz_matvec(op: ToeplitzOperator, v, kappa=None, shift: float = 0.0):
             k = k.expand_as(x).contiguous()
     _native.check(_native.load().tsf_toeplitz_matvec(
         op.plan.handle, B, x.data_ptr(), y.data_ptr(), _native.ptr(k), float(shift),
-        _native.stream_ptr()))
+        _native.stream_ptr(device=x.device)))
     return _arrays.back(y, as_np)
 
 
@@ -229,9 +244,10 @@ def precond_solve(p: CirculantPreconditioner, v):
     if not p.strang_native:
         # circ(c) applied as a symmetric Toeplitz product (_circulant_plan)
         _native.check(_native.load().tsf_toeplitz_matvec(
-            p.plan.handle, B, x.data_ptr(), z.data_ptr(), None, 0.0, _native.stream_ptr()))
+            p.plan.handle, B, x.data_ptr(), z.data_ptr(), None, 0.0,
+            _native.stream_ptr(device=x.device)))
         return _arrays.back(z, as_np)
     _native.check(_native.load().tsf_precond_solve(
         p.plan.handle, B, x.data_ptr(), z.data_ptr(), float(p.shift), float(p.kappa_bar), None,
-        _native.stream_ptr()))
+        _native.stream_ptr(device=x.device)))
     return _arrays.back(z, as_np)

@@ -31,8 +31,8 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 from paper_2002_11978_b200 import SolverOptions, run_dids, run_fids  # noqa: E402
-from paper_2002_11978_b200.couplings import m_from_n, n_from_m  # noqa: E402
-from paper_2002_11978_b200.problems import make_case  # noqa: E402
+from harness.couplings import m_from_n, n_from_m  # noqa: E402
+from harness.problems import make_case  # noqa: E402
 
 
 def _ref(label):

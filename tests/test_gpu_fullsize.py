@@ -1,17 +1,20 @@
 """Parity at BASELINE.json's full sizes.
 
-configs[2] (n = 4096, M = 512) for a 256-instance batch of the seeded
-workload: two instances against the reference's own full-size goldens
-(tests/golden/cfg2.npz), and size-independent properties of the whole batch:
+configs[2] (n = 4096, M = 512): 48 instances of the seeded batch (global
+indices in tests/golden/cfg2_many.npz, oracle/gen_fullsize.py) marched as one
+batch against the reference's own full-size runs, gated at the reference's
+engine-swap floor on the SAME instances (tests/golden/cfg2_floor.json: the
+unmodified reference with only numpy -> scipy.fft swapped; pooled ±1 on
+98.5% of levels, per instance 77-100%, max |Δ| 4, u^M within 2.7e-12); plus
+size-independent properties of a 256-instance batch:
   * position invariance — the same instances marched as a different batch
     give bit-identical u^M and iteration counts (each CTA is deterministic);
   * exact homogeneity — doubling f and u^0 doubles u^M bit for bit with the
     same iteration counts (every operation is linear; scaling by 2 is exact).
-configs[3] (n = 2^20): the first levels against the oracle.
-
-Gates for the goldens come from the reference's engine-swap floor on these
-two instances (numpy -> scipy.fft, measured on the CPU): ±1 iteration on 75-77%
-of levels, max |Δ| 4-6, u^M within 1.9e-12.
+configs[3] (n = 2^20, M = 256): the whole march against the reference's run
+(tests/golden/cfg3.npz: all 256 per-level iteration counts, u at levels
+1/64/128/256 sub-sampled every 16th point, its l2 norm and four seeded
+projections), gated at that config's engine-swap floor (cfg3_floor.json).
 """
 
 import math
@@ -19,7 +22,6 @@ import math
 import numpy as np
 import pytest
 
-import oracle as O
 from tsf_testlib import golden, rel_l2
 
 pytestmark = pytest.mark.gpu
@@ -64,15 +66,67 @@ def batch():
     return _march(0, 256)
 
 
-def test_cfg2_full_size_vs_reference_goldens(batch):
-    uB, itB = batch
-    g = golden("cfg2")
-    for b in (37, 200):
-        ref_its, ref_u = g[f"b{b}_its"], g[f"b{b}_uM"]
-        d = itB[:, b] - ref_its
-        assert rel_l2(uB[b], ref_u) <= 1e-10
-        assert np.mean(np.abs(d) <= 1) >= 0.70, (b, np.unique(d, return_counts=True))
-        assert np.max(np.abs(d)) <= 8 and abs(d.mean()) <= 0.3, (b, d.mean())
+def _march_instances(idx):
+    """The configs[2] instances with the given GLOBAL indices as one batch."""
+    gam, alpha = 0.5, 1.5
+    r = (2 - gam) / gam
+    parts = [WL.instance_fields(N_, int(b), 1) for b in idx]
+    x = parts[0][0]
+    kx = np.concatenate([p[1] for p in parts])
+    fx = np.concatenate([p[2] for p in parts])
+    u0 = np.concatenate([p[3] for p in parts])
+    B = len(idx)
+    kap = P.SeparableField([np.ones(N_)], lambda t: [1.0 + 0.2 * t])
+    src = P.SeparableField([np.ones(N_)], lambda t: [1.0 + t])
+    mesh = P.build_mesh(M_, r, 1.0)
+    soe = P.build_soe(gam, 1e-12, (1.0 / M_) ** r, 1.0)
+    dev = torch.device("cuda:0")
+    m = FidsMarch(gam, alpha, 1.0, 1.0, M_, r, N_ + 1, soe, method=0, precond=1, tol=1e-12,
+                  max_iters=None, B=B, kappa=_field_separable(kap, x, mesh.t, B, kx[None], dev),
+                  source=_field_separable(src, x, mesh.t, B, fx[None], dev),
+                  u0=torch.from_numpy(np.ascontiguousarray(u0)).to(dev), device=0,
+                  private_plan=True)
+    m.run(64)
+    u64 = m.u_level(64).cpu().numpy().copy()
+    m.run()
+    res = m.result()
+    assert np.all(res.status == 0)
+    out = u64, res.u_final.cpu().numpy().copy(), res.iterations.copy()
+    del m, res
+    torch.cuda.empty_cache()
+    return out
+
+
+def test_cfg2_full_size_vs_reference_goldens():
+    """48 configs[2] instances vs the reference (cfg2_many.npz), gated at the
+    reference's own engine-swap floor on the same instances."""
+    import json
+    from pathlib import Path
+    g = golden("cfg2_many")
+    floor = json.loads((Path(__file__).parent / "golden" / "cfg2_floor.json").read_text())
+    idx = g["instances"]
+    u64, uM, its = _march_instances(idx)
+    all_d = []
+    for i, b in enumerate(idx):
+        fl = floor[f"b{b}"]
+        d = its[:, i] - g[f"b{b}_its"]
+        all_d.append(d)
+        frac = float(np.mean(np.abs(d) <= 1))
+        e64 = rel_l2(u64[i], g[f"b{b}_u64"])
+        eM = rel_l2(uM[i], g[f"b{b}_uM"])
+        # per instance: the floor of this very instance, minus the spread a
+        # second FFT engine shows on the sensitive instances (77-100%)
+        assert frac >= min(0.95, fl["within1"]) - 0.15, (b, frac, fl["within1"])
+        assert np.max(np.abs(d)) <= 2 * max(2, fl["max_abs_d"]), (b, np.abs(d).max())
+        assert e64 <= max(1e-10, 10 * fl["rel_l2_u64"]), (b, e64)
+        assert eM <= max(1e-10, 10 * fl["rel_l2_uM"]), (b, eM)
+    D = np.concatenate(all_d)
+    pooled = float(np.mean(np.abs(D) <= 1))
+    print(f"cfg2 x{len(idx)}: within+-1 {pooled:.4f} (floor {floor['pooled']['within1']:.4f}) "
+          f"mean d {D.mean():+.4f} (floor {floor['pooled']['mean_d']:+.4f}) max|d| "
+          f"{np.abs(D).max()}")
+    assert pooled >= floor["pooled"]["within1"] - 0.03
+    assert abs(D.mean()) <= max(0.05, 3.0 * D.std() / math.sqrt(D.size)), (D.mean(), D.std())
 
 
 def test_cfg2_full_size_position_invariance(batch):
@@ -89,14 +143,16 @@ def test_cfg2_full_size_exact_homogeneity(batch):
     np.testing.assert_array_equal(u2, 2.0 * uB[:32])
 
 
-def test_cfg3_first_levels_vs_oracle():
-    """configs[3] size (n = 2^20, M = 256, gamma = 0.7, alpha = 1.2): levels
-    1..3 of run_fids's device march against the oracle's fids_step."""
+def test_cfg3_full_march_vs_reference():
+    """configs[3] (n = 2^20, M = 256, gamma = 0.7, alpha = 1.2): all 256 levels
+    of run_fids's device march against the reference's own run
+    (cfg3.npz), gated at the engine-swap floor of the same run (cfg3_floor.json)."""
+    import json
+    from pathlib import Path
+    g = golden("cfg3")
+    floor = json.loads((Path(__file__).parent / "golden" / "cfg3_floor.json").read_text())
     n, M, gam, alpha = 1 << 20, 256, 0.7, 1.2
     r = (2 - gam) / gam
-    N = n + 1
-    kappa = lambda xx, t: 1.0 + 0.5 * np.sin(np.pi * xx) * np.exp(-t)  # noqa: E731
-    source = lambda xx, t: (1.0 + t) * np.sin(np.pi * xx)  # noqa: E731
     x = WL.grid(n)
     kap = P.SeparableField([np.ones(n), 0.5 * np.sin(np.pi * x)], lambda t: [1.0, math.exp(-t)])
     src = P.SeparableField([np.sin(np.pi * x)], lambda t: [1.0 + t])
@@ -104,26 +160,31 @@ def test_cfg3_first_levels_vs_oracle():
     soe = P.build_soe(gam, 1e-12, (1.0 / M) ** r, 1.0)
     dev = torch.device("cuda:0")
     u0 = (1.0 - x * x) ** 2
-    m = FidsMarch(gam, alpha, 1.0, 1.0, M, r, N, soe, method=0, precond=1, tol=1e-12,
+    m = FidsMarch(gam, alpha, 1.0, 1.0, M, r, n + 1, soe, method=0, precond=1, tol=1e-12,
                   max_iters=None, B=1, kappa=_field_separable(kap, x, mesh.t, 1, None, dev),
                   source=_field_separable(src, x, mesh.t, 1, None, dev),
-                  u0=torch.from_numpy(u0[None, :].copy()).to(dev), hist_B=1, device=0)
-    levels = 3
-    m.run(levels)
-    torch.cuda.synchronize()
-    hist = m.hist[: levels + 1, 0].cpu().numpy()
-    its = m.iters[:levels, 0].cpu().numpy()
-    # oracle, same levels
-    t, tau = O.graded_mesh(M, r, 1.0)
-    col, h, _ = O.ifl_column(alpha, 1.0 + alpha / 2.0, 1.0, N)
-    _, symbol = O.toeplitz_symbol(col)
-    lam = O.strang_eigs(col)
-    G = math.exp(math.lgamma(1.0 - gam))
-    s, w = soe.nodes, soe.weights
-    W = np.zeros((s.size, n))
-    u = u0.copy()
-    for k in range(1, levels + 1):
-        u, _, out = O.fids_step(u, W, s, w, tau[k - 1], gam, G, kappa(x, t[k]), source(x, t[k]),
-                                symbol, lam, 1e-12)
-        assert rel_l2(hist[k], u) <= 1e-10, k
-        assert abs(int(its[k - 1]) - out.iterations) <= 2, (k, its[k - 1], out.iterations)
+                  u0=torch.from_numpy(u0[None, :].copy()).to(dev), device=0)
+    sub = int(g["sub"][0])
+    Pj = np.random.default_rng(int(g["proj_seed"][0])).standard_normal((4, n))
+    done = 0
+    for lv in g["levels"]:
+        m.run(int(lv) - done)
+        done = int(lv)
+        u = m.u_level(done)[0].cpu().numpy()
+        e_sub = rel_l2(u[::sub], g[f"u{lv}_sub"])
+        nref = float(g[f"u{lv}_norm"][0])
+        e_norm = abs(np.linalg.norm(u) - nref) / nref
+        e_proj = float(np.max(np.abs(Pj @ u - g[f"u{lv}_proj"]))) / (nref * math.sqrt(n))
+        tol_u = max(1e-10, 10 * floor[f"rel_l2_u{lv}"])
+        print(f"cfg3 level {lv}: sub rel-l2 {e_sub:.2e} norm {e_norm:.2e} proj {e_proj:.2e} "
+              f"(floor {floor[f'rel_l2_u{lv}']:.2e})")
+        assert e_sub <= tol_u and e_norm <= tol_u and e_proj <= tol_u, lv
+    res = m.result()
+    assert np.all(res.status == 0)
+    d = res.iterations[:, 0] - g["its"]
+    frac = float(np.mean(np.abs(d) <= 1))
+    print(f"cfg3: within+-1 {frac:.3f} (floor {floor['within1']:.3f}) mean d {d.mean():+.3f} "
+          f"(floor {floor['mean_d']:+.3f}) max|d| {np.abs(d).max()} (floor {floor['max_abs_d']})")
+    assert frac >= min(0.95, floor["within1"] - 0.05)
+    assert abs(d.mean()) <= max(0.1, 3.0 * d.std() / math.sqrt(d.size)), (d.mean(), d.std())
+    assert np.max(np.abs(d)) <= 2 * max(2, floor["max_abs_d"])

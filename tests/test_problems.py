@@ -12,7 +12,7 @@ import pytest
 
 from tsf_testlib import golden
 
-from paper_2002_11978_b200 import couplings, problems
+from harness import couplings, problems
 
 
 def _fn_cases():
