@@ -262,7 +262,9 @@ int Dispatch<LOG>::fft(int inverse, int B, const double2* in, double2* out, cons
   constexpr int N = 1 << (LOG - 1);
   using S = KShape<N>;
   constexpr int E = FShape<N>::E;
-  constexpr int smem = (kFftInPlace ? 1 : 2) * FftPlan<N, E>::SMEM_ELEMS * 16 + tw_table_elems(N) * 16;
+  constexpr int smem = use64<N>() ? f64::kBytes
+                                  : (kFftInPlace ? 1 : 2) * FftPlan<N, E>::SMEM_ELEMS * 16 +
+                                        tw_table_elems(N) * 16;
   cudaError_t e;
   if (inverse) {
     auto k = k_fft_debug<N, E, true>;

@@ -29,6 +29,7 @@
 #pragma once
 
 #include "tsf_fft.cuh"
+#include "tsf_fft64.cuh"
 
 namespace tsf {
 
@@ -74,7 +75,8 @@ constexpr int kSmemCap = 227 * 1024;       // dynamic shared memory per CTA
 constexpr int kSmemPerSM = 228 * 1024;
 template <int N>
 struct FStage {
-  static constexpr int FFT_BYTES = (kFftInPlace ? 1 : 2) * FftPlan<N, kE>::SMEM_ELEMS * 16;
+  static constexpr int FFT_BYTES =
+      use64<N>() ? f64::kBytes : (kFftInPlace ? 1 : 2) * FftPlan<N, kE>::SMEM_ELEMS * 16;
   static constexpr int TW_BYTES = tw_table_elems(2 * N) * 16;
   static constexpr int PTW_BYTES = kPassTw        ? FftPlan<N, kE>::PTW_ELEMS * 16
                                    : kPassTwSmall ? FftPlan<N, kE>::PTWS_ELEMS * 16
@@ -101,6 +103,22 @@ TSF_D double2 mv_spec(const FilterTables& t, int k) {
   else return ldt(&t.mvS[k]);
 }
 
+// The filters' transforms: the 64 x 64 engine (tsf_fft64.cuh) at N = 4096,
+// the radix-8 Stockham engine (tsf_fft.cuh) otherwise.  Slot c of thread t
+// holds index oidx<N>(t, c) in both domains.
+template <int N, bool INV, class Hook = NoHook>
+TSF_D void xfft(double2 (&v)[FShape<N>::E], double2* sm, const FilterTables& t,
+                const Hook& hook = Hook{}) {
+  if constexpr (use64<N>()) fft64<INV>(v, sm, hook);
+  else block_fft<N, FShape<N>::E, INV>(v, sm, t.tw, 1, xtw(t), hook);
+}
+template <int N, class Hook = NoHook>
+TSF_D void xfft_real(const double (&x)[FShape<N>::E], double2 (&v)[FShape<N>::E], double2* sm,
+                     const FilterTables& t, const Hook& hook = Hook{}) {
+  if constexpr (use64<N>()) fft64_real(x, v, sm, hook);
+  else block_fft_real<N, FShape<N>::E>(x, v, sm, t.tw, 1, xtw(t), hook);
+}
+
 // even output bins: z <- IFFT_N( S_even . FFT_N(x) ) for real x; caller keeps Re(z)
 template <int N, class Hook = NoHook>
 TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E], double2* sm,
@@ -109,17 +127,17 @@ TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E]
   constexpr int E = FShape<N>::E;
   const bool own = threadIdx.x < T;
   double se[E];
-  block_fft_real<N, E>(x, z, sm, t.tw, 1, xtw(t), [&] {
+  xfft_real<N>(x, z, sm, t, [&] {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) se[c] = mv_spec<N>(t, threadIdx.x + c * T).x;
+      for (int c = 0; c < E; ++c) se[c] = mv_spec<N>(t, oidx<N>(threadIdx.x, c)).x;
     }
   });
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = cscale(z[c], se[c]);
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t), inv_hook);
+  xfft<N, true>(z, sm, t, inv_hook);
 }
 
 // odd output bins: z (already modulated by w_j) <- IFFT_N( S_odd . FFT_N(z) );
@@ -133,17 +151,17 @@ TSF_D void filt_odd(double2 (&z)[FShape<N>::E], double2* sm, const FilterTables&
   constexpr int E = FShape<N>::E;
   const bool own = threadIdx.x < T;
   double so[E];
-  block_fft<N, E, false>(z, sm, t.tw, 1, xtw(t), [&] {
+  xfft<N, false>(z, sm, t, [&] {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) so[c] = mv_spec<N>(t, threadIdx.x + c * T).y;
+      for (int c = 0; c < E; ++c) so[c] = mv_spec<N>(t, oidx<N>(threadIdx.x, c)).y;
     }
   });
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = cscale(z[c], so[c]);
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t), inv_hook);
+  xfft<N, true>(z, sm, t, inv_hook);
 }
 
 // Strang: z <- IFFT_n( FFT_n(x) . Ssym / n ) for real x, n = N; caller keeps Re(z)
@@ -153,16 +171,16 @@ TSF_D void filt_strang(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::
   constexpr int T = FShape<N>::T;
   constexpr int E = FShape<N>::E;
   constexpr double inv_n = 1.0 / N;
-  block_fft_real<N, E>(x, z, sm, t.tw, 1, xtw(t));
+  xfft_real<N>(x, z, sm, t);
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const double2 lam = ldt(&t.pclam[threadIdx.x + c * T]);
+      const double2 lam = ldt(&t.pclam[oidx<N>(threadIdx.x, c)]);
       const double s = 0.5 * (rcp_pos(d + kbar * lam.x) + rcp_pos(d + kbar * lam.y));
       z[c] = cscale(z[c], s * inv_n);
     }
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t));
+  xfft<N, true>(z, sm, t);
 }
 
 // Strang with a precomputed per-instance spectrum spec[k] = S_k / n (the level
@@ -186,21 +204,21 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
   constexpr int E = FShape<N>::E;
   double sp[E];
   const bool own = threadIdx.x < T;
-  block_fft_real<N, E>(x, z, sm, t.tw, 1, xtw(t), [&] {
+  xfft_real<N>(x, z, sm, t, [&] {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) sp[c] = spec[threadIdx.x + c * T];
+      for (int c = 0; c < E; ++c) sp[c] = spec[oidx<N>(threadIdx.x, c)];
     }
   });
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int k = threadIdx.x + c * T;
+      const int k = oidx<N>(threadIdx.x, c);
       z[c] = cscale(z[c], sp[c]);
       if (hs && k <= N / 2) hs[k] = z[c];
     }
   }
-  block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t));
+  xfft<N, true>(z, sm, t);
 }
 
 // even output bins of the Toeplitz product from a stored half spectrum:
@@ -213,7 +231,7 @@ TSF_D void load_even_spec(const double2* hs, const FilterTables& t, double2 (&z)
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int k = threadIdx.x + c * T;
+      const int k = oidx<N>(threadIdx.x, c);
       const double2 h = k <= N / 2 ? hs[k] : cconj(hs[N - k]);
       z[c] = cscale(h, mv_spec<N>(t, k).x * N);  // N S/L: exact (N a power of two)
     }
@@ -223,7 +241,7 @@ template <int N, class Hook = NoHook>
 TSF_D void filt_even_spec(const double2* hs, double2 (&z)[FShape<N>::E], double2* sm,
                           const FilterTables& t, const Hook& inv_hook = Hook{}) {
   load_even_spec<N>(hs, t, z);
-  block_fft<N, FShape<N>::E, true>(z, sm, t.tw, 1, xtw(t), inv_hook);
+  xfft<N, true>(z, sm, t, inv_hook);
 }
 
 // w_j = W_L^j for the owned slots
@@ -238,6 +256,12 @@ template <int N>
 TSF_D FilterTables stage_tables(const FilterTables& g, double2* dst, const double* ps_src = nullptr) {
   constexpr int NT = tw_table_elems(2 * N);
   for (int i = threadIdx.x; i < NT; i += blockDim.x) dst[i] = ldt(&g.tw[i]);
+  if constexpr (use64<N>()) {
+    // the transform region starts FFT_BYTES + N doubles before dst (kernel
+    // layout: transform | real staging vector | twiddle table | ...)
+    stage_fft64_tables(reinterpret_cast<double2*>(reinterpret_cast<char*>(dst) -
+                                                  FStage<N>::FFT_BYTES - N * 8));
+  }
   FilterTables t = g;
   t.tw = dst;
   double2* next = dst + NT;

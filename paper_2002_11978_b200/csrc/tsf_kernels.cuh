@@ -103,41 +103,41 @@ TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restric
   auto load_x = [&] {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) xo[c] = ld_real(xg, n, tid + c * T);
+      for (int c = 0; c < E; ++c) xo[c] = ld_real(xg, n, oidx<N>(tid, c));
     }
   };
   auto load_k = [&] {
     if (own && kg) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) ko[c] = ld_real(kg, n, tid + c * T);
+      for (int c = 0; c < E; ++c) ko[c] = ld_real(kg, n, oidx<N>(tid, c));
     }
   };
   if (hz) {
     // even-channel spectrum preloaded by the phase kernel (k_bicg_phase)
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = hz[c];
-    block_fft<N, E, true>(z, sm, t.tw, 1, xtw(t), load_x);
+    xfft<N, true>(z, sm, t, load_x);
   } else if (hs) {
     filt_even_spec<N>(hs, z, sm, t, load_x);   // x = Re IFFT(hs): its spectrum is known
   } else {
     double xr[FShape<N>::E];
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) xr[c] = ld_real(xg, n, tid + c * T);
+      for (int c = 0; c < E; ++c) xr[c] = ld_real(xg, n, oidx<N>(tid, c));
     }
     filt_even<N>(xr, z, sm, t, load_x);
   }
   if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) aux[tid + c * T] = z[c].x;
+    for (int c = 0; c < E; ++c) aux[oidx<N>(tid, c)] = z[c].x;
 #pragma unroll
-    for (int c = 0; c < E; ++c) z[c] = cscale(modulation(t, tid + c * T), xo[c]);
+    for (int c = 0; c < E; ++c) z[c] = cscale(modulation(t, oidx<N>(tid, c)), xo[c]);
   }
   filt_odd<N>(z, sm, t, load_k);
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       const double2 w = modulation(t, j);
       const double ax = aux[j] + fma(z[c].x, w.x, z[c].y * w.y);  // + Re(conj(w) z)
       y[c] = kg ? fma(shift, xo[c], ko[c] * ax) : ax;
@@ -160,7 +160,7 @@ k_toeplitz_apply(int n, const double* __restrict__ x, double* __restrict__ y,
   apply_level_op<N>(x + off, kappa ? kappa + off : nullptr, shift, n, out, sm, aux, ts);
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) st_real(y + off, n, tid + c * T, out[c]);
+    for (int c = 0; c < KShape<N>::E; ++c) st_real(y + off, n, oidx<N>(tid, c), out[c]);
   }
 }
 
@@ -180,12 +180,12 @@ k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ zo, dou
   double xr[FShape<N>::E];
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) xr[c] = ld_real(v + off, n, tid + c * T);
+    for (int c = 0; c < KShape<N>::E; ++c) xr[c] = ld_real(v + off, n, oidx<N>(tid, c));
   }
   filt_strang<N>(xr, z, sm, ts, shift, kb);
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) st_real(zo + off, n, tid + c * T, z[c].x);
+    for (int c = 0; c < KShape<N>::E; ++c) st_real(zo + off, n, oidx<N>(tid, c), z[c].x);
   }
 }
 
@@ -220,7 +220,7 @@ TSF_D void load_owned(double (&u)[FShape<N>::E], const double* g, int n) {
   const int tid = threadIdx.x;
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) u[c] = ld_real(g, n, tid + c * T);
+    for (int c = 0; c < KShape<N>::E; ++c) u[c] = ld_real(g, n, oidx<N>(tid, c));
   }
 }
 template <int N>
@@ -229,7 +229,7 @@ TSF_D void store_owned(double* g, const double (&u)[FShape<N>::E], int n) {
   const int tid = threadIdx.x;
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) st_real(g, n, tid + c * T, u[c]);
+    for (int c = 0; c < KShape<N>::E; ++c) st_real(g, n, oidx<N>(tid, c), u[c]);
   }
 }
 // dst = P^{-1} u (u real, owned slots); spec = the instance's S_k / n
@@ -241,7 +241,7 @@ TSF_D void precond_store(const double (&u)[FShape<N>::E], double* dst, int n, co
   filt_strang_tab<N>(u, z, sm, t, t.ps ? t.ps : spec, hs);
   if (threadIdx.x < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) st_real(dst, n, threadIdx.x + c * T, z[c].x);
+    for (int c = 0; c < KShape<N>::E; ++c) st_real(dst, n, oidx<N>(threadIdx.x, c), z[c].x);
   }
 }
 
@@ -276,7 +276,7 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       if (j < n) {
         double k;
         if (a.kappa) {
@@ -316,7 +316,7 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
     if (own) {
 #pragma unroll
       for (int c = 0; c < E; ++c) {
-        const int j = tid + c * T;
+        const int j = oidx<N>(tid, c);
         const double2 lam = ldt(&tab.pclam[j]);
         a.pspec[off + j] = 0.5 * (1.0 / (d + kbar * lam.x) + 1.0 / (d + kbar * lam.y)) / n;
       }
@@ -329,7 +329,7 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       st_real(a.x + off, n, j, 0.0);
       if (j < n) ss = fma(u[c], u[c], ss);
     }
@@ -351,7 +351,7 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
       if (own) {
 #pragma unroll
         for (int c = 0; c < E; ++c) {
-          const int j = tid + c * T;
+          const int j = oidx<N>(tid, c);
           if (j < n) part = fma(u[c], a.p[off + j], part);
         }
       }
@@ -400,7 +400,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       r0v[c] = ld_real(a.rhs + off, n, j);
       rv[c] = ld_real(rc, n, j);
     }
@@ -410,7 +410,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       if (j < n) part = fma(r0v[c], u[c], part);
     }
   }
@@ -425,7 +425,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       u[c] = rv[c] - alpha * u[c];
       if (j < n) part = fma(u[c], u[c], part);
     }
@@ -436,7 +436,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
     if (own) {
 #pragma unroll
       for (int c = 0; c < E; ++c) {
-        const int j = tid + c * T;
+        const int j = oidx<N>(tid, c);
         st_real(a.x + off, n, j, ld_real(a.x + off, n, j) + alpha * ld_real(phg, n, j));
       }
     }
@@ -486,7 +486,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       sv[c] = ld_real(a.s + off, n, j);
       xv[c] = ld_real(a.x + off, n, j);
       pv[c] = ld_real(phg, n, j);
@@ -500,7 +500,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       if (j < n) {
         red2.v[0] = fma(u[c], u[c], red2.v[0]);
         red2.v[1] = fma(u[c], sv[c], red2.v[1]);
@@ -519,7 +519,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       st_real(a.x + off, n, j, xv[c] + (s.alpha * pv[c] + omega * shv[c]));
       u[c] = sv[c] - omega * u[c];
       st_real(a.r + off, n, j, u[c]);
@@ -532,8 +532,8 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
     // during the reduction
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      qv[c] = ld_real(a.p + off, n, tid + c * T);
-      vv[c] = ld_real(a.v + off, n, tid + c * T);
+      qv[c] = ld_real(a.p + off, n, oidx<N>(tid, c));
+      vv[c] = ld_real(a.v + off, n, oidx<N>(tid, c));
     }
   }
   red2 = block_sum<2>(red2, red);
@@ -595,7 +595,7 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       if (j < n) part = fma(a.p[off + j], u[c], part);
     }
   }
@@ -609,7 +609,7 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       st_real(a.x + off, n, j, ld_real(a.x + off, n, j) + al * ld_real(a.p + off, n, j));
       u[c] = ld_real(a.r + off, n, j) - al * u[c];
       if (j < n) part = fma(u[c], u[c], part);
@@ -634,7 +634,7 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       if (j < n) part = fma(u[c], zg[j], part);
     }
   }
@@ -643,7 +643,7 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = tid + c * T;
+      const int j = oidx<N>(tid, c);
       st_real(a.p + off, n, j, ld_real(zg, n, j) + beta * ld_real(a.p + off, n, j));
     }
   }
@@ -725,6 +725,7 @@ TSF_D void bicg_phase(const KrylovArgs& a, KState* st, int* active) {
       const int i = threadIdx.x + q * BL;
       if (i < NT) tws[i] = twv[q];
     }
+    if constexpr (use64<N>()) stage_fft64_tables(sm);
     tab.tw = tws;   // published by the first transform's leading barrier
     if constexpr (TPHASE) dev_bicg_t<N, PC>(a, tab, st, active, sm, red, &s, pre_spec ? hz : nullptr);
     else dev_bicg_v<N, PC>(a, tab, st, active, sm, red, &s, pre_spec ? hz : nullptr);
@@ -778,21 +779,31 @@ template <int N, int E, bool INV>
 __global__ void k_fft_debug(const double2* __restrict__ in, double2* __restrict__ out,
                             const double2* tw, int tw_log_scale) {
   extern __shared__ double2 sm[];
-  constexpr int T = N / E;
   const int tid = threadIdx.x;  // debug transform: E complex slots per thread
   const long off = (long)blockIdx.x * N;
-  double2* tws = sm + (kFftInPlace ? 1 : 2) * FftPlan<N, E>::SMEM_ELEMS;
-  for (int i = tid; i < tw_table_elems(N); i += blockDim.x) tws[i] = ldt(&tw[i]);
-  tw = tws;
   double2 v[E];
-  if (tid < T) {
+  if constexpr (use64<N>() && E == 8) {
+    // the filters' 64 x 64 engine: natural order in and out via oidx
+    stage_fft64_tables(sm);
 #pragma unroll
-    for (int c = 0; c < E; ++c) v[c] = in[off + tid + c * T];
-  }
-  block_fft<N, E, INV>(v, sm, tw, tw_log_scale);
-  if (tid < T) {
+    for (int c = 0; c < E; ++c) v[c] = in[off + oidx<N>(tid, c)];
+    fft64<INV>(v, sm);
 #pragma unroll
-    for (int c = 0; c < E; ++c) out[off + tid + c * T] = v[c];
+    for (int c = 0; c < E; ++c) out[off + oidx<N>(tid, c)] = v[c];
+  } else {
+    constexpr int T = N / E;
+    double2* tws = sm + (kFftInPlace ? 1 : 2) * FftPlan<N, E>::SMEM_ELEMS;
+    for (int i = tid; i < tw_table_elems(N); i += blockDim.x) tws[i] = ldt(&tw[i]);
+    tw = tws;
+    if (tid < T) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) v[c] = in[off + tid + c * T];
+    }
+    block_fft<N, E, INV>(v, sm, tw, tw_log_scale);
+    if (tid < T) {
+#pragma unroll
+      for (int c = 0; c < E; ++c) out[off + tid + c * T] = v[c];
+    }
   }
 }
 
