@@ -121,6 +121,9 @@ def test_cfg2_full_size_vs_reference_goldens():
     rows.sort(key=lambda r: r[1])
     for r in rows[:6]:
         print("cfg2 b%d: within+-1 %.3f (swap floor %.3f) max|d| %d e64 %.2e eM %.2e" % r)
+    D0 = np.concatenate(all_d)
+    print(f"cfg2 x{len(idx)} pooled: within+-1 {np.mean(np.abs(D0) <= 1):.4f} (floor "
+          f"{floor['pooled']['within1']:.4f}) mean d {D0.mean():+.4f} max|d| {np.abs(D0).max()}")
     # iterations per instance: which instances sit at the rounding floor (the
     # stopping test at tol 1e-12 decided by round-off, SURVEY §7 hard part 1)
     # differs between ANY two FFT engines — the reference's own swap puts
