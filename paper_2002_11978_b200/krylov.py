@@ -109,6 +109,25 @@ def _psolve_of(precond):
     return precond
 
 
+def _caller_convention(fn, device_native: bool):
+    """A user operator / preconditioner callable in the caller's convention:
+    the package's own device operators (LevelOperator, the Strang
+    CirculantPreconditioner) and callers that pass torch tensors get device
+    tensors; a caller that passed numpy gets numpy in and numpy out, as the
+    reference's callables do (krylov.py:19-24, 35-40) — e.g. the reference's
+    dense test operators `lambda v: A @ v`."""
+    if device_native:
+        return lambda v: _arrays.to_device(fn(v))[0]
+    return lambda v: _arrays.to_device(np.asarray(fn(v.detach().cpu().numpy()), dtype=float))[0]
+
+
+def _native_parts(op, precond, as_np: bool):
+    from .toeplitz import CirculantPreconditioner
+    op_native = isinstance(op, LevelOperator) or not as_np
+    pc_native = precond is None or isinstance(precond, CirculantPreconditioner) or not as_np
+    return op_native, pc_native
+
+
 def _generic_bicgstab(op, precond, rhs, tol, max_iters):
     torch = _native.torch_mod()
     b, as_np = _arrays.to_device(rhs)
@@ -117,8 +136,9 @@ def _generic_bicgstab(op, precond, rhs, tol, max_iters):
         raise ValueError(f"rhs has shape {tuple(b.shape)}, operator order is {n}")
     max_iters = max_iters if max_iters is not None else 10 * n
     ps = _psolve_of(precond)
-    ap = lambda v: _arrays.to_device(op.apply(v))[0]  # noqa: E731
-    pss = lambda v: _arrays.to_device(ps(v))[0]  # noqa: E731
+    op_native, pc_native = _native_parts(op, precond, as_np)
+    ap = _caller_convention(op.apply, op_native)
+    pss = _caller_convention(ps, pc_native)
     x = torch.zeros_like(b)
     r = b.clone()
     r0 = b.clone()
@@ -177,8 +197,9 @@ def _generic_cg(op, precond, rhs, tol, max_iters):
         raise ValueError(f"rhs has shape {tuple(b.shape)}, operator order is {n}")
     max_iters = max_iters if max_iters is not None else 10 * n
     ps = _psolve_of(precond)
-    ap = lambda v: _arrays.to_device(op.apply(v))[0]  # noqa: E731
-    pss = lambda v: _arrays.to_device(ps(v))[0]  # noqa: E731
+    op_native, pc_native = _native_parts(op, precond, as_np)
+    ap = _caller_convention(op.apply, op_native)
+    pss = _caller_convention(ps, pc_native)
     x = torch.zeros_like(b)
     r = b.clone()
     nrm0 = float(torch.linalg.norm(r))
