@@ -51,15 +51,26 @@ CFG3_SUB = 16          # sub-sampling stride of the stored configs[3] levels
 CFG3_PROJ_SEED = 33
 
 
-def _reference(swap: bool):
+def _reference(swap):
+    """The reference with its FFT engine as given: False = stock numpy
+    pocketfft; True / "scipy" = scipy.fft (note: scipy's complex ifft is
+    bit-identical to numpy's, only real-input forward transforms differ);
+    "exact" = the correctly rounded DFT (scipy.fft in long double, rounded
+    once to double) — the most accurate engine there is, so its spread
+    against the stock run is the floor ANY accurate second engine sees."""
     from gen_golden import _import_reference
     tsfrac = _import_reference()
     if swap:
+        import numpy as _np
         import scipy.fft as sf
         import tsfrac.fourier as fourier
         import tsfrac.toeplitz as tz
-        fourier.fft = lambda x: sf.fft(x)
-        fourier.ifft = lambda x: sf.ifft(x)
+        if swap == "exact":
+            fourier.fft = lambda x: sf.fft(_np.asarray(x).astype(_np.clongdouble)).astype(_np.complex128)
+            fourier.ifft = lambda x: sf.ifft(_np.asarray(x).astype(_np.clongdouble)).astype(_np.complex128)
+        else:
+            fourier.fft = lambda x: sf.fft(x)
+            fourier.ifft = lambda x: sf.ifft(x)
         tz.fourier = fourier
     return tsfrac
 
@@ -162,6 +173,27 @@ def run_cfg2(pool):
     print("cfg2 floor pooled", floor["pooled"], flush=True)
 
 
+def run_cfg2_exact(pool):
+    """cfg2_floor.json gains per-instance and pooled stats of the correctly
+    rounded engine against the stock run (the realistic floor)."""
+    g = np.load(OUT / "cfg2_many.npz")
+    floor = json.loads((OUT / "cfg2_floor.json").read_text())
+    res = pool.map(_cfg2_one, [(int(b), "exact") for b in g["instances"]])
+    all_d = []
+    ex = {}
+    for b, _, its, u64, uM in res:
+        d = its - g[f"b{b}_its"]
+        all_d.append(d)
+        ex[f"b{b}"] = dict(_stats(d), rel_l2_uM=_rl2(uM, g[f"b{b}_uM"]),
+                           rel_l2_u64=_rl2(u64, g[f"b{b}_u64"]))
+    D = np.concatenate(all_d)
+    ex["pooled"] = dict(_stats(D), min_within1=min(v["within1"] for v in ex.values()),
+                        max_rel_l2_uM=max(v["rel_l2_uM"] for v in ex.values()))
+    floor["exact_engine"] = ex
+    (OUT / "cfg2_floor.json").write_text(json.dumps(floor, indent=1) + "\n")
+    print("cfg2 exact-engine floor pooled", ex["pooled"], flush=True)
+
+
 def run_cfg3(pool):
     res = dict((s, (its, keep)) for s, its, keep in pool.map(_cfg3_one, [False, True]))
     its, keep = res[False]
@@ -195,6 +227,8 @@ def main():
             a3 = pool.map_async(_cfg3_one, [False, True])
         if "cfg2" in which:
             run_cfg2(pool)
+        if "cfg2exact" in which:
+            run_cfg2_exact(pool)
         if "cfg3" in which:
             res = a3.get()
 

@@ -147,6 +147,8 @@ struct tsf_plan {
   double2* mvS = nullptr;  // (S_{2k}, S_{2k+1}) / L, even part of the symbol
   double2* pclam = nullptr;  // (lam_k, lam_{n-k})
   double2* ptw = nullptr;    // per-pass twiddles of the length-L/2 transform
+  int layout = 0;            // 1: 64 x 64 engine (permuted tables / workspaces)
+  int vs = 0;                // per-instance stride of the workspace vectors
   // Krylov workspaces [cap][n] x 6
   int cap = 0;
   double* ws = nullptr;
@@ -187,6 +189,10 @@ struct PrecondF {
   static int call(A... a) { return Dispatch<LOG>::precond(a...); }
 };
 template <int LOG>
+struct LayoutF {
+  static int call() { return Dispatch<LOG>::layout(); }
+};
+template <int LOG>
 struct SolveF {
   template <typename... A>
   static int call(A... a) { return Dispatch<LOG>::solve(a...); }
@@ -198,6 +204,7 @@ struct FftF {
 };
 
 
+constexpr int kWsVectors = 11;
 int ensure_reserved(tsf_plan* p, int B) {
   if (p->large) {
     const int rc = large_reserve(p->large, B);
@@ -215,8 +222,11 @@ int ensure_reserved(tsf_plan* p, int B) {
   p->kst = nullptr;
   p->cap = 0;
   CK(cudaSetDevice(p->device));
-  // 9 vectors [B][n] + the Strang half spectra [B][L/4+1] complex (hspec)
-  CK(cudaMalloc(&p->ws, sizeof(double) * ((size_t)B * p->n * 9 + (size_t)B * (p->L / 2 + 2))));
+  // 11 vectors [B][vs] (r p v ph s sh t kwork pspec r0w xw) + the Strang
+  // spectra of the last preconditioner output (hspec): half spectra
+  // [B][L/4+1] complex, full [B][L/2] complex for the 64 x 64 engine
+  const size_t hs = p->layout ? (size_t)p->L : (size_t)(p->L / 2 + 2);
+  CK(cudaMalloc(&p->ws, sizeof(double) * ((size_t)B * p->vs * kWsVectors + (size_t)B * hs)));
   CK(cudaMalloc(&p->ist, sizeof(int) * (size_t)B * 2));
   CK(cudaMalloc(&p->dst, sizeof(double) * (size_t)B));
   CK(cudaMalloc(&p->kst, sizeof(KState) * (size_t)B));
@@ -294,6 +304,8 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
     return rc;
   };
   if (cudaSetDevice(device) != cudaSuccess) return cleanup(fail(TSF_E_CUDA, "cudaSetDevice(%d)", device));
+  p->layout = ForLog<LayoutF>::run(lg);
+  p->vs = p->layout ? L / 2 : n;
   // twiddles W_L^e: modulation of the odd-bin half; the length-N transforms use stride 2
   std::vector<double2> tw = twiddle_table(L);
   // The reference keeps Re IFFT(S . FFT(pad x)) (toeplitz.py:62-63): its
@@ -309,6 +321,20 @@ int tsf_plan_create(tsf_plan** out, int n, int L, const double* symbol_re, const
   if (lam) {
     pl.resize(n);
     for (int k = 0; k < n; ++k) pl[k] = make_double2(lam[k], lam[(n - k) % n]);
+  }
+  if (p->layout) {
+    // 64 x 64 engine: bin oidx(t, c) stored at position spos(t, c)
+    // (tsf_fft64.cuh), so a warp's table loads are contiguous
+    const int N = L / 2, T = N / 8;
+    auto permute = [&](std::vector<double2>& v) {
+      if (v.empty()) return;
+      std::vector<double2> w(v.size());
+      for (int t = 0; t < T; ++t)
+        for (int c = 0; c < 8; ++c) w[t + c * T] = v[oidx<4096>(t, c)];
+      v.swap(w);
+    };
+    permute(S);
+    permute(pl);
   }
   auto up = [&](auto** d, const auto& h) -> int {
     if (h.empty()) return TSF_SUCCESS;
@@ -395,9 +421,10 @@ static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cud
   }
   int rc = ensure_reserved(p, B);
   if (rc) return rc;
-  const size_t vn = (size_t)p->cap * p->n;
+  const size_t vn = (size_t)p->cap * p->vs;
   a.n = p->n;
   a.B = B;
+  a.vs = p->vs;
   a.r = p->ws;
   a.p = p->ws + vn;
   a.v = p->ws + 2 * vn;
@@ -406,7 +433,15 @@ static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cud
   a.sh = p->ws + 5 * vn;
   a.t = p->ws + 6 * vn;
   a.pspec = p->ws + 8 * vn;
-  a.hspec = spec_reuse() ? reinterpret_cast<double2*>(p->ws + 9 * vn) : nullptr;
+  a.hspec = spec_reuse() ? reinterpret_cast<double2*>(p->ws + kWsVectors * vn) : nullptr;
+  if (p->layout) {
+    a.r0w = p->ws + 9 * vn;
+    a.xw = p->ws + 10 * vn;
+    a.kwork = p->ws + 7 * vn;   // internal layout (the caller's kwork has stride n)
+  } else {
+    a.r0w = a.rhs;
+    a.xw = a.x;
+  }
   a.kst = p->kst;
   a.active = p->ist;
   a.h_active = p->h_active;

@@ -45,6 +45,9 @@ struct Dispatch {
   static int solve(int B, int method, int pc, const KrylovArgs& a, cudaStream_t st);
   static int fft(int inverse, int B, const double2* in, double2* out, const double2* tw,
                  cudaStream_t st);
+  // 1: the 64 x 64 engine (tsf_fft64.cuh) — plan tables and workspace
+  // vectors in the permuted internal layout, per-instance stride N
+  static int layout();
 };
 
 #define TSF_EXTERN_DISPATCH(L) extern template struct Dispatch<L>;

@@ -79,24 +79,27 @@ cudaKernelNodeParams knode(K kernel, dim3 grid, dim3 block, int smem, void** arg
 
 // Instance group [o, o + Bg) of a level solve: every per-instance pointer
 // offset, its own active counter (a.active + g).
-inline KrylovArgs group_args(const KrylovArgs& a, int N, int o, int Bg, int g) {
+inline KrylovArgs group_args(const KrylovArgs& a, int N, bool full_spec, int o, int Bg, int g) {
   KrylovArgs r = a;
-  const long vo = (long)o * a.n;
+  const long vo = (long)o * a.n;    // caller vectors
+  const long wo = (long)o * a.vs;   // workspace vectors
   r.B = Bg;
   r.rhs = a.rhs + vo;
   r.x = a.x + vo;
+  r.r0w = a.r0w == a.rhs ? r.rhs : a.r0w + wo;
+  r.xw = a.xw == a.x ? r.x : a.xw + wo;
   if (a.kappa) r.kappa = a.kappa + vo;
   if (a.kmodes) r.kmodes = a.kmodes + (long)o * a.kb_stride;
-  if (a.kwork) r.kwork = a.kwork + vo;
-  r.r = a.r + vo;
-  r.p = a.p + vo;
-  r.v = a.v + vo;
-  r.ph = a.ph + vo;
-  r.s = a.s + vo;
-  r.sh = a.sh + vo;
-  r.t = a.t + vo;
-  if (a.pspec) r.pspec = a.pspec + vo;
-  if (a.hspec) r.hspec = a.hspec + (long)o * (N / 2 + 1);
+  if (a.kwork) r.kwork = a.kwork + wo;
+  r.r = a.r + wo;
+  r.p = a.p + wo;
+  r.v = a.v + wo;
+  r.ph = a.ph + wo;
+  r.s = a.s + wo;
+  r.sh = a.sh + wo;
+  r.t = a.t + wo;
+  if (a.pspec) r.pspec = a.pspec + wo;
+  if (a.hspec) r.hspec = a.hspec + (long)o * (full_spec ? N : N / 2 + 1);
   r.kst = a.kst + o;
   r.active = a.active + g;
   r.iters = a.iters + o;
@@ -140,7 +143,7 @@ int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
   for (int g = 0; g < ng; ++g) {
     const int o = g * bg;
     const int Bg = std::min(bg, B - o);
-    KrylovArgs a = group_args(a_in, N, o, Bg, g);
+    KrylovArgs a = group_args(a_in, N, use64<N>(), o, Bg, g);
     KState* kst = a.kst;
     int* active = a.active;
     int bval = Bg;
@@ -254,6 +257,11 @@ int Dispatch<LOG>::solve(int B, int method, int pc, const KrylovArgs& a, cudaStr
   constexpr int N = 1 << (LOG - 1);
   if (method == 0) return pc ? solve_t<N, 1, false>(B, a, st) : solve_t<N, 0, false>(B, a, st);
   return pc ? solve_t<N, 1, true>(B, a, st) : solve_t<N, 0, true>(B, a, st);
+}
+
+template <int LOG>
+int Dispatch<LOG>::layout() {
+  return use64<(1 << (LOG - 1))>() ? 1 : 0;
 }
 
 template <int LOG>

@@ -68,6 +68,19 @@ TSF_HD int oidx(int tid, int c) {
   else return tid + c * (N / TSF_KE);
 }
 
+// storage position of slot c of thread tid in the workspace vectors, the
+// spectrum tables and the shared staging vector: thread-major, so a warp's
+// access at fixed c is 32 consecutive doubles.  Equal to oidx for the
+// Stockham engine; for the 64 x 64 engine the Krylov workspace vectors, the
+// Strang spectra and the plan's spectrum tables are stored permuted this way
+// (index oidx(t, c) at position spos(t, c)) — with the logical order a warp
+// touched 8 lines per access (ncu: LSU/MIO throttling, 8-way conflicts on
+// the staging vector).  Caller-visible vectors keep the natural order.
+template <int N>
+TSF_HD int spos(int tid, int c) {
+  return tid + c * (N / TSF_KE);
+}
+
 // copy the twiddle tables into the transform region (published by the first
 // transform's leading barrier)
 TSF_D void stage_fft64_tables(double2* sm) {

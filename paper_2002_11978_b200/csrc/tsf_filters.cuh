@@ -130,7 +130,7 @@ TSF_D void filt_even(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::E]
   xfft_real<N>(x, z, sm, t, [&] {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) se[c] = mv_spec<N>(t, oidx<N>(threadIdx.x, c)).x;
+      for (int c = 0; c < E; ++c) se[c] = mv_spec<N>(t, spos<N>(threadIdx.x, c)).x;
     }
   });
   if (own) {
@@ -154,7 +154,7 @@ TSF_D void filt_odd(double2 (&z)[FShape<N>::E], double2* sm, const FilterTables&
   xfft<N, false>(z, sm, t, [&] {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) so[c] = mv_spec<N>(t, oidx<N>(threadIdx.x, c)).y;
+      for (int c = 0; c < E; ++c) so[c] = mv_spec<N>(t, spos<N>(threadIdx.x, c)).y;
     }
   });
   if (own) {
@@ -175,7 +175,7 @@ TSF_D void filt_strang(const double (&x)[FShape<N>::E], double2 (&z)[FShape<N>::
   if (threadIdx.x < T) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const double2 lam = ldt(&t.pclam[oidx<N>(threadIdx.x, c)]);
+      const double2 lam = ldt(&t.pclam[spos<N>(threadIdx.x, c)]);
       const double s = 0.5 * (rcp_pos(d + kbar * lam.x) + rcp_pos(d + kbar * lam.y));
       z[c] = cscale(z[c], s * inv_n);
     }
@@ -207,7 +207,7 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
   xfft_real<N>(x, z, sm, t, [&] {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) sp[c] = spec[oidx<N>(threadIdx.x, c)];
+      for (int c = 0; c < E; ++c) sp[c] = spec[spos<N>(threadIdx.x, c)];
     }
   });
   if (own) {
@@ -215,7 +215,11 @@ TSF_D void filt_strang_tab(const double (&x)[FShape<N>::E], double2 (&z)[FShape<
     for (int c = 0; c < E; ++c) {
       const int k = oidx<N>(threadIdx.x, c);
       z[c] = cscale(z[c], sp[c]);
-      if (hs && k <= N / 2) hs[k] = z[c];
+      if constexpr (use64<N>()) {
+        if (hs) hs[spos<N>(threadIdx.x, c)] = z[c];   // full spectrum, stored permuted
+      } else {
+        if (hs && k <= N / 2) hs[k] = z[c];
+      }
     }
   }
   xfft<N, true>(z, sm, t);
@@ -232,8 +236,10 @@ TSF_D void load_even_spec(const double2* hs, const FilterTables& t, double2 (&z)
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int k = oidx<N>(threadIdx.x, c);
-      const double2 h = k <= N / 2 ? hs[k] : cconj(hs[N - k]);
-      z[c] = cscale(h, mv_spec<N>(t, k).x * N);  // N S/L: exact (N a power of two)
+      double2 h;
+      if constexpr (use64<N>()) h = hs[spos<N>(threadIdx.x, c)];
+      else h = k <= N / 2 ? hs[k] : cconj(hs[N - k]);
+      z[c] = cscale(h, mv_spec<N>(t, spos<N>(threadIdx.x, c)).x * N);  // N S/L: exact (pow2 N)
     }
   }
 }

@@ -51,9 +51,18 @@ struct KrylovArgs {
   double* s;
   double* sh;
   double* t;
-  double* pspec;            // [B, n] Strang spectrum S_k / n of the level (PC == 1)
+  double* pspec;            // [B, vs] Strang spectrum S_k / n of the level (PC == 1)
   double2* hspec;           // [B, N/2+1] half spectrum of the last Strang output (BiCGSTAB,
-                            // PC == 1), or null: recompute the even channel's transform
+                            // PC == 1; 64 x 64 engine: [B, N] full spectrum, permuted),
+                            // or null: recompute the even channel's transform
+  // Internal layout (tsf_fft64.cuh spos): the workspace vectors r, p, v, ph,
+  // s, sh, t, kwork, pspec, r0w, xw have per-instance stride vs and hold
+  // index oidx(t, c) at position spos(t, c); rhs, x and kappa are the
+  // caller's [B, n] natural-order vectors.  For the Stockham engine vs = n,
+  // spos == oidx, r0w == rhs and xw == x.
+  int vs;
+  const double* r0w;        // r0 (= rhs) in the internal layout
+  double* xw;               // the iterate x in the internal layout
   KState* kst;              // [B] per-instance Krylov scalars (phase kernels)
   SoeArgs soe;              // fused SOE epilogue of converged instances (march)
   int soe_epilogue;         // 1: run it
@@ -82,11 +91,32 @@ struct KShape {
 #endif
 };
 
+// slot c of thread t: INT = internal workspace layout (position spos, per
+// instance stride vs), else the caller's natural order; zero beyond n
+template <int N, bool INT>
+TSF_D double ldv(const double* __restrict__ base, int n, int t, int c) {
+  const int j = oidx<N>(t, c);
+  if constexpr (INT) return j < n ? base[spos<N>(t, c)] : 0.0;
+  else return j < n ? base[j] : 0.0;
+}
+template <int N, bool INT>
+TSF_D void stv(double* __restrict__ base, int n, int t, int c, double v) {
+  const int j = oidx<N>(t, c);
+  if (j < n) base[INT ? spos<N>(t, c) : j] = v;
+}
+// the level's diffusivity in the internal layout: the 64 x 64 engine copies a
+// given kappa into kwork in k_solve_begin; the Stockham engine reads it in place
+template <int N>
+TSF_D const double* kap_ptr(const KrylovArgs& a) {
+  if constexpr (use64<N>()) return a.kwork;
+  else return a.kappa ? a.kappa : (const double*)a.kwork;
+}
+
 // y = shift*x + kappa .* (A x) on the owned slots (kappa == nullptr: y = A x).
 // x is read from global (twice); result returned in y[].  hs: x's half
 // spectrum from the Strang solve that produced x (filt_strang_tab), or null;
 // hz: that spectrum already loaded into the owned slots (load_even_spec).
-template <int N>
+template <int N, bool INT = true>
 TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restrict__ kg,
                           double shift, int n, double (&y)[FShape<N>::E], double2* sm, double* aux,
                           const FilterTables& t, const double2* hs = nullptr,
@@ -103,13 +133,13 @@ TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restric
   auto load_x = [&] {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) xo[c] = ld_real(xg, n, oidx<N>(tid, c));
+      for (int c = 0; c < E; ++c) xo[c] = ldv<N, INT>(xg, n, tid, c);
     }
   };
   auto load_k = [&] {
     if (own && kg) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) ko[c] = ld_real(kg, n, oidx<N>(tid, c));
+      for (int c = 0; c < E; ++c) ko[c] = ldv<N, INT>(kg, n, tid, c);
     }
   };
   if (hz) {
@@ -123,13 +153,13 @@ TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restric
     double xr[FShape<N>::E];
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) xr[c] = ld_real(xg, n, oidx<N>(tid, c));
+      for (int c = 0; c < E; ++c) xr[c] = ldv<N, INT>(xg, n, tid, c);
     }
     filt_even<N>(xr, z, sm, t, load_x);
   }
   if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) aux[oidx<N>(tid, c)] = z[c].x;
+    for (int c = 0; c < E; ++c) aux[spos<N>(tid, c)] = z[c].x;
 #pragma unroll
     for (int c = 0; c < E; ++c) z[c] = cscale(modulation(t, oidx<N>(tid, c)), xo[c]);
   }
@@ -137,9 +167,8 @@ TSF_D void apply_level_op(const double* __restrict__ xg, const double* __restric
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = oidx<N>(tid, c);
-      const double2 w = modulation(t, j);
-      const double ax = aux[j] + fma(z[c].x, w.x, z[c].y * w.y);  // + Re(conj(w) z)
+      const double2 w = modulation(t, oidx<N>(tid, c));
+      const double ax = aux[spos<N>(tid, c)] + fma(z[c].x, w.x, z[c].y * w.y);  // + Re(conj(w) z)
       y[c] = kg ? fma(shift, xo[c], ko[c] * ax) : ax;
     }
   }
@@ -157,7 +186,7 @@ k_toeplitz_apply(int n, const double* __restrict__ x, double* __restrict__ y,
   const int tid = threadIdx.x;
   const long off = (long)blockIdx.x * n;
   double out[FShape<N>::E];
-  apply_level_op<N>(x + off, kappa ? kappa + off : nullptr, shift, n, out, sm, aux, ts);
+  apply_level_op<N, false>(x + off, kappa ? kappa + off : nullptr, shift, n, out, sm, aux, ts);
   if (tid < T) {
 #pragma unroll
     for (int c = 0; c < KShape<N>::E; ++c) st_real(y + off, n, oidx<N>(tid, c), out[c]);
@@ -206,7 +235,8 @@ k_strang_apply(int n, const double* __restrict__ v, double* __restrict__ zo, dou
 
 template <int N>
 TSF_D double2* hspec_of(const KrylovArgs& a, int b) {
-  return a.hspec ? a.hspec + (long)b * (N / 2 + 1) : nullptr;
+  if constexpr (use64<N>()) return a.hspec ? a.hspec + (long)b * N : nullptr;
+  else return a.hspec ? a.hspec + (long)b * (N / 2 + 1) : nullptr;
 }
 
 struct KState {
@@ -214,22 +244,32 @@ struct KState {
   int it, done;
 };
 
-template <int N>
+template <int N, bool INT = true>
 TSF_D void load_owned(double (&u)[FShape<N>::E], const double* g, int n) {
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) u[c] = ld_real(g, n, oidx<N>(tid, c));
+    for (int c = 0; c < KShape<N>::E; ++c) u[c] = ldv<N, INT>(g, n, tid, c);
   }
 }
-template <int N>
+template <int N, bool INT = true>
 TSF_D void store_owned(double* g, const double (&u)[FShape<N>::E], int n) {
   constexpr int T = KShape<N>::T;
   const int tid = threadIdx.x;
   if (tid < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) st_real(g, n, oidx<N>(tid, c), u[c]);
+    for (int c = 0; c < KShape<N>::E; ++c) stv<N, INT>(g, n, tid, c, u[c]);
+  }
+}
+// the caller's x (natural order) from the internal iterate, before an
+// instance finishes (64 x 64 engine; with the Stockham engine xw IS x)
+template <int N>
+TSF_D void publish_x(const KrylovArgs& a, int b) {
+  if constexpr (use64<N>()) {
+    double u[FShape<N>::E];
+    load_owned<N, true>(u, a.xw + (long)b * a.vs, a.n);
+    store_owned<N, false>(a.x + (long)b * a.n, u, a.n);
   }
 }
 // dst = P^{-1} u (u real, owned slots); spec = the instance's S_k / n
@@ -241,7 +281,7 @@ TSF_D void precond_store(const double (&u)[FShape<N>::E], double* dst, int n, co
   filt_strang_tab<N>(u, z, sm, t, t.ps ? t.ps : spec, hs);
   if (threadIdx.x < T) {
 #pragma unroll
-    for (int c = 0; c < KShape<N>::E; ++c) st_real(dst, n, oidx<N>(threadIdx.x, c), z[c].x);
+    for (int c = 0; c < KShape<N>::E; ++c) stv<N, true>(dst, n, threadIdx.x, c, z[c].x);
   }
 }
 
@@ -254,8 +294,10 @@ TSF_D void finish_instance(const KrylovArgs& a, KState* st, int* active, int b, 
     st[b].done = 1;
     atomicSub(active, 1);
   }
-  if (status == TSF_OK && a.soe_epilogue)
+  if (status == TSF_OK && a.soe_epilogue) {
+    __syncthreads();   // the instance's published x (every thread's slots)
     soe_instance_epilogue(a.soe, reinterpret_cast<double*>(sm), b);
+  }
 }
 
 // ---- begin (both methods)
@@ -270,7 +312,8 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
   const bool own = tid < T;
   const int b = blockIdx.x;
   const int n = a.n;
-  const long off = (long)b * n;
+  const long off = (long)b * n;       // caller vectors
+  const long ow = (long)b * a.vs;     // workspace vectors
   // kappa on the grid (scheme.py:156-160,280) and kappa_bar (scheme.py:135)
   double ksum = 0.0, kmin = 1e308;
   if (own) {
@@ -281,6 +324,7 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
         double k;
         if (a.kappa) {
           k = a.kappa[off + j];
+          if constexpr (use64<N>()) a.kwork[ow + spos<N>(tid, c)] = k;
         } else {
           k = 0.0;
           for (int q = 0; q < a.nk; ++q) {
@@ -288,7 +332,7 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
             // no contraction: reproduce numpy's  acc + mode*coef  rounding
             k = __dadd_rn(k, __dmul_rn(mq, a.kcoef[q]));
           }
-          a.kwork[off + j] = k;
+          a.kwork[(use64<N>() ? ow + spos<N>(tid, c) : off + j)] = k;
         }
         ksum += k;
         kmin = fmin(kmin, k);
@@ -304,7 +348,8 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
   const double kbar = a.kbar > 0.0 ? a.kbar : kmean;
   const double d = a.shift;
   if constexpr (PC == 1) {
-    // total eigenvalues d + kbar*lam > 0  (toeplitz.py:122-124)
+    // total eigenvalues d + kbar*lam > 0  (toeplitz.py:122-124); the table
+    // is stored in the internal order (every position is some k < n)
     double tmin = 1e308;
     for (int k = tid; k < n; k += blockDim.x) tmin = fmin(tmin, d + kbar * ldt(&tab.pclam[k]).x);
     tmin = block_min1(tmin, red);
@@ -316,43 +361,43 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
     if (own) {
 #pragma unroll
       for (int c = 0; c < E; ++c) {
-        const int j = oidx<N>(tid, c);
-        const double2 lam = ldt(&tab.pclam[j]);
-        a.pspec[off + j] = 0.5 * (1.0 / (d + kbar * lam.x) + 1.0 / (d + kbar * lam.y)) / n;
+        const int q = spos<N>(tid, c);
+        const double2 lam = ldt(&tab.pclam[q]);
+        a.pspec[ow + q] = 0.5 * (1.0 / (d + kbar * lam.x) + 1.0 / (d + kbar * lam.y)) / n;
       }
     }
   }
   // r = r0 = rhs, x = 0  (krylov.py:107-113 / 64-69)
   double u[FShape<N>::E];
-  load_owned<N>(u, a.rhs + off, n);
+  load_owned<N, false>(u, a.rhs + off, n);
   double ss = 0.0;
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = oidx<N>(tid, c);
-      st_real(a.x + off, n, j, 0.0);
-      if (j < n) ss = fma(u[c], u[c], ss);
+      stv<N, true>(a.xw + ow, n, tid, c, 0.0);
+      if (oidx<N>(tid, c) < n) ss = fma(u[c], u[c], ss);
     }
   }
   ss = block_sum1(ss, red);
   if (sqrt(ss) == 0.0) {
+    publish_x<N>(a, b);
     finish_instance(a, st, active, b, 0, 0.0, TSF_OK, sm);
     return true;
   }
-  if (CG) store_owned<N>(a.r + off, u, n);        // r = b
-  store_owned<N>(a.p + off, u, n);                // BiCGSTAB: p = r (it 1); CG: p = z (PC=0)
+  if constexpr (use64<N>()) store_owned<N>(const_cast<double*>(a.r0w) + ow, u, n);
+  if (CG) store_owned<N>(a.r + ow, u, n);         // r = b
+  store_owned<N>(a.p + ow, u, n);                 // BiCGSTAB: p = r (it 1); CG: p = z (PC=0)
   double rz = ss;
   if constexpr (PC == 1) {
     // BiCGSTAB: p_hat = P^{-1} p ; CG: z = P^{-1} r written to p (p = z)
-    precond_store<N>(u, CG ? a.p + off : a.ph + off, n, a.pspec + off, sm, tab,
+    precond_store<N>(u, CG ? a.p + ow : a.ph + ow, n, a.pspec + ow, sm, tab,
                      CG ? nullptr : hspec_of<N>(a, b));
     if (CG) {
       double part = 0.0;
       if (own) {
 #pragma unroll
         for (int c = 0; c < E; ++c) {
-          const int j = oidx<N>(tid, c);
-          if (j < n) part = fma(u[c], a.p[off + j], part);
+          if (oidx<N>(tid, c) < n) part = fma(u[c], ldv<N, true>(a.p + ow, n, tid, c), part);
         }
       }
       rz = block_sum1(part, red);
@@ -384,28 +429,28 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
-  const long off = (long)b * n;
+  const long off = (long)b * n;       // caller vectors
+  const long ow = (long)b * a.vs;     // workspace vectors
   const KState s = pre ? *pre : st[b];
-  const double* phg = (PC ? a.ph : a.p) + off;
-  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
-  prefetch_l2(kg, n);                  // epilogue operands (x is loaded at once)
-  prefetch_l2(a.rhs + off, n);
-  if (s.it != 1) prefetch_l2(a.r + off, n);
+  const double* phg = (PC ? a.ph : a.p) + ow;
+  const double* kg = kap_ptr<N>(a) + ow;
+  prefetch_l2(kg, a.vs);               // epilogue operands (x is loaded at once)
+  prefetch_l2(a.r0w + ow, a.vs);
+  if (s.it != 1) prefetch_l2(a.r + ow, a.vs);
   double u[FShape<N>::E];
   double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
   apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, tab, hs, hz);   // u = v = M p_hat
   // epilogue operands loaded at once (one exposed latency, see the t-phase)
-  const double* rc = (s.it == 1 ? a.rhs : a.r) + off;
+  const double* rc = (s.it == 1 ? a.r0w : a.r) + ow;
   double r0v[E], rv[E];
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = oidx<N>(tid, c);
-      r0v[c] = ld_real(a.rhs + off, n, j);
-      rv[c] = ld_real(rc, n, j);
+      r0v[c] = ldv<N, true>(a.r0w + ow, n, tid, c);
+      rv[c] = ldv<N, true>(rc, n, tid, c);
     }
   }
-  store_owned<N>(a.v + off, u, n);
+  store_owned<N>(a.v + ow, u, n);
   double part = 0.0;
   if (own) {
 #pragma unroll
@@ -416,6 +461,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   }
   const double denom = block_sum1(part, red);
   if (denom == 0.0) {
+    publish_x<N>(a, b);
     finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_R0V, sm);
     return true;
   }
@@ -435,16 +481,15 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
     // x += alpha p_hat (early exit counts as a full iteration, krylov.py:135-137)
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) {
-        const int j = oidx<N>(tid, c);
-        st_real(a.x + off, n, j, ld_real(a.x + off, n, j) + alpha * ld_real(phg, n, j));
-      }
+      for (int c = 0; c < E; ++c)
+        stv<N, false>(a.x + off, n, tid, c,
+                      ldv<N, true>(a.xw + ow, n, tid, c) + alpha * ldv<N, true>(phg, n, tid, c));
     }
     finish_instance(a, st, active, b, s.it, snorm / s.nrm0, TSF_OK, sm);
     return true;
   }
-  store_owned<N>(a.s + off, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.sh + off, n, a.pspec + off, sm, tab, hs);
+  store_owned<N>(a.s + ow, u, n);
+  if constexpr (PC == 1) precond_store<N>(u, a.sh + ow, n, a.pspec + ow, sm, tab, hs);
   if (tid == 0) {
     st[b].alpha = alpha;
     st[b].snorm = snorm;
@@ -464,34 +509,34 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
-  const long off = (long)b * n;
+  const long ow = (long)b * a.vs;     // workspace vectors
+  const int vs = a.vs;
   const KState s = pre ? *pre : st[b];
-  const double* shg = (PC ? a.sh : a.s) + off;
-  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
-  prefetch_l2(kg, n);                  // epilogue operands (x is loaded at once)
-  prefetch_l2(a.s + off, n);
-  prefetch_l2(a.x + off, n);
-  if (PC) prefetch_l2(a.ph + off, n);
-  prefetch_l2(a.rhs + off, n);
-  prefetch_l2(a.p + off, n);
-  prefetch_l2(a.v + off, n);
+  const double* shg = (PC ? a.sh : a.s) + ow;
+  const double* kg = kap_ptr<N>(a) + ow;
+  prefetch_l2(kg, vs);                 // epilogue operands (x is loaded at once)
+  prefetch_l2(a.s + ow, vs);
+  prefetch_l2(a.xw + ow, vs);
+  if (PC) prefetch_l2(a.ph + ow, vs);
+  prefetch_l2(a.r0w + ow, vs);
+  prefetch_l2(a.p + ow, vs);
+  prefetch_l2(a.v + ow, vs);
   double u[FShape<N>::E];
   double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
   apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, tab, hs, hz);   // u = t = M s_hat
   // Every epilogue operand is loaded here at once, while the transform's
   // registers are dead: one exposed memory latency per phase instead of one
   // per reduction step (ncu: these loads were 40% of the t-phase's stalls).
-  const double* phg = (PC ? a.ph : a.p) + off;
+  const double* phg = (PC ? a.ph : a.p) + ow;
   double sv[E], xv[E], pv[E], shv[E], r0v[E], qv[E], vv[E];
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = oidx<N>(tid, c);
-      sv[c] = ld_real(a.s + off, n, j);
-      xv[c] = ld_real(a.x + off, n, j);
-      pv[c] = ld_real(phg, n, j);
-      shv[c] = ld_real(shg, n, j);
-      r0v[c] = ld_real(a.rhs + off, n, j);
+      sv[c] = ldv<N, true>(a.s + ow, n, tid, c);
+      xv[c] = ldv<N, true>(a.xw + ow, n, tid, c);
+      pv[c] = ldv<N, true>(phg, n, tid, c);
+      shv[c] = ldv<N, true>(shg, n, tid, c);
+      r0v[c] = ldv<N, true>(a.r0w + ow, n, tid, c);
     }
   }
   Vals<2> red2;
@@ -509,6 +554,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   }
   red2 = block_sum<2>(red2, red);
   if (red2.v[0] == 0.0) {
+    publish_x<N>(a, b);
     finish_instance(a, st, active, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN, sm);
     return true;
   }
@@ -520,9 +566,9 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int j = oidx<N>(tid, c);
-      st_real(a.x + off, n, j, xv[c] + (s.alpha * pv[c] + omega * shv[c]));
+      stv<N, true>(a.xw + ow, n, tid, c, xv[c] + (s.alpha * pv[c] + omega * shv[c]));
       u[c] = sv[c] - omega * u[c];
-      st_real(a.r + off, n, j, u[c]);
+      stv<N, true>(a.r + ow, n, tid, c, u[c]);
       if (j < n) {
         red2.v[0] = fma(u[c], u[c], red2.v[0]);
         red2.v[1] = fma(r0v[c], u[c], red2.v[1]);
@@ -532,28 +578,23 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
     // during the reduction
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      qv[c] = ld_real(a.p + off, n, oidx<N>(tid, c));
-      vv[c] = ld_real(a.v + off, n, oidx<N>(tid, c));
+      qv[c] = ldv<N, true>(a.p + ow, n, tid, c);
+      vv[c] = ldv<N, true>(a.v + ow, n, tid, c);
     }
   }
   red2 = block_sum<2>(red2, red);
   const double rnorm = sqrt(red2.v[0]);
   const double rel = rnorm / s.nrm0;
-  if (rel < a.tol) {
-    finish_instance(a, st, active, b, s.it, rel, TSF_OK, sm);
-    return true;
-  }
-  if (omega == 0.0) {
-    finish_instance(a, st, active, b, s.it, rel, TSF_BD_OMEGA, sm);
-    return true;
-  }
-  if (s.it >= a.max_iters) {
-    finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED, sm);
-    return true;
-  }
   const double rho_new = red2.v[1];
-  if (rho_new == 0.0) {  // the next iteration's first test (krylov.py:118-121)
-    finish_instance(a, st, active, b, s.it + 1, rel, TSF_BD_RHO, sm);
+  const int fin = rel < a.tol ? 1 : omega == 0.0 ? 2 : s.it >= a.max_iters ? 3
+                  : rho_new == 0.0 ? 4 : 0;
+  if (fin) {
+    publish_x<N>(a, b);
+    if (fin == 1) finish_instance(a, st, active, b, s.it, rel, TSF_OK, sm);
+    else if (fin == 2) finish_instance(a, st, active, b, s.it, rel, TSF_BD_OMEGA, sm);
+    else if (fin == 3) finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED, sm);
+    // rho vanished: the next iteration's first test (krylov.py:118-121)
+    else finish_instance(a, st, active, b, s.it + 1, rel, TSF_BD_RHO, sm);
     return true;
   }
   // next p = r + beta (p - omega v)
@@ -562,8 +603,8 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
 #pragma unroll
     for (int c = 0; c < E; ++c) u[c] = u[c] + beta * (qv[c] - omega * vv[c]);
   }
-  store_owned<N>(a.p + off, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.ph + off, n, a.pspec + off, sm, tab, hs);
+  store_owned<N>(a.p + ow, u, n);
+  if constexpr (PC == 1) precond_store<N>(u, a.ph + ow, n, a.pspec + ow, sm, tab, hs);
   if (tid == 0) {
     st[b].rho = s.rho_new;
     st[b].rho_new = rho_new;
@@ -586,21 +627,21 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   const int tid = threadIdx.x;
   const bool own = tid < T;
   const int n = a.n;
-  const long off = (long)b * n;
+  const long ow = (long)b * a.vs;     // workspace vectors
   const KState s = st[b];
-  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + off;
+  const double* kg = kap_ptr<N>(a) + ow;
   double u[FShape<N>::E];
-  apply_level_op<N>(a.p + off, kg, a.shift, n, u, sm, aux, tab);  // u = q = M p
+  apply_level_op<N>(a.p + ow, kg, a.shift, n, u, sm, aux, tab);  // u = q = M p
   double part = 0.0;
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = oidx<N>(tid, c);
-      if (j < n) part = fma(a.p[off + j], u[c], part);
+      if (oidx<N>(tid, c) < n) part = fma(ldv<N, true>(a.p + ow, n, tid, c), u[c], part);
     }
   }
   const double curv = block_sum1(part, red);
   if (curv <= 0.0) {
+    publish_x<N>(a, b);
     finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_CURVATURE, sm);
     return true;
   }
@@ -609,43 +650,43 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = oidx<N>(tid, c);
-      st_real(a.x + off, n, j, ld_real(a.x + off, n, j) + al * ld_real(a.p + off, n, j));
-      u[c] = ld_real(a.r + off, n, j) - al * u[c];
-      if (j < n) part = fma(u[c], u[c], part);
+      stv<N, true>(a.xw + ow, n, tid, c,
+                   ldv<N, true>(a.xw + ow, n, tid, c) + al * ldv<N, true>(a.p + ow, n, tid, c));
+      u[c] = ldv<N, true>(a.r + ow, n, tid, c) - al * u[c];
+      if (oidx<N>(tid, c) < n) part = fma(u[c], u[c], part);
     }
   }
-  store_owned<N>(a.r + off, u, n);
+  store_owned<N>(a.r + ow, u, n);
   const double rnorm = sqrt(block_sum1(part, red));
   const double rel = rnorm / s.nrm0;
   if (rel < a.tol) {
+    publish_x<N>(a, b);
     finish_instance(a, st, active, b, s.it, rel, TSF_OK, sm);
     return true;
   }
   if (s.it >= a.max_iters) {
+    publish_x<N>(a, b);
     finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED, sm);
     return true;
   }
   // z = P^{-1} r (into s), rz_new = r.z, p = z + beta p
-  const double* zg = (PC ? a.s : a.r) + off;
-  if constexpr (PC == 1) precond_store<N>(u, a.s + off, n, a.pspec + off, sm, tab);
+  const double* zg = (PC ? a.s : a.r) + ow;
+  if constexpr (PC == 1) precond_store<N>(u, a.s + ow, n, a.pspec + ow, sm, tab);
   __syncthreads();
   part = 0.0;
   if (own) {
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-      const int j = oidx<N>(tid, c);
-      if (j < n) part = fma(u[c], zg[j], part);
+      if (oidx<N>(tid, c) < n) part = fma(u[c], ldv<N, true>(zg, n, tid, c), part);
     }
   }
   const double rz_new = block_sum1(part, red);
   const double beta = rz_new / s.rz;
   if (own) {
 #pragma unroll
-    for (int c = 0; c < E; ++c) {
-      const int j = oidx<N>(tid, c);
-      st_real(a.p + off, n, j, ld_real(zg, n, j) + beta * ld_real(a.p + off, n, j));
-    }
+    for (int c = 0; c < E; ++c)
+      stv<N, true>(a.p + ow, n, tid, c,
+                   ldv<N, true>(zg, n, tid, c) + beta * ldv<N, true>(a.p + ow, n, tid, c));
   }
   if (tid == 0) {
     st[b].rz = rz_new;
@@ -654,8 +695,6 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   }
   return false;
 }
-
-
 
 template <int N, int PC, bool CG>
 __global__ void __launch_bounds__(KShape<N>::BLOCK, KShape<N>::MIN_BLOCKS)
@@ -676,7 +715,7 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
     if (st[blockIdx.x].done) return;                                                   \
     const FilterTables tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(        \
         reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES + N * 8),                   \
-        PC ? a.pspec + (long)blockIdx.x * a.n : nullptr);                              \
+        PC ? a.pspec + (long)blockIdx.x * a.vs : nullptr);                              \
     DNAME<N, PC>(a, tab, st, active, sm, red);                                         \
   }
 TSF_PHASE_KERNEL(k_cg_iter, dev_cg_iter)
@@ -701,7 +740,7 @@ TSF_D void bicg_phase(const KrylovArgs& a, KState* st, int* active) {
   if constexpr (!TSF_ENTRY_PRELOAD || kAsyncStaging || FStage<N>::MV || FStage<N>::PS) {
     // table-staging variants: the plain entry sequence
     if (st[blockIdx.x].done) return;
-    const FilterTables tab = stage_tables<N>(a.tab, tws, PC ? a.pspec + (long)blockIdx.x * a.n : nullptr);
+    const FilterTables tab = stage_tables<N>(a.tab, tws, PC ? a.pspec + (long)blockIdx.x * a.vs : nullptr);
     if constexpr (TPHASE) dev_bicg_t<N, PC>(a, tab, st, active, sm, red);
     else dev_bicg_v<N, PC>(a, tab, st, active, sm, red);
   } else {
