@@ -194,6 +194,100 @@ def run_cfg2_exact(pool):
     print("cfg2 exact-engine floor pooled", ex["pooled"], flush=True)
 
 
+def _cfg0_exact(_):
+    tsfrac = _reference("exact")
+    from gen_golden import _march
+    from tsfrac.scheme import ProblemSpec
+    kappa, source, initial = cfg3_fields()
+    spec = ProblemSpec(gamma=0.5, alpha=1.5, l=1.0, T=1.0, kappa=kappa, source=source,
+                       initial=initial)
+    hist, rep, its, rel = _march(tsfrac, spec, 256, 3.0, 1025, 1e-12, 1e-12)
+    return its, hist
+
+
+def _cfg1_exact(ga):
+    g, a = ga
+    tsfrac = _reference("exact")
+    from gen_golden import _march
+    from tsfrac.scheme import ProblemSpec
+    kappa, source, initial = cfg3_fields()
+    spec = ProblemSpec(gamma=g, alpha=a, l=1.0, T=1.0, kappa=kappa, source=source,
+                       initial=initial)
+    t0 = time.time()
+    hist, rep, its, rel = _march(tsfrac, spec, 1024, (2.0 - g) / g, 16385, 1e-12, 1e-12)
+    print(f"cfg1 g{g} a{a} exact avg {its.mean():.2f} {time.time() - t0:.0f}s", flush=True)
+    return its, hist[64].copy(), hist[-1].copy()
+
+
+def run_cfg0_exact(pool):
+    """march.npz's configs[0] run vs the correctly rounded engine ->
+    cfg0_floor.json (per-level iterations, max rel-l2 over all levels)."""
+    gm = np.load(OUT / "march.npz")
+    its, hist = pool.map(_cfg0_exact, [0])[0]
+    d = its - gm["cfg0_its"]
+    rl = max(_rl2(hist[m], gm["cfg0_hist"][m]) for m in range(1, hist.shape[0]))
+    out = {"exact_engine": dict(_stats(d), max_rel_l2=rl)}
+    (OUT / "cfg0_floor.json").write_text(json.dumps(out, indent=1) + "\n")
+    print("cfg0 exact-engine floor", out, flush=True)
+
+
+def run_cfg1_exact(pool):
+    """cfg1_floor.json gains, per (gamma, alpha), the correctly rounded
+    engine's spread against the stock run (cfg1.npz)."""
+    g1 = np.load(OUT / "cfg1.npz")
+    floor = json.loads((OUT / "cfg1_floor.json").read_text())
+    combos = [(g, a) for g in (0.3, 0.5, 0.8) for a in (0.5, 1.0, 1.5, 1.9)]
+    for (g, a), (its, u64, uM) in zip(combos, pool.map(_cfg1_exact, combos)):
+        tag = f"cfg1_g{int(g * 10)}_a{int(a * 10)}"
+        d = its - g1[f"{tag}_its"]
+        floor[tag]["exact_engine"] = dict(_stats(d), rel_l2_u64=_rl2(u64, g1[f"{tag}_u64"]),
+                                          rel_l2_uM=_rl2(uM, g1[f"{tag}_uM"]))
+        print(tag, floor[tag]["exact_engine"], flush=True)
+    (OUT / "cfg1_floor.json").write_text(json.dumps(floor, indent=1) + "\n")
+
+
+def _linalg_exact(i):
+    """One linalg.npz case's Krylov solves through the reference with the
+    correctly rounded engine: iterations of the preconditioned BiCGSTAB at
+    tol 1e-10 / 1e-12 and of the unpreconditioned solve at 1e-10."""
+    tsfrac = _reference("exact")
+    from tsfrac.krylov import MatrixFreeOperator, solve_bicgstab
+    from tsfrac.toeplitz import build_preconditioner, build_toeplitz
+    from tsfrac.ifl import build_ifl  # noqa: F401
+    g = np.load(OUT / "linalg.npz")
+    col = g[f"tp{i}_col"]
+    n = col.size
+    op = build_toeplitz(col)
+    shift = float(g[f"tp{i}_shift"][0])
+    kap = g[f"tp{i}_kappa"]
+    apply = lambda q: shift * q + kap * op.matvec(q)  # noqa: E731
+    out = {}
+    # build_preconditioner takes the IFL discretisation in the reference;
+    # restate its use: Strang column of the first column (toeplitz.py:101-128)
+    from tsfrac.toeplitz import CirculantPreconditioner, strang_first_column
+    import tsfrac.fourier as fourier
+    lam = fourier.fft(strang_first_column(col)).real
+    total = shift + float(kap.mean()) * lam
+    pc = CirculantPreconditioner(n=n, shift=shift, kappa_bar=float(kap.mean()), lam=lam,
+                                 total_eigs=total)
+    for tol in (10, 12):
+        _, rep = solve_bicgstab(MatrixFreeOperator(n, apply), pc, g[f"tp{i}_bicg_{tol}_b"],
+                                tol=10.0 ** -tol)
+        out[f"bicg_{tol}"] = rep.iterations
+    _, rep = solve_bicgstab(MatrixFreeOperator(n, apply), None, g[f"tp{i}_bicg_12_b"], tol=1e-10)
+    out["plain"] = rep.iterations
+    return i, out
+
+
+def run_linalg_exact(pool):
+    g = np.load(OUT / "linalg.npz")
+    cases = [i for i in range(32) if f"tp{i}_col" in g]
+    res = dict(pool.map(_linalg_exact, cases))
+    (OUT / "linalg_exact.json").write_text(json.dumps({f"tp{i}": v for i, v in res.items()},
+                                                      indent=1) + "\n")
+    print("linalg exact", res, flush=True)
+
+
 def run_cfg3(pool):
     res = dict((s, (its, keep)) for s, its, keep in pool.map(_cfg3_one, [False, True]))
     its, keep = res[False]
@@ -229,6 +323,12 @@ def main():
             run_cfg2(pool)
         if "cfg2exact" in which:
             run_cfg2_exact(pool)
+        if "linalgexact" in which:
+            run_linalg_exact(pool)
+        if "cfg0exact" in which:
+            run_cfg0_exact(pool)
+        if "cfg1exact" in which:
+            run_cfg1_exact(pool)
         if "cfg3" in which:
             res = a3.get()
 

@@ -99,7 +99,9 @@ TSF_D void f64_octet(double2 (&v)[8], double2* loc, const double2* w64, int g) {
     const double2 w = w64[a * 8 + g];
     v[a] = INV ? cmulc(v[a], w) : cmul(v[a], w);
   }
-  __syncwarp();   // the octet's previous readers of the tile are done
+  // no barrier before the tile stores: the octet's previous readers of the
+  // tile (the other stage, or the previous transform) are behind the
+  // exchange's / the transform's leading __syncthreads
 #pragma unroll
   for (int a = 0; a < 8; ++a) loc[a * f64::kLocStride + g] = v[a];
   __syncwarp();
