@@ -38,7 +38,7 @@
 #include "tsf_fft64_tab.h"
 
 #ifndef TSF_FFT64
-#define TSF_FFT64 1
+#define TSF_FFT64 0
 #endif
 
 namespace tsf {

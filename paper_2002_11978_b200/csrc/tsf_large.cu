@@ -16,8 +16,14 @@
 //   8  x, r update           elementwise (||r||^2, r0.r partials)
 //   9  convergence, rho      scalar kernel
 // Without the preconditioner steps 1/4 are elementwise kernels.
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "../../include/tsfrac_b200.h"
@@ -875,6 +881,79 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
     if (*lp->h_active == 0) break;
   }
   return TSF_SUCCESS;
+}
+
+
+// ---------------------------------------------------------------- TMA maps
+// (tsf_tma.cuh) encoded once per (pointer, shape) and cached: the workspace
+// pointers of a plan never move, so a solve's launches hit the cache.
+bool tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_TMA");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+using MapKey = std::tuple<const void*, unsigned long long, unsigned long long, unsigned long long,
+                          unsigned long long, unsigned long long, unsigned, unsigned>;
+std::mutex g_map_mu;
+std::map<MapKey, CUtensorMap> g_maps;
+
+// 3-D tiled map of fp64 elements: dims {d0, d1, d2}, byte strides of dims 1
+// and 2, box {b0, b1, 1}
+int encode3(CUtensorMap* m, const void* base, unsigned long long d0, unsigned long long d1,
+            unsigned long long d2, unsigned long long s1, unsigned long long s2, unsigned b0,
+            unsigned b1) {
+  const MapKey key{base, d0, d1, d2, s1, s2, b0, b1};
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  auto it = g_maps.find(key);
+  if (it != g_maps.end()) {
+    *m = it->second;
+    return 0;
+  }
+  auto fn = encode_fn();
+  if (!fn) return report_error(TSF_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {s1, s2};
+  const cuuint32_t box[3] = {b0, b1, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims,
+                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return report_error(TSF_E_CUDA, "cuTensorMapEncodeTiled failed");
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps[key] = *m;
+  return 0;
+}
+}  // namespace
+
+int tma_map_vector(CUtensorMap* m, const double* base, long n, int N1, int N2, int B, int G) {
+  return encode3(m, base, (unsigned long long)N2, (unsigned long long)N1, (unsigned long long)B,
+                 (unsigned long long)N2 * 8, (unsigned long long)n * 8, (unsigned)G,
+                 (unsigned)std::min(N1, kTmaMaxBox));
+}
+
+int tma_map_z(CUtensorMap* m, const double2* Z, int N1, int N2, int B, int G) {
+  return encode3(m, Z, 2ULL * N2, (unsigned long long)N1, 2ULL * B, 2ULL * N2 * 8,
+                 (unsigned long long)N1 * N2 * 16, 2u * G, (unsigned)std::min(N1, kTmaMaxBox));
 }
 
 }  // namespace tsf

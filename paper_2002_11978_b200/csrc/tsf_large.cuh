@@ -24,6 +24,7 @@
 #pragma once
 
 #include "tsf_kernels.cuh"
+#include "tsf_tma.cuh"
 
 namespace tsf {
 
@@ -121,6 +122,10 @@ struct LCol {
   static constexpr int BLOCK = G * T;
   static constexpr int BUF = 2 * FftPlan<N1, E>::SMEM_ELEMS;  // ping-pong, per group
   static constexpr int SMEM = (G * BUF + tw_table_elems(N1)) * 16;
+  // column-inverse kernels: + the two Z channel tiles (TMA landing zone),
+  // 128-byte aligned after the twiddle table
+  static constexpr int ZT_OFF = (SMEM + 127) / 128 * 128;
+  static constexpr int SMEM_INV = ZT_OFF + 2 * N1 * G * 16;
 };
 template <int N2>
 struct LRow {
@@ -141,14 +146,16 @@ TSF_D void stage_tw(double2* dst, const double2* src) {
 // launches of single large instances, which are latency-bound (configs[1]).
 template <int N1, int MB = LCol<N1>::MINB>
 __global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)
-k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
+k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode,
+           const __grid_constant__ ColMaps cm) {
   pdl_enter();
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
   const int N2 = a.nt / N1;
   const long N = a.nt;
-  extern __shared__ double2 sm[];
+  extern __shared__ __align__(128) double2 sm[];
   __shared__ double red[4 * 32];
+  __shared__ unsigned long long bar;
   const int b = blockIdx.y;
   const int g = threadIdx.x % G, tid = threadIdx.x / G;
   const int t2 = blockIdx.x * G + g;
@@ -159,6 +166,54 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   double xr[E];
   double2 z[E];
   double part = 0.0;
+  if (cm.use) {
+    // TMA path (tsf_tma.cuh): the operand tiles land in the (not yet used)
+    // transform buffers while the CTA stages its twiddles and reads the state
+    double* tile = reinterpret_cast<double*>(sm);
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      unsigned bytes = 0;
+      mbar_expect_tx(&bar, (unsigned)(cm.nv * N1 * G * 8));
+      for (int q = 0; q < cm.nv; ++q)
+        bytes += tma_tile(tile + q * N1 * G, &cm.v[q], blockIdx.x * G, N1, G, b, 8, &bar);
+      (void)bytes;
+    }
+    stage_tw<N1>(tw1, a.lt.tw1);
+    const LState stv = a.st ? a.st[b] : LState{};
+    __syncthreads();   // barrier initialised before anyone waits on it
+    mbar_wait(&bar, 0);
+    if (inst_skip(a, b)) return;
+    const bool upd = in_mode == CI_PUPD || in_mode == CI_SUPD;
+    const bool pupd_it1 = in_mode == CI_PUPD && stv.it == 1;
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int t1 = tid + c * T;
+      const long j = (long)N2 * t1 + t2;
+      const double l0 = pupd_it1 ? a.r0[off + j] : tile[t1 * G + g];
+      double val;
+      if (in_mode == CI_PUPD) {
+        if (pupd_it1) {
+          val = l0;
+        } else {
+          const double beta = (stv.rho_new / stv.rho) * (stv.alpha / stv.omega);
+          val = l0 + beta * (tile[N1 * G + t1 * G + g] - stv.omega * tile[2 * N1 * G + t1 * G + g]);
+        }
+      } else if (in_mode == CI_SUPD) {
+        val = (stv.it == 1 ? a.r0[off + j] : l0) - stv.alpha * tile[N1 * G + t1 * G + g];
+        part = fma(val, val, part);
+      } else {
+        val = l0;
+      }
+      xr[c] = val;
+    }
+    (void)upd;
+    if (in_mode == CI_PUPD || in_mode == CI_SUPD) {
+      double* dst = in_mode == CI_PUPD ? a.p : a.s;
+#pragma unroll
+      for (int c = 0; c < E; ++c) dst[off + (long)N2 * (tid + c * T) + t2] = xr[c];
+    }
+  } else {
+  // plain-load path (n not a multiple-of-rows view, or TSF_TMA=0)
   // Every operand is loaded before the first store: the vectors are plain
   // pointers that may alias, so a store between two elements' loads kept
   // the compiler from issuing the next element's loads early and serialised
@@ -212,6 +267,7 @@ k_lcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
     }
     xr[c] = val;
   }
+  }  // plain-load path
   if (in_mode == CI_SUPD) {
     part = block_sum1(part, red);
     if (threadIdx.x == 0) a.part[((long)b * 4 + 2) * a.np + blockIdx.x] = part;
@@ -369,29 +425,44 @@ __global__ void __launch_bounds__(64) k_lrow_small(LargeArgs a, int spec_mode) {
 template <int N1, int MB = LCol<N1>::MINB>
 __global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)
 k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __restrict__ xin,
-           const double* __restrict__ w1, int pslot) {
+           const double* __restrict__ w1, int pslot, const __grid_constant__ ColMaps cm) {
   pdl_enter();
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
   const int N2 = a.nt / N1;
   const long N = a.nt;
-  extern __shared__ double2 sm[];
+  extern __shared__ __align__(128) double2 sm[];
   __shared__ double red[4 * 32];
+  __shared__ unsigned long long bar;
   const int b = blockIdx.y;
   if (inst_skip(a, b)) return;
   const int g = threadIdx.x % G, tid = threadIdx.x / G;
   const int t2 = blockIdx.x * G + g;
   double2* smg = sm + g * C::BUF;
   double2* tw1 = sm + G * C::BUF;
+  double2* ztile = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + C::ZT_OFF);
+  const int nch = out_mode == CO_APPLY ? 2 : 1;
+  if (cm.use && threadIdx.x == 0) {
+    // both channels' [N1 x G] tiles of Z by TMA (tsf_tma.cuh)
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (unsigned)(nch * N1 * G * 16));
+    for (int ch = 0; ch < nch; ++ch)
+      tma_tile(reinterpret_cast<double*>(ztile + ch * N1 * G), &cm.z, 2 * blockIdx.x * G, N1,
+               2 * G, ch * a.B + b, 8, &bar);
+  }
   stage_tw<N1>(tw1, a.lt.tw1);
   const long off = (long)b * a.n;   // vectors [B][n]
   const long offz = (long)b * N;    // transform work [B][nt]
   double2 z[E];
+  if (cm.use) {
+    __syncthreads();   // barrier initialised before anyone waits on it
+    mbar_wait(&bar, 0);
+  }
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const int k1 = tid + c * T;
     const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
-    z[c] = cmulc(a.Z[offz + (long)k1 * N2 + t2], w);
+    z[c] = cmulc(cm.use ? ztile[k1 * G + g] : a.Z[offz + (long)k1 * N2 + t2], w);
   }
   group_fft<N1, E, true>(z, smg, tw1, 0, tid);
   if (out_mode == CO_REAL) {
@@ -411,7 +482,7 @@ k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __
   for (int c = 0; c < E; ++c) {
     const int k1 = tid + c * T;
     const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
-    z[c] = cmulc(Zo[offz + (long)k1 * N2 + t2], w);
+    z[c] = cmulc(cm.use ? ztile[N1 * G + k1 * G + g] : Zo[offz + (long)k1 * N2 + t2], w);
   }
   group_fft<N1, E, true>(z, smg, tw1, 0, tid);
   Vals<2> pr;

@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "tsf_dispatch.h"
 #include "tsf_large.cuh"
 
@@ -18,18 +20,43 @@ inline cudaError_t large_prep(K kernel, int smem) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
+// TMA tile loads (tsf_tma.cuh) apply when the vectors are exact N1 x N2
+// views (n = nt: power-of-two n) and a G-column row segment is >= 16 bytes
+template <int N1>
+inline bool col_tma_ok(const LargeArgs& a) {
+  return tma_enabled() && a.n == a.nt && LCol<N1>::G * 8 >= 16;
+}
+
 template <int LOG>
 int LargeDispatch<LOG>::col_fwd(const LargeArgs& a, const double* src, int in_mode,
                                 cudaStream_t st) {
   constexpr int N1 = 1 << LOG;
   using S = LCol<N1>;
   const dim3 grid(a.nt / N1 / S::G, a.B);
+  ColMaps cm;
+  memset(&cm, 0, sizeof(cm));
+  if (col_tma_ok<N1>(a)) {
+    const int N2 = (int)(a.nt / N1);
+    const double* vs[3] = {src, nullptr, nullptr};
+    int nv = 1;
+    if (in_mode == CI_PUPD) {
+      vs[0] = a.r; vs[1] = a.p; vs[2] = a.v; nv = 3;
+    } else if (in_mode == CI_SUPD) {
+      vs[0] = a.r; vs[1] = a.v; nv = 2;
+    }
+    int rc = 0;
+    for (int q = 0; q < nv && !rc; ++q)
+      rc = tma_map_vector(&cm.v[q], vs[q], a.n, N1, N2, a.B, S::G);
+    if (rc) return rc;
+    cm.nv = nv;
+    cm.use = 1;
+  }
   auto k = few_ctas((long)grid.x * grid.y) ? k_lcol_fwd<N1, 1> : k_lcol_fwd<N1>;
   static cudaError_t prep = large_prep(k_lcol_fwd<N1>, S::SMEM);
   static cudaError_t prep1 = large_prep(k_lcol_fwd<N1, 1>, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
   if (prep1 != cudaSuccess) return large_launch_error(prep1);
-  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, src, in_mode);
+  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, src, in_mode, cm);
   return large_launch_error(cudaGetLastError());
 }
 
@@ -62,12 +89,22 @@ int LargeDispatch<LOG>::col_inv(const LargeArgs& a, double* dst, int out_mode, c
   constexpr int N1 = 1 << LOG;
   using S = LCol<N1>;
   const dim3 grid(a.nt / N1 / S::G, a.B);
+  ColMaps cm;
+  memset(&cm, 0, sizeof(cm));
+  if (col_tma_ok<N1>(a)) {
+    const int rc = tma_map_z(&cm.z, a.Z, N1, (int)(a.nt / N1), a.B, S::G);
+    if (rc) return rc;
+    cm.use = 1;
+  }
+  // the Z tile landing zone only when TMA is on (otherwise the smaller
+  // footprint keeps more CTAs per SM)
+  const int smem = cm.use ? S::SMEM_INV : S::SMEM;
   auto k = few_ctas((long)grid.x * grid.y) ? k_lcol_inv<N1, 1> : k_lcol_inv<N1>;
-  static cudaError_t prep = large_prep(k_lcol_inv<N1>, S::SMEM);
-  static cudaError_t prep1 = large_prep(k_lcol_inv<N1, 1>, S::SMEM);
+  static cudaError_t prep = large_prep(k_lcol_inv<N1>, S::SMEM_INV);
+  static cudaError_t prep1 = large_prep(k_lcol_inv<N1, 1>, S::SMEM_INV);
   if (prep != cudaSuccess) return large_launch_error(prep);
   if (prep1 != cudaSuccess) return large_launch_error(prep1);
-  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, dst, out_mode, xin, w1, pslot);
+  launch_pdl(k, grid, S::BLOCK, smem, st, a, dst, out_mode, xin, w1, pslot, cm);
   return large_launch_error(cudaGetLastError());
 }
 

@@ -134,17 +134,41 @@ def fast_coefficients(soe: SoeApproximation, mesh, m: int) -> np.ndarray:
 
 @dataclass
 class FastHistory:
-    """Accumulators W (N_exp, n) held on the device; single owner (soe.py:73-87)."""
+    """Accumulators W (N_exp, n); single owner (soe.py:73-87).
+
+    `fresh(soe, n)` — the reference's call — gives W as a host numpy array, as
+    the reference's does (callers index, copy and multiply it with numpy);
+    `history_push` / `fast_caputo_rhs` still run on the device (the array is
+    staged to the GPU and written back in place).  `fresh(soe, n, device=d)`
+    keeps W resident on device d as a torch tensor (the package's own level
+    loops); the batched march holds its W[B][N_exp][n] itself (scheme.py).
+    """
 
     soe: SoeApproximation
-    W: object = field(default=None)  # torch CUDA tensor (N_exp, n)
+    W: object = field(default=None)  # numpy (N_exp, n) or torch CUDA tensor (N_exp, n)
     level: int = 0
 
     @classmethod
-    def fresh(cls, soe: SoeApproximation, n_spatial: int, device: int = 0) -> "FastHistory":
+    def fresh(cls, soe: SoeApproximation, n_spatial: int,
+              device: Optional[int] = None) -> "FastHistory":
+        if device is None:
+            return cls(soe=soe, W=np.zeros((soe.n_exp, n_spatial)), level=0)
         torch = _native.torch_mod()
         return cls(soe=soe, W=torch.zeros((soe.n_exp, n_spatial), dtype=torch.float64,
                                           device=f"cuda:{device}"), level=0)
+
+
+def _device_W(h: FastHistory):
+    """(device tensor, write-back) for h.W: a host array is staged to cuda:0
+    and copied back in place after the kernel."""
+    if _arrays.is_torch(h.W):
+        return h.W, None
+    torch = _native.torch_mod()
+    host = h.W
+    if host.dtype != np.float64 or not host.flags.c_contiguous:
+        raise ValueError("FastHistory.W must be a C-contiguous float64 array")
+    dW = torch.from_numpy(host).to("cuda:0")
+    return dW, lambda: np.copyto(host, dW.cpu().numpy())
 
 
 def _coef_tables(soe: SoeApproximation, tau_push: Optional[float], tau_next: Optional[float],
@@ -167,19 +191,22 @@ def history_push(h: FastHistory, delta_u, tau_m: float) -> FastHistory:
     if tau_m <= 0.0:
         raise ValueError(f"tau_m must be > 0, got {tau_m}")
     torch = _native.torch_mod()
-    du, _ = _arrays.to_device(delta_u, h.W.device.index or 0)
     n = h.W.shape[1]
-    if du.shape[0] != n:
+    if tuple(getattr(delta_u, 'shape', np.shape(delta_u))) != (n,):
         raise ValueError("delta_u length does not match the history width")
-    dev = h.W.device
+    W, write_back = _device_W(h)
+    dev = W.device
+    du, _ = _arrays.to_device(delta_u, dev.index or 0)
     tab = _coef_tables(h.soe, tau_m, None, dev)
     zero = torch.zeros(n, dtype=torch.float64, device=dev)
     # push with u = delta_u, uprev = 0 reproduces (u - 0)/tau == delta_u/tau exactly
     with torch.cuda.device(dev):
         _native.check(_native.load().tsf_soe_push_rhs(
-            1, n, h.soe.n_exp, h.W.data_ptr(), du.data_ptr(), zero.data_ptr(),
+            1, n, h.soe.n_exp, W.data_ptr(), du.data_ptr(), zero.data_ptr(),
             float(tau_m), tab[0].data_ptr(), tab[1].data_ptr(), tab[2].data_ptr(), 1, 0, 0,
             0.0, 1.0, None, None, _native.stream_ptr(device=dev)))
+    if write_back:
+        write_back()
     h.level += 1
     return h
 
@@ -187,18 +214,19 @@ def history_push(h: FastHistory, delta_u, tau_m: float) -> FastHistory:
 def fast_caputo_rhs(h: FastHistory, a_mm: float, u_prev, gamma: float, tau_m: float):
     """(a_mm u^{m-1} - sum_j w_j e^{-s_j tau_m} W_j) / Gamma(1-gamma)  (soe.py:228-246)."""
     torch = _native.torch_mod()
-    up, as_np = _arrays.to_device(u_prev, h.W.device.index or 0)
     n = h.W.shape[1]
-    if up.shape[0] != n:
+    if tuple(getattr(u_prev, 'shape', np.shape(u_prev))) != (n,):
         raise ValueError("u_prev length does not match the history width")
-    dev = h.W.device
+    W, _ = _device_W(h)
+    dev = W.device
+    up, as_np = _arrays.to_device(u_prev, dev.index or 0)
     tab = _coef_tables(h.soe, None, tau_m, dev)
     out = torch.empty(n, dtype=torch.float64, device=dev)
     zero_f = torch.zeros(n, dtype=torch.float64, device=dev)
     G = math.exp(gammaln(1.0 - gamma))
     with torch.cuda.device(dev):
         _native.check(_native.load().tsf_soe_push_rhs(
-            1, n, h.soe.n_exp, h.W.data_ptr(), up.data_ptr(), None, 0.0,
+            1, n, h.soe.n_exp, W.data_ptr(), up.data_ptr(), None, 0.0,
             None, None, tab[2].data_ptr(), 0, 0, 1, float(a_mm), G, zero_f.data_ptr(),
             out.data_ptr(), _native.stream_ptr(device=dev)))
     return _arrays.back(out, as_np)

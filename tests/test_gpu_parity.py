@@ -171,16 +171,26 @@ def test_max_iters_exhaustion():
     assert not rep.converged and rep.iterations == 1
 
 
-def test_soe_push_bit_exact():
+@pytest.mark.parametrize("resident", [False, True])
+def test_soe_push_bit_exact(resident):
+    """history_push / fast_caputo_rhs on the device: W host numpy (the
+    reference's FastHistory.fresh(soe, n) convention, staged to the GPU) or
+    device-resident (fresh(..., device=0))."""
     g = golden("linalg")
     soe = P.build_soe(0.5, 1e-12, (1.0 / 256) ** 3, 1.0)
-    h = P.FastHistory.fresh(soe, g["push_W0"].shape[1])
-    h.W.copy_(torch.from_numpy(g["push_W0"]))
+    h = P.FastHistory.fresh(soe, g["push_W0"].shape[1], device=0 if resident else None)
+    if resident:
+        h.W.copy_(torch.from_numpy(g["push_W0"]))
+    else:
+        h.W[:] = g["push_W0"]
     tau_push, tau_rhs = g["push_tau"]
     rhs = P.fast_caputo_rhs(h, 12.5, g["push_uprev"], 0.5, tau_rhs)
     assert rel_err(rhs, g["push_rhs"]) <= 1e-14
+    W_obj = h.W
     P.history_push(h, g["push_du"], tau_push)
-    np.testing.assert_array_equal(h.W.cpu().numpy(), g["push_W1"])
+    W1 = h.W.cpu().numpy() if resident else h.W
+    assert h.W is W_obj      # updated in place (soe.py:209-225 mutates its history)
+    np.testing.assert_array_equal(W1, g["push_W1"])
 
 
 @pytest.mark.parametrize("tag", ["s1", "s2", "s3", "s4", "s5"])
