@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define TSF_ABI_VERSION 2
+#define TSF_ABI_VERSION 3
 
 /* API return codes */
 #define TSF_SUCCESS 0
@@ -110,6 +110,24 @@ int tsf_krylov_solve(tsf_plan* plan, int B, int method, int precond,
                      const double* rhs, double* x, const double* kappa, double shift,
                      double kappa_bar, double tol, int max_iters, int* iters, double* relres, int* status,
                      void* stream);
+
+/*
+ * Level solve with the circulant preconditioner of a NON-power-of-two n
+ * (n <= 4096).  Reference: build_preconditioner + precond_solve
+ * (toeplitz.py:101-136) — P^{-1} v = Re IFFT_n(FFT_n(v) / total) — which in
+ * exact arithmetic is the symmetric Toeplitz product with the circulant's
+ * first column c = Re IFFT_n(1/total); the fused level-solve kernels apply it
+ * through the same even/odd-bin filters as the operator.
+ *   pc_spec    device [B or 1][L/2] pairs (S_2k, S_2k+1)/L of the length-L
+ *              embedding of c (natural bin order; the even part of the
+ *              symbol, as tsf_plan_create stores the operator's), stride
+ *              pc_stride pairs per instance (0: one table for every instance)
+ * Other arguments as tsf_krylov_solve (precond implied).
+ */
+int tsf_krylov_solve_circ(tsf_plan* plan, int B, int method, const double* rhs, double* x,
+                          const double* kappa, double shift, const double* pc_spec,
+                          int64_t pc_stride, double tol, int max_iters, int* iters,
+                          double* relres, int* status, void* stream);
 
 /*
  * SOE accumulator update fused with the next level's right-hand side.

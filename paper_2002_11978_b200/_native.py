@@ -40,8 +40,8 @@ BREAKDOWN = {
 EXPORTS = (
     "tsf_abi_version", "tsf_last_error", "tsf_plan_create", "tsf_plan_destroy",
     "tsf_plan_info", "tsf_plan_reserve", "tsf_toeplitz_matvec", "tsf_precond_solve",
-    "tsf_krylov_solve", "tsf_soe_push_rhs", "tsf_fids_march", "tsf_fft_debug",
-    "tsf_l1_history_rhs",
+    "tsf_krylov_solve", "tsf_krylov_solve_circ", "tsf_soe_push_rhs", "tsf_fids_march",
+    "tsf_fft_debug", "tsf_l1_history_rhs",
 )
 
 P = C.c_void_p
@@ -96,6 +96,7 @@ def load(path: Optional[os.PathLike] = None):
         "tsf_toeplitz_matvec": (I, [P, I, P, P, P, D, P]),
         "tsf_precond_solve": (I, [P, I, P, P, D, D, P, P]),
         "tsf_krylov_solve": (I, [P, I, I, I, P, P, P, D, D, D, I, P, P, P, P]),
+        "tsf_krylov_solve_circ": (I, [P, I, I, P, P, P, D, P, I64, D, I, P, P, P, P]),
         "tsf_soe_push_rhs": (I, [I, I, I, P, P, P, D, P, P, P, I, I, I, D, D, P, P, P]),
         "tsf_fids_march": (I, [P, C.POINTER(March), P]),
         "tsf_fft_debug": (I, [I, I, I, P, P, P]),

@@ -411,7 +411,10 @@ int tsf_precond_solve(tsf_plan* p, int B, const double* v, double* z, double shi
 }
 
 static int solve_impl(tsf_plan* p, int B, int method, int pc, KrylovArgs& a, cudaStream_t st) {
-  if (pc && !p->has_pc) return fail(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner");
+  if (pc == 1 && !p->has_pc) return fail(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner");
+  if (pc == 2 && (p->large || p->layout))
+    return fail(TSF_E_UNSUPPORTED, "circulant-column preconditioner needs the single-CTA "
+                                   "Stockham engine (n <= 4096)");
   DeviceGuard dg(p->device);
   if (p->large) {
     if (a.soe_epilogue) return fail(TSF_E_UNSUPPORTED, "fused SOE epilogue needs n <= 4096");
@@ -475,6 +478,32 @@ int tsf_krylov_solve(tsf_plan* p, int B, int method, int precond, const double* 
   a.relres = relres;
   a.status = status;
   return solve_impl(p, B, method, precond, a, (cudaStream_t)stream);
+}
+
+int tsf_krylov_solve_circ(tsf_plan* p, int B, int method, const double* rhs, double* x,
+                          const double* kappa, double shift, const double* pc_spec,
+                          int64_t pc_stride, double tol, int max_iters, int* iters,
+                          double* relres, int* status, void* stream) {
+  if (!p || !rhs || !x || !kappa || !pc_spec || !iters || !relres || !status || B < 0)
+    return fail(TSF_E_INVALID, "bad argument");
+  if (method != 0 && method != 1) return fail(TSF_E_INVALID, "method must be 0 or 1");
+  if (pc_stride != 0 && pc_stride < p->L / 2)
+    return fail(TSF_E_INVALID, "pc_stride must be 0 or >= L/2");
+  if (B == 0) return TSF_SUCCESS;
+  KrylovArgs a{};
+  a.rhs = rhs;
+  a.x = x;
+  a.kappa = kappa;
+  a.shift = shift;
+  a.kbar = 1.0;   // unused by the circulant-column preconditioner
+  a.tol = tol;
+  a.max_iters = max_iters;
+  a.iters = iters;
+  a.relres = relres;
+  a.status = status;
+  a.pcS = reinterpret_cast<const double2*>(pc_spec);
+  a.pcS_stride = (long)pc_stride;
+  return solve_impl(p, B, method, 2, a, (cudaStream_t)stream);
 }
 
 static int soe_launch(int B, SoeArgs& s, cudaStream_t st) {

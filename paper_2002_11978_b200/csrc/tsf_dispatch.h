@@ -30,7 +30,7 @@ struct SolveGraph {
 };
 int solve_groups(int B);  // TSF_SOLVE_GROUPS (default: 4 for B >= 1024, else 1)
 struct SolveGraphs {
-  SolveGraph slot[kMaxLogL + 1][2][2];  // [log L][pc][cg]
+  SolveGraph slot[kMaxLogL + 1][3][2];  // [log L][pc: none / Strang / circulant column][cg]
   ~SolveGraphs();
 };
 bool graph_mode();  // TSF_SOLVE_GRAPH (default 1)

@@ -255,7 +255,11 @@ int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
 template <int LOG>
 int Dispatch<LOG>::solve(int B, int method, int pc, const KrylovArgs& a, cudaStream_t st) {
   constexpr int N = 1 << (LOG - 1);
-  if (method == 0) return pc ? solve_t<N, 1, false>(B, a, st) : solve_t<N, 0, false>(B, a, st);
+  if (method == 0) {
+    if (pc == 2) return solve_t<N, 2, false>(B, a, st);
+    return pc ? solve_t<N, 1, false>(B, a, st) : solve_t<N, 0, false>(B, a, st);
+  }
+  if (pc == 2) return solve_t<N, 2, true>(B, a, st);
   return pc ? solve_t<N, 1, true>(B, a, st) : solve_t<N, 0, true>(B, a, st);
 }
 

@@ -61,6 +61,12 @@ struct KrylovArgs {
   // caller's [B, n] natural-order vectors.  For the Stockham engine vs = n,
   // spos == oidx, r0w == rhs and xw == x.
   int vs;
+  // PC == 2 (non-power-of-two n): P^{-1} = circ(c), c = Re IFFT_n(1/total),
+  // applied as the symmetric Toeplitz product with first column c: its
+  // embedding spectrum (S_2k, S_2k+1)/L per instance (stride pcS_stride
+  // double2; 0 = shared), natural bin order (Stockham layout)
+  const double2* pcS;
+  long pcS_stride;
   const double* r0w;        // r0 (= rhs) in the internal layout
   double* xw;               // the iterate x in the internal layout
   KState* kst;              // [B] per-instance Krylov scalars (phase kernels)
@@ -285,6 +291,48 @@ TSF_D void precond_store(const double (&u)[FShape<N>::E], double* dst, int n, co
   }
 }
 
+// dst = circ(c) u for the non-power-of-two preconditioner (PC == 2): the
+// Toeplitz product of the instance's circulant column through the same
+// even/odd-bin filters as the operator (toeplitz.py:131-136 in exact
+// arithmetic)
+template <int N>
+TSF_D void precond_toeplitz(const double (&u)[FShape<N>::E], double* dst, int n, double2* sm,
+                            const FilterTables& tab, const double2* pcS) {
+  constexpr int T = KShape<N>::T;
+  constexpr int E = KShape<N>::E;
+  const int tid = threadIdx.x;
+  const bool own = tid < T;
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES);
+  FilterTables t = tab;
+  t.mvS = pcS;
+  double2 z[FShape<N>::E];
+  filt_even<N>(u, z, sm, t);
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) aux[spos<N>(tid, c)] = z[c].x;
+#pragma unroll
+    for (int c = 0; c < E; ++c) z[c] = cscale(modulation(t, oidx<N>(tid, c)), u[c]);
+  }
+  filt_odd<N>(z, sm, t);
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const double2 w = modulation(t, oidx<N>(tid, c));
+      stv<N, true>(dst, n, tid, c, aux[spos<N>(tid, c)] + fma(z[c].x, w.x, z[c].y * w.y));
+    }
+  }
+}
+
+// dst = P^{-1} u: Strang (PC == 1) or circulant-as-Toeplitz (PC == 2)
+template <int N, int PC>
+TSF_D void precond_any(const double (&u)[FShape<N>::E], double* dst, const KrylovArgs& a, int b,
+                       double2* sm, const FilterTables& tab, double2* hs = nullptr) {
+  if constexpr (PC == 1)
+    precond_store<N>(u, dst, a.n, a.pspec + (long)b * a.vs, sm, tab, hs);
+  else
+    precond_toeplitz<N>(u, dst, a.n, sm, tab, a.pcS + (long)b * a.pcS_stride);
+}
+
 TSF_D void finish_instance(const KrylovArgs& a, KState* st, int* active, int b, int it,
                            double rel, int status, double2* sm) {
   if (threadIdx.x == 0) {
@@ -388,10 +436,10 @@ TSF_D bool dev_begin(const KrylovArgs& a, const FilterTables& tab, KState* st, i
   if (CG) store_owned<N>(a.r + ow, u, n);         // r = b
   store_owned<N>(a.p + ow, u, n);                 // BiCGSTAB: p = r (it 1); CG: p = z (PC=0)
   double rz = ss;
-  if constexpr (PC == 1) {
+  if constexpr (PC >= 1) {
     // BiCGSTAB: p_hat = P^{-1} p ; CG: z = P^{-1} r written to p (p = z)
-    precond_store<N>(u, CG ? a.p + ow : a.ph + ow, n, a.pspec + ow, sm, tab,
-                     CG ? nullptr : hspec_of<N>(a, b));
+    precond_any<N, PC>(u, CG ? a.p + ow : a.ph + ow, a, b, sm, tab,
+                       (CG || PC != 1) ? nullptr : hspec_of<N>(a, b));
     if (CG) {
       double part = 0.0;
       if (own) {
@@ -438,7 +486,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   prefetch_l2(a.r0w + ow, a.vs);
   if (s.it != 1) prefetch_l2(a.r + ow, a.vs);
   double u[FShape<N>::E];
-  double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
+  double2* hs = PC == 1 ? hspec_of<N>(a, b) : nullptr;
   apply_level_op<N>(phg, kg, a.shift, n, u, sm, aux, tab, hs, hz);   // u = v = M p_hat
   // epilogue operands loaded at once (one exposed latency, see the t-phase)
   const double* rc = (s.it == 1 ? a.r0w : a.r) + ow;
@@ -489,7 +537,7 @@ TSF_D bool dev_bicg_v(const KrylovArgs& a, const FilterTables& tab, KState* st, 
     return true;
   }
   store_owned<N>(a.s + ow, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.sh + ow, n, a.pspec + ow, sm, tab, hs);
+  if constexpr (PC >= 1) precond_any<N, PC>(u, a.sh + ow, a, b, sm, tab, hs);
   if (tid == 0) {
     st[b].alpha = alpha;
     st[b].snorm = snorm;
@@ -522,7 +570,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
   prefetch_l2(a.p + ow, vs);
   prefetch_l2(a.v + ow, vs);
   double u[FShape<N>::E];
-  double2* hs = PC ? hspec_of<N>(a, b) : nullptr;
+  double2* hs = PC == 1 ? hspec_of<N>(a, b) : nullptr;
   apply_level_op<N>(shg, kg, a.shift, n, u, sm, aux, tab, hs, hz);   // u = t = M s_hat
   // Every epilogue operand is loaded here at once, while the transform's
   // registers are dead: one exposed memory latency per phase instead of one
@@ -604,7 +652,7 @@ TSF_D bool dev_bicg_t(const KrylovArgs& a, const FilterTables& tab, KState* st, 
     for (int c = 0; c < E; ++c) u[c] = u[c] + beta * (qv[c] - omega * vv[c]);
   }
   store_owned<N>(a.p + ow, u, n);
-  if constexpr (PC == 1) precond_store<N>(u, a.ph + ow, n, a.pspec + ow, sm, tab, hs);
+  if constexpr (PC >= 1) precond_any<N, PC>(u, a.ph + ow, a, b, sm, tab, hs);
   if (tid == 0) {
     st[b].rho = s.rho_new;
     st[b].rho_new = rho_new;
@@ -671,7 +719,7 @@ TSF_D bool dev_cg_iter(const KrylovArgs& a, const FilterTables& tab, KState* st,
   }
   // z = P^{-1} r (into s), rz_new = r.z, p = z + beta p
   const double* zg = (PC ? a.s : a.r) + ow;
-  if constexpr (PC == 1) precond_store<N>(u, a.s + ow, n, a.pspec + ow, sm, tab);
+  if constexpr (PC >= 1) precond_any<N, PC>(u, a.s + ow, a, b, sm, tab);
   __syncthreads();
   part = 0.0;
   if (own) {
@@ -715,7 +763,7 @@ k_solve_begin(KrylovArgs a, KState* st, int* active) {
     if (st[blockIdx.x].done) return;                                                   \
     const FilterTables tab = stage_tables<N>(a.tab, reinterpret_cast<double2*>(        \
         reinterpret_cast<char*>(sm) + KShape<N>::FFT_BYTES + N * 8),                   \
-        PC ? a.pspec + (long)blockIdx.x * a.vs : nullptr);                              \
+        PC == 1 ? a.pspec + (long)blockIdx.x * a.vs : nullptr);                              \
     DNAME<N, PC>(a, tab, st, active, sm, red);                                         \
   }
 TSF_PHASE_KERNEL(k_cg_iter, dev_cg_iter)
@@ -740,7 +788,7 @@ TSF_D void bicg_phase(const KrylovArgs& a, KState* st, int* active) {
   if constexpr (!TSF_ENTRY_PRELOAD || kAsyncStaging || FStage<N>::MV || FStage<N>::PS) {
     // table-staging variants: the plain entry sequence
     if (st[blockIdx.x].done) return;
-    const FilterTables tab = stage_tables<N>(a.tab, tws, PC ? a.pspec + (long)blockIdx.x * a.vs : nullptr);
+    const FilterTables tab = stage_tables<N>(a.tab, tws, PC == 1 ? a.pspec + (long)blockIdx.x * a.vs : nullptr);
     if constexpr (TPHASE) dev_bicg_t<N, PC>(a, tab, st, active, sm, red);
     else dev_bicg_v<N, PC>(a, tab, st, active, sm, red);
   } else {
@@ -755,7 +803,7 @@ TSF_D void bicg_phase(const KrylovArgs& a, KState* st, int* active) {
     }
     const KState s = st[blockIdx.x];
     double2 hz[E];
-    const bool pre_spec = PC && a.hspec;
+    const bool pre_spec = PC == 1 && a.hspec;
     FilterTables tab = a.tab;
     if (pre_spec) load_even_spec<N>(hspec_of<N>(a, blockIdx.x), tab, hz);
     if (s.done) return;

@@ -887,13 +887,17 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
 // ---------------------------------------------------------------- TMA maps
 // (tsf_tma.cuh) encoded once per (pointer, shape) and cached: the workspace
 // pointers of a plan never move, so a solve's launches hit the cache.
-bool tma_enabled() {
+int tma_mode() {
+  // TSF_TMA: unset/"1"/"3" both column kernels, "0" none, "fwd"/"2"... per bit
   static int v = -1;
   if (v < 0) {
     const char* s = getenv("TSF_TMA");
-    v = (s && s[0] == '0') ? 0 : 1;
+    if (!s) v = 3;
+    else if (!strcmp(s, "fwd")) v = 1;
+    else if (!strcmp(s, "inv")) v = 2;
+    else v = atoi(s) == 1 ? 3 : atoi(s) & 3;
   }
-  return v == 1;
+  return v;
 }
 
 namespace {

@@ -124,8 +124,7 @@ struct LCol {
   static constexpr int SMEM = (G * BUF + tw_table_elems(N1)) * 16;
   // column-inverse kernels: + the two Z channel tiles (TMA landing zone),
   // 128-byte aligned after the twiddle table
-  static constexpr int ZT_OFF = (SMEM + 127) / 128 * 128;
-  static constexpr int SMEM_INV = ZT_OFF + 2 * N1 * G * 16;
+
 };
 template <int N2>
 struct LRow {
@@ -440,15 +439,14 @@ k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __
   const int t2 = blockIdx.x * G + g;
   double2* smg = sm + g * C::BUF;
   double2* tw1 = sm + G * C::BUF;
-  double2* ztile = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + C::ZT_OFF);
-  const int nch = out_mode == CO_APPLY ? 2 : 1;
+  // the channel tiles of Z land in the transform buffers (free until the
+  // channel's transform starts): no extra shared memory, same CTAs per SM
+  double2* ztile = sm;
   if (cm.use && threadIdx.x == 0) {
-    // both channels' [N1 x G] tiles of Z by TMA (tsf_tma.cuh)
+    // channel 0's [N1 x G] tile of Z by TMA (tsf_tma.cuh)
     mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, (unsigned)(nch * N1 * G * 16));
-    for (int ch = 0; ch < nch; ++ch)
-      tma_tile(reinterpret_cast<double*>(ztile + ch * N1 * G), &cm.z, 2 * blockIdx.x * G, N1,
-               2 * G, ch * a.B + b, 8, &bar);
+    mbar_expect_tx(&bar, (unsigned)(N1 * G * 16));
+    tma_tile(reinterpret_cast<double*>(ztile), &cm.z, 2 * blockIdx.x * G, N1, 2 * G, b, 8, &bar);
   }
   stage_tw<N1>(tw1, a.lt.tw1);
   const long off = (long)b * a.n;   // vectors [B][n]
@@ -478,11 +476,21 @@ k_lcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, const double* __
 #pragma unroll
   for (int c = 0; c < E; ++c) ye[c] = z[c].x;
   const double2* Zo = a.Z + (long)a.B * N;
+  if (cm.use) {
+    // channel 1's tile, once every thread's last transform pass is done
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bar, (unsigned)(N1 * G * 16));
+      tma_tile(reinterpret_cast<double*>(ztile), &cm.z, 2 * blockIdx.x * G, N1, 2 * G, a.B + b, 8,
+               &bar);
+    }
+    mbar_wait(&bar, 1);
+  }
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const int k1 = tid + c * T;
     const double2 w = tw_get_g(a.lt.twN, ((long)t2 * k1) & (N - 1));
-    z[c] = cmulc(cm.use ? ztile[N1 * G + k1 * G + g] : Zo[offz + (long)k1 * N2 + t2], w);
+    z[c] = cmulc(cm.use ? ztile[k1 * G + g] : Zo[offz + (long)k1 * N2 + t2], w);
   }
   group_fft<N1, E, true>(z, smg, tw1, 0, tid);
   Vals<2> pr;

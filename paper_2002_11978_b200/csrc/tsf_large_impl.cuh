@@ -23,8 +23,8 @@ inline cudaError_t large_prep(K kernel, int smem) {
 // TMA tile loads (tsf_tma.cuh) apply when the vectors are exact N1 x N2
 // views (n = nt: power-of-two n) and a G-column row segment is >= 16 bytes
 template <int N1>
-inline bool col_tma_ok(const LargeArgs& a) {
-  return tma_enabled() && a.n == a.nt && LCol<N1>::G * 8 >= 16;
+inline bool col_tma_ok(const LargeArgs& a, int which) {
+  return (tma_mode() & which) && a.n == a.nt && LCol<N1>::G * 8 >= 16;
 }
 
 template <int LOG>
@@ -35,7 +35,7 @@ int LargeDispatch<LOG>::col_fwd(const LargeArgs& a, const double* src, int in_mo
   const dim3 grid(a.nt / N1 / S::G, a.B);
   ColMaps cm;
   memset(&cm, 0, sizeof(cm));
-  if (col_tma_ok<N1>(a)) {
+  if (col_tma_ok<N1>(a, 1)) {
     const int N2 = (int)(a.nt / N1);
     const double* vs[3] = {src, nullptr, nullptr};
     int nv = 1;
@@ -91,17 +91,15 @@ int LargeDispatch<LOG>::col_inv(const LargeArgs& a, double* dst, int out_mode, c
   const dim3 grid(a.nt / N1 / S::G, a.B);
   ColMaps cm;
   memset(&cm, 0, sizeof(cm));
-  if (col_tma_ok<N1>(a)) {
+  if (col_tma_ok<N1>(a, 2)) {
     const int rc = tma_map_z(&cm.z, a.Z, N1, (int)(a.nt / N1), a.B, S::G);
     if (rc) return rc;
     cm.use = 1;
   }
-  // the Z tile landing zone only when TMA is on (otherwise the smaller
-  // footprint keeps more CTAs per SM)
-  const int smem = cm.use ? S::SMEM_INV : S::SMEM;
+  const int smem = S::SMEM;
   auto k = few_ctas((long)grid.x * grid.y) ? k_lcol_inv<N1, 1> : k_lcol_inv<N1>;
-  static cudaError_t prep = large_prep(k_lcol_inv<N1>, S::SMEM_INV);
-  static cudaError_t prep1 = large_prep(k_lcol_inv<N1, 1>, S::SMEM_INV);
+  static cudaError_t prep = large_prep(k_lcol_inv<N1>, S::SMEM);
+  static cudaError_t prep1 = large_prep(k_lcol_inv<N1, 1>, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
   if (prep1 != cudaSuccess) return large_launch_error(prep1);
   launch_pdl(k, grid, S::BLOCK, smem, st, a, dst, out_mode, xin, w1, pslot, cm);

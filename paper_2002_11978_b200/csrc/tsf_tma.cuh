@@ -81,6 +81,6 @@ TSF_D unsigned tma_tile(double* dst, const CUtensorMap* map, int col0, int rows,
 // host side (tsf_large.cu): encode / cache the maps of a launch
 int tma_map_vector(CUtensorMap* m, const double* base, long n, int N1, int N2, int B, int G);
 int tma_map_z(CUtensorMap* m, const double2* Z, int N1, int N2, int B, int G);
-bool tma_enabled();
+int tma_mode();   // TSF_TMA: bit 0 column-forward tiles, bit 1 column-inverse tiles
 
 }  // namespace tsf

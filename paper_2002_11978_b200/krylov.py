@@ -82,13 +82,23 @@ def _device_solve(op: LevelOperator, precond, rhs, tol, max_iters, method):
             raise TypeError("device solve supports the Strang CirculantPreconditioner or None")
         if precond.n != op.n:
             raise ValueError("preconditioner order differs from the operator")
-        pc = 1
+        pc = 1 if precond.strang_native else 2
         kbar = float(precond.kappa_bar)
     x = torch.empty_like(b)
     iters = torch.empty(B, dtype=torch.int32, device=b.device)
     relres = torch.empty(B, dtype=torch.float64, device=b.device)
     status = torch.empty(B, dtype=torch.int32, device=b.device)
     plan = op.toeplitz.plan
+    if pc == 2:
+        tab = torch.from_numpy(_circ_spectrum(precond, plan.L)).to(b.device)
+        _native.check(_native.load().tsf_krylov_solve_circ(
+            plan.handle, B, method, b.data_ptr(), x.data_ptr(), kap.data_ptr(), op.shift,
+            tab.data_ptr(), 0, float(tol), int(max_iters) if max_iters is not None else 0,
+            iters.data_ptr(), relres.data_ptr(), status.data_ptr(),
+            _native.stream_ptr(device=b.device)))
+        reps = _reports(iters.cpu(), relres.cpu(), status.cpu())
+        xs = _arrays.back(x, as_np)
+        return (xs, reps[0]) if b.dim() == 1 else (xs, reps)
     if pc and not plan.has_precond:
         raise NotImplementedError(
             f"device Strang preconditioner needs a power-of-two n >= 16 (got n={op.n})")
@@ -243,11 +253,35 @@ def _fused_ok(op, precond) -> bool:
         return False
     if precond is None:
         return True
-    if not getattr(precond, "strang_native", False):
+    from .toeplitz import CirculantPreconditioner
+    if not isinstance(precond, CirculantPreconditioner) or precond.n != op.n:
         return False
+    if not precond.strang_native:
+        # non-power-of-two n: the circulant-column preconditioner inside the
+        # fused kernels (tsf_krylov_solve_circ) uses THIS preconditioner's
+        # eigenvalues, so any shift / lam is honoured; single-CTA engine only
+        return op.n <= 4096
     if float(precond.shift) != float(op.shift):
         return False
     return precond.plan is op.toeplitz.plan or _same_strang(precond, op)
+
+
+def _circ_spectrum(precond, L: int):
+    """(S_2k, S_2k+1)/L of the length-L embedding of the circulant column
+    c = Re IFFT_n(1/total) (symmetrised: c_j = c_{n-j}), even part of the
+    symbol in extended precision — the table tsf_krylov_solve_circ takes.
+    Cached on the preconditioner."""
+    cached = getattr(precond, "_circ_tab", None)
+    if cached is not None and cached[0] == L:
+        return cached[1]
+    from .toeplitz import _even_embedding
+    c = np.fft.ifft(1.0 / np.asarray(precond.total_eigs, dtype=float)).real
+    c = 0.5 * (c + np.roll(c[::-1], 1))
+    sym = np.fft.fft(_even_embedding(c, L)).real.astype(np.longdouble)
+    ev = (0.5 * (sym + np.roll(sym[::-1], 1)) / L).astype(np.float64)
+    tab = np.ascontiguousarray(np.stack([ev[0::2], ev[1::2]], axis=1))   # [L/2, 2]
+    object.__setattr__(precond, "_circ_tab", (L, tab))
+    return tab
 
 
 def _same_strang(precond, op) -> bool:
