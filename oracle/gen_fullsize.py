@@ -288,6 +288,22 @@ def run_linalg_exact(pool):
     print("linalg exact", res, flush=True)
 
 
+def run_cfg3_exact(pool):
+    """cfg3_floor.json gains the correctly rounded engine's spread against
+    the stock run (cfg3.npz): all 256 levels' iterations and the stored
+    levels (sub-sampled rel-l2, as the GPU test measures them)."""
+    g = np.load(OUT / "cfg3.npz")
+    floor = json.loads((OUT / "cfg3_floor.json").read_text())
+    swap, its, keep = pool.map(_cfg3_one, ["exact"])[0]
+    ex = dict(_stats(its - g["its"]))
+    for m in CFG3_LEVELS:
+        ex[f"rel_l2_u{m}_sub"] = _rl2(keep[m][::CFG3_SUB], g[f"u{m}_sub"])
+        ex[f"rel_l2_u{m}"] = ex[f"rel_l2_u{m}_sub"]
+    floor["exact_engine"] = ex
+    (OUT / "cfg3_floor.json").write_text(json.dumps(floor, indent=1) + "\n")
+    print("cfg3 exact-engine floor", ex, flush=True)
+
+
 def run_cfg3(pool):
     res = dict((s, (its, keep)) for s, its, keep in pool.map(_cfg3_one, [False, True]))
     its, keep = res[False]
@@ -325,6 +341,8 @@ def main():
             run_cfg2_exact(pool)
         if "linalgexact" in which:
             run_linalg_exact(pool)
+        if "cfg3exact" in which:
+            run_cfg3_exact(pool)
         if "cfg0exact" in which:
             run_cfg0_exact(pool)
         if "cfg1exact" in which:
