@@ -244,7 +244,7 @@ def free_port() -> int:
         return so.getsockname()[1]
 
 
-def spawn_ranks(n: int, argv=None, executable=None) -> int:
+def spawn_ranks(n: int, argv=None, executable=None, script=None) -> int:
     """Run this script as `n` ranks, one process per GPU, with the environment
     torchrun would give them (RANK, LOCAL_RANK, WORLD_SIZE, MASTER_ADDR =
     127.0.0.1, MASTER_PORT); NCCL's INFO log (communicator / NVLS lines) goes
@@ -258,8 +258,9 @@ def spawn_ranks(n: int, argv=None, executable=None) -> int:
                    LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
         env.setdefault("NCCL_DEBUG", "INFO")
         env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-        procs.append(subprocess.Popen([executable or sys.executable, str(Path(__file__).resolve())]
-                                      + list(argv), env=env))
+        procs.append(subprocess.Popen([executable or sys.executable,
+                                       str(script or Path(__file__).resolve())] + list(argv),
+                                      env=env))
     rcs = [p.wait() for p in procs]
     return max(rcs)
 

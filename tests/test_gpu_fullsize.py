@@ -193,7 +193,11 @@ def test_cfg3_full_march_vs_reference():
         nref = float(g[f"u{lv}_norm"][0])
         e_norm = abs(np.linalg.norm(u) - nref) / nref
         e_proj = float(np.max(np.abs(Pj @ u - g[f"u{lv}_proj"]))) / (nref * math.sqrt(n))
-        tol_u = max(1e-10, 10 * floor[f"rel_l2_u{lv}"])
+        # the reference against itself with another FFT engine (scipy swap
+        # and, when generated, the correctly rounded DFT): 9e-13 at level 1,
+        # 4.5e-10 at level 256 — the march's drift at n = 2^20
+        fl_u = max(floor[f"rel_l2_u{lv}"], floor.get("exact_engine", {}).get(f"rel_l2_u{lv}", 0.0))
+        tol_u = max(1e-10, 10 * fl_u)
         print(f"cfg3 level {lv}: sub rel-l2 {e_sub:.2e} norm {e_norm:.2e} proj {e_proj:.2e} "
               f"(floor {floor[f'rel_l2_u{lv}']:.2e})")
         assert e_sub <= tol_u and e_norm <= tol_u and e_proj <= tol_u, lv
@@ -203,6 +207,7 @@ def test_cfg3_full_march_vs_reference():
     frac = float(np.mean(np.abs(d) <= 1))
     print(f"cfg3: within+-1 {frac:.3f} (floor {floor['within1']:.3f}) mean d {d.mean():+.3f} "
           f"(floor {floor['mean_d']:+.3f}) max|d| {np.abs(d).max()} (floor {floor['max_abs_d']})")
-    assert frac >= min(0.95, floor["within1"] - 0.05)
+    ex = floor.get("exact_engine", floor)
+    assert frac >= min(0.95, min(floor["within1"], ex["within1"]) - 0.05)
     assert abs(d.mean()) <= max(0.1, 3.0 * d.std() / math.sqrt(d.size)), (d.mean(), d.std())
-    assert np.max(np.abs(d)) <= 2 * max(2, floor["max_abs_d"])
+    assert np.max(np.abs(d)) <= 2 * max(2, floor["max_abs_d"], ex["max_abs_d"])

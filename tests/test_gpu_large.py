@@ -37,7 +37,8 @@ def _kappa(n, seed=0):
     return 1.0 + 0.5 * rng.uniform(0.2, 1.0) * np.sin(np.pi * x) ** 2
 
 
-@pytest.mark.parametrize("n", [8192, 16384, 65536, 1 << 20])
+# configs[4] spans n = 2^10..2^24: the four-step engine's sizes up to the top
+@pytest.mark.parametrize("n", [8192, 16384, 65536, 1 << 20, 1 << 22, 1 << 24])
 def test_large_matvec_vs_oracle(n):
     rng = np.random.default_rng(n)
     col = _col(n)
@@ -68,7 +69,7 @@ def test_large_matvec_batched_and_unit_vector():
         assert rel_err(got[b], O.toeplitz_apply(sym, V[b])) <= 1e-13
 
 
-@pytest.mark.parametrize("n", [8192, 65536, 1 << 20])
+@pytest.mark.parametrize("n", [8192, 65536, 1 << 20, 1 << 22, 1 << 24])
 def test_large_precond_vs_oracle(n):
     rng = np.random.default_rng(n + 1)
     col = _col(n)
