@@ -638,9 +638,20 @@ int large_plan_init(LargePlan* lp, int n, int L, const double* symbol_re, const 
   *lp = LargePlan{};
   lp->n = n;
   lp->nt = nt;
-  // columns short (cheap, G per CTA), rows up to the single-CTA limit 4096
-  lp->N1 = std::max(64, nt >> kLargeMaxLog);
+  // columns short (cheap, G per CTA), rows up to the single-CTA limit 4096;
+  // TSF_LARGE_ROWLOG caps log2(N2) lower (experiments: more, shorter rows)
+  int rowlog = kLargeMaxLog;
+  if (const char* e = getenv("TSF_LARGE_ROWLOG")) {
+    const int v = atoi(e);
+    if (v >= kLargeMinLog && v <= kLargeMaxLog) rowlog = v;
+  }
+  lp->N1 = std::max(64, nt >> rowlog);
+  if (lp->N1 > (1 << kLargeMaxLog)) lp->N1 = 1 << kLargeMaxLog;
   lp->N2 = nt / lp->N1;
+  if (lp->N2 > (1 << kLargeMaxLog) || lp->N2 < (1 << kLargeMinLog)) {
+    lp->N1 = std::max(64, nt >> kLargeMaxLog);
+    lp->N2 = nt / lp->N1;
+  }
   lp->ncol_cta = lp->N2 / col_group_at(ilog2i(lp->N1));
   lp->np = std::max(lp->ncol_cta, (n + kLelChunk - 1) / kLelChunk);
   lp->has_pc = lam != nullptr;

@@ -50,7 +50,9 @@ def main():
     if out.returncode != 0 or not line:
         raise SystemExit(f"ncu run failed: {out.returncode}\n{out.stderr[-2000:]}")
     bl = json.loads(line[-1])
-    rows = list(csv.DictReader(io.StringIO(log.read_text())))
+    txt = log.read_text().splitlines()
+    start_row = next(i for i, ln in enumerate(txt) if ln.startswith('"ID"'))
+    rows = list(csv.DictReader(io.StringIO("\n".join(txt[start_row:]))))
     # kernels of the timed region: the last `steps` levels' launches (the
     # bench's warm-up levels run first); take every launch after the
     # (warmup)th SOE launch, i.e. group the list by level via the SOE kernels
