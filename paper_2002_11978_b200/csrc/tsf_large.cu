@@ -851,11 +851,32 @@ static int loop_graph(LargePlan* lp, const Runner& R0, int method, int pc, cudaS
   return cuda_check(cudaGraphLaunch(G.exec, st), "cudaGraphLaunch");
 }
 
+// TSF_L2_PERSIST=1 (experiment): keep Z L2-resident through a persisting
+// access-policy window when it fits (tsf_large.cuh L2Window)
+struct L2Scope {
+  explicit L2Scope(const LargePlan* lp, int B) {
+    static int on = -1;
+    if (on < 0) {
+      const char* s = getenv("TSF_L2_PERSIST");
+      on = (s && s[0] == '1') ? 1 : 0;
+    }
+    const size_t bytes = 2 * (size_t)B * lp->nt * sizeof(double2);
+    if (!on || bytes > (64u << 20)) return;
+    static size_t limit = 0;
+    if (limit < bytes && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) == cudaSuccess)
+      limit = bytes;
+    l2_window().base = lp->Z;
+    l2_window().bytes = bytes;
+  }
+  ~L2Scope() { l2_window() = L2Window{}; }
+};
+
 int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, cudaStream_t st) {
   if (method != 0 && method != 1) return report_error(TSF_E_INVALID, "method must be 0 or 1");
   if (pc && !lp->has_pc) return report_error(TSF_E_UNSUPPORTED, "plan has no Strang preconditioner");
   int rc = large_reserve(lp, B);
   if (rc) return rc;
+  L2Scope l2(lp, B);
   Runner R = make_runner(lp, B, st);
   LargeArgs& a = R.a;
   KrylovArgs kk = k;

@@ -568,6 +568,19 @@ inline bool pdl_enabled() {
   }
   return v == 1;
 }
+// L2 persistence window of the running solve (TSF_L2_PERSIST=1, experiment):
+// the transform work array Z of a single large instance (32 MB at n = 2^20)
+// fits the 126 MB L2; a persisting access-policy window on every launch keeps
+// it there between the column / row / column kernels.  Set by the host around
+// the launches of one solve (tsf_large.cu), read by launch_pdl.
+struct L2Window {
+  void* base = nullptr;
+  size_t bytes = 0;
+};
+inline L2Window& l2_window() {
+  static thread_local L2Window w;
+  return w;
+}
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t st, Args... args) {
@@ -576,11 +589,25 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  const L2Window& w = l2_window();
+  if (w.base) {
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na].val.accessPolicyWindow.base_ptr = w.base;
+    at[na].val.accessPolicyWindow.num_bytes = w.bytes;
+    at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 

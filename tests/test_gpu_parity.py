@@ -252,6 +252,61 @@ def test_kappa_positivity_enforced():
         P.run_fids(spec, 4, 1.0, 257, options=P.SolverOptions(solver="pkrylov"))
 
 
+def test_failure_raises_at_the_failing_level():
+    """kappa turns non-positive only after t = 0.5: run_fids raises the
+    reference's ValueError for that level (scheme.py:156-160) — the march runs
+    in chunks of levels, so it stops there instead of after all M levels —
+    and a non-converging level raises the reference's RuntimeError
+    (scheme.py:139-142)."""
+    import time
+    M = 200
+    calls = []
+
+    def kappa(x, t):
+        calls.append(t)
+        return np.full_like(x, 1.0 if t <= 0.5 else -1.0)
+    spec = P.ProblemSpec(gamma=0.5, alpha=1.5, l=1.0, T=1.0, kappa=kappa,
+                         source=lambda x, t: np.sin(np.pi * x),
+                         initial=lambda x: (1 - x * x) ** 2)
+    mesh = P.build_mesh(M, 2.0, 1.0)
+    first_bad = int(np.argmax(mesh.t > 0.5))
+    with pytest.raises(ValueError, match=f"t={mesh.t[first_bad]}"):
+        P.run_fids(spec, M, 2.0, 257, options=P.SolverOptions(solver="pkrylov"))
+    # kappa was evaluated no further than the chunk holding the failing level
+    assert max(calls) <= mesh.t[min(M, first_bad + 32)]
+    spec_ok = P.ProblemSpec(gamma=0.5, alpha=1.5, l=1.0, T=1.0,
+                            kappa=lambda x, t: np.ones_like(x),
+                            source=lambda x, t: np.sin(np.pi * x),
+                            initial=lambda x: (1 - x * x) ** 2)
+    with pytest.raises(RuntimeError, match="did not converge"):
+        P.run_fids(spec_ok, M, 2.0, 257,
+                   options=P.SolverOptions(solver="pkrylov", tol=1e-14, max_iters=1))
+
+
+def test_generic_loop_takes_numpy_callables():
+    """An arbitrary MatrixFreeOperator over a dense numpy matrix with a numpy
+    preconditioner callable (the reference's own test operators,
+    pkg/tests/test_krylov.py:12-13) runs the reference's control flow with
+    numpy in and out of the callables."""
+    rng = np.random.default_rng(5)
+    n = 40
+    Q = rng.standard_normal((n, n))
+    A = Q @ Q.T + n * np.eye(n)
+    b = rng.standard_normal(n)
+    seen = []
+
+    def apply(v):
+        seen.append(type(v))
+        return A @ v
+    x, rep = P.solve_bicgstab(P.MatrixFreeOperator(n, apply), None, b, tol=1e-12)
+    assert rep.converged and isinstance(x, np.ndarray)
+    assert all(t is np.ndarray for t in seen)
+    assert np.linalg.norm(x - np.linalg.solve(A, b)) <= 1e-10 * np.linalg.norm(x)
+    Ainv = np.linalg.inv(A)
+    x, rep = P.solve_cg(P.MatrixFreeOperator(n, apply), lambda v: Ainv @ v, b)
+    assert rep.converged and rep.iterations <= 2
+
+
 def test_batched_march_matches_single_instances():
     """Instances in one batched march equal the same instances run alone."""
     n, M, gam, a = 256, 24, 0.5, 1.5
