@@ -241,6 +241,18 @@ int tsf_fids_march(tsf_plan* plan, const tsf_march* desc, void* stream);
  * block Stockham engine.  inverse != 0 gives the unnormalised inverse. */
 int tsf_fft_debug(int N, int inverse, int B, const double* in, double* out, void* stream);
 
+/* Test hook for the half-length transform engine of the level solve
+ * (csrc/tsf_half.cuh; power-of-two n, 512 <= n <= 4096), the device form of
+ * toeplitz.py:131-136 (mode 0) and toeplitz.py:51-63 + scheme.py:129-130
+ * (mode 1):
+ *   mode 0: out[B][n] = Re IFFT_n(FFT_n(x) . aux), aux[B][n] = the real even
+ *           filter S_k / n; hs[B][n/2+1] (complex, interleaved) receives the
+ *           filtered half spectrum.
+ *   mode 1: out = shift*x + aux .* (A x) for x = Re IFFT_n(hs) (aux = kappa).
+ * Returns TSF_E_UNSUPPORTED when the size is outside the engine. */
+int tsf_half_debug(tsf_plan* plan, int mode, int B, const double* x, const double* aux,
+                   double shift, double* hs, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

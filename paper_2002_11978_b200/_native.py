@@ -41,7 +41,7 @@ EXPORTS = (
     "tsf_abi_version", "tsf_last_error", "tsf_plan_create", "tsf_plan_destroy",
     "tsf_plan_info", "tsf_plan_reserve", "tsf_toeplitz_matvec", "tsf_precond_solve",
     "tsf_krylov_solve", "tsf_krylov_solve_circ", "tsf_soe_push_rhs", "tsf_fids_march",
-    "tsf_fft_debug", "tsf_l1_history_rhs",
+    "tsf_fft_debug", "tsf_l1_history_rhs", "tsf_half_debug",
 )
 
 P = C.c_void_p
@@ -101,6 +101,7 @@ def load(path: Optional[os.PathLike] = None):
         "tsf_fids_march": (I, [P, C.POINTER(March), P]),
         "tsf_fft_debug": (I, [I, I, I, P, P, P]),
         "tsf_l1_history_rhs": (I, [I, I, I, P, C.c_int64, P, D, D, P, P, P]),
+        "tsf_half_debug": (I, [P, I, I, P, P, D, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

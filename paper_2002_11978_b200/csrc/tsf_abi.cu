@@ -74,6 +74,17 @@ bool spec_reuse() {
   return v == 1;
 }
 
+// Half-length transform engine of the Strang-preconditioned BiCGSTAB level
+// solve (tsf_half.cuh); TSF_HALF=0 restores the full-length phase kernels.
+bool half_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_HALF");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int solve_groups(int B) {
   static int env = -2;
   if (env == -2) {
@@ -201,6 +212,11 @@ template <int LOG>
 struct FftF {
   template <typename... A>
   static int call(A... a) { return Dispatch<LOG>::fft(a...); }
+};
+template <int LOG>
+struct HalfDebugF {
+  template <typename... A>
+  static int call(A... a) { return Dispatch<LOG>::half_debug(a...); }
 };
 
 
@@ -790,6 +806,19 @@ int tsf_fft_debug(int N, int inverse, int B, const double* in, double* out, void
   }
   return ForLog<FftF>::run(lg, inverse, B, (const double2*)in, (double2*)out,
                            (const double2*)dtw[lg], (cudaStream_t)stream);
+}
+
+int tsf_half_debug(tsf_plan* p, int mode, int B, const double* x, const double* aux, double shift,
+                   double* hs, double* out, void* stream) {
+  if (!p || !x || !aux || !hs || !out || B < 1 || (mode != 0 && mode != 1))
+    return fail(TSF_E_INVALID, "bad half-engine debug arguments");
+  if (p->large || p->layout || !p->has_pc || p->n * 2 != p->L)
+    return fail(TSF_E_UNSUPPORTED, "half-length engine needs a power-of-two n <= 4096");
+  DeviceGuard dg(p->device);
+  const int rc = ForLog<HalfDebugF>::run(p->log_L, mode, B, x, aux, shift, (double2*)hs, out,
+                                         p->tables(), (cudaStream_t)stream);
+  if (rc == -1) return fail(TSF_E_UNSUPPORTED, "half-length engine not built for this size");
+  return rc;
 }
 
 }  // extern "C"

@@ -21,6 +21,7 @@ int report_cuda(cudaError_t e, const char* what);
 constexpr int kMaxSolveGroups = 8;
 struct SolveGraph {
   bool built = false;
+  bool half = false;   // built from the half-length kernels (tsf_half.cuh)
   int groups = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -35,6 +36,7 @@ struct SolveGraphs {
 };
 bool graph_mode();  // TSF_SOLVE_GRAPH (default 1)
 bool spec_reuse();  // TSF_SPEC_REUSE (default 1)
+bool half_mode();   // TSF_HALF (default 1): half-length transform engine, tsf_half.cuh
 
 template <int LOG>
 struct Dispatch {
@@ -48,6 +50,9 @@ struct Dispatch {
   // 1: the 64 x 64 engine (tsf_fft64.cuh) — plan tables and workspace
   // vectors in the permuted internal layout, per-instance stride N
   static int layout();
+  // building blocks of the half-length engine alone (tests): -1 = not built for this size
+  static int half_debug(int mode, int B, const double* x, const double* aux_in, double shift,
+                        double2* hs, double* out, const FilterTables& t, cudaStream_t st);
 };
 
 #define TSF_EXTERN_DISPATCH(L) extern template struct Dispatch<L>;

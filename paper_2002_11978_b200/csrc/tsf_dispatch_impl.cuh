@@ -8,6 +8,7 @@
 #include <cstdlib>
 
 #include "tsf_dispatch.h"
+#include "tsf_half.cuh"
 
 namespace tsf {
 
@@ -108,6 +109,44 @@ inline KrylovArgs group_args(const KrylovArgs& a, int N, bool full_spec, int o, 
   return r;
 }
 
+// Half-length transform engine (tsf_half.cuh): Strang-preconditioned BiCGSTAB
+// with the spectrum reuse on a power-of-two grid, 16-byte aligned vectors.
+template <int N, int PC, bool CG>
+bool use_half(const KrylovArgs& a) {
+  if constexpr (PC == 1 && !CG && half_ok<N>()) {
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return half_mode() && a.hspec && !a.soe_epilogue && a.n == N && a.vs == N && al(a.rhs) &&
+           al(a.x) &&
+           (a.kappa ? al(a.kappa)
+                    : (al(a.kmodes) && al(a.kwork) && a.kq_stride % 2 == 0 && a.kb_stride % 2 == 0));
+  } else {
+    return false;
+  }
+}
+using SolveKernel = void (*)(KrylovArgs, KState*, int*);
+template <int N, int PC, bool CG>
+struct SolveKernels {
+  SolveKernel kb, kv, kt, kc;
+  int block, smem;
+  explicit SolveKernels(bool half) {
+    kb = k_solve_begin<N, PC, CG>;
+    kv = k_bicg_v<N, PC>;
+    kt = k_bicg_t<N, PC>;
+    kc = k_cg_iter<N, PC>;
+    block = KShape<N>::BLOCK;
+    smem = KShape<N>::SMEM;
+    if constexpr (PC == 1 && !CG && half_ok<N>()) {
+      if (half) {
+        kb = k_solve_begin_h<N>;
+        kv = k_bicg_v_h<N>;
+        kt = k_bicg_t_h<N>;
+        block = HShape<N>::BLOCK;
+        smem = HShape<N>::SMEM;
+      }
+    }
+  }
+};
+
 // The level solve as one graph launch of G independent branches over
 // contiguous instance groups.  With one branch, the level's tail (a few
 // slow instances, ~30-40 us per phase launch) leaves the GPU nearly idle;
@@ -117,28 +156,27 @@ inline KrylovArgs group_args(const KrylovArgs& a, int N, bool full_spec, int o, 
 // with one branch (per-instance CTAs), so results do not depend on G.
 template <int N, int PC, bool CG>
 int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
-  using S = KShape<N>;
   constexpr int LOG = ilog2(2 * N);
   SolveGraphs* cache = static_cast<SolveGraphs*>(a_in.graphs);
   SolveGraph& G = cache->slot[LOG][PC][CG ? 1 : 0];
   const int ng = solve_groups(B);
   const int bg = (B + ng - 1) / ng;
+  const bool half = use_half<N, PC, CG>(a_in);
+  const SolveKernels<N, PC, CG> K(half);
   cudaError_t e;
-  if (G.built && G.groups != ng) {
+  if (G.built && (G.groups != ng || G.half != half)) {
     cudaGraphExecDestroy(G.exec);
     cudaGraphDestroy(G.graph);
     G = SolveGraph{};
   }
-  auto kb = k_solve_begin<N, PC, CG>;
-  auto kv = k_bicg_v<N, PC>;
-  auto kt = k_bicg_t<N, PC>;
-  auto kc = k_cg_iter<N, PC>;
+  const SolveKernel kb = K.kb, kv = K.kv, kt = K.kt, kc = K.kc;
   if (!G.built) {
-    if ((e = prep_kernel(kb, S::SMEM)) != cudaSuccess) return launch_error(e);
-    if ((e = prep_kernel(CG ? kc : kv, S::SMEM)) != cudaSuccess) return launch_error(e);
-    if (!CG && (e = prep_kernel(kt, S::SMEM)) != cudaSuccess) return launch_error(e);
+    if ((e = prep_kernel(kb, K.smem)) != cudaSuccess) return launch_error(e);
+    if ((e = prep_kernel(CG ? kc : kv, K.smem)) != cudaSuccess) return launch_error(e);
+    if (!CG && (e = prep_kernel(kt, K.smem)) != cudaSuccess) return launch_error(e);
     if ((e = cudaGraphCreate(&G.graph, 0)) != cudaSuccess) return launch_error(e);
     G.groups = ng;
+    G.half = half;
   }
   for (int g = 0; g < ng; ++g) {
     const int o = g * bg;
@@ -150,10 +188,10 @@ int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
     void* set_args[] = {&active, &bval};
     void* k_args[] = {&a, &kst, &active};
     const cudaKernelNodeParams p_set = knode(k_set_int, dim3(1), dim3(1), 0, set_args);
-    const cudaKernelNodeParams p_begin = knode(kb, dim3(Bg), dim3(S::BLOCK), S::SMEM, k_args);
-    const cudaKernelNodeParams p_a = CG ? knode(kc, dim3(Bg), dim3(S::BLOCK), S::SMEM, k_args)
-                                        : knode(kv, dim3(Bg), dim3(S::BLOCK), S::SMEM, k_args);
-    const cudaKernelNodeParams p_b = knode(kt, dim3(Bg), dim3(S::BLOCK), S::SMEM, k_args);
+    const cudaKernelNodeParams p_begin = knode(kb, dim3(Bg), dim3(K.block), K.smem, k_args);
+    const cudaKernelNodeParams p_a = CG ? knode(kc, dim3(Bg), dim3(K.block), K.smem, k_args)
+                                        : knode(kv, dim3(Bg), dim3(K.block), K.smem, k_args);
+    const cudaKernelNodeParams p_b = knode(kt, dim3(Bg), dim3(K.block), K.smem, k_args);
     // the loop test reads the group's active counter, which moves when the
     // plan's workspaces grow (ensure_reserved): its node is rewritten too
     cudaGraphConditionalHandle h = G.cond[g];
@@ -219,27 +257,25 @@ int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
     kp<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
     return launch_error(cudaGetLastError());
   }
-  auto kb = k_solve_begin<N, PC, CG>;
-  if ((e = prep_kernel(kb, S::SMEM)) != cudaSuccess) return launch_error(e);
-  auto kv = k_bicg_v<N, PC>;
-  auto kt = k_bicg_t<N, PC>;
-  auto kc = k_cg_iter<N, PC>;
+  const SolveKernels<N, PC, CG> K(use_half<N, PC, CG>(a));
+  const SolveKernel kb = K.kb, kv = K.kv, kt = K.kt, kc = K.kc;
+  if ((e = prep_kernel(kb, K.smem)) != cudaSuccess) return launch_error(e);
   if (!CG) {
-    if ((e = prep_kernel(kv, S::SMEM)) != cudaSuccess) return launch_error(e);
-    if ((e = prep_kernel(kt, S::SMEM)) != cudaSuccess) return launch_error(e);
-  } else if ((e = prep_kernel(kc, S::SMEM)) != cudaSuccess) {
+    if ((e = prep_kernel(kv, K.smem)) != cudaSuccess) return launch_error(e);
+    if ((e = prep_kernel(kt, K.smem)) != cudaSuccess) return launch_error(e);
+  } else if ((e = prep_kernel(kc, K.smem)) != cudaSuccess) {
     return launch_error(e);
   }
   k_set_int<<<1, 1, 0, st>>>(a.active, B);
-  kb<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
+  kb<<<B, K.block, K.smem, st>>>(a, a.kst, a.active);
   if ((e = cudaGetLastError()) != cudaSuccess) return launch_error(e);
   for (int it = 0; it < a.max_iters; it += kChunk) {
     for (int k = 0; k < kChunk && it + k < a.max_iters; ++k) {
       if (!CG) {
-        kv<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
-        kt<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
+        kv<<<B, K.block, K.smem, st>>>(a, a.kst, a.active);
+        kt<<<B, K.block, K.smem, st>>>(a, a.kst, a.active);
       } else {
-        kc<<<B, S::BLOCK, S::SMEM, st>>>(a, a.kst, a.active);
+        kc<<<B, K.block, K.smem, st>>>(a, a.kst, a.active);
       }
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return launch_error(e);
@@ -261,6 +297,21 @@ int Dispatch<LOG>::solve(int B, int method, int pc, const KrylovArgs& a, cudaStr
   }
   if (pc == 2) return solve_t<N, 2, true>(B, a, st);
   return pc ? solve_t<N, 1, true>(B, a, st) : solve_t<N, 0, true>(B, a, st);
+}
+
+template <int LOG>
+int Dispatch<LOG>::half_debug(int mode, int B, const double* x, const double* aux_in, double shift,
+                              double2* hs, double* out, const FilterTables& t, cudaStream_t st) {
+  constexpr int N = 1 << (LOG - 1);
+  if constexpr (half_ok<N>()) {
+    auto k = k_half_debug<N>;
+    cudaError_t e = prep_kernel(k, HShape<N>::SMEM);
+    if (e != cudaSuccess) return launch_error(e);
+    k<<<B, HShape<N>::BLOCK, HShape<N>::SMEM, st>>>(mode, x, aux_in, shift, hs, out, t);
+    return launch_error(cudaGetLastError());
+  } else {
+    return -1;
+  }
 }
 
 template <int LOG>

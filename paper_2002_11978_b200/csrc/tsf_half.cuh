@@ -1,0 +1,517 @@
+// Half-length transform engine of the Strang-preconditioned BiCGSTAB level
+// solve (power-of-two n = N, 512 <= N <= 4096).
+//
+// Every transform of a level solve (scheme.py:120-143, krylov.py:88-153,
+// toeplitz.py:51-63 and 131-136) acts on real data, or on the odd bins of a
+// real sequence, so each runs as ONE complex transform of length H = N/2:
+//
+//  * Strang solve of a real vector u: z_m = u_{2m} + i u_{2m+1}, Z = FFT_H(z),
+//    split step  P_k = E_k + W_N^k O_k,  E = (Z_k + conj Z_{H-k})/2,
+//    O = -i (Z_k - conj Z_{H-k})/2  (k = 0..H; the thread owning bin k gets
+//    Z_{H-k} through one shared-memory mirror exchange and forms both P_k and
+//    conj(P_{H-k}) = E_k - W_N^k O_k), filter Q = P . S/n, inverse pre-step
+//    Z'_k = (Q_k + conj Q_{H-k}) + i conj(W_N^k)(Q_k - conj Q_{H-k}),
+//    IFFT_H(Z')_m = q_{2m} + i q_{2m+1}.
+//  * Toeplitz product, even bins: spectrum N Herm(Q) of the Strang output is
+//    already known (tsf_filters.cuh filt_strang_tab), so only the pre-step
+//    and one inverse transform.
+//  * Toeplitz product, odd bins: X_{4m+1} = FFT_H[ W_L^j (x_j - i x_{j+H}) ]_m
+//    exactly (DIF step; the bins 4m+3 are the conjugate mirrors of a real
+//    sequence), g = IFFT_H(S_{4m+1} X_{4m+1}),
+//    y_j = 2 Re(conj(w_j) g_j),  y_{j+H} = -2 Im(conj(w_j) g_j).
+//
+// Five length-H transforms per BiCGSTAB half-iteration instead of five of
+// length N: half the FP64 and shared-memory work, and a 256-thread CTA per
+// instance at N = 4096, so two CTAs share an SM and overlap each other's
+// barrier phases.  Parity: the odd-bin channel is the pruned complex
+// transform (same rounding structure), the packed forward transform only
+// feeds the preconditioner, and the packed inverse has the error of a complex
+// inverse; tools/half_probe.py measures the reference's iteration counts
+// under this arithmetic on the CPU (identical +-1 statistics to the
+// full-length structure), DESIGN.md §3.8.
+//
+// Real-vector ownership: thread t owns the 16 reals (2m, 2m+1), m = t + c T,
+// c < 8 (one 16-byte access per slot) for every elementwise step; the odd
+// channel reads x at (m, m+H) and returns its result through the shared
+// staging vector.
+#pragma once
+
+#include "tsf_kernels.cuh"
+
+#ifndef TSF_HALF
+#define TSF_HALF 1
+#endif
+
+namespace tsf {
+
+template <int N>
+struct HShape {
+  static constexpr int H = N / 2;
+  static constexpr int E = 8;
+  static constexpr int T = H / E;
+  static constexpr int BLOCK = T < 32 ? 32 : T;
+  using PL = FftPlan<(H < 8 ? 8 : H), E>;
+  static constexpr int FFT_BYTES = 2 * PL::SMEM_ELEMS * 16;
+  static constexpr int TW_BYTES = tw_table_elems(2 * N) * 16;
+  // transform buffers | real staging vector (N doubles) | twiddle table
+  static constexpr int SMEM = FFT_BYTES + N * 8 + TW_BYTES;
+  static constexpr int MIN_BLOCKS = BLOCK >= 512 ? 1 : 512 / BLOCK;  // <= 128 registers
+};
+
+template <int N>
+constexpr bool half_ok() {
+  return TSF_HALF && N >= 512 && !use64<N>() && !kFftInPlace && kE == 8 && !kAsyncStaging &&
+         !kPassTw && !kPassTwSmall;
+}
+
+template <int N>
+TSF_D const double2* stage_tw_half(const double2* g, double2* dst) {
+  constexpr int NT = tw_table_elems(2 * N);
+  for (int i = threadIdx.x; i < NT; i += blockDim.x) dst[i] = ldt(&g[i]);
+  return dst;
+}
+
+template <int N>
+TSF_D void ld2(double2 (&u)[8], const double* g) {
+  const double2* g2 = reinterpret_cast<const double2*>(g);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) u[c] = g2[threadIdx.x + c * HShape<N>::T];
+}
+template <int N>
+TSF_D void st2(double* g, const double2 (&u)[8]) {
+  double2* g2 = reinterpret_cast<double2*>(g);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) g2[threadIdx.x + c * HShape<N>::T] = u[c];
+}
+
+template <int N, bool INV, class Hook = NoHook>
+TSF_D void hfft(double2 (&z)[8], double2* sm, const double2* tw, const Hook& hook = Hook{}) {
+  // W_H^e = W_L^{4e}: the staged table is the length-L one (tw_log_scale 2)
+  block_fft<N / 2, 8, INV>(z, sm, tw, 2, static_cast<const double2*>(nullptr), hook);
+}
+
+// inverse pre-step of a Hermitian spectrum given as (Q_k, conj Q_{H-k}):
+// the packed slot Z'_k whose inverse transform is (q_{2m}, q_{2m+1})
+TSF_D double2 pack_inverse(double2 Q, double2 cQm, double2 w) {
+  const double2 Ep = cadd(Q, cQm);
+  const double2 Op = cmulc(csub(Q, cQm), w);   // (Q - conj Q_{H-k}) conj(W_N^k)
+  return make_double2(Ep.x - Op.y, Ep.y + Op.x);
+}
+
+// z[c] = (u_{2m}, u_{2m+1}) in; (q_{2m}, q_{2m+1}) out, q = Re IFFT_N(FFT_N(u) . spec)
+// with spec[k] = S_k / n for k <= H.  hs (may be null) receives Q_k, k <= H.
+template <int N>
+TSF_D void strang_half(double2 (&z)[8], double2* sm, const double2* tw,
+                       const double* __restrict__ spec, double2* __restrict__ hs) {
+  constexpr int H = N / 2;
+  constexpr int T = HShape<N>::T;
+  using PL = typename HShape<N>::PL;
+  const int tid = threadIdx.x;
+  double sk[8], sr[8];
+  hfft<N, false>(z, sm, tw, [&] {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int k = tid + c * T;
+      sk[c] = 0.5 * spec[k];        // the split step's 1/2 folded in (exact)
+      sr[c] = 0.5 * spec[H - k];
+    }
+  });
+  // mirror exchange through the buffer the last pass did not read
+  double2* xb = sm + ((PL::NPASS - 1) & 1) * PL::SMEM_ELEMS;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) xb[PL::pad(tid + c * T)] = z[c];
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int k = tid + c * T;
+    const double2 zm = xb[PL::pad((H - k) & (H - 1))];
+    const double2 A = z[c];
+    const double2 s = make_double2(A.x + zm.x, A.y - zm.y);   // A + conj(Zm)
+    const double2 d = make_double2(A.x - zm.x, A.y + zm.y);   // A - conj(Zm)
+    const double2 w = tw_get(tw, 2 * k);                      // W_N^k
+    const double2 Tt = cmul(w, make_double2(d.y, -d.x));      // W_N^k (-i d)
+    const double2 Q = cscale(cadd(s, Tt), sk[c]);
+    const double2 cQm = cscale(csub(s, Tt), sr[c]);           // conj Q_{H-k}
+    if (hs) {
+      hs[k] = Q;
+      if (k == 0) hs[H] = cconj(cQm);
+    }
+    z[c] = pack_inverse(Q, cQm, w);
+  }
+  hfft<N, true>(z, sm, tw);
+}
+
+// even bins of the Toeplitz product of x = Re IFFT_N(hs) from its stored half
+// spectrum: z[c] = (ye_{2m}, ye_{2m+1}) on return
+template <int N, class Hook = NoHook>
+TSF_D void even_half(const double2* __restrict__ hs, const FilterTables& t, double2 (&z)[8],
+                     double2* sm, const Hook& hook = Hook{}) {
+  constexpr int H = N / 2;
+  constexpr int T = HShape<N>::T;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int k = tid + c * T;
+    const double2 a = hs[k], bm = hs[H - k];
+    const double fa = ldt(&t.mvS[k]).x * N, fb = ldt(&t.mvS[H - k]).x * N;  // N S_2k / L (exact)
+    const double2 Q = cscale(a, fa);
+    const double2 cQm = make_double2(bm.x * fb, -bm.y * fb);
+    z[c] = pack_inverse(Q, cQm, tw_get(t.tw, 2 * k));
+  }
+  hfft<N, true>(z, sm, t.tw, hook);
+}
+
+// y = shift*x + kappa .* (A x) for x = the last Strang output (half spectrum
+// hs), result in the (2m, 2m+1) ownership
+template <int N>
+TSF_D void apply_level_op_half(const double* __restrict__ xg, const double* __restrict__ kg,
+                               double shift, double2 (&y)[8], double2* sm, double* aux,
+                               const FilterTables& t, const double2* __restrict__ hs) {
+  constexpr int H = N / 2;
+  constexpr int T = HShape<N>::T;
+  const int tid = threadIdx.x;
+  double2 z[8];
+  double xa[8], xb[8];
+  even_half<N>(hs, t, z, sm, [&] {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      xa[c] = xg[tid + c * T];
+      xb[c] = xg[tid + c * T + H];
+    }
+  });
+  double2* aux2 = reinterpret_cast<double2*>(aux);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) aux2[tid + c * T] = z[c];
+  // odd bins: z_m = w_m (x_m - i x_{m+H})
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double2 w = tw_get(t.tw, tid + c * T);
+    z[c] = make_double2(fma(w.x, xa[c], w.y * xb[c]), fma(w.y, xa[c], -(w.x * xb[c])));
+  }
+  double so[8];
+  hfft<N, false>(z, sm, t.tw, [&] {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) so[c] = 2.0 * ldt(&t.mvS[2 * (tid + c * T)]).y;   // 2 S_{4m+1} / L
+  });
+#pragma unroll
+  for (int c = 0; c < 8; ++c) z[c] = cscale(z[c], so[c]);
+  double2 x2[8], k2[8];
+  hfft<N, true>(z, sm, t.tw, [&] {
+    ld2<N>(x2, xg);
+    if (kg) ld2<N>(k2, kg);
+  });
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int m = tid + c * T;
+    const double2 w = tw_get(t.tw, m);
+    aux[m] += fma(w.x, z[c].x, w.y * z[c].y);          //  Re(conj(w) g)
+    aux[m + H] -= fma(w.x, z[c].y, -(w.y * z[c].x));   // -Im(conj(w) g)
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double2 ax = aux2[tid + c * T];
+    y[c] = kg ? make_double2(fma(shift, x2[c].x, k2[c].x * ax.x), fma(shift, x2[c].y, k2[c].y * ax.y))
+              : ax;
+  }
+}
+
+// ---- begin: kappa, kappa_bar, checks, Strang filter of the level, r0, p_hat
+template <int N>
+__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
+k_solve_begin_h(KrylovArgs a, KState* st, int* active) {
+  using S = HShape<N>;
+  constexpr int T = S::T;
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
+  const double2* tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
+  const int tid = threadIdx.x;
+  const int b = blockIdx.x;
+  const long ow = (long)b * N;
+  double ksum = 0.0, kmin = 1e308;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int j = 2 * (tid + c * T);
+    double2 k;
+    if (a.kappa) {
+      k = *reinterpret_cast<const double2*>(a.kappa + ow + j);
+    } else {
+      k = make_double2(0.0, 0.0);
+      for (int q = 0; q < a.nk; ++q) {
+        const double* mq = a.kmodes + q * a.kq_stride + (long)b * a.kb_stride + j;
+        // no contraction: reproduce numpy's  acc + mode*coef  rounding
+        k.x = __dadd_rn(k.x, __dmul_rn(mq[0], a.kcoef[q]));
+        k.y = __dadd_rn(k.y, __dmul_rn(mq[1], a.kcoef[q]));
+      }
+      *reinterpret_cast<double2*>(a.kwork + ow + j) = k;
+    }
+    ksum += k.x;
+    ksum += k.y;
+    kmin = fmin(kmin, fmin(k.x, k.y));
+  }
+  kmin = block_min1(kmin, red);
+  if (kmin <= 0.0) {
+    finish_instance(a, st, active, b, 0, 0.0, TSF_KAPPA_NONPOS, sm);
+    return;
+  }
+  const double kmean = block_sum1(ksum, red) / N;
+  const double kbar = a.kbar > 0.0 ? a.kbar : kmean;
+  const double d = a.shift;
+  double tmin = 1e308;
+  for (int k = tid; k < N; k += blockDim.x) tmin = fmin(tmin, d + kbar * ldt(&a.tab.pclam[k]).x);
+  tmin = block_min1(tmin, red);
+  if (tmin <= 0.0) {
+    finish_instance(a, st, active, b, 0, 0.0, TSF_PRECOND_NONPOS, sm);
+    return;
+  }
+  // the level's Strang filter (even part of 1/total, 1/n folded in), k < n
+  for (int k = tid; k < N; k += blockDim.x) {
+    const double2 lam = ldt(&a.tab.pclam[k]);
+    a.pspec[ow + k] = 0.5 * (1.0 / (d + kbar * lam.x) + 1.0 / (d + kbar * lam.y)) / N;
+  }
+  double2 u[8];
+  ld2<N>(u, a.rhs + ow);
+  double ss = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    ss = fma(u[c].x, u[c].x, ss);
+    ss = fma(u[c].y, u[c].y, ss);
+  }
+  ss = block_sum1(ss, red);   // (its barriers publish pspec and the twiddle table)
+  {
+    double2 zero[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) zero[c] = make_double2(0.0, 0.0);
+    st2<N>(a.x + ow, zero);
+  }
+  if (sqrt(ss) == 0.0) {
+    finish_instance(a, st, active, b, 0, 0.0, TSF_OK, sm);
+    return;
+  }
+  st2<N>(a.p + ow, u);
+  strang_half<N>(u, sm, tw, a.pspec + ow, a.hspec + (long)b * (N / 2 + 1));
+  st2<N>(a.ph + ow, u);
+  if (tid == 0) {
+    KState s;
+    s.rho = s.alpha = s.omega = 1.0;
+    s.rho_new = ss;
+    s.nrm0 = s.rnorm = s.snorm = sqrt(ss);
+    s.kbar = kbar;
+    s.rz = ss;
+    s.it = 1;
+    s.done = 0;
+    st[b] = s;
+  }
+}
+
+// ---- v-phase: v = M p_hat, alpha, s = r - alpha v, ||s|| (early exit), s_hat
+template <int N>
+__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
+k_bicg_v_h(KrylovArgs a, KState* st, int* active) {
+  using S = HShape<N>;
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  const int b = blockIdx.x;
+  if (st[b].done) return;
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
+  FilterTables tab = a.tab;
+  tab.tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
+  const KState s = st[b];
+  const int tid = threadIdx.x;
+  const long ow = (long)b * N;
+  const double* phg = a.ph + ow;
+  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + ow;
+  double2* hs = a.hspec + (long)b * (N / 2 + 1);
+  prefetch_l2(kg, N);
+  prefetch_l2(a.r0w + ow, N);
+  if (s.it != 1) prefetch_l2(a.r + ow, N);
+  __syncthreads();   // twiddle table staged
+  double2 u[8];
+  apply_level_op_half<N>(phg, kg, a.shift, u, sm, aux, tab, hs);   // u = v = M p_hat
+  const double* rc = (s.it == 1 ? a.r0w : a.r) + ow;
+  double2 r0v[8], rv[8];
+  ld2<N>(r0v, a.r0w + ow);
+  ld2<N>(rv, rc);
+  st2<N>(a.v + ow, u);
+  double part = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    part = fma(r0v[c].x, u[c].x, part);
+    part = fma(r0v[c].y, u[c].y, part);
+  }
+  const double denom = block_sum1(part, red);
+  if (denom == 0.0) {
+    finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_R0V, sm);
+    return;
+  }
+  const double alpha = s.rho_new / denom;
+  part = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    u[c].x = rv[c].x - alpha * u[c].x;
+    u[c].y = rv[c].y - alpha * u[c].y;
+    part = fma(u[c].x, u[c].x, part);
+    part = fma(u[c].y, u[c].y, part);
+  }
+  const double snorm = sqrt(block_sum1(part, red));
+  if (snorm / s.nrm0 < a.tol) {
+    // x += alpha p_hat (early exit counts as a full iteration, krylov.py:135-137)
+    double2 xv[8], pv[8];
+    ld2<N>(xv, a.xw + ow);
+    ld2<N>(pv, phg);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      xv[c].x = xv[c].x + alpha * pv[c].x;
+      xv[c].y = xv[c].y + alpha * pv[c].y;
+    }
+    st2<N>(a.x + ow, xv);
+    finish_instance(a, st, active, b, s.it, snorm / s.nrm0, TSF_OK, sm);
+    return;
+  }
+  st2<N>(a.s + ow, u);
+  strang_half<N>(u, sm, tab.tw, a.pspec + ow, hs);
+  st2<N>(a.sh + ow, u);
+  if (tid == 0) {
+    st[b].alpha = alpha;
+    st[b].snorm = snorm;
+  }
+}
+
+// ---- t-phase: t = M s_hat, omega, x/r update, ||r||, rho, beta, next p, p_hat
+template <int N>
+__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
+k_bicg_t_h(KrylovArgs a, KState* st, int* active) {
+  using S = HShape<N>;
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  const int b = blockIdx.x;
+  if (st[b].done) return;
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
+  FilterTables tab = a.tab;
+  tab.tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
+  const KState s = st[b];
+  const int tid = threadIdx.x;
+  const long ow = (long)b * N;
+  const double* shg = a.sh + ow;
+  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + ow;
+  double2* hs = a.hspec + (long)b * (N / 2 + 1);
+  prefetch_l2(kg, N);
+  prefetch_l2(a.s + ow, N);
+  prefetch_l2(a.xw + ow, N);
+  prefetch_l2(a.ph + ow, N);
+  prefetch_l2(a.r0w + ow, N);
+  prefetch_l2(a.p + ow, N);
+  prefetch_l2(a.v + ow, N);
+  __syncthreads();   // twiddle table staged
+  double2 u[8];
+  apply_level_op_half<N>(shg, kg, a.shift, u, sm, aux, tab, hs);   // u = t = M s_hat
+  double2 sv[8];
+  ld2<N>(sv, a.s + ow);
+  Vals<2> red2;
+  red2.v[0] = 0.0;
+  red2.v[1] = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    red2.v[0] = fma(u[c].x, u[c].x, red2.v[0]);
+    red2.v[0] = fma(u[c].y, u[c].y, red2.v[0]);
+    red2.v[1] = fma(u[c].x, sv[c].x, red2.v[1]);
+    red2.v[1] = fma(u[c].y, sv[c].y, red2.v[1]);
+  }
+  red2 = block_sum<2>(red2, red);
+  if (red2.v[0] == 0.0) {
+    finish_instance(a, st, active, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN, sm);
+    return;
+  }
+  const double omega = red2.v[1] / red2.v[0];
+  // x += alpha p_hat + omega s_hat
+  {
+    const double2* x2 = reinterpret_cast<const double2*>(a.xw + ow);
+    const double2* p2 = reinterpret_cast<const double2*>(a.ph + ow);
+    const double2* h2 = reinterpret_cast<const double2*>(shg);
+    double2* xo = reinterpret_cast<double2*>(a.xw + ow);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int m = tid + c * S::T;
+      const double2 xv = x2[m], pv = p2[m], hv = h2[m];
+      xo[m] = make_double2(xv.x + (s.alpha * pv.x + omega * hv.x),
+                           xv.y + (s.alpha * pv.y + omega * hv.y));
+    }
+  }
+  // r = s - omega t
+  double2 r0v[8];
+  ld2<N>(r0v, a.r0w + ow);
+  red2.v[0] = 0.0;
+  red2.v[1] = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    u[c].x = sv[c].x - omega * u[c].x;
+    u[c].y = sv[c].y - omega * u[c].y;
+    red2.v[0] = fma(u[c].x, u[c].x, red2.v[0]);
+    red2.v[0] = fma(u[c].y, u[c].y, red2.v[0]);
+    red2.v[1] = fma(r0v[c].x, u[c].x, red2.v[1]);
+    red2.v[1] = fma(r0v[c].y, u[c].y, red2.v[1]);
+  }
+  st2<N>(a.r + ow, u);
+  // operands of the next p: in flight during the reduction
+  double2 qv[8], vv[8];
+  ld2<N>(qv, a.p + ow);
+  ld2<N>(vv, a.v + ow);
+  red2 = block_sum<2>(red2, red);
+  const double rnorm = sqrt(red2.v[0]);
+  const double rel = rnorm / s.nrm0;
+  const double rho_new = red2.v[1];
+  const int fin = rel < a.tol ? 1 : omega == 0.0 ? 2 : s.it >= a.max_iters ? 3
+                  : rho_new == 0.0 ? 4 : 0;
+  if (fin) {
+    if (fin == 1) finish_instance(a, st, active, b, s.it, rel, TSF_OK, sm);
+    else if (fin == 2) finish_instance(a, st, active, b, s.it, rel, TSF_BD_OMEGA, sm);
+    else if (fin == 3) finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED, sm);
+    else finish_instance(a, st, active, b, s.it + 1, rel, TSF_BD_RHO, sm);
+    return;
+  }
+  // next p = r + beta (p - omega v)
+  const double beta = (rho_new / s.rho_new) * (s.alpha / omega);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    u[c].x = u[c].x + beta * (qv[c].x - omega * vv[c].x);
+    u[c].y = u[c].y + beta * (qv[c].y - omega * vv[c].y);
+  }
+  st2<N>(a.p + ow, u);
+  strang_half<N>(u, sm, tab.tw, a.pspec + ow, hs);
+  st2<N>(a.ph + ow, u);
+  if (tid == 0) {
+    st[b].rho = s.rho_new;
+    st[b].rho_new = rho_new;
+    st[b].omega = omega;
+    st[b].rnorm = rnorm;
+    st[b].it = s.it + 1;
+  }
+}
+
+// ---- debug: the two building blocks alone (tests/test_gpu_half.py)
+//  mode 0: out = P^{-1} x with spec = S_k / n [B][N] given, hs <- half spectrum
+//  mode 1: out = shift*x + kappa .* (A x), x = Re IFFT_N(hs)
+template <int N>
+__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
+k_half_debug(int mode, const double* __restrict__ x, const double* __restrict__ aux_in,
+             double shift, double2* hs, double* __restrict__ out, FilterTables tabg) {
+  using S = HShape<N>;
+  extern __shared__ double2 sm[];
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
+  FilterTables tab = tabg;
+  tab.tw = stage_tw_half<N>(tabg.tw, reinterpret_cast<double2*>(aux + N));
+  __syncthreads();
+  const long ow = (long)blockIdx.x * N;
+  double2* hsb = hs + (long)blockIdx.x * (N / 2 + 1);
+  double2 u[8];
+  if (mode == 0) {
+    ld2<N>(u, x + ow);
+    strang_half<N>(u, sm, tab.tw, aux_in + ow, hsb);
+  } else {
+    apply_level_op_half<N>(x + ow, aux_in + ow, shift, u, sm, aux, tab, hsb);
+  }
+  st2<N>(out + ow, u);
+}
+
+}  // namespace tsf
