@@ -16,6 +16,8 @@ inline int launch_error(cudaError_t e) {
   return e == cudaSuccess ? 0 : report_cuda(e, "kernel launch");
 }
 
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 template <typename K>
 inline cudaError_t prep_kernel(K kernel, int smem) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -26,6 +28,15 @@ int Dispatch<LOG>::matvec(int n, const FilterTables& t, int B, const double* x, 
                           const double* kappa, double shift, cudaStream_t st) {
   constexpr int N = 1 << (LOG - 1);
   using S = KShape<N>;
+  if constexpr (half_ok<N>()) {
+    if (half_mode() && n == N && aligned16(x) && aligned16(y) && (!kappa || aligned16(kappa))) {
+      auto kh = k_toeplitz_apply_h<N>;
+      cudaError_t eh = prep_kernel(kh, HShape<N>::SMEM);
+      if (eh != cudaSuccess) return launch_error(eh);
+      kh<<<B, HShape<N>::BLOCK, HShape<N>::SMEM, st>>>(x, y, kappa, shift, t);
+      return launch_error(cudaGetLastError());
+    }
+  }
   auto k = k_toeplitz_apply<N>;
   cudaError_t e = prep_kernel(k, S::SMEM);
   if (e != cudaSuccess) return launch_error(e);
@@ -38,6 +49,15 @@ int Dispatch<LOG>::precond(int n, const FilterTables& t, int B, const double* v,
                            double shift, double kbar, const double* kbar_dev, cudaStream_t st) {
   constexpr int N = 1 << (LOG - 1);
   using S = KShape<N>;
+  if constexpr (half_ok<N>()) {
+    if (half_mode() && n == N && aligned16(v) && aligned16(z)) {
+      auto kh = k_strang_apply_h<N>;
+      cudaError_t eh = prep_kernel(kh, HShape<N>::SMEM);
+      if (eh != cudaSuccess) return launch_error(eh);
+      kh<<<B, HShape<N>::BLOCK, HShape<N>::SMEM, st>>>(v, z, shift, kbar, kbar_dev, t);
+      return launch_error(cudaGetLastError());
+    }
+  }
   auto k = k_strang_apply<N>;
   cudaError_t e = prep_kernel(k, S::SMEM);
   if (e != cudaSuccess) return launch_error(e);

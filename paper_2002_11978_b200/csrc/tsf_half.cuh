@@ -100,9 +100,11 @@ TSF_D double2 pack_inverse(double2 Q, double2 cQm, double2 w) {
 
 // z[c] = (u_{2m}, u_{2m+1}) in; (q_{2m}, q_{2m+1}) out, q = Re IFFT_N(FFT_N(u) . spec)
 // with spec[k] = S_k / n for k <= H.  hs (may be null) receives Q_k, k <= H.
-template <int N>
-TSF_D void strang_half(double2 (&z)[8], double2* sm, const double2* tw,
-                       const double* __restrict__ spec, double2* __restrict__ hs) {
+// spec(k) = S_k / n for k <= H (a callable; evaluated inside the forward
+// transform's load hook); inv_hook runs inside the inverse transform.
+template <int N, class Spec, class Hook = NoHook>
+TSF_D void strang_half(double2 (&z)[8], double2* sm, const double2* tw, const Spec& spec,
+                       double2* __restrict__ hs, const Hook& inv_hook = Hook{}) {
   constexpr int H = N / 2;
   constexpr int T = HShape<N>::T;
   using PL = typename HShape<N>::PL;
@@ -112,8 +114,8 @@ TSF_D void strang_half(double2 (&z)[8], double2* sm, const double2* tw,
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int k = tid + c * T;
-      sk[c] = 0.5 * spec[k];        // the split step's 1/2 folded in (exact)
-      sr[c] = 0.5 * spec[H - k];
+      sk[c] = 0.5 * spec(k);        // the split step's 1/2 folded in (exact)
+      sr[c] = 0.5 * spec(H - k);
     }
   });
   // mirror exchange through the buffer the last pass did not read
@@ -138,8 +140,13 @@ TSF_D void strang_half(double2 (&z)[8], double2* sm, const double2* tw,
     }
     z[c] = pack_inverse(Q, cQm, w);
   }
-  hfft<N, true>(z, sm, tw);
+  hfft<N, true>(z, sm, tw, inv_hook);
 }
+// the level's tabulated Strang filter
+struct SpecTable {
+  const double* __restrict__ p;
+  TSF_D double operator()(int k) const { return p[k]; }
+};
 
 // even bins of the Toeplitz product of x = Re IFFT_N(hs) from its stored half
 // spectrum: z[c] = (ye_{2m}, ye_{2m+1}) on return
@@ -161,9 +168,11 @@ TSF_D void even_half(const double2* __restrict__ hs, const FilterTables& t, doub
   hfft<N, true>(z, sm, t.tw, hook);
 }
 
-// y = shift*x + kappa .* (A x) for x = the last Strang output (half spectrum
-// hs), result in the (2m, 2m+1) ownership
-template <int N>
+// y = shift*x + kappa .* (A x), result in the (2m, 2m+1) ownership.  hs: the
+// half spectrum of x when x is the last Strang output (even bins need no
+// forward transform); null: the even bins through the packed forward
+// transform of x (the standalone product, tsf_toeplitz_matvec).
+template <int N, bool SPEC>
 TSF_D void apply_level_op_half(const double* __restrict__ xg, const double* __restrict__ kg,
                                double shift, double2 (&y)[8], double2* sm, double* aux,
                                const FilterTables& t, const double2* __restrict__ hs) {
@@ -172,13 +181,20 @@ TSF_D void apply_level_op_half(const double* __restrict__ xg, const double* __re
   const int tid = threadIdx.x;
   double2 z[8];
   double xa[8], xb[8];
-  even_half<N>(hs, t, z, sm, [&] {
+  auto load_x = [&] {
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       xa[c] = xg[tid + c * T];
       xb[c] = xg[tid + c * T + H];
     }
-  });
+  };
+  if constexpr (SPEC) {
+    even_half<N>(hs, t, z, sm, load_x);
+  } else {
+    ld2<N>(z, xg);
+    const double2* mvS = t.mvS;
+    strang_half<N>(z, sm, t.tw, [mvS](int k) { return ldt(&mvS[k]).x; }, nullptr, load_x);
+  }
   double2* aux2 = reinterpret_cast<double2*>(aux);
 #pragma unroll
   for (int c = 0; c < 8; ++c) aux2[tid + c * T] = z[c];
@@ -290,7 +306,7 @@ k_solve_begin_h(KrylovArgs a, KState* st, int* active) {
     return;
   }
   st2<N>(a.p + ow, u);
-  strang_half<N>(u, sm, tw, a.pspec + ow, a.hspec + (long)b * (N / 2 + 1));
+  strang_half<N>(u, sm, tw, SpecTable{a.pspec + ow}, a.hspec + (long)b * (N / 2 + 1));
   st2<N>(a.ph + ow, u);
   if (tid == 0) {
     KState s;
@@ -328,7 +344,7 @@ k_bicg_v_h(KrylovArgs a, KState* st, int* active) {
   if (s.it != 1) prefetch_l2(a.r + ow, N);
   __syncthreads();   // twiddle table staged
   double2 u[8];
-  apply_level_op_half<N>(phg, kg, a.shift, u, sm, aux, tab, hs);   // u = v = M p_hat
+  apply_level_op_half<N, true>(phg, kg, a.shift, u, sm, aux, tab, hs);   // u = v = M p_hat
   const double* rc = (s.it == 1 ? a.r0w : a.r) + ow;
   double2 r0v[8], rv[8];
   ld2<N>(r0v, a.r0w + ow);
@@ -370,7 +386,7 @@ k_bicg_v_h(KrylovArgs a, KState* st, int* active) {
     return;
   }
   st2<N>(a.s + ow, u);
-  strang_half<N>(u, sm, tab.tw, a.pspec + ow, hs);
+  strang_half<N>(u, sm, tab.tw, SpecTable{a.pspec + ow}, hs);
   st2<N>(a.sh + ow, u);
   if (tid == 0) {
     st[b].alpha = alpha;
@@ -405,7 +421,7 @@ k_bicg_t_h(KrylovArgs a, KState* st, int* active) {
   prefetch_l2(a.v + ow, N);
   __syncthreads();   // twiddle table staged
   double2 u[8];
-  apply_level_op_half<N>(shg, kg, a.shift, u, sm, aux, tab, hs);   // u = t = M s_hat
+  apply_level_op_half<N, true>(shg, kg, a.shift, u, sm, aux, tab, hs);   // u = t = M s_hat
   double2 sv[8];
   ld2<N>(sv, a.s + ow);
   Vals<2> red2;
@@ -478,7 +494,7 @@ k_bicg_t_h(KrylovArgs a, KState* st, int* active) {
     u[c].y = u[c].y + beta * (qv[c].y - omega * vv[c].y);
   }
   st2<N>(a.p + ow, u);
-  strang_half<N>(u, sm, tab.tw, a.pspec + ow, hs);
+  strang_half<N>(u, sm, tab.tw, SpecTable{a.pspec + ow}, hs);
   st2<N>(a.ph + ow, u);
   if (tid == 0) {
     st[b].rho = s.rho_new;
@@ -507,11 +523,49 @@ k_half_debug(int mode, const double* __restrict__ x, const double* __restrict__ 
   double2 u[8];
   if (mode == 0) {
     ld2<N>(u, x + ow);
-    strang_half<N>(u, sm, tab.tw, aux_in + ow, hsb);
+    strang_half<N>(u, sm, tab.tw, SpecTable{aux_in + ow}, hsb);
   } else {
-    apply_level_op_half<N>(x + ow, aux_in + ow, shift, u, sm, aux, tab, hsb);
+    apply_level_op_half<N, true>(x + ow, aux_in + ow, shift, u, sm, aux, tab, hsb);
   }
   st2<N>(out + ow, u);
+}
+
+// ---- standalone operators (tsf_toeplitz_matvec / tsf_precond_solve, power-of-two n = N)
+template <int N>
+__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
+k_toeplitz_apply_h(const double* __restrict__ x, double* __restrict__ y,
+                   const double* __restrict__ kappa, double shift, FilterTables tabg) {
+  using S = HShape<N>;
+  extern __shared__ double2 sm[];
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
+  FilterTables tab = tabg;
+  tab.tw = stage_tw_half<N>(tabg.tw, reinterpret_cast<double2*>(aux + N));
+  __syncthreads();
+  const long ow = (long)blockIdx.x * N;
+  double2 u[8];
+  apply_level_op_half<N, false>(x + ow, kappa ? kappa + ow : nullptr, shift, u, sm, aux, tab, nullptr);
+  st2<N>(y + ow, u);
+}
+
+template <int N>
+__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
+k_strang_apply_h(const double* __restrict__ v, double* __restrict__ zo, double shift, double kbar,
+                 const double* __restrict__ kbar_dev, FilterTables tabg) {
+  using S = HShape<N>;
+  extern __shared__ double2 sm[];
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
+  const double2* tw = stage_tw_half<N>(tabg.tw, reinterpret_cast<double2*>(aux + N));
+  __syncthreads();
+  const long ow = (long)blockIdx.x * N;
+  const double kb = kbar_dev ? kbar_dev[blockIdx.x] : kbar;
+  const double2* pclam = tabg.pclam;
+  double2 u[8];
+  ld2<N>(u, v + ow);
+  strang_half<N>(u, sm, tw, [=](int k) {
+    const double2 lam = ldt(&pclam[k & (N - 1)]);
+    return 0.5 * (rcp_pos(shift + kb * lam.x) + rcp_pos(shift + kb * lam.y)) * (1.0 / N);
+  }, nullptr);
+  st2<N>(zo + ow, u);
 }
 
 }  // namespace tsf
