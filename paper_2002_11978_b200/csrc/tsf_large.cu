@@ -235,6 +235,27 @@ __global__ void __launch_bounds__(kLelThreads) k_lspec(LargeArgs a, double kbar,
   }
 }
 
+// The level's Strang filter for the half-length engine: (S_k, S_{H-k}) / n at
+// the half geometry's position of bin k (tsf_hlarge.cuh)
+__global__ void __launch_bounds__(kLelThreads) k_hspec(LargeArgs a) {
+  pdl_enter();
+  const int b = blockIdx.y, tid = threadIdx.x;
+  if (inst_skip(a, b)) return;
+  const double kb = a.st[b].kbar;
+  const double d = a.shift;
+  const double inv_n = 1.0 / a.nt;
+  const long H = a.nt / 2;
+#pragma unroll
+  for (int c = 0; c < kLelPer; ++c) {
+    const long idx = (long)blockIdx.x * kLelChunk + c * kLelThreads + tid;
+    if (idx >= H) break;
+    const double2 l0 = ldt(&a.hg.lamH[2 * idx]), l1 = ldt(&a.hg.lamH[2 * idx + 1]);
+    a.hg.pspec2[(long)b * H + idx] =
+        make_double2(0.5 * (1.0 / (d + kb * l0.x) + 1.0 / (d + kb * l0.y)) * inv_n,
+                     0.5 * (1.0 / (d + kb * l1.x) + 1.0 / (d + kb * l1.y)) * inv_n);
+  }
+}
+
 // ---- PCG elementwise kernels (krylov.py:43-85)
 // dst = src
 __global__ void __launch_bounds__(kLelThreads) k_lel_copy(LargeArgs a, double* __restrict__ dst,
@@ -460,6 +481,33 @@ int col_inv_at(int lg, const LargeArgs& a, double* dst, int mode, const double* 
   return report_error(TSF_E_UNSUPPORTED, "large-n column length out of range");
 }
 
+template <int LOG = kLargeMinLog>
+int hcol_fwd_at(int lg, const LargeArgs& a, const double* src, int mode, cudaStream_t st) {
+  if (lg == LOG) return LargeDispatch<LOG>::hcol_fwd(a, src, mode, st);
+  if constexpr (LOG < kLargeMaxLog) return hcol_fwd_at<LOG + 1>(lg, a, src, mode, st);
+  return report_error(TSF_E_UNSUPPORTED, "half-length column length out of range");
+}
+template <int LOG = kLargeMinLog>
+int hrow_strang_at(int lg, const LargeArgs& a, cudaStream_t st) {
+  if (lg == LOG) return LargeDispatch<LOG>::hrow_strang(a, st);
+  if constexpr (LOG < kLargeMaxLog) return hrow_strang_at<LOG + 1>(lg, a, st);
+  return report_error(TSF_E_UNSUPPORTED, "half-length row length out of range");
+}
+template <int LOG = kLargeMinLog>
+int hrow_mv_at(int lg, const LargeArgs& a, cudaStream_t st) {
+  if (lg == LOG) return LargeDispatch<LOG>::hrow_mv(a, st);
+  if constexpr (LOG < kLargeMaxLog) return hrow_mv_at<LOG + 1>(lg, a, st);
+  return report_error(TSF_E_UNSUPPORTED, "half-length row length out of range");
+}
+template <int LOG = kLargeMinLog>
+int hcol_inv_at(int lg, const LargeArgs& a, double* dst, int mode, int ch, const double* xin,
+                const double* ye, const double* w1, int slot, cudaStream_t st) {
+  if (lg == LOG) return LargeDispatch<LOG>::hcol_inv(a, dst, mode, ch, xin, ye, w1, slot, st);
+  if constexpr (LOG < kLargeMaxLog)
+    return hcol_inv_at<LOG + 1>(lg, a, dst, mode, ch, xin, ye, w1, slot, st);
+  return report_error(TSF_E_UNSUPPORTED, "half-length column length out of range");
+}
+
 int ilog2i(long x) {
   int r = 0;
   while ((1L << r) < x) ++r;
@@ -473,6 +521,41 @@ struct Runner {
   LargeArgs a;
   cudaStream_t st;
   int lg1, lg2;
+  int lg1h = 0, lg2h = 0;
+  bool half = false;   // this solve runs the half-length engine (tsf_hlarge.cuh)
+
+  // dst = P^{-1} src through ONE length-n/2 transform pair; the half spectrum
+  // of dst stays in hg.hspec for the next product's even bins
+  int hstrang(int in_mode, const double* src, double* dst) {
+    int rc;
+    if ((rc = hcol_fwd_at(lg1h, a, src, in_mode, st))) return rc;
+    if ((rc = hrow_strang_at(lg2h, a, st))) return rc;
+    return hcol_inv_at(lg1h, a, dst, HO_PACK, 0, nullptr, nullptr, nullptr, -1, st);
+  }
+  // dst = d src + kappa . (A src) for src = the last hstrang output; tmp: a
+  // free vector for the even-bin half of the product
+  int happly(const double* src, double* dst, const double* w1, int slot, double* tmp) {
+    int rc;
+    if ((rc = hcol_fwd_at(lg1h, a, src, HF_ODD, st))) return rc;
+    if ((rc = hrow_mv_at(lg2h, a, st))) return rc;
+    if ((rc = hcol_inv_at(lg1h, a, tmp, HO_PACK, 1, nullptr, nullptr, nullptr, -1, st))) return rc;
+    return hcol_inv_at(lg1h, a, dst, HO_ODD, 0, src, tmp, w1, slot, st);
+  }
+  int bicg_iteration_half() {
+    int rc;
+    const int NC = lp->ncol_cta_h, NR = (a.n + kLelChunk - 1) / kLelChunk;
+    if ((rc = hstrang(HF_PUPD, nullptr, a.ph))) return rc;
+    if ((rc = happly(a.ph, a.v, a.r0, 0, a.t))) return rc;      // t is free until the t-product
+    if ((rc = sc(LS_ALPHA, NC, 1))) return rc;
+    if ((rc = hstrang(HF_SUPD, nullptr, a.sh))) return rc;
+    if ((rc = sc(LS_SNORM, NC, 1))) return rc;
+    if ((rc = happly(a.sh, a.t, a.s, 0, a.r))) return rc;       // r is dead once s exists
+    if ((rc = sc(LS_OMEGA, NC, 1))) return rc;
+    launch_pdl(k_lel_xr, lel_grid(), kLelThreads, 0, st, a, (const double*)a.ph,
+               (const double*)a.sh);
+    if ((rc = cuda_check(cudaGetLastError(), "k_lel_xr"))) return rc;
+    return sc(LS_REL, NR, 1);
+  }
 
   // dst = Re IFFT_n(S . FFT_n(src)) with the Strang spectrum (pspec);
   // in_mode: the column prologue that forms src (p / s update) on the fly
@@ -497,6 +580,7 @@ struct Runner {
   }
   // one BiCGSTAB iteration for every unfinished instance
   int bicg_iteration(int pc) {
+    if (half) return bicg_iteration_half();
     int rc;
     const int NC = lp->ncol_cta, NR = (a.n + kLelChunk - 1) / kLelChunk;
     const double* ph = pc ? a.ph : a.p;
@@ -620,10 +704,25 @@ Runner make_runner(const LargePlan* lp, int B, cudaStream_t st) {
   // w + 7 vn: kwork ; w + 8 vn: the Strang spectrum [cap][nt]
   a.pspec = w + 8 * vn;
   a.active = lp->active;
+  a.hg = lp->hg;
+  a.hg.hspec = lp->Z + (size_t)lp->cap * lp->nt;   // the upper half of Z is free in half mode
+  a.hg.pspec2 = reinterpret_cast<double2*>(a.pspec);
+  R.lg1h = ilog2i(lp->hg.N1 > 0 ? lp->hg.N1 : 1);
+  R.lg2h = ilog2i(lp->hg.N2 > 0 ? lp->hg.N2 : 1);
   return R;
 }
 
 }  // namespace
+
+// smallest n the half-length four-step engine takes (TSF_HLARGE_MIN_N)
+static long hlarge_min_n() {
+  static long v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_HLARGE_MIN_N");
+    v = s ? atol(s) : (1L << 14);
+  }
+  return v;
+}
 
 // ======================================================================
 int large_plan_init(LargePlan* lp, int n, int L, const double* symbol_re, const double* lam,
@@ -677,7 +776,37 @@ int large_plan_init(LargePlan* lp, int n, int L, const double* symbol_re, const 
   if (lam)
     for (int k = 0; k < n; ++k) lam_min = std::min(lam_min, lam[k]);
   lp->lam_min = lam_min;
-  const size_t total = tw1.size() + tw2.size() + twN.size() + twL.size() + sEO.size() + lamP.size();
+  // half-length geometry (tsf_hlarge.cuh): H = nt/2 = N1h x N2h, rows <= 2048
+  std::vector<double2> tw1h, tw2h, twH, sEh, lamH;
+  std::vector<double> sO4;
+  const long Hh = nt / 2;
+  if (lam && n == nt && Hh >= 64L * 128) {
+    int N1h = (int)std::max(64L, Hh >> 11);
+    int N2h = (int)(Hh / N1h);
+    lp->half = 1;
+    lp->hg.N1 = N1h;
+    lp->hg.N2 = N2h;
+    lp->ncol_cta_h = N2h / col_group_at(ilog2i(N1h));
+    lp->np = std::max(lp->np, lp->ncol_cta_h);
+    tw1h = twiddle_table(N1h);
+    tw2h = twiddle_table(N2h);
+    twH = twiddle_table((int)Hh);
+    sEh.resize((size_t)Hh);
+    lamH.resize((size_t)2 * Hh);
+    sO4.resize((size_t)Hh);
+    for (int k1 = 0; k1 < N1h; ++k1)
+      for (int k2 = 0; k2 < N2h; ++k2) {
+        const long k = k1 + (long)N1h * k2;
+        const size_t pos = (size_t)k1 * N2h + k2;
+        sEh[pos] = make_double2(Ssym(2 * k) * nt, Ssym(2 * (Hh - k)) * nt);
+        sO4[pos] = 2.0 * Ssym(4 * k + 1);
+        lamH[2 * pos] = make_double2(lam[k], lam[(n - k) % n]);
+        lamH[2 * pos + 1] = make_double2(lam[Hh - k], lam[(n - Hh + k) % n]);
+      }
+  }
+  const size_t total = tw1.size() + tw2.size() + twN.size() + twL.size() + sEO.size() + lamP.size() +
+                       tw1h.size() + tw2h.size() + twH.size() + sEh.size() + lamH.size() +
+                       (sO4.size() + 1) / 2;
   int rc;
   if ((rc = cuda_check(cudaSetDevice(device), "cudaSetDevice"))) return rc;
   if ((rc = cuda_check(cudaMalloc(&lp->tables, total * sizeof(double2)), "cudaMalloc(tables)")))
@@ -697,6 +826,17 @@ int large_plan_init(LargePlan* lp, int n, int L, const double* symbol_re, const 
   lp->lt.twL = put(twL);
   lp->lt.sEO = put(sEO);
   lp->lt.lamP = put(lamP);
+  if (lp->half) {
+    lp->hg.tw1 = put(tw1h);
+    lp->hg.tw2 = put(tw2h);
+    lp->hg.twH = put(twH);
+    lp->hg.sEh = put(sEh);
+    lp->hg.lamH = put(lamH);
+    double* d = reinterpret_cast<double*>(cur);
+    if (cudaMemcpy(d, sO4.data(), sO4.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = report_cuda(cudaGetLastError(), "cudaMemcpy(tables)");
+    lp->hg.sO4 = d;
+  }
   return rc;
 }
 
@@ -782,7 +922,7 @@ static int loop_graph(LargePlan* lp, const Runner& R0, int method, int pc, cudaS
   // (tsf_large_impl.cuh few_ctas): one cached chain per choice, so a cached
   // node never changes its kernel function
   const int few = few_ctas((long)lp->ncol_cta * R0.a.B) ? 1 : 0;
-  LargeLoopGraph& G = lp->loops[method][pc][few];
+  LargeLoopGraph& G = lp->loops[method][pc][few + (R0.half ? 2 : 0)];
   int rc;
   if (!lp->cap_stream &&
       (rc = cuda_check(cudaStreamCreateWithFlags(&lp->cap_stream, cudaStreamNonBlocking),
@@ -891,13 +1031,19 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
   a.relres = k.relres;
   a.status = k.status;
   a.st = lp->st;
+  R.half = method == 0 && pc == 1 && lp->half && half_mode() && lp->n >= hlarge_min_n() &&
+           (reinterpret_cast<uintptr_t>(k.rhs) & 15) == 0;
   k_set_int<<<1, 1, 0, st>>>(lp->active, B);
   launch_pdl(k_lel_begin, R.lel_grid(), kLelThreads, 0, st, a, kk);
   if ((rc = cuda_check(cudaGetLastError(), "k_lel_begin"))) return rc;
   launch_pdl(k_lsc, B, kLscThreads, 0, st, a, LS_BEGIN, (a.n + kLelChunk - 1) / kLelChunk, k.kbar,
                                    lp->lam_min, pc);
   if ((rc = cuda_check(cudaGetLastError(), "k_lsc(begin)"))) return rc;
-  if (pc) {
+  if (pc && R.half) {
+    launch_pdl(k_hspec, dim3((unsigned)((a.nt / 2 + kLelChunk - 1) / kLelChunk), B), kLelThreads, 0,
+               st, a);
+    if ((rc = cuda_check(cudaGetLastError(), "k_hspec"))) return rc;
+  } else if (pc) {
     launch_pdl(k_lspec, R.lel_grid(), kLelThreads, 0, st, a, 0.0, nullptr, 1);
     if ((rc = cuda_check(cudaGetLastError(), "k_lspec"))) return rc;
   }

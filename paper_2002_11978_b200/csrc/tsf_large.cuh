@@ -37,6 +37,19 @@ struct LargeTables {
   const double2* lamP;  // [k1][k2] -> (lam_k, lam_{n-k}) at k = k1 + N1 k2 (Strang)
 };
 
+// Half-length geometry and tables (tsf_hlarge.cuh): H = n/2 = N1 x N2
+struct HalfGeom {
+  int N1 = 0, N2 = 0;
+  const double2* tw1 = nullptr;   // two-level W_N1
+  const double2* tw2 = nullptr;   // two-level W_N2
+  const double2* twH = nullptr;   // two-level W_H: inter-pass twiddles
+  const double2* sEh = nullptr;   // [k1][k2] -> (n S_2k / L, n S_2(H-k) / L), k = k1 + N1 k2
+  const double* sO4 = nullptr;    // [k1][k2] -> 2 S_{4k+1} / L
+  const double2* lamH = nullptr;  // [k1][k2][2] -> (lam_k, lam_{n-k}), (lam_{H-k}, lam_{n-H+k})
+  double2* hspec = nullptr;       // [B][H+1] half spectrum of the last Strang output
+  double2* pspec2 = nullptr;      // [B][H] the level's Strang filter (S_k, S_{H-k}) / n
+};
+
 // BiCGSTAB per-instance control (scalar kernels)
 enum LMode : int { LM_ACTIVE = 0, LM_EARLY = 1, LM_DONE = 2 };
 
@@ -57,6 +70,9 @@ enum ColOut : int {
   CO_REAL = 0,     // y_j = Re z   (store)
   CO_APPLY = 1,    // y_j = d x_j + kappa_j (Re z0_j + Re(conj(w_j) z1_j)) ; dot partials
 };
+// Half-length engine (tsf_hlarge.cuh): column prologues / epilogues
+enum HColIn : int { HF_LOAD = 0, HF_PUPD = 2, HF_SUPD = 3, HF_ODD = 4 };
+enum HColOut : int { HO_PACK = 0, HO_ODD = 1 };
 // Row spectra
 enum RowSpec : int { RS_APPLY = 0, RS_STRANG = 2 };
 
@@ -87,6 +103,7 @@ struct LargeArgs {
   double* relres;
   int* status;
   int* active;
+  HalfGeom hg;
 };
 
 TSF_D bool inst_skip(const LargeArgs& a, int b) { return a.st && a.st[b].mode != LM_ACTIVE; }
@@ -554,6 +571,12 @@ struct LargeDispatch {
   static int col_inv(const LargeArgs& a, double* dst, int out_mode, const double* xin,
                      const double* w1, int pslot, cudaStream_t st);
   static int col_group();  // G: columns per column CTA
+  // half-length engine (tsf_hlarge.cuh); LOG = log2 of N1 (columns) or N2 (rows)
+  static int hcol_fwd(const LargeArgs& a, const double* src, int in_mode, cudaStream_t st);
+  static int hrow_strang(const LargeArgs& a, cudaStream_t st);
+  static int hrow_mv(const LargeArgs& a, cudaStream_t st);
+  static int hcol_inv(const LargeArgs& a, double* dst, int out_mode, int ch, const double* xin,
+                      const double* ye, const double* w1, int pslot, cudaStream_t st);
 };
 
 // Launches of the large-n engine are programmatic dependent launches

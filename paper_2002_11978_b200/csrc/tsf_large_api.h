@@ -44,7 +44,11 @@ struct LargePlan {
   int* active = nullptr;
   int* h_active = nullptr;
   cudaStream_t cap_stream = nullptr;   // graph capture (non-blocking)
-  LargeLoopGraph loops[2][2][2];       // [method][pc][few-CTA column kernels]
+  LargeLoopGraph loops[2][2][4];       // [method][pc][few-CTA column kernels + 2 * half-length engine]
+  // half-length engine (tsf_hlarge.cuh): power-of-two n >= 2^14 with Strang tables
+  int half = 0;
+  int ncol_cta_h = 0;
+  HalfGeom hg{};
 };
 
 // embedding L a power of two in [2^14, 2^25] with 2n-1 <= L (vectors of length n are

@@ -8,8 +8,11 @@
 
 #include "tsf_dispatch.h"
 #include "tsf_large.cuh"
+#include "tsf_hlarge.cuh"
 
 namespace tsf {
+
+int report_error(int code, const char* msg);   // tsf_abi.cu
 
 inline int large_launch_error(cudaError_t e) {
   return e == cudaSuccess ? 0 : report_cuda(e, "large-n kernel launch");
@@ -103,6 +106,63 @@ int LargeDispatch<LOG>::col_inv(const LargeArgs& a, double* dst, int out_mode, c
   if (prep != cudaSuccess) return large_launch_error(prep);
   if (prep1 != cudaSuccess) return large_launch_error(prep1);
   launch_pdl(k, grid, S::BLOCK, smem, st, a, dst, out_mode, xin, w1, pslot, cm);
+  return large_launch_error(cudaGetLastError());
+}
+
+template <int LOG>
+int LargeDispatch<LOG>::hcol_fwd(const LargeArgs& a, const double* src, int in_mode,
+                                 cudaStream_t st) {
+  constexpr int N1 = 1 << LOG;
+  using S = LCol<N1>;
+  const dim3 grid(a.hg.N2 / S::G, a.B);
+  auto k = k_hcol_fwd<N1>;
+  static cudaError_t prep = large_prep(k, S::SMEM);
+  if (prep != cudaSuccess) return large_launch_error(prep);
+  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, src, in_mode);
+  return large_launch_error(cudaGetLastError());
+}
+
+template <int LOG>
+int LargeDispatch<LOG>::hrow_strang(const LargeArgs& a, cudaStream_t st) {
+  constexpr int N2 = 1 << LOG;
+  if constexpr (HRow<N2>::OK) {
+    using S = HRow<N2>;
+    auto k = k_hrow_strang<N2>;
+    static cudaError_t prep = large_prep(k, S::SMEM);
+    if (prep != cudaSuccess) return large_launch_error(prep);
+    launch_pdl(k, dim3(a.hg.N1 / 2, a.B), S::BLOCK, S::SMEM, st, a);
+    return large_launch_error(cudaGetLastError());
+  } else {
+    return report_error(-3, "half-length row pairs need 128 <= N2 <= 2048");
+  }
+}
+
+template <int LOG>
+int LargeDispatch<LOG>::hrow_mv(const LargeArgs& a, cudaStream_t st) {
+  constexpr int N2 = 1 << LOG;
+  if constexpr (HRow<N2>::OK) {
+    using S = LRow<N2>;
+    auto k = k_hrow_mv<N2>;
+    static cudaError_t prep = large_prep(k, S::SMEM);
+    if (prep != cudaSuccess) return large_launch_error(prep);
+    launch_pdl(k, dim3(2 * a.hg.N1, a.B), S::BLOCK, S::SMEM, st, a);
+    return large_launch_error(cudaGetLastError());
+  } else {
+    return report_error(-3, "half-length rows need 128 <= N2 <= 2048");
+  }
+}
+
+template <int LOG>
+int LargeDispatch<LOG>::hcol_inv(const LargeArgs& a, double* dst, int out_mode, int ch,
+                                 const double* xin, const double* ye, const double* w1, int pslot,
+                                 cudaStream_t st) {
+  constexpr int N1 = 1 << LOG;
+  using S = LCol<N1>;
+  const dim3 grid(a.hg.N2 / S::G, a.B);
+  auto k = k_hcol_inv<N1>;
+  static cudaError_t prep = large_prep(k, S::SMEM);
+  if (prep != cudaSuccess) return large_launch_error(prep);
+  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, dst, out_mode, ch, xin, ye, w1, pslot);
   return large_launch_error(cudaGetLastError());
 }
 
