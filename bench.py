@@ -281,6 +281,8 @@ def main():
                     help="configs[2] instances timed by the CPU legs (default max(64, cores))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-matvec", action="store_true",
+                    help="skip the standalone Toeplitz-product measurement")
     ap.add_argument("--tol", type=float, default=0.0,
                     help="experiments only: override the Krylov tolerance (not a bench number)")
     args = ap.parse_args()
@@ -490,12 +492,21 @@ def main():
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    if large:
+    half = os.environ.get("TSF_HALF", "1") != "0"   # half-length engines (tsf_half.cuh, tsf_hlarge.cuh)
+    if large and half and n & (n - 1) == 0 and n >= int(os.environ.get("TSF_HLARGE_MIN_N", 1 << 14)):
+        n1 = max(64, (n // 2) >> 11)   # tsf_large.cu large_plan_init, half geometry
+        sname = (f"tsf large-n level solve, half-length transforms: k_hcol_fwd/k_hcol_inv<{n1}> "
+                 f"+ k_hrow_strang/k_hrow_mv<{n // 2 // n1}> + k_lsc/k_lel_xr "
+                 "(19 kernels per BiCGSTAB iteration)")
+    elif large:
         n1 = max(64, n >> 12)   # tsf_large.cu large_plan_init
         sname = (f"tsf large-n level solve: k_lcol_fwd/k_lcol_inv<{n1}> + k_lrow<{n // n1}> "
-                 "+ k_lsc/k_lel_* (23 kernels per BiCGSTAB iteration)")
+                 "+ k_lsc/k_lel_* (17 kernels per BiCGSTAB iteration)")
     else:
-        sname = (f"tsf level solve: k_solve_begin + k_bicg_v/k_bicg_t<{n},1>"
+        hk = half and n >= 512 and n & (n - 1) == 0 and not fused
+        sname = ((f"tsf level solve: k_solve_begin_h + k_bicg_v_h/k_bicg_t_h<{n}> (half-length "
+                  f"transforms, {n // 16}-thread CTAs)" if hk else
+                  f"tsf level solve: k_solve_begin + k_bicg_v/k_bicg_t<{n},1>")
                  + (" with fused SOE epilogue" if fused else "")
                  + (" (one CUDA graph per level: instance-group branches, each a conditional "
                     "WHILE loop)" if graph else ""))
@@ -529,9 +540,9 @@ def main():
             "share_of_step": (solve_ms if dom is k_solve else soe_ms) / ms,
             "note": ("large-n level solve: four-step transforms through L2/HBM"
                      if large else
-                     "level solve is transform (FP64/shared-memory) bound: ncu FP64 pipe "
-                     "~35% active (see fp64); the SOE kernel alone runs at ~98% of the "
-                     "HBM peak")}
+                     "level solve is transform (shared-memory latency / FP64) bound: ncu "
+                     "FP64 pipe 25-31%, LSU wavefronts 48-55% (profiles/r02/half_ncu.md); the "
+                     "SOE kernel alone runs at ~98% of the HBM peak")}
     # FP64 view of the same launch: algorithmic flops per BiCGSTAB iteration
     # (SURVEY.md §8(d)): 2 Toeplitz products (5 L log2 L + L + 3n each: two
     # real length-L transforms), 2 Strang solves (5 n log2 n + 3n), ~20n
@@ -552,9 +563,9 @@ def main():
                     "peak_tflops": fp64_peak,
                     "frac": solve_flops / (solve_ms / K * 1e-3) / 1e12 / fp64_peak,
                     "peak_source": "measured DFMA peak, profiles/r01_fp64_peak.json",
-                    "note": "algorithmic flops count real-input transforms; the engine runs "
-                            "full complex transforms of the real data (parity with the "
-                            "reference's numpy path, DESIGN.md §3.2), ~2x these flops"}
+                    "note": "algorithmic flops count real-input transforms; the half-length "
+                            "engine (DESIGN.md §3.8) runs about these flops, the full-length "
+                            "one (TSF_HALF=0, PCG, non-power-of-two n) ~2x"}
     value = world * B * n * K / (ms * 1e-3)
 
     # ---- end to end through the public API with host buffers
@@ -595,7 +606,7 @@ def main():
 
     # ---- standalone Toeplitz matvec throughput (configs[4] point at this n, B*n=2^26)
     mv = None
-    if rank == 0 and n <= (1 << 20):
+    if rank == 0 and n <= (1 << 20) and not args.no_matvec:
         col = P.build_ifl(1.5, 1.75, 1.0, n + 1).first_col
         op = P.build_toeplitz(col)
         Bm = (1 << 26) // n

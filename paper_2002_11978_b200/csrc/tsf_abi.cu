@@ -85,6 +85,15 @@ bool half_mode() {
   return v == 1;
 }
 
+bool fuse_vt() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_FUSE_VT");
+    v = (s && s[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int solve_groups(int B) {
   static int env = -2;
   if (env == -2) {

@@ -36,6 +36,7 @@ struct SolveGraphs {
 };
 bool graph_mode();  // TSF_SOLVE_GRAPH (default 1)
 bool spec_reuse();  // TSF_SPEC_REUSE (default 1)
+bool fuse_vt();     // TSF_FUSE_VT (default 0): both BiCGSTAB phases of an iteration in one kernel
 bool half_mode();   // TSF_HALF (default 1): half-length transform engine, tsf_half.cuh
 
 template <int LOG>

@@ -148,6 +148,7 @@ template <int N, int PC, bool CG>
 struct SolveKernels {
   SolveKernel kb, kv, kt, kc;
   int block, smem;
+  bool one = CG;   // one kernel per iteration (PCG, or the fused BiCGSTAB phases)
   explicit SolveKernels(bool half) {
     kb = k_solve_begin<N, PC, CG>;
     kv = k_bicg_v<N, PC>;
@@ -158,8 +159,9 @@ struct SolveKernels {
     if constexpr (PC == 1 && !CG && half_ok<N>()) {
       if (half) {
         kb = k_solve_begin_h<N>;
-        kv = k_bicg_v_h<N>;
-        kt = k_bicg_t_h<N>;
+        kv = fuse_vt() ? k_bicg_h<N, 3> : k_bicg_h<N, 1>;
+        kt = k_bicg_h<N, 2>;
+        one = fuse_vt();
         block = HShape<N>::BLOCK;
         smem = HShape<N>::SMEM;
       }
@@ -193,7 +195,7 @@ int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
   if (!G.built) {
     if ((e = prep_kernel(kb, K.smem)) != cudaSuccess) return launch_error(e);
     if ((e = prep_kernel(CG ? kc : kv, K.smem)) != cudaSuccess) return launch_error(e);
-    if (!CG && (e = prep_kernel(kt, K.smem)) != cudaSuccess) return launch_error(e);
+    if (!K.one && (e = prep_kernel(kt, K.smem)) != cudaSuccess) return launch_error(e);
     if ((e = cudaGraphCreate(&G.graph, 0)) != cudaSuccess) return launch_error(e);
     G.groups = ng;
     G.half = half;
@@ -237,7 +239,7 @@ int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
       if ((e = cudaGraphAddKernelNode(&G.n_a[g], body, nullptr, 0, &p_a)) != cudaSuccess)
         return launch_error(e);
       cudaGraphNode_t last = G.n_a[g];
-      if (!CG) {
+      if (!K.one) {
         if ((e = cudaGraphAddKernelNode(&G.n_b[g], body, &G.n_a[g], 1, &p_b)) != cudaSuccess)
           return launch_error(e);
         last = G.n_b[g];
@@ -250,7 +252,7 @@ int solve_graph(int B, const KrylovArgs& a_in, cudaStream_t st) {
       if ((e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_set[g], &p_set)) != cudaSuccess ||
           (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_begin[g], &p_begin)) != cudaSuccess ||
           (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_a[g], &p_a)) != cudaSuccess ||
-          (!CG && (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_b[g], &p_b)) != cudaSuccess))
+          (!K.one && (e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_b[g], &p_b)) != cudaSuccess))
         return launch_error(e);
       const cudaKernelNodeParams p_c = knode(k_loop_cond, dim3(1), dim3(1), 0, c_args);
       if ((e = cudaGraphExecKernelNodeSetParams(G.exec, G.n_c[g], &p_c)) != cudaSuccess)
@@ -282,7 +284,7 @@ int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
   if ((e = prep_kernel(kb, K.smem)) != cudaSuccess) return launch_error(e);
   if (!CG) {
     if ((e = prep_kernel(kv, K.smem)) != cudaSuccess) return launch_error(e);
-    if ((e = prep_kernel(kt, K.smem)) != cudaSuccess) return launch_error(e);
+    if (!K.one && (e = prep_kernel(kt, K.smem)) != cudaSuccess) return launch_error(e);
   } else if ((e = prep_kernel(kc, K.smem)) != cudaSuccess) {
     return launch_error(e);
   }
@@ -293,7 +295,7 @@ int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
     for (int k = 0; k < kChunk && it + k < a.max_iters; ++k) {
       if (!CG) {
         kv<<<B, K.block, K.smem, st>>>(a, a.kst, a.active);
-        kt<<<B, K.block, K.smem, st>>>(a, a.kst, a.active);
+        if (!K.one) kt<<<B, K.block, K.smem, st>>>(a, a.kst, a.active);
       } else {
         kc<<<B, K.block, K.smem, st>>>(a, a.kst, a.active);
       }

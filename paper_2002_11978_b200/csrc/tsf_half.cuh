@@ -322,17 +322,11 @@ k_solve_begin_h(KrylovArgs a, KState* st, int* active) {
 }
 
 // ---- v-phase: v = M p_hat, alpha, s = r - alpha v, ||s|| (early exit), s_hat
+// (returns true when the instance finished)
 template <int N>
-__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
-k_bicg_v_h(KrylovArgs a, KState* st, int* active) {
-  using S = HShape<N>;
-  extern __shared__ double2 sm[];
-  __shared__ double red[4 * 32];
+TSF_D bool dev_bicg_v_h(const KrylovArgs& a, KState* st, int* active, double2* sm, double* red,
+                        double* aux, const FilterTables& tab) {
   const int b = blockIdx.x;
-  if (st[b].done) return;
-  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
-  FilterTables tab = a.tab;
-  tab.tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
   const KState s = st[b];
   const int tid = threadIdx.x;
   const long ow = (long)b * N;
@@ -342,7 +336,6 @@ k_bicg_v_h(KrylovArgs a, KState* st, int* active) {
   prefetch_l2(kg, N);
   prefetch_l2(a.r0w + ow, N);
   if (s.it != 1) prefetch_l2(a.r + ow, N);
-  __syncthreads();   // twiddle table staged
   double2 u[8];
   apply_level_op_half<N, true>(phg, kg, a.shift, u, sm, aux, tab, hs);   // u = v = M p_hat
   const double* rc = (s.it == 1 ? a.r0w : a.r) + ow;
@@ -359,7 +352,7 @@ k_bicg_v_h(KrylovArgs a, KState* st, int* active) {
   const double denom = block_sum1(part, red);
   if (denom == 0.0) {
     finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_R0V, sm);
-    return;
+    return true;
   }
   const double alpha = s.rho_new / denom;
   part = 0.0;
@@ -383,7 +376,7 @@ k_bicg_v_h(KrylovArgs a, KState* st, int* active) {
     }
     st2<N>(a.x + ow, xv);
     finish_instance(a, st, active, b, s.it, snorm / s.nrm0, TSF_OK, sm);
-    return;
+    return true;
   }
   st2<N>(a.s + ow, u);
   strang_half<N>(u, sm, tab.tw, SpecTable{a.pspec + ow}, hs);
@@ -392,20 +385,15 @@ k_bicg_v_h(KrylovArgs a, KState* st, int* active) {
     st[b].alpha = alpha;
     st[b].snorm = snorm;
   }
+  return false;
 }
 
 // ---- t-phase: t = M s_hat, omega, x/r update, ||r||, rho, beta, next p, p_hat
 template <int N>
-__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
-k_bicg_t_h(KrylovArgs a, KState* st, int* active) {
+TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* sm, double* red,
+                        double* aux, const FilterTables& tab) {
   using S = HShape<N>;
-  extern __shared__ double2 sm[];
-  __shared__ double red[4 * 32];
   const int b = blockIdx.x;
-  if (st[b].done) return;
-  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
-  FilterTables tab = a.tab;
-  tab.tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
   const KState s = st[b];
   const int tid = threadIdx.x;
   const long ow = (long)b * N;
@@ -419,7 +407,6 @@ k_bicg_t_h(KrylovArgs a, KState* st, int* active) {
   prefetch_l2(a.r0w + ow, N);
   prefetch_l2(a.p + ow, N);
   prefetch_l2(a.v + ow, N);
-  __syncthreads();   // twiddle table staged
   double2 u[8];
   apply_level_op_half<N, true>(shg, kg, a.shift, u, sm, aux, tab, hs);   // u = t = M s_hat
   double2 sv[8];
@@ -437,7 +424,7 @@ k_bicg_t_h(KrylovArgs a, KState* st, int* active) {
   red2 = block_sum<2>(red2, red);
   if (red2.v[0] == 0.0) {
     finish_instance(a, st, active, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN, sm);
-    return;
+    return true;
   }
   const double omega = red2.v[1] / red2.v[0];
   // x += alpha p_hat + omega s_hat
@@ -484,7 +471,7 @@ k_bicg_t_h(KrylovArgs a, KState* st, int* active) {
     else if (fin == 2) finish_instance(a, st, active, b, s.it, rel, TSF_BD_OMEGA, sm);
     else if (fin == 3) finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED, sm);
     else finish_instance(a, st, active, b, s.it + 1, rel, TSF_BD_RHO, sm);
-    return;
+    return true;
   }
   // next p = r + beta (p - omega v)
   const double beta = (rho_new / s.rho_new) * (s.alpha / omega);
@@ -503,6 +490,26 @@ k_bicg_t_h(KrylovArgs a, KState* st, int* active) {
     st[b].rnorm = rnorm;
     st[b].it = s.it + 1;
   }
+  return false;
+}
+
+// phase kernels, and both phases of an iteration in one kernel (TSF_FUSE_VT)
+template <int N, int PHASES>
+__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
+k_bicg_h(KrylovArgs a, KState* st, int* active) {
+  using S = HShape<N>;
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  if (st[blockIdx.x].done) return;
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
+  FilterTables tab = a.tab;
+  tab.tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
+  __syncthreads();   // twiddle table staged
+  if constexpr (PHASES & 1) {
+    if (dev_bicg_v_h<N>(a, st, active, sm, red, aux, tab)) return;
+  }
+  if constexpr (PHASES == 3) __syncthreads();   // st[b] (alpha, ||s||), s_hat and its spectrum
+  if constexpr (PHASES & 2) dev_bicg_t_h<N>(a, st, active, sm, red, aux, tab);
 }
 
 // ---- debug: the two building blocks alone (tests/test_gpu_half.py)

@@ -170,7 +170,16 @@ __global__ void __launch_bounds__(HRow<N2>::BLOCK, 1) k_hrow_strang(LargeArgs a)
   {
     const bool self = cp == 0;
     const double2* pb = (self ? smg : sm + (1 - g) * R::BUF) + ((PL::NPASS - 1) & 1) * PL::SMEM_ELEMS;
-    double2* hs = a.hg.hspec + (long)b * (H + 1);
+    // The filtered spectrum Q = FFT_n(q) / n of the output q is in hand, so the
+    // even bins of the NEXT Toeplitz product (of q) are formed here too:
+    // pre-step of n S_2k/L . Q into channel 1, transformed after the Strang
+    // rows (parked in its own row of channel 1 meanwhile: same thread, same
+    // addresses).
+    double2* rowe = a.Z + (long)a.B * H + (long)b * H + (long)k1 * N2;
+    const double2* se = a.hg.sEh + (long)k1 * N2;
+    double2 fe[E];
+#pragma unroll
+    for (int c = 0; c < E; ++c) fe[c] = ldt(&se[tid + c * T]);
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int k2 = tid + c * T;
@@ -184,20 +193,25 @@ __global__ void __launch_bounds__(HRow<N2>::BLOCK, 1) k_hrow_strang(LargeArgs a)
       const double2 Tt = cmul(w, make_double2(d.y, -d.x));
       const double2 Q = cscale(cadd(s, Tt), 0.5 * sp[c].x);
       const double2 cQm = cscale(csub(s, Tt), 0.5 * sp[c].y);
-      hs[(long)k1 * N2 + k2] = Q;
-      if (k == 0) hs[H] = cconj(cQm);
       z[c] = pack_inverse(Q, cQm, w);
+      rowe[k2] = pack_inverse(cscale(Q, fe[c].x), cscale(cQm, fe[c].y), w);
     }
     group_fft<N2, E, true>(z, smg, tw2, 0, tid);
+    double2 ze[E];
 #pragma unroll
-    for (int c = 0; c < E; ++c) row[tid + c * T] = z[c];
+    for (int c = 0; c < E; ++c) {
+      row[tid + c * T] = z[c];
+      ze[c] = rowe[tid + c * T];
+    }
+    group_fft<N2, E, true>(ze, smg, tw2, 0, tid);
+#pragma unroll
+    for (int c = 0; c < E; ++c) rowe[tid + c * T] = ze[c];
   }
 }
 
 // ------------------------------------------------------------ hrow_mv
-// Rows of the Toeplitz product: CTAs [0, N1) the odd-bin rows (forward,
-// 2 S_{4k+1}/L, inverse, in place in channel 0), CTAs [N1, 2 N1) the even-bin
-// rows (pre-step of the stored Strang spectrum, inverse only, into channel 1).
+// Odd-bin rows of the Toeplitz product: forward, 2 S_{4k+1}/L, inverse, in
+// place in channel 0 (the even-bin rows were formed by hrow_strang).
 template <int N2>
 __global__ void __launch_bounds__(LRow<N2>::BLOCK, 1) k_hrow_mv(LargeArgs a) {
   pdl_enter();
@@ -209,65 +223,37 @@ __global__ void __launch_bounds__(LRow<N2>::BLOCK, 1) k_hrow_mv(LargeArgs a) {
   const int b = blockIdx.y, tid = threadIdx.x;
   if (inst_skip(a, b)) return;
   const bool own = tid < T;
-  const bool odd = (int)blockIdx.x < N1;
-  const int k1 = odd ? blockIdx.x : blockIdx.x - N1;
+  const int k1 = blockIdx.x;
   double2* tw2 = sm + 2 * FftPlan<N2, E>::SMEM_ELEMS;
   double2 z[E];
-  if (odd) {
-    double2* row = a.Z + (long)b * H + (long)k1 * N2;
+  double2* row = a.Z + (long)b * H + (long)k1 * N2;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < E; ++c) z[c] = row[tid + c * T];
+  }
+  stage_tw<N2>(tw2, a.hg.tw2);
+  double so[E];
+  block_fft<N2, E, false>(z, sm, tw2, 0, static_cast<const double2*>(nullptr), [&] {
     if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) z[c] = row[tid + c * T];
+      for (int c = 0; c < E; ++c) so[c] = a.hg.sO4[(long)k1 * N2 + tid + c * T];
     }
-    stage_tw<N2>(tw2, a.hg.tw2);
-    double so[E];
-    block_fft<N2, E, false>(z, sm, tw2, 0, static_cast<const double2*>(nullptr), [&] {
-      if (own) {
+  });
+  if (own) {
 #pragma unroll
-        for (int c = 0; c < E; ++c) so[c] = a.hg.sO4[(long)k1 * N2 + tid + c * T];
-      }
-    });
-    if (own) {
+    for (int c = 0; c < E; ++c) z[c] = cscale(z[c], so[c]);
+  }
+  block_fft<N2, E, true>(z, sm, tw2, 0);
+  if (own) {
 #pragma unroll
-      for (int c = 0; c < E; ++c) z[c] = cscale(z[c], so[c]);
-    }
-    block_fft<N2, E, true>(z, sm, tw2, 0);
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < E; ++c) row[tid + c * T] = z[c];
-    }
-  } else {
-    const double2* hs = a.hg.hspec + (long)b * (H + 1);
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < E; ++c) {
-        const int k2 = tid + c * T;
-        const long pos = (long)k1 * N2 + k2;
-        const long k = k1 + (long)N1 * k2;
-        const long posm = k == 0 ? H
-                          : k1 == 0 ? (long)(N2 - k2)
-                                    : (long)(N1 - k1) * N2 + (N2 - 1 - k2);
-        const double2 qa = hs[pos], qm = hs[posm];
-        const double2 f = ldt(&a.hg.sEh[pos]);     // n S_2k / L, n S_2(H-k) / L
-        const double2 Q = cscale(qa, f.x);
-        const double2 cQm = make_double2(qm.x * f.y, -qm.y * f.y);
-        z[c] = pack_inverse(Q, cQm, tw_get_g(a.lt.twL, 2 * k));
-      }
-    }
-    stage_tw<N2>(tw2, a.hg.tw2);
-    block_fft<N2, E, true>(z, sm, tw2, 0);
-    double2* row = a.Z + (long)a.B * H + (long)b * H + (long)k1 * N2;
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < E; ++c) row[tid + c * T] = z[c];
-    }
+    for (int c = 0; c < E; ++c) row[tid + c * T] = z[c];
   }
 }
 
 // ------------------------------------------------------------ hcol_inv
 template <int N1, int MB = LCol<N1>::MINB>
 __global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)
-k_hcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, int ch,
+k_hcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, double* __restrict__ dst1,
            const double* __restrict__ xin, const double* __restrict__ ye,
            const double* __restrict__ w1, int pslot) {
   pdl_enter();
@@ -286,6 +272,9 @@ k_hcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, int ch,
   stage_tw<N1>(tw1, a.hg.tw1);
   const long off = (long)b * a.n;
   const long off2 = (long)b * H;
+  // HO_PACK: grid.z = 2 runs both channels (Strang output -> dst, the even
+  // bins of its Toeplitz product -> dst1)
+  const int ch = blockIdx.z;
   const double2* Zc = a.Z + (long)ch * a.B * H + off2;
   double2 z[E];
 #pragma unroll
@@ -296,7 +285,7 @@ k_hcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, int ch,
   }
   group_fft<N1, E, true>(z, smg, tw1, 0, tid);
   if (out_mode == HO_PACK) {
-    double2* d2 = reinterpret_cast<double2*>(dst) + off2;
+    double2* d2 = reinterpret_cast<double2*>(ch ? dst1 : dst) + off2;
 #pragma unroll
     for (int c = 0; c < E; ++c) d2[(long)N2 * (tid + c * T) + t2] = z[c];
     return;

@@ -500,11 +500,11 @@ int hrow_mv_at(int lg, const LargeArgs& a, cudaStream_t st) {
   return report_error(TSF_E_UNSUPPORTED, "half-length row length out of range");
 }
 template <int LOG = kLargeMinLog>
-int hcol_inv_at(int lg, const LargeArgs& a, double* dst, int mode, int ch, const double* xin,
+int hcol_inv_at(int lg, const LargeArgs& a, double* dst, int mode, double* dst1, const double* xin,
                 const double* ye, const double* w1, int slot, cudaStream_t st) {
-  if (lg == LOG) return LargeDispatch<LOG>::hcol_inv(a, dst, mode, ch, xin, ye, w1, slot, st);
+  if (lg == LOG) return LargeDispatch<LOG>::hcol_inv(a, dst, mode, dst1, xin, ye, w1, slot, st);
   if constexpr (LOG < kLargeMaxLog)
-    return hcol_inv_at<LOG + 1>(lg, a, dst, mode, ch, xin, ye, w1, slot, st);
+    return hcol_inv_at<LOG + 1>(lg, a, dst, mode, dst1, xin, ye, w1, slot, st);
   return report_error(TSF_E_UNSUPPORTED, "half-length column length out of range");
 }
 
@@ -524,32 +524,32 @@ struct Runner {
   int lg1h = 0, lg2h = 0;
   bool half = false;   // this solve runs the half-length engine (tsf_hlarge.cuh)
 
-  // dst = P^{-1} src through ONE length-n/2 transform pair; the half spectrum
-  // of dst stays in hg.hspec for the next product's even bins
-  int hstrang(int in_mode, const double* src, double* dst) {
+  // dst = P^{-1} src through ONE length-n/2 transform pair; ye receives the
+  // even-bin half of the Toeplitz product of dst (formed from the same
+  // filtered spectrum inside the row kernel: no forward transform)
+  int hstrang(int in_mode, const double* src, double* dst, double* ye) {
     int rc;
     if ((rc = hcol_fwd_at(lg1h, a, src, in_mode, st))) return rc;
     if ((rc = hrow_strang_at(lg2h, a, st))) return rc;
-    return hcol_inv_at(lg1h, a, dst, HO_PACK, 0, nullptr, nullptr, nullptr, -1, st);
+    return hcol_inv_at(lg1h, a, dst, HO_PACK, ye, nullptr, nullptr, nullptr, -1, st);
   }
-  // dst = d src + kappa . (A src) for src = the last hstrang output; tmp: a
-  // free vector for the even-bin half of the product
-  int happly(const double* src, double* dst, const double* w1, int slot, double* tmp) {
+  // dst = d src + kappa . (A src) for src = the last hstrang output, ye its
+  // even-bin half
+  int happly(const double* src, double* dst, const double* w1, int slot, const double* ye) {
     int rc;
     if ((rc = hcol_fwd_at(lg1h, a, src, HF_ODD, st))) return rc;
     if ((rc = hrow_mv_at(lg2h, a, st))) return rc;
-    if ((rc = hcol_inv_at(lg1h, a, tmp, HO_PACK, 1, nullptr, nullptr, nullptr, -1, st))) return rc;
-    return hcol_inv_at(lg1h, a, dst, HO_ODD, 0, src, tmp, w1, slot, st);
+    return hcol_inv_at(lg1h, a, dst, HO_ODD, nullptr, src, ye, w1, slot, st);
   }
   int bicg_iteration_half() {
     int rc;
     const int NC = lp->ncol_cta_h, NR = (a.n + kLelChunk - 1) / kLelChunk;
-    if ((rc = hstrang(HF_PUPD, nullptr, a.ph))) return rc;
-    if ((rc = happly(a.ph, a.v, a.r0, 0, a.t))) return rc;      // t is free until the t-product
+    if ((rc = hstrang(HF_PUPD, nullptr, a.ph, a.t))) return rc;  // t is free until the t-product
+    if ((rc = happly(a.ph, a.v, a.r0, 0, a.t))) return rc;
     if ((rc = sc(LS_ALPHA, NC, 1))) return rc;
-    if ((rc = hstrang(HF_SUPD, nullptr, a.sh))) return rc;
+    if ((rc = hstrang(HF_SUPD, nullptr, a.sh, a.r))) return rc;  // r is dead once s exists
     if ((rc = sc(LS_SNORM, NC, 1))) return rc;
-    if ((rc = happly(a.sh, a.t, a.s, 0, a.r))) return rc;       // r is dead once s exists
+    if ((rc = happly(a.sh, a.t, a.s, 0, a.r))) return rc;
     if ((rc = sc(LS_OMEGA, NC, 1))) return rc;
     launch_pdl(k_lel_xr, lel_grid(), kLelThreads, 0, st, a, (const double*)a.ph,
                (const double*)a.sh);

@@ -575,8 +575,9 @@ struct LargeDispatch {
   static int hcol_fwd(const LargeArgs& a, const double* src, int in_mode, cudaStream_t st);
   static int hrow_strang(const LargeArgs& a, cudaStream_t st);
   static int hrow_mv(const LargeArgs& a, cudaStream_t st);
-  static int hcol_inv(const LargeArgs& a, double* dst, int out_mode, int ch, const double* xin,
-                      const double* ye, const double* w1, int pslot, cudaStream_t st);
+  static int hcol_inv(const LargeArgs& a, double* dst, int out_mode, double* dst1,
+                      const double* xin, const double* ye, const double* w1, int pslot,
+                      cudaStream_t st);
 };
 
 // Launches of the large-n engine are programmatic dependent launches

@@ -145,7 +145,7 @@ int LargeDispatch<LOG>::hrow_mv(const LargeArgs& a, cudaStream_t st) {
     auto k = k_hrow_mv<N2>;
     static cudaError_t prep = large_prep(k, S::SMEM);
     if (prep != cudaSuccess) return large_launch_error(prep);
-    launch_pdl(k, dim3(2 * a.hg.N1, a.B), S::BLOCK, S::SMEM, st, a);
+    launch_pdl(k, dim3(a.hg.N1, a.B), S::BLOCK, S::SMEM, st, a);
     return large_launch_error(cudaGetLastError());
   } else {
     return report_error(-3, "half-length rows need 128 <= N2 <= 2048");
@@ -153,16 +153,16 @@ int LargeDispatch<LOG>::hrow_mv(const LargeArgs& a, cudaStream_t st) {
 }
 
 template <int LOG>
-int LargeDispatch<LOG>::hcol_inv(const LargeArgs& a, double* dst, int out_mode, int ch,
+int LargeDispatch<LOG>::hcol_inv(const LargeArgs& a, double* dst, int out_mode, double* dst1,
                                  const double* xin, const double* ye, const double* w1, int pslot,
                                  cudaStream_t st) {
   constexpr int N1 = 1 << LOG;
   using S = LCol<N1>;
-  const dim3 grid(a.hg.N2 / S::G, a.B);
+  const dim3 grid(a.hg.N2 / S::G, a.B, (out_mode == HO_PACK && dst1) ? 2 : 1);
   auto k = k_hcol_inv<N1>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, dst, out_mode, ch, xin, ye, w1, pslot);
+  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, dst, out_mode, dst1, xin, ye, w1, pslot);
   return large_launch_error(cudaGetLastError());
 }
 

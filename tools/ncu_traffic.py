@@ -24,7 +24,8 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 SOLVE = ("k_solve_begin", "k_bicg_v", "k_bicg_t", "k_cg_iter", "k_lcol_fwd", "k_lcol_inv",
-         "k_lrow", "k_lsc", "k_lel_", "k_lspec", "k_lloop_cond", "k_loop_cond", "k_set_int")
+         "k_lrow", "k_lsc", "k_lel_", "k_lspec", "k_lloop_cond", "k_loop_cond", "k_set_int",
+         "k_hcol_fwd", "k_hcol_inv", "k_hrow_strang", "k_hrow_mv", "k_hspec")
 SOE = ("k_soe",)
 
 
@@ -38,13 +39,14 @@ def main():
     from paper_2002_11978_b200 import _native
     env = dict(os.environ, TSF_SOLVE_GRAPH="0")
     bench = [sys.executable, str(ROOT / "bench.py"), "--workload", args.workload, "--steps",
-             str(args.steps), "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
+             str(args.steps), "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-matvec"]
     if args.batch:
         bench += ["--batch", str(args.batch)]
     log = ROOT / "gpurun_out" / f"ncu_traffic_{args.workload}.csv"
     log.parent.mkdir(exist_ok=True)
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--clock-control", "none", "--csv", "--log-file", str(log)] + bench
+           "--clock-control", "none", "--cache-control", "none", "--csv", "--log-file",
+           str(log)] + bench
     out = subprocess.run(cmd, env=env, capture_output=True, text=True)
     line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     if out.returncode != 0 or not line:
@@ -82,8 +84,8 @@ def main():
            "dram_bytes_per_instance_iteration": solve / its,
            "soe_dram_bytes_per_level": soe / K,
            "algorithmic_bytes_per_instance_iteration": 216 * bl["config"]["n"],
-           "capture": f"ncu dram__bytes_read/write.sum, {K} levels of bench.py --workload "
-                      f"{args.workload} (B = {bl['config']['instances_per_gpu']}), "
+           "capture": f"ncu dram__bytes_read/write.sum --cache-control none, {K} levels of "
+                      f"bench.py --workload {args.workload} (B = {bl['config']['instances_per_gpu']}), "
                       "TSF_SOLVE_GRAPH=0"}
     p = Path(args.out)
     allr = json.loads(p.read_text()) if p.exists() else {}
