@@ -138,7 +138,7 @@ k_hcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
 // mirror): forward row transforms, split step + Strang filter + half spectrum
 // + inverse pre-step on the mirror pairs, inverse row transforms.
 template <int N2>
-__global__ void __launch_bounds__(HRow<N2>::BLOCK, 1) k_hrow_strang(LargeArgs a) {
+__global__ void __launch_bounds__(HRow<N2>::BLOCK, 1) k_hrow_strang(LargeArgs a, int mode) {
   pdl_enter();
   using R = HRow<N2>;
   using PL = FftPlan<N2, 8>;
@@ -157,11 +157,19 @@ __global__ void __launch_bounds__(HRow<N2>::BLOCK, 1) k_hrow_strang(LargeArgs a)
 #pragma unroll
   for (int c = 0; c < E; ++c) z[c] = row[tid + c * T];
   stage_tw<N2>(tw2, a.hg.tw2);
-  const double2* spec = a.hg.pspec2 + (long)b * H + (long)k1 * N2;
+  // mode bit 0: the filter is the symbol's even bins (standalone Toeplitz
+  // product: sEh / n, shared) instead of the instance's Strang filter;
+  // bit 1: also form the even-bin rows of the output's Toeplitz product
+  const bool sym = mode & 1, side = mode & 2;
+  const double2* spec = sym ? a.hg.sEh + (long)k1 * N2 : a.hg.pspec2 + (long)b * H + (long)k1 * N2;
+  const double fs = sym ? 1.0 / (2.0 * (double)H) : 1.0;   // exact (power of two)
   double2 sp[E];
   group_fft<N2, E, false>(z, smg, tw2, 0, tid, [&] {
 #pragma unroll
-    for (int c = 0; c < E; ++c) sp[c] = spec[tid + c * T];
+    for (int c = 0; c < E; ++c) {
+      sp[c] = spec[tid + c * T];
+      sp[c] = make_double2(sp[c].x * fs, sp[c].y * fs);
+    }
   });
   double2* xb = smg + ((PL::NPASS - 1) & 1) * PL::SMEM_ELEMS;
 #pragma unroll
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(HRow<N2>::BLOCK, 1) k_hrow_strang(LargeArgs a)
     const double2* se = a.hg.sEh + (long)k1 * N2;
     double2 fe[E];
 #pragma unroll
-    for (int c = 0; c < E; ++c) fe[c] = ldt(&se[tid + c * T]);
+    for (int c = 0; c < E; ++c) fe[c] = side ? ldt(&se[tid + c * T]) : make_double2(0.0, 0.0);
 #pragma unroll
     for (int c = 0; c < E; ++c) {
       const int k2 = tid + c * T;
@@ -194,9 +202,14 @@ __global__ void __launch_bounds__(HRow<N2>::BLOCK, 1) k_hrow_strang(LargeArgs a)
       const double2 Q = cscale(cadd(s, Tt), 0.5 * sp[c].x);
       const double2 cQm = cscale(csub(s, Tt), 0.5 * sp[c].y);
       z[c] = pack_inverse(Q, cQm, w);
-      rowe[k2] = pack_inverse(cscale(Q, fe[c].x), cscale(cQm, fe[c].y), w);
+      if (side) rowe[k2] = pack_inverse(cscale(Q, fe[c].x), cscale(cQm, fe[c].y), w);
     }
     group_fft<N2, E, true>(z, smg, tw2, 0, tid);
+    if (!side) {   // (uniform over the launch)
+#pragma unroll
+      for (int c = 0; c < E; ++c) row[tid + c * T] = z[c];
+      return;
+    }
     double2 ze[E];
 #pragma unroll
     for (int c = 0; c < E; ++c) {

@@ -237,11 +237,18 @@ __global__ void __launch_bounds__(kLelThreads) k_lspec(LargeArgs a, double kbar,
 
 // The level's Strang filter for the half-length engine: (S_k, S_{H-k}) / n at
 // the half geometry's position of bin k (tsf_hlarge.cuh)
-__global__ void __launch_bounds__(kLelThreads) k_hspec(LargeArgs a) {
+__global__ void __launch_bounds__(kLelThreads) k_hspec(LargeArgs a, double kbar,
+                                                       const double* __restrict__ kbar_dev,
+                                                       int use_state) {
   pdl_enter();
   const int b = blockIdx.y, tid = threadIdx.x;
-  if (inst_skip(a, b)) return;
-  const double kb = a.st[b].kbar;
+  double kb = kbar;
+  if (use_state) {
+    if (inst_skip(a, b)) return;
+    kb = a.st[b].kbar;
+  } else if (kbar_dev) {
+    kb = kbar_dev[b];
+  }
   const double d = a.shift;
   const double inv_n = 1.0 / a.nt;
   const long H = a.nt / 2;
@@ -488,9 +495,9 @@ int hcol_fwd_at(int lg, const LargeArgs& a, const double* src, int mode, cudaStr
   return report_error(TSF_E_UNSUPPORTED, "half-length column length out of range");
 }
 template <int LOG = kLargeMinLog>
-int hrow_strang_at(int lg, const LargeArgs& a, cudaStream_t st) {
-  if (lg == LOG) return LargeDispatch<LOG>::hrow_strang(a, st);
-  if constexpr (LOG < kLargeMaxLog) return hrow_strang_at<LOG + 1>(lg, a, st);
+int hrow_strang_at(int lg, const LargeArgs& a, int mode, cudaStream_t st) {
+  if (lg == LOG) return LargeDispatch<LOG>::hrow_strang(a, mode, st);
+  if constexpr (LOG < kLargeMaxLog) return hrow_strang_at<LOG + 1>(lg, a, mode, st);
   return report_error(TSF_E_UNSUPPORTED, "half-length row length out of range");
 }
 template <int LOG = kLargeMinLog>
@@ -530,8 +537,18 @@ struct Runner {
   int hstrang(int in_mode, const double* src, double* dst, double* ye) {
     int rc;
     if ((rc = hcol_fwd_at(lg1h, a, src, in_mode, st))) return rc;
-    if ((rc = hrow_strang_at(lg2h, a, st))) return rc;
+    if ((rc = hrow_strang_at(lg2h, a, ye ? 2 : 0, st))) return rc;
     return hcol_inv_at(lg1h, a, dst, HO_PACK, ye, nullptr, nullptr, nullptr, -1, st);
+  }
+  // standalone product (no Strang spectrum to start from): the even bins
+  // through the packed forward transform with the symbol as filter
+  int happly_plain(const double* src, double* dst, double* tmp) {
+    int rc;
+    if ((rc = hcol_fwd_at(lg1h, a, src, HF_LOAD, st))) return rc;
+    if ((rc = hrow_strang_at(lg2h, a, 1, st))) return rc;
+    if ((rc = hcol_inv_at(lg1h, a, tmp, HO_PACK, nullptr, nullptr, nullptr, nullptr, -1, st)))
+      return rc;
+    return happly(src, dst, nullptr, -1, tmp);
   }
   // dst = d src + kappa . (A src) for src = the last hstrang output, ye its
   // even-bin half
@@ -900,6 +917,9 @@ int large_matvec(LargePlan* lp, int B, const double* x, double* y, const double*
   Runner R = make_runner(lp, B, st);
   R.a.kappa = kappa;
   R.a.shift = shift;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (lp->half && half_mode() && lp->n >= hlarge_min_n() && al(x) && al(y) && y != x)
+    return R.happly_plain(x, y, R.a.t);
   return R.apply(x, y, nullptr, -1);
 }
 
@@ -909,6 +929,13 @@ int large_precond(LargePlan* lp, int B, const double* v, double* z, double shift
   if (rc) return rc;
   Runner R = make_runner(lp, B, st);
   R.a.shift = shift;
+  if (lp->half && half_mode() && lp->n >= hlarge_min_n() &&
+      ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(z)) & 15) == 0) {
+    launch_pdl(k_hspec, dim3((unsigned)((R.a.nt / 2 + kLelChunk - 1) / kLelChunk), B), kLelThreads,
+               0, st, R.a, kbar, kbar_dev, 0);
+    if ((rc = cuda_check(cudaGetLastError(), "k_hspec"))) return rc;
+    return R.hstrang(HF_LOAD, v, z, nullptr);
+  }
   launch_pdl(k_lspec, R.lel_grid(), kLelThreads, 0, st, R.a, kbar, kbar_dev, 0);
   if ((rc = cuda_check(cudaGetLastError(), "k_lspec"))) return rc;
   return R.strang(CI_LOAD, v, z);
@@ -1041,7 +1068,7 @@ int large_solve(LargePlan* lp, int B, int method, int pc, const KrylovArgs& k, c
   if ((rc = cuda_check(cudaGetLastError(), "k_lsc(begin)"))) return rc;
   if (pc && R.half) {
     launch_pdl(k_hspec, dim3((unsigned)((a.nt / 2 + kLelChunk - 1) / kLelChunk), B), kLelThreads, 0,
-               st, a);
+               st, a, 0.0, (const double*)nullptr, 1);
     if ((rc = cuda_check(cudaGetLastError(), "k_hspec"))) return rc;
   } else if (pc) {
     launch_pdl(k_lspec, R.lel_grid(), kLelThreads, 0, st, a, 0.0, nullptr, 1);

@@ -573,7 +573,7 @@ struct LargeDispatch {
   static int col_group();  // G: columns per column CTA
   // half-length engine (tsf_hlarge.cuh); LOG = log2 of N1 (columns) or N2 (rows)
   static int hcol_fwd(const LargeArgs& a, const double* src, int in_mode, cudaStream_t st);
-  static int hrow_strang(const LargeArgs& a, cudaStream_t st);
+  static int hrow_strang(const LargeArgs& a, int mode, cudaStream_t st);
   static int hrow_mv(const LargeArgs& a, cudaStream_t st);
   static int hcol_inv(const LargeArgs& a, double* dst, int out_mode, double* dst1,
                       const double* xin, const double* ye, const double* w1, int pslot,

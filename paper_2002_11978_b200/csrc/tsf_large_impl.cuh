@@ -123,14 +123,14 @@ int LargeDispatch<LOG>::hcol_fwd(const LargeArgs& a, const double* src, int in_m
 }
 
 template <int LOG>
-int LargeDispatch<LOG>::hrow_strang(const LargeArgs& a, cudaStream_t st) {
+int LargeDispatch<LOG>::hrow_strang(const LargeArgs& a, int mode, cudaStream_t st) {
   constexpr int N2 = 1 << LOG;
   if constexpr (HRow<N2>::OK) {
     using S = HRow<N2>;
     auto k = k_hrow_strang<N2>;
     static cudaError_t prep = large_prep(k, S::SMEM);
     if (prep != cudaSuccess) return large_launch_error(prep);
-    launch_pdl(k, dim3(a.hg.N1 / 2, a.B), S::BLOCK, S::SMEM, st, a);
+    launch_pdl(k, dim3(a.hg.N1 / 2, a.B), S::BLOCK, S::SMEM, st, a, mode);
     return large_launch_error(cudaGetLastError());
   } else {
     return report_error(-3, "half-length row pairs need 128 <= N2 <= 2048");
