@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define TSF_ABI_VERSION 3
+#define TSF_ABI_VERSION 4
 
 /* API return codes */
 #define TSF_SUCCESS 0

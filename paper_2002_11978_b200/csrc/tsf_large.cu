@@ -798,7 +798,15 @@ int large_plan_init(LargePlan* lp, int n, int L, const double* symbol_re, const 
   std::vector<double> sO4;
   const long Hh = nt / 2;
   if (lam && n == nt && Hh >= 64L * 128) {
-    int N1h = (int)std::max(64L, Hh >> 11);
+    // rows up to 2048 points (the row-pair CTA's shared memory);
+    // TSF_HLARGE_ROWLOG caps log2(N2h) lower (experiments)
+    int hrowlog = 11;
+    if (const char* e = getenv("TSF_HLARGE_ROWLOG")) {
+      const int v = atoi(e);
+      if (v >= 7 && v <= 11) hrowlog = v;
+    }
+    int N1h = (int)std::max(64L, Hh >> hrowlog);
+    if (N1h > (1 << kLargeMaxLog)) N1h = 1 << kLargeMaxLog;
     int N2h = (int)(Hh / N1h);
     lp->half = 1;
     lp->hg.N1 = N1h;

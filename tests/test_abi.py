@@ -29,7 +29,7 @@ def test_library_loads_and_exports_all_symbols():
     for name in _declared():
         assert hasattr(lib, name), name
     lib.tsf_abi_version.restype = ctypes.c_int
-    assert lib.tsf_abi_version() == 3
+    assert lib.tsf_abi_version() == 4
 
 
 def test_invalid_arguments_fail_without_a_device():
