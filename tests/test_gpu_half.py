@@ -123,3 +123,47 @@ def test_half_level_solve_vs_full_engine_and_oracle(n, tmp_path):
             assert abs(int(out[tag]["its"][b]) - rep.iterations) <= 2, (tag, b)
             assert rel_l2(out[tag]["x"][b], xr) <= 1e-10, (tag, b)
         assert rel_l2(out["half"]["x"][b], out["full"]["x"][b]) <= 1e-10
+
+
+def test_half_control_flow_edges():
+    """The reference's control flow on the half-length kernels (n = 1024):
+    max_iters exhaustion (krylov.py:100), zero right-hand side (krylov.py:
+    109-111), non-positive kappa (scheme.py:156-160)."""
+    n = 1024
+    col, sym, lam = _setup(n)
+    x, kx, fx, u0 = WL.instance_fields(n, 0, 1)
+    lev = P.LevelOperator(P.build_toeplitz(col), 411.0, kx[0])
+    pc = P.build_preconditioner(col, 411.0, float(kx[0].mean()))
+    rhs = fx[0] + 411.0 * u0[0]
+    xs, rep = P.solve_bicgstab(lev, pc, rhs, tol=1e-15, max_iters=1)
+    assert not rep.converged and rep.iterations == 1
+    xs, rep = P.solve_bicgstab(lev, pc, np.zeros(n))
+    assert rep.converged and rep.iterations == 0
+    np.testing.assert_array_equal(xs, 0.0)
+    spec = P.ProblemSpec(gamma=0.5, alpha=1.5, l=1.0, T=1.0,
+                         kappa=lambda x, t: np.where(x > 0, 1.0, -1.0),
+                         source=lambda x, t: np.zeros_like(x),
+                         initial=lambda x: (1 - x * x) ** 2)
+    with pytest.raises(ValueError, match="kappa"):
+        P.run_fids(spec, 4, 1.0, n + 1, options=P.SolverOptions(solver="pkrylov"))
+
+
+def test_half_large_control_flow_edges():
+    """Same on the half-length four-step kernels (n = 2^15)."""
+    n = 1 << 15
+    col, sym, lam = _setup(n)
+    xg = WL.grid(n)
+    kap = 1.0 + 0.5 * np.sin(np.pi * xg)
+    lev = P.LevelOperator(P.build_toeplitz(col), 411.0, kap)
+    pc = P.build_preconditioner(col, 411.0, float(kap.mean()))
+    rhs = np.sin(np.pi * xg) + 411.0 * (1 - xg * xg) ** 2
+    xs, rep = P.solve_bicgstab(lev, pc, rhs, tol=1e-15, max_iters=2)
+    assert not rep.converged and rep.iterations == 2
+    xs, rep = P.solve_bicgstab(lev, pc, np.zeros(n))
+    assert rep.converged and rep.iterations == 0
+    total = 411.0 + float(kap.mean()) * lam
+    xr, ref = O.bicgstab(lambda q: 411.0 * q + kap * O.toeplitz_apply(sym, q),
+                         lambda q: O.precond_apply(total, q), rhs, tol=1e-12)
+    xs, rep = P.solve_bicgstab(lev, pc, rhs, tol=1e-12)
+    assert rep.converged and abs(rep.iterations - ref.iterations) <= 2
+    assert rel_l2(xs, xr) <= 1e-10

@@ -23,7 +23,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-SOLVE = ("k_solve_begin", "k_bicg_v", "k_bicg_t", "k_cg_iter", "k_lcol_fwd", "k_lcol_inv",
+SOLVE = ("k_solve_begin", "k_bicg_v", "k_bicg_t", "k_bicg_h", "k_cg_iter", "k_lcol_fwd", "k_lcol_inv",
          "k_lrow", "k_lsc", "k_lel_", "k_lspec", "k_lloop_cond", "k_loop_cond", "k_set_int",
          "k_hcol_fwd", "k_hcol_inv", "k_hrow_strang", "k_hrow_mv", "k_hspec")
 SOE = ("k_soe",)
