@@ -41,6 +41,20 @@
 #ifndef TSF_HALF
 #define TSF_HALF 1
 #endif
+// Two ncu-driven changes, measured and NOT adopted (configs[2]
+// level solve, one box): an unpadded mirror-exchange buffer removes the
+// kernel's only bank conflicts (2-way on the descending mirror reads, 2% of
+// its wavefronts) but ran 17.25 -> 17.38 ms; loading 2 / 4 slots of the x
+// update before their stores removes eight serialised memory latencies (11%
+// of the t-phase's stall samples) but ran 17.36 / 18.00 ms — with two CTAs
+// per SM the other CTA already fills those stalls, and the extra live
+// registers cost more elsewhere.
+#ifndef TSF_H_XB_PAD
+#define TSF_H_XB_PAD 1      // 0: unpadded mirror exchange
+#endif
+#ifndef TSF_H_XUPD_CHUNK
+#define TSF_H_XUPD_CHUNK 1  // slots of the x update loaded before their stores (1, 2, 4, 8)
+#endif
 
 namespace tsf {
 
@@ -121,12 +135,13 @@ TSF_D void strang_half(double2 (&z)[8], double2* sm, const double2* tw, const Sp
   // mirror exchange through the buffer the last pass did not read
   double2* xb = sm + ((PL::NPASS - 1) & 1) * PL::SMEM_ELEMS;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) xb[PL::pad(tid + c * T)] = z[c];
+  for (int c = 0; c < 8; ++c) xb[TSF_H_XB_PAD ? PL::pad(tid + c * T) : tid + c * T] = z[c];
   __syncthreads();
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const int k = tid + c * T;
-    const double2 zm = xb[PL::pad((H - k) & (H - 1))];
+    const int km = (H - k) & (H - 1);
+    const double2 zm = xb[TSF_H_XB_PAD ? PL::pad(km) : km];
     const double2 A = z[c];
     const double2 s = make_double2(A.x + zm.x, A.y - zm.y);   // A + conj(Zm)
     const double2 d = make_double2(A.x - zm.x, A.y + zm.y);   // A - conj(Zm)
@@ -246,25 +261,33 @@ k_solve_begin_h(KrylovArgs a, KState* st, int* active) {
   const int b = blockIdx.x;
   const long ow = (long)b * N;
   double ksum = 0.0, kmin = 1e308;
+  {
+    // every slot's modes before the first store (aliasing, as above)
+    double2 kk[8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int j = 2 * (tid + c * T);
-    double2 k;
+    for (int c = 0; c < 8; ++c) kk[c] = make_double2(0.0, 0.0);
     if (a.kappa) {
-      k = *reinterpret_cast<const double2*>(a.kappa + ow + j);
+      ld2<N>(kk, a.kappa + ow);
     } else {
-      k = make_double2(0.0, 0.0);
       for (int q = 0; q < a.nk; ++q) {
-        const double* mq = a.kmodes + q * a.kq_stride + (long)b * a.kb_stride + j;
-        // no contraction: reproduce numpy's  acc + mode*coef  rounding
-        k.x = __dadd_rn(k.x, __dmul_rn(mq[0], a.kcoef[q]));
-        k.y = __dadd_rn(k.y, __dmul_rn(mq[1], a.kcoef[q]));
+        double2 mq[8];
+        ld2<N>(mq, a.kmodes + q * a.kq_stride + (long)b * a.kb_stride);
+        const double cq = a.kcoef[q];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          // no contraction: reproduce numpy's  acc + mode*coef  rounding
+          kk[c].x = __dadd_rn(kk[c].x, __dmul_rn(mq[c].x, cq));
+          kk[c].y = __dadd_rn(kk[c].y, __dmul_rn(mq[c].y, cq));
+        }
       }
-      *reinterpret_cast<double2*>(a.kwork + ow + j) = k;
+      st2<N>(a.kwork + ow, kk);
     }
-    ksum += k.x;
-    ksum += k.y;
-    kmin = fmin(kmin, fmin(k.x, k.y));
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      ksum += kk[c].x;
+      ksum += kk[c].y;
+      kmin = fmin(kmin, fmin(kk[c].x, kk[c].y));
+    }
   }
   kmin = block_min1(kmin, red);
   if (kmin <= 0.0) {
@@ -433,12 +456,25 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
     const double2* p2 = reinterpret_cast<const double2*>(a.ph + ow);
     const double2* h2 = reinterpret_cast<const double2*>(shg);
     double2* xo = reinterpret_cast<double2*>(a.xw + ow);
+    // XC slots' operands before their stores (TSF_H_XUPD_CHUNK above)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int m = tid + c * S::T;
-      const double2 xv = x2[m], pv = p2[m], hv = h2[m];
-      xo[m] = make_double2(xv.x + (s.alpha * pv.x + omega * hv.x),
-                           xv.y + (s.alpha * pv.y + omega * hv.y));
+    constexpr int XC = TSF_H_XUPD_CHUNK;
+#pragma unroll
+    for (int c0 = 0; c0 < 8; c0 += XC) {
+      double2 xv[XC], pv[XC], hv[XC];
+#pragma unroll
+      for (int q = 0; q < XC; ++q) {
+        const int m = tid + (c0 + q) * S::T;
+        xv[q] = x2[m];
+        pv[q] = p2[m];
+        hv[q] = h2[m];
+      }
+#pragma unroll
+      for (int q = 0; q < XC; ++q) {
+        const int m = tid + (c0 + q) * S::T;
+        xo[m] = make_double2(xv[q].x + (s.alpha * pv[q].x + omega * hv[q].x),
+                             xv[q].y + (s.alpha * pv[q].y + omega * hv[q].y));
+      }
     }
   }
   // r = s - omega t
