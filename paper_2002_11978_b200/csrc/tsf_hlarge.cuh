@@ -42,7 +42,8 @@ struct HRow {
 // ------------------------------------------------------------ hcol_fwd
 template <int N1, int MB = LCol<N1>::MINB>
 __global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)
-k_hcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
+k_hcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode,
+           const __grid_constant__ ColMaps cm) {
   pdl_enter();
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
@@ -50,6 +51,7 @@ k_hcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   const long H = (long)N1 * N2;
   extern __shared__ __align__(128) double2 sm[];
   __shared__ double red[4 * 32];
+  __shared__ unsigned long long bar;
   const int b = blockIdx.y;
   const int g = threadIdx.x % G, tid = threadIdx.x / G;
   const int t2 = blockIdx.x * G + g;
@@ -59,7 +61,61 @@ k_hcol_fwd(LargeArgs a, const double* __restrict__ src, int in_mode) {
   const long off2 = (long)b * H;    // 16-byte words (n = 2H)
   double2 z[E];
   double part = 0.0;
-  if (in_mode == HF_ODD) {
+  if (cm.use) {
+    // TMA path (packed modes): up to two [N1 x G] tiles of 16-byte words land
+    // in the (not yet used) transform buffers while the CTA stages its
+    // twiddles and reads the state — HF_LOAD: src; HF_SUPD: r, v; HF_PUPD:
+    // p, v (r by plain loads: it is r0 at the first iteration)
+    double2* tile = sm;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, (unsigned)(cm.nv * N1 * G * 16));
+      for (int q = 0; q < cm.nv; ++q)
+        tma_tile(reinterpret_cast<double*>(tile + q * N1 * G), &cm.v[q], 2 * blockIdx.x * G, N1,
+                 2 * G, b, 8, &bar);
+    }
+    stage_tw<N1>(tw1, a.hg.tw1);
+    const LState stv = a.st ? a.st[b] : LState{};
+    double2 rr[E];
+    if (in_mode == HF_PUPD) {
+      const double2* r2 = reinterpret_cast<const double2*>(stv.it == 1 ? a.r0 : a.r);
+#pragma unroll
+      for (int c = 0; c < E; ++c) rr[c] = r2[off2 + (long)N2 * (tid + c * T) + t2];
+    }
+    __syncthreads();   // barrier initialised before anyone waits on it
+    mbar_wait(&bar, 0);
+    if (inst_skip(a, b)) return;
+    const double2* r02 = reinterpret_cast<const double2*>(a.r0);
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      const int t1 = tid + c * T;
+      const long m = off2 + (long)N2 * t1 + t2;
+      const double2 t0 = tile[t1 * G + g];
+      double2 val = t0;
+      if (in_mode == HF_PUPD) {
+        val = rr[c];
+        if (stv.it != 1) {
+          const double2 t1v = tile[N1 * G + t1 * G + g];   // v
+          const double beta = (stv.rho_new / stv.rho) * (stv.alpha / stv.omega);
+          val.x = rr[c].x + beta * (t0.x - stv.omega * t1v.x);
+          val.y = rr[c].y + beta * (t0.y - stv.omega * t1v.y);
+        }
+      } else if (in_mode == HF_SUPD) {
+        const double2 l0 = stv.it == 1 ? r02[m] : t0;
+        const double2 vv = tile[N1 * G + t1 * G + g];
+        val.x = l0.x - stv.alpha * vv.x;
+        val.y = l0.y - stv.alpha * vv.y;
+        part = fma(val.x, val.x, part);
+        part = fma(val.y, val.y, part);
+      }
+      z[c] = val;
+    }
+    if (in_mode == HF_PUPD || in_mode == HF_SUPD) {
+      double2* dp = reinterpret_cast<double2*>(in_mode == HF_PUPD ? a.p : a.s);
+#pragma unroll
+      for (int c = 0; c < E; ++c) dp[off2 + (long)N2 * (tid + c * T) + t2] = z[c];
+    }
+  } else if (in_mode == HF_ODD) {
     double xa[E], xb[E];
 #pragma unroll
     for (int c = 0; c < E; ++c) {
@@ -268,7 +324,7 @@ template <int N1, int MB = LCol<N1>::MINB>
 __global__ void __launch_bounds__(LCol<N1>::BLOCK, MB)
 k_hcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, double* __restrict__ dst1,
            const double* __restrict__ xin, const double* __restrict__ ye,
-           const double* __restrict__ w1, int pslot) {
+           const double* __restrict__ w1, int pslot, const __grid_constant__ ColMaps cm) {
   pdl_enter();
   using C = LCol<N1>;
   constexpr int E = C::E, T = C::T, G = C::G;
@@ -276,25 +332,39 @@ k_hcol_inv(LargeArgs a, double* __restrict__ dst, int out_mode, double* __restri
   const long H = (long)N1 * N2;
   extern __shared__ __align__(128) double2 sm[];
   __shared__ double red[4 * 32];
+  __shared__ unsigned long long bar;
   const int b = blockIdx.y;
   if (inst_skip(a, b)) return;
   const int g = threadIdx.x % G, tid = threadIdx.x / G;
   const int t2 = blockIdx.x * G + g;
   double2* smg = sm + g * C::BUF;
   double2* tw1 = sm + G * C::BUF;
-  stage_tw<N1>(tw1, a.hg.tw1);
-  const long off = (long)b * a.n;
-  const long off2 = (long)b * H;
   // HO_PACK: grid.z = 2 runs both channels (Strang output -> dst, the even
   // bins of its Toeplitz product -> dst1)
   const int ch = blockIdx.z;
+  // the channel's [N1 x G] tile of Z by TMA (tsf_tma.cuh) into the transform
+  // buffers, free until the transform starts: no extra shared memory
+  double2* ztile = sm;
+  if (cm.use && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (unsigned)(N1 * G * 16));
+    tma_tile(reinterpret_cast<double*>(ztile), &cm.z, 2 * blockIdx.x * G, N1, 2 * G,
+             ch * a.B + b, 8, &bar);
+  }
+  stage_tw<N1>(tw1, a.hg.tw1);
+  const long off = (long)b * a.n;
+  const long off2 = (long)b * H;
   const double2* Zc = a.Z + (long)ch * a.B * H + off2;
   double2 z[E];
+  if (cm.use) {
+    __syncthreads();   // barrier initialised before anyone waits on it
+    mbar_wait(&bar, 0);
+  }
 #pragma unroll
   for (int c = 0; c < E; ++c) {
     const int k1 = tid + c * T;
     const double2 w = tw_get_g(a.hg.twH, ((long)t2 * k1) & (H - 1));
-    z[c] = cmulc(Zc[(long)k1 * N2 + t2], w);
+    z[c] = cmulc(cm.use ? ztile[k1 * G + g] : Zc[(long)k1 * N2 + t2], w);
   }
   group_fft<N1, E, true>(z, smg, tw1, 0, tid);
   if (out_mode == HO_PACK) {

@@ -1113,6 +1113,18 @@ int tma_mode() {
   return v;
 }
 
+int tma_half_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_TMA_HALF");
+    if (!s) v = 2;
+    else if (!strcmp(s, "fwd")) v = 1;
+    else if (!strcmp(s, "inv")) v = 2;
+    else v = atoi(s) & 3;
+  }
+  return v;
+}
+
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;

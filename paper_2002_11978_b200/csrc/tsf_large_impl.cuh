@@ -115,10 +115,30 @@ int LargeDispatch<LOG>::hcol_fwd(const LargeArgs& a, const double* src, int in_m
   constexpr int N1 = 1 << LOG;
   using S = LCol<N1>;
   const dim3 grid(a.hg.N2 / S::G, a.B);
+  ColMaps cm;
+  memset(&cm, 0, sizeof(cm));
+  // packed [N1 x G] operand tiles (16-byte words) by TMA: the vector as
+  // {2 N2, N1, B} doubles, boxes of 2 G doubles
+  if ((tma_half_mode() & 1) && in_mode != HF_ODD && N1 <= 2048 &&
+      !few_ctas((long)grid.x * grid.y)) {
+    const double* vs[2] = {src, nullptr};
+    int nv = 1;
+    if (in_mode == HF_PUPD) {
+      vs[0] = a.p; vs[1] = a.v; nv = 2;
+    } else if (in_mode == HF_SUPD) {
+      vs[0] = a.r; vs[1] = a.v; nv = 2;
+    }
+    int rc = 0;
+    for (int q = 0; q < nv && !rc; ++q)
+      rc = tma_map_vector(&cm.v[q], vs[q], a.n, N1, 2 * a.hg.N2, a.B, 2 * S::G);
+    if (rc) return rc;
+    cm.nv = nv;
+    cm.use = 1;
+  }
   auto k = k_hcol_fwd<N1>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, src, in_mode);
+  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, src, in_mode, cm);
   return large_launch_error(cudaGetLastError());
 }
 
@@ -159,10 +179,17 @@ int LargeDispatch<LOG>::hcol_inv(const LargeArgs& a, double* dst, int out_mode, 
   constexpr int N1 = 1 << LOG;
   using S = LCol<N1>;
   const dim3 grid(a.hg.N2 / S::G, a.B, (out_mode == HO_PACK && dst1) ? 2 : 1);
+  ColMaps cm;
+  memset(&cm, 0, sizeof(cm));
+  if ((tma_half_mode() & 2) && N1 <= 2048 && !few_ctas((long)grid.x * grid.y)) {
+    const int rc = tma_map_z(&cm.z, a.Z, N1, a.hg.N2, a.B, S::G);
+    if (rc) return rc;
+    cm.use = 1;
+  }
   auto k = k_hcol_inv<N1>;
   static cudaError_t prep = large_prep(k, S::SMEM);
   if (prep != cudaSuccess) return large_launch_error(prep);
-  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, dst, out_mode, dst1, xin, ye, w1, pslot);
+  launch_pdl(k, grid, S::BLOCK, S::SMEM, st, a, dst, out_mode, dst1, xin, ye, w1, pslot, cm);
   return large_launch_error(cudaGetLastError());
 }
 

@@ -82,5 +82,12 @@ TSF_D unsigned tma_tile(double* dst, const CUtensorMap* map, int col0, int rows,
 int tma_map_vector(CUtensorMap* m, const double* base, long n, int N1, int N2, int B, int G);
 int tma_map_z(CUtensorMap* m, const double2* Z, int N1, int N2, int B, int G);
 int tma_mode();   // TSF_TMA: bit 0 column-forward tiles, bit 1 column-inverse tiles
+// the half-length column kernels (tsf_hlarge.cuh): TSF_TMA_HALF, default 2 —
+// the Z tiles of k_hcol_inv (measured neutral on configs[3]; the operand
+// tiles of k_hcol_fwd measured 0.4% slower), and only for launches of two
+// waves or more (each map costs a host-side cache lookup per launch, which a
+// latency-bound single small instance notices: configs[1] 0.70 -> 0.76 ms per
+// level)
+int tma_half_mode();
 
 }  // namespace tsf
