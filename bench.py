@@ -578,6 +578,12 @@ def main():
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        # result buffers a caller of the API would hold: pinned, allocated once
+        u_out = torch.empty((B, n), dtype=torch.float64).pin_memory()
+        its_out = torch.empty((levels, B), dtype=march.iters.dtype).pin_memory()
+        rel_out = torch.empty((levels, B), dtype=march.relres.dtype).pin_memory()
+        barrier()
         e0.record()
         h2d = u0_h.numel() * 8
         march.u0.copy_(u0_h, non_blocking=True)
@@ -585,14 +591,21 @@ def main():
             kdev.modes.copy_(km_h, non_blocking=True)
             fdev.modes.copy_(fm_h, non_blocking=True)
             h2d += (km_h.numel() + fm_h.numel()) * 8
+        ev[0].record()
         march.reset()
+        ev[1].record()
         march.run(levels)
-        u_out = march.u_level(march.next_level - 1).to("cpu", non_blocking=False)
-        its_out = march.iters[:levels].to("cpu")
-        rel_out = march.relres[:levels].to("cpu")
+        ev[2].record()
+        u_out.copy_(march.u_level(march.next_level - 1), non_blocking=True)
+        its_out.copy_(march.iters[:levels], non_blocking=True)
+        rel_out.copy_(march.relres[:levels], non_blocking=True)
+        ev[3].record()
         e1.record()
+        torch.cuda.synchronize()
         barrier()
         ems = e0.elapsed_time(e1)
+        e2e_parts = {"h2d_ms": e0.elapsed_time(ev[0]), "reset_ms": ev[0].elapsed_time(ev[1]),
+                     "march_ms": ev[1].elapsed_time(ev[2]), "d2h_ms": ev[2].elapsed_time(ev[3])}
         if dist is not None:
             tt = torch.tensor([ems], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -600,9 +613,10 @@ def main():
         d2h = u_out.numel() * 8 + its_out.numel() * 4 + rel_out.numel() * 8
         e2e = {"value": world * B * n * levels / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": h2d / levels, "d2h_bytes_per_step": d2h / levels,
-               "levels": levels,
+               "levels": levels, "parts": e2e_parts,
                "note": "pinned host u0 + coefficient modes -> device, march levels "
-                       f"1..{levels}, final u + per-level iterations/residuals -> host"}
+                       f"1..{levels}, final u + per-level iterations/residuals -> pinned host "
+                       "buffers; device events around the whole region"}
 
     # ---- standalone Toeplitz matvec throughput (configs[4] point at this n, B*n=2^26)
     mv = None
