@@ -493,7 +493,7 @@ def main():
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     half = os.environ.get("TSF_HALF", "1") != "0"   # half-length engines (tsf_half.cuh, tsf_hlarge.cuh)
-    if large and half and n & (n - 1) == 0 and n >= int(os.environ.get("TSF_HLARGE_MIN_N", 1 << 14)):
+    if large and half and n & (n - 1) == 0 and n >= int(os.environ.get("TSF_HLARGE_MIN_N", 1 << 13)):
         n1 = max(64, (n // 2) >> 11)   # tsf_large.cu large_plan_init, half geometry
         sname = (f"tsf large-n level solve, half-length transforms: k_hcol_fwd/k_hcol_inv<{n1}> "
                  f"+ k_hrow_strang/k_hrow_mv<{n // 2 // n1}> + k_lsc/k_lel_xr "

@@ -33,10 +33,12 @@ template <int N2>
 struct HRow {
   static constexpr int E = 8;
   static constexpr int T = N2 / E;
-  static constexpr int BLOCK = 2 * T;   // N2 >= 128: at least one warp
+  // row pairs per CTA: one, or as many as fill a warp (N2 = 64: two pairs)
+  static constexpr int NP = 2 * T >= 32 ? 1 : 32 / (2 * T);
+  static constexpr int BLOCK = 2 * T * NP;
   static constexpr int BUF = 2 * FftPlan<N2, E>::SMEM_ELEMS;
-  static constexpr int SMEM = (2 * BUF + tw_table_elems(N2)) * 16;
-  static constexpr bool OK = SMEM <= kSmemCap && N2 >= 128;
+  static constexpr int SMEM = (2 * NP * BUF + tw_table_elems(N2)) * 16;
+  static constexpr bool OK = SMEM <= kSmemCap && N2 >= 64;
 };
 
 // ------------------------------------------------------------ hcol_fwd
@@ -201,13 +203,15 @@ __global__ void __launch_bounds__(HRow<N2>::BLOCK, 1) k_hrow_strang(LargeArgs a,
   constexpr int E = 8, T = R::T;
   const int N1 = a.hg.N1;
   const long H = (long)N1 * N2;
-  const int cp = blockIdx.x, b = blockIdx.y;
+  const int b = blockIdx.y;
   if (inst_skip(a, b)) return;
   extern __shared__ __align__(128) double2 sm[];
-  const int g = threadIdx.x / T, tid = threadIdx.x % T;
+  const int gg = threadIdx.x / T, tid = threadIdx.x % T;   // gg: group (pair, side)
+  const int g = gg & 1;
+  const int cp = blockIdx.x * R::NP + (gg >> 1);
   const int k1 = cp == 0 ? (g ? N1 / 2 : 0) : (g ? N1 - cp : cp);
-  double2* smg = sm + g * R::BUF;
-  double2* tw2 = sm + 2 * R::BUF;
+  double2* smg = sm + gg * R::BUF;
+  double2* tw2 = sm + 2 * R::NP * R::BUF;
   double2* row = a.Z + (long)b * H + (long)k1 * N2;
   double2 z[E];
 #pragma unroll
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(HRow<N2>::BLOCK, 1) k_hrow_strang(LargeArgs a,
   __syncthreads();
   {
     const bool self = cp == 0;
-    const double2* pb = (self ? smg : sm + (1 - g) * R::BUF) + ((PL::NPASS - 1) & 1) * PL::SMEM_ELEMS;
+    const double2* pb = (self ? smg : sm + (gg ^ 1) * R::BUF) + ((PL::NPASS - 1) & 1) * PL::SMEM_ELEMS;
     // The filtered spectrum Q = FFT_n(q) / n of the output q is in hand, so the
     // even bins of the NEXT Toeplitz product (of q) are formed here too:
     // pre-step of n S_2k/L . Q into channel 1, transformed after the Strang

@@ -756,7 +756,7 @@ static long hlarge_min_n() {
   static long v = -1;
   if (v < 0) {
     const char* s = getenv("TSF_HLARGE_MIN_N");
-    v = s ? atol(s) : (1L << 14);
+    v = s ? atol(s) : (1L << 13);
   }
   return v;
 }
@@ -817,7 +817,7 @@ int large_plan_init(LargePlan* lp, int n, int L, const double* symbol_re, const 
   std::vector<double2> tw1h, tw2h, twH, sEh, lamH;
   std::vector<double> sO4;
   const long Hh = nt / 2;
-  if (lam && n == nt && Hh >= 64L * 128) {
+  if (lam && n == nt && Hh >= 64L * 64) {
     // rows up to 2048 points (the row-pair CTA's shared memory);
     // TSF_HLARGE_ROWLOG caps log2(N2h) lower (experiments)
     int hrowlog = 11;

@@ -150,10 +150,10 @@ int LargeDispatch<LOG>::hrow_strang(const LargeArgs& a, int mode, cudaStream_t s
     auto k = k_hrow_strang<N2>;
     static cudaError_t prep = large_prep(k, S::SMEM);
     if (prep != cudaSuccess) return large_launch_error(prep);
-    launch_pdl(k, dim3(a.hg.N1 / 2, a.B), S::BLOCK, S::SMEM, st, a, mode);
+    launch_pdl(k, dim3(a.hg.N1 / 2 / S::NP, a.B), S::BLOCK, S::SMEM, st, a, mode);
     return large_launch_error(cudaGetLastError());
   } else {
-    return report_error(-3, "half-length row pairs need 128 <= N2 <= 2048");
+    return report_error(-3, "half-length row pairs need 64 <= N2 <= 2048");
   }
 }
 
@@ -168,7 +168,7 @@ int LargeDispatch<LOG>::hrow_mv(const LargeArgs& a, cudaStream_t st) {
     launch_pdl(k, dim3(a.hg.N1, a.B), S::BLOCK, S::SMEM, st, a);
     return large_launch_error(cudaGetLastError());
   } else {
-    return report_error(-3, "half-length rows need 128 <= N2 <= 2048");
+    return report_error(-3, "half-length rows need 64 <= N2 <= 2048");
   }
 }
 
