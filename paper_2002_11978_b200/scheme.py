@@ -207,17 +207,17 @@ def _soe_block_default(B: int, n: int) -> int:
     """Levels per W pass of the march's blocked SOE schedule.
 
     TSF_SOE_BLOCK overrides (0 or 1: one W pass per level).  By default the
-    schedule is blocked (K = 8) on the single-CTA engine (n <= 4096), where
+    schedule is blocked (K = 8) on both engines: on the single-CTA engine
     batches make the SOE pass a large share of a level (configs[2]: 16%), and
-    per-level on the large-n engine, where single instances make it ~1-4%
-    (configs[1], configs[3]) and the per-level schedule keeps the history
-    term in the reference's order.  The choice depends on n
-    only, so an instance's result does not depend on the batch it is in."""
+    since the half-length four-step engine the per-level pass
+    was 10% of a configs[3] level (0.29 of 2.80 ms; blocked: 0.06 ms).  The
+    choice does not depend on B, so an instance's result does not depend on
+    the batch it is in."""
     env = os.environ.get("TSF_SOE_BLOCK")
     if env is not None:
         k = int(env)
         return k if 2 <= k <= 16 else 1
-    return 8 if n <= 4096 else 1
+    return 8
 
 
 def soe_block_tables(tab: np.ndarray, K: int):
