@@ -22,7 +22,11 @@ LARGE_FLAGS ?=
 all: $(LIB)
 
 $(OBJDIR)/gen/inst_L13.o: NVFLAGS += $(L13_FLAGS)
-$(OBJDIR)/gen/inst_%.o: NVFLAGS += $(INST_FLAGS)
+# -fmad=false: no implicit multiply-add contraction in the single-CTA engines —
+# every fused multiply-add there is written out (fma()), so the phase kernels
+# and the persistent kernel, which inline the same bodies in different
+# contexts, give bit-identical results (tests/test_gpu_half.py)
+$(OBJDIR)/gen/inst_%.o: NVFLAGS += -fmad=false $(INST_FLAGS)
 $(OBJDIR)/gen/large_%.o $(OBJDIR)/tsf_large.o: NVFLAGS += $(LARGE_FLAGS)
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)

@@ -94,6 +94,15 @@ bool fuse_vt() {
   return v == 1;
 }
 
+int persist_h_max_b() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TSF_PERSIST_MAX_B");
+    v = s ? atoi(s) : 0x7fffffff;   // every batch (0: the phase kernels in a graph)
+  }
+  return v;
+}
+
 int solve_groups(int B) {
   static int env = -2;
   if (env == -2) {

@@ -37,6 +37,8 @@ struct SolveGraphs {
 bool graph_mode();  // TSF_SOLVE_GRAPH (default 1)
 bool spec_reuse();  // TSF_SPEC_REUSE (default 1)
 bool fuse_vt();     // TSF_FUSE_VT (default 0): both BiCGSTAB phases of an iteration in one kernel
+int persist_h_max_b();   // TSF_PERSIST_MAX_B (default: no limit): largest batch the half-length
+                         // engine solves with one persistent kernel per instance (0: phase kernels)
 bool half_mode();   // TSF_HALF (default 1): half-length transform engine, tsf_half.cuh
 
 template <int LOG>

@@ -271,6 +271,24 @@ int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
   using S = KShape<N>;
   constexpr int kChunk = 4;
   cudaError_t e;
+  if constexpr (PC == 1 && !CG && half_ok<N>()) {
+    // small batches (one CTA per SM at most): the whole solve in one kernel
+    if (B <= persist_h_max_b() && use_half<N, PC, CG>(a)) {
+      // TSF_PERSIST_CTAS=2: the register-capped instantiation (two CTAs per SM)
+      static const bool two = [] {
+        const char* s = getenv("TSF_PERSIST_CTAS");
+        return s && s[0] == '2';
+      }();
+      SolveKernel kp = two ? k_krylov_persist_h<N, (HShape<N>::MIN_BLOCKS > 1 ? HShape<N>::MIN_BLOCKS : 1)>
+                           : k_krylov_persist_h<N, 1>;
+      const int smem = two ? HShape<N>::SMEM : HPersist<N>::BYTES;
+      static cudaError_t prep = prep_kernel(kp, smem);
+      if (prep != cudaSuccess) return launch_error(prep);
+      k_set_int<<<1, 1, 0, st>>>(a.active, B);
+      kp<<<B, HShape<N>::BLOCK, smem, st>>>(a, a.kst, a.active);
+      return launch_error(cudaGetLastError());
+    }
+  }
   if (a.graphs && graph_mode() && !persist_mode()) return solve_graph<N, PC, CG>(B, a, st);
   if (persist_mode()) {
     auto kp = k_krylov_persist<N, PC, CG>;

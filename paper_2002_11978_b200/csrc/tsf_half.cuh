@@ -247,16 +247,31 @@ TSF_D void apply_level_op_half(const double* __restrict__ xg, const double* __re
   }
 }
 
-// ---- begin: kappa, kappa_bar, checks, Strang filter of the level, r0, p_hat
+// Where an instance's p_hat, s_hat and stored half spectrum live: the plan's
+// global workspaces (phase kernels) or the CTA's shared memory (persistent
+// kernel) — generic pointers either way.
+struct HVec {
+  double* ph;
+  double* sh;
+  double2* hs;
+};
 template <int N>
-__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
-k_solve_begin_h(KrylovArgs a, KState* st, int* active) {
-  using S = HShape<N>;
-  constexpr int T = S::T;
-  extern __shared__ double2 sm[];
-  __shared__ double red[4 * 32];
-  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
-  const double2* tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
+TSF_D HVec hvec_global(const KrylovArgs& a) {
+  const int b = blockIdx.x;
+  return HVec{a.ph + (long)b * N, a.sh + (long)b * N, a.hspec + (long)b * (N / 2 + 1)};
+}
+
+// Every multiply-add of the phase bodies below is written out (fma /
+// __dmul_rn / __dadd_rn): the phase kernels and the persistent kernel inline
+// the same bodies in different contexts, and implicit contraction choices
+// that differ between them would make an instance's result depend on the
+// batch it is solved in (tests/test_gpu_half.py checks bit-identity).
+// ---- begin: kappa, kappa_bar, checks, Strang filter of the level, r0, p_hat
+// (returns true when the instance finished; tw: the staged twiddle table,
+// published by this function's first block reduction)
+template <int N>
+TSF_D bool dev_begin_h(const KrylovArgs& a, KState* st, int* active, double2* sm, double* red,
+                       const double2* tw, const HVec hv) {
   const int tid = threadIdx.x;
   const int b = blockIdx.x;
   const long ow = (long)b * N;
@@ -292,22 +307,22 @@ k_solve_begin_h(KrylovArgs a, KState* st, int* active) {
   kmin = block_min1(kmin, red);
   if (kmin <= 0.0) {
     finish_instance(a, st, active, b, 0, 0.0, TSF_KAPPA_NONPOS, sm);
-    return;
+    return true;
   }
   const double kmean = block_sum1(ksum, red) / N;
   const double kbar = a.kbar > 0.0 ? a.kbar : kmean;
   const double d = a.shift;
   double tmin = 1e308;
-  for (int k = tid; k < N; k += blockDim.x) tmin = fmin(tmin, d + kbar * ldt(&a.tab.pclam[k]).x);
+  for (int k = tid; k < N; k += blockDim.x) tmin = fmin(tmin, fma(kbar, ldt(&a.tab.pclam[k]).x, d));
   tmin = block_min1(tmin, red);
   if (tmin <= 0.0) {
     finish_instance(a, st, active, b, 0, 0.0, TSF_PRECOND_NONPOS, sm);
-    return;
+    return true;
   }
   // the level's Strang filter (even part of 1/total, 1/n folded in), k < n
   for (int k = tid; k < N; k += blockDim.x) {
     const double2 lam = ldt(&a.tab.pclam[k]);
-    a.pspec[ow + k] = 0.5 * (1.0 / (d + kbar * lam.x) + 1.0 / (d + kbar * lam.y)) / N;
+    a.pspec[ow + k] = 0.5 * (1.0 / fma(kbar, lam.x, d) + 1.0 / fma(kbar, lam.y, d)) / N;
   }
   double2 u[8];
   ld2<N>(u, a.rhs + ow);
@@ -326,11 +341,11 @@ k_solve_begin_h(KrylovArgs a, KState* st, int* active) {
   }
   if (sqrt(ss) == 0.0) {
     finish_instance(a, st, active, b, 0, 0.0, TSF_OK, sm);
-    return;
+    return true;
   }
   st2<N>(a.p + ow, u);
-  strang_half<N>(u, sm, tw, SpecTable{a.pspec + ow}, a.hspec + (long)b * (N / 2 + 1));
-  st2<N>(a.ph + ow, u);
+  strang_half<N>(u, sm, tw, SpecTable{a.pspec + ow}, hv.hs);
+  st2<N>(hv.ph, u);
   if (tid == 0) {
     KState s;
     s.rho = s.alpha = s.omega = 1.0;
@@ -342,20 +357,32 @@ k_solve_begin_h(KrylovArgs a, KState* st, int* active) {
     s.done = 0;
     st[b] = s;
   }
+  return false;
+}
+
+template <int N>
+__global__ void __launch_bounds__(HShape<N>::BLOCK, HShape<N>::MIN_BLOCKS)
+k_solve_begin_h(KrylovArgs a, KState* st, int* active) {
+  using S = HShape<N>;
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
+  const double2* tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
+  dev_begin_h<N>(a, st, active, sm, red, tw, hvec_global<N>(a));
 }
 
 // ---- v-phase: v = M p_hat, alpha, s = r - alpha v, ||s|| (early exit), s_hat
 // (returns true when the instance finished)
 template <int N>
 TSF_D bool dev_bicg_v_h(const KrylovArgs& a, KState* st, int* active, double2* sm, double* red,
-                        double* aux, const FilterTables& tab) {
+                        double* aux, const FilterTables& tab, const HVec hv) {
   const int b = blockIdx.x;
   const KState s = st[b];
   const int tid = threadIdx.x;
   const long ow = (long)b * N;
-  const double* phg = a.ph + ow;
+  const double* phg = hv.ph;
   const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + ow;
-  double2* hs = a.hspec + (long)b * (N / 2 + 1);
+  double2* hs = hv.hs;
   prefetch_l2(kg, N);
   prefetch_l2(a.r0w + ow, N);
   if (s.it != 1) prefetch_l2(a.r + ow, N);
@@ -381,8 +408,8 @@ TSF_D bool dev_bicg_v_h(const KrylovArgs& a, KState* st, int* active, double2* s
   part = 0.0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    u[c].x = rv[c].x - alpha * u[c].x;
-    u[c].y = rv[c].y - alpha * u[c].y;
+    u[c].x = fma(-alpha, u[c].x, rv[c].x);
+    u[c].y = fma(-alpha, u[c].y, rv[c].y);
     part = fma(u[c].x, u[c].x, part);
     part = fma(u[c].y, u[c].y, part);
   }
@@ -394,8 +421,8 @@ TSF_D bool dev_bicg_v_h(const KrylovArgs& a, KState* st, int* active, double2* s
     ld2<N>(pv, phg);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      xv[c].x = xv[c].x + alpha * pv[c].x;
-      xv[c].y = xv[c].y + alpha * pv[c].y;
+      xv[c].x = fma(alpha, pv[c].x, xv[c].x);
+      xv[c].y = fma(alpha, pv[c].y, xv[c].y);
     }
     st2<N>(a.x + ow, xv);
     finish_instance(a, st, active, b, s.it, snorm / s.nrm0, TSF_OK, sm);
@@ -403,7 +430,7 @@ TSF_D bool dev_bicg_v_h(const KrylovArgs& a, KState* st, int* active, double2* s
   }
   st2<N>(a.s + ow, u);
   strang_half<N>(u, sm, tab.tw, SpecTable{a.pspec + ow}, hs);
-  st2<N>(a.sh + ow, u);
+  st2<N>(hv.sh, u);
   if (tid == 0) {
     st[b].alpha = alpha;
     st[b].snorm = snorm;
@@ -412,21 +439,22 @@ TSF_D bool dev_bicg_v_h(const KrylovArgs& a, KState* st, int* active, double2* s
 }
 
 // ---- t-phase: t = M s_hat, omega, x/r update, ||r||, rho, beta, next p, p_hat
-template <int N>
+// SMV: p_hat / s_hat live in shared memory (persistent kernel): no global prefetch of them
+template <int N, bool SMV = false>
 TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* sm, double* red,
-                        double* aux, const FilterTables& tab) {
+                        double* aux, const FilterTables& tab, const HVec hv) {
   using S = HShape<N>;
   const int b = blockIdx.x;
   const KState s = st[b];
   const int tid = threadIdx.x;
   const long ow = (long)b * N;
-  const double* shg = a.sh + ow;
+  const double* shg = hv.sh;
   const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + ow;
-  double2* hs = a.hspec + (long)b * (N / 2 + 1);
+  double2* hs = hv.hs;
   prefetch_l2(kg, N);
   prefetch_l2(a.s + ow, N);
   prefetch_l2(a.xw + ow, N);
-  prefetch_l2(a.ph + ow, N);
+  if (!SMV) prefetch_l2(hv.ph, N);
   prefetch_l2(a.r0w + ow, N);
   prefetch_l2(a.p + ow, N);
   prefetch_l2(a.v + ow, N);
@@ -453,7 +481,7 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
   // x += alpha p_hat + omega s_hat
   {
     const double2* x2 = reinterpret_cast<const double2*>(a.xw + ow);
-    const double2* p2 = reinterpret_cast<const double2*>(a.ph + ow);
+    const double2* p2 = reinterpret_cast<const double2*>(hv.ph);
     const double2* h2 = reinterpret_cast<const double2*>(shg);
     double2* xo = reinterpret_cast<double2*>(a.xw + ow);
     // XC slots' operands before their stores (TSF_H_XUPD_CHUNK above)
@@ -472,8 +500,9 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
 #pragma unroll
       for (int q = 0; q < XC; ++q) {
         const int m = tid + (c0 + q) * S::T;
-        xo[m] = make_double2(xv[q].x + (s.alpha * pv[q].x + omega * hv[q].x),
-                             xv[q].y + (s.alpha * pv[q].y + omega * hv[q].y));
+        xo[m] = make_double2(
+            __dadd_rn(xv[q].x, fma(s.alpha, pv[q].x, __dmul_rn(omega, hv[q].x))),
+            __dadd_rn(xv[q].y, fma(s.alpha, pv[q].y, __dmul_rn(omega, hv[q].y))));
       }
     }
   }
@@ -484,8 +513,8 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
   red2.v[1] = 0.0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    u[c].x = sv[c].x - omega * u[c].x;
-    u[c].y = sv[c].y - omega * u[c].y;
+    u[c].x = fma(-omega, u[c].x, sv[c].x);
+    u[c].y = fma(-omega, u[c].y, sv[c].y);
     red2.v[0] = fma(u[c].x, u[c].x, red2.v[0]);
     red2.v[0] = fma(u[c].y, u[c].y, red2.v[0]);
     red2.v[1] = fma(r0v[c].x, u[c].x, red2.v[1]);
@@ -513,12 +542,12 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
   const double beta = (rho_new / s.rho_new) * (s.alpha / omega);
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    u[c].x = u[c].x + beta * (qv[c].x - omega * vv[c].x);
-    u[c].y = u[c].y + beta * (qv[c].y - omega * vv[c].y);
+    u[c].x = fma(beta, fma(-omega, vv[c].x, qv[c].x), u[c].x);
+    u[c].y = fma(beta, fma(-omega, vv[c].y, qv[c].y), u[c].y);
   }
   st2<N>(a.p + ow, u);
   strang_half<N>(u, sm, tab.tw, SpecTable{a.pspec + ow}, hs);
-  st2<N>(a.ph + ow, u);
+  st2<N>(hv.ph, u);
   if (tid == 0) {
     st[b].rho = s.rho_new;
     st[b].rho_new = rho_new;
@@ -541,11 +570,57 @@ k_bicg_h(KrylovArgs a, KState* st, int* active) {
   FilterTables tab = a.tab;
   tab.tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
   __syncthreads();   // twiddle table staged
+  const HVec hv = hvec_global<N>(a);
   if constexpr (PHASES & 1) {
-    if (dev_bicg_v_h<N>(a, st, active, sm, red, aux, tab)) return;
+    if (dev_bicg_v_h<N>(a, st, active, sm, red, aux, tab, hv)) return;
   }
   if constexpr (PHASES == 3) __syncthreads();   // st[b] (alpha, ||s||), s_hat and its spectrum
-  if constexpr (PHASES & 2) dev_bicg_t_h<N>(a, st, active, sm, red, aux, tab);
+  if constexpr (PHASES & 2) dev_bicg_t_h<N>(a, st, active, sm, red, aux, tab, hv);
+}
+
+// Whole level solve of one instance in ONE kernel (batches of at most one CTA
+// per SM: configs[0], single mid-size instances): the same phase bodies in a
+// loop, so the result is bit-identical to the phase kernels', without the
+// 3 graph nodes per iteration and the per-phase table staging.  One CTA per
+// SM lifts the register cap (launch bound 1: up to 255 registers), which is
+// what the full-length engine's persistent kernel lacked (it spilled 1.3 KB
+// per thread under the 128-register cap of 512-thread CTAs).
+// Its CTA is alone on the SM, so the shared memory the second CTA would use
+// holds the instance's hottest vectors instead: p_hat, s_hat (three reads and
+// a write per iteration each) and the stored half spectrum (generic
+// addressing: the phase bodies see ordinary pointers).
+template <int N>
+struct HPersist {
+  static constexpr int VEC_OFF = HShape<N>::SMEM;                    // p_hat | s_hat | spectrum
+  static constexpr int SMEM = VEC_OFF + 2 * N * 8 + (N / 2 + 2) * 16;
+#ifndef TSF_PERSIST_SMV
+#define TSF_PERSIST_SMV 1
+#endif
+  static constexpr bool SMV = TSF_PERSIST_SMV && SMEM <= kSmemCap;
+  static constexpr int BYTES = SMV ? SMEM : HShape<N>::SMEM;
+};
+template <int N, int MB>
+__global__ void __launch_bounds__(HShape<N>::BLOCK, MB)
+k_krylov_persist_h(KrylovArgs a, KState* st, int* active) {
+  using S = HShape<N>;
+  constexpr bool SMV = HPersist<N>::SMV && MB == 1;
+  extern __shared__ double2 sm[];
+  __shared__ double red[4 * 32];
+  double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
+  FilterTables tab = a.tab;
+  tab.tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
+  HVec hv = hvec_global<N>(a);
+  if constexpr (SMV) {
+    double* vec = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + HPersist<N>::VEC_OFF);
+    hv = HVec{vec, vec + N, reinterpret_cast<double2*>(vec + 2 * N)};
+  }
+  if (dev_begin_h<N>(a, st, active, sm, red, tab.tw, hv)) return;
+  for (;;) {
+    __syncthreads();   // st[b] and the previous phase's vectors (other threads' slots)
+    if (dev_bicg_v_h<N>(a, st, active, sm, red, aux, tab, hv)) return;
+    __syncthreads();
+    if (dev_bicg_t_h<N, SMV>(a, st, active, sm, red, aux, tab, hv)) return;
+  }
 }
 
 // ---- debug: the two building blocks alone (tests/test_gpu_half.py)

@@ -167,3 +167,21 @@ def test_half_large_control_flow_edges():
     xs, rep = P.solve_bicgstab(lev, pc, rhs, tol=1e-12)
     assert rep.converged and abs(rep.iterations - ref.iterations) <= 2
     assert rel_l2(xs, xr) <= 1e-10
+
+
+def test_half_persistent_kernel_bit_identical():
+    """Small batches run the whole solve in one persistent kernel per instance
+    (k_krylov_persist_h: the same phase bodies in a loop); its results must
+    equal the phase kernels' bit for bit (TSF_PERSIST_MAX_B=0 in a
+    subprocess), so an instance's result does not depend on its batch."""
+    import tempfile
+    n, B = 1024, 4
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        for tag, mb in (("persist", "148"), ("phases", "0")):
+            f = Path(td) / f"{tag}.npz"
+            env = dict(os.environ, TSF_PERSIST_MAX_B=mb)
+            subprocess.run([sys.executable, "-c", _solve_script(n, B), str(f)], check=True, env=env)
+            out[tag] = {k: v.copy() for k, v in np.load(f).items()}
+    np.testing.assert_array_equal(out["persist"]["its"], out["phases"]["its"])
+    np.testing.assert_array_equal(out["persist"]["x"], out["phases"]["x"])
