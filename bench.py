@@ -441,6 +441,11 @@ def main():
             launches += int(np.sum(4 + 18 * np.maximum(mx, 1)))
         elif large:    # host-driven chunks of 4 iterations, 17 kernels each
             launches += int(np.sum(4 + 17 * 4 * np.ceil(np.maximum(mx, 1) / 4.0)))
+        elif (os.environ.get("TSF_HALF", "1") != "0" and n >= 512 and n & (n - 1) == 0
+              and not fused and int(os.environ.get("TSF_PERSIST_MAX_B", "1000000000")) >= B):
+            # half-length persistent solve: counter init + ONE kernel per level
+            # (csrc/tsf_half.cuh k_krylov_persist_h, tsf_dispatch_impl.cuh solve_t)
+            launches += 2 * (m1 - m0)
         elif graph:    # one graph per level, G instance-group branches each
             # set, begin, WHILE { v, t, test } (csrc/tsf_dispatch_impl.cuh
             # solve_graph; G = solve_groups(B): TSF_SOLVE_GROUPS, default 4 for B >= 1024)
@@ -504,12 +509,16 @@ def main():
                  "+ k_lsc/k_lel_* (17 kernels per BiCGSTAB iteration)")
     else:
         hk = half and n >= 512 and n & (n - 1) == 0 and not fused
-        sname = ((f"tsf level solve: k_solve_begin_h + k_bicg_v_h/k_bicg_t_h<{n}> (half-length "
+        hp = hk and int(os.environ.get("TSF_PERSIST_MAX_B", "1000000000")) >= B
+        sname = ((f"tsf level solve: k_krylov_persist_h<{n},1> (half-length transforms, one "
+                  f"persistent {n // 16}-thread CTA per instance runs the whole BiCGSTAB solve)"
+                  if hp else
+                  f"tsf level solve: k_solve_begin_h + k_bicg_h<{n},1|2> (half-length "
                   f"transforms, {n // 16}-thread CTAs)" if hk else
                   f"tsf level solve: k_solve_begin + k_bicg_v/k_bicg_t<{n},1>")
                  + (" with fused SOE epilogue" if fused else "")
                  + (" (one CUDA graph per level: instance-group branches, each a conditional "
-                    "WHILE loop)" if graph else ""))
+                    "WHILE loop)" if graph and not hp else ""))
     k_solve = {"name": sname, "avg_ms": solve_ms / K,
                "GBps": solve_bytes / (solve_ms / K * 1e-3) / 1e9,
                "iterations_per_launch": its_sum / K, "algorithmic_bytes": solve_bytes}
@@ -540,9 +549,10 @@ def main():
             "share_of_step": (solve_ms if dom is k_solve else soe_ms) / ms,
             "note": ("large-n level solve: four-step transforms through L2/HBM"
                      if large else
-                     "level solve is transform (shared-memory latency / FP64) bound: ncu "
-                     "FP64 pipe 25-31%, LSU wavefronts 48-55% (profiles/r02/half_ncu.md); the "
-                     "SOE kernel alone runs at ~98% of the HBM peak")}
+                     "level solve is transform (shared-memory latency / FP64) bound "
+                     "(profiles/r02/half_ncu.md); an instance's vectors stay in L2 between "
+                     "its iterations (persistent CTA); the SOE kernel alone runs at ~98% of "
+                     "the HBM peak")}
     # FP64 view of the same launch: algorithmic flops per BiCGSTAB iteration
     # (SURVEY.md §8(d)): 2 Toeplitz products (5 L log2 L + L + 3n each: two
     # real length-L transforms), 2 Strang solves (5 n log2 n + 3n), ~20n

@@ -23,7 +23,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-SOLVE = ("k_solve_begin", "k_bicg_v", "k_bicg_t", "k_bicg_h", "k_cg_iter", "k_lcol_fwd", "k_lcol_inv",
+SOLVE = ("k_solve_begin", "k_bicg_v", "k_bicg_t", "k_bicg_h", "k_krylov_persist", "k_cg_iter", "k_lcol_fwd", "k_lcol_inv",
          "k_lrow", "k_lsc", "k_lel_", "k_lspec", "k_lloop_cond", "k_loop_cond", "k_set_int",
          "k_hcol_fwd", "k_hcol_inv", "k_hrow_strang", "k_hrow_mv", "k_hspec")
 SOE = ("k_soe",)
@@ -37,7 +37,7 @@ def main():
     ap.add_argument("--out", default=str(ROOT / "profiles" / "ncu_traffic.json"))
     args = ap.parse_args()
     from paper_2002_11978_b200 import _native
-    env = dict(os.environ, TSF_SOLVE_GRAPH="0")
+    env = dict(os.environ, TSF_SOLVE_GRAPH="0")   # (the persistent solve is one kernel anyway)
     bench = [sys.executable, str(ROOT / "bench.py"), "--workload", args.workload, "--steps",
              str(args.steps), "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-matvec"]
     if args.batch:
