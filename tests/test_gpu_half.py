@@ -169,16 +169,17 @@ def test_half_large_control_flow_edges():
     assert rel_l2(xs, xr) <= 1e-10
 
 
-def test_half_persistent_kernel_bit_identical():
-    """Small batches run the whole solve in one persistent kernel per instance
-    (k_krylov_persist_h: the same phase bodies in a loop); its results must
-    equal the phase kernels' bit for bit (TSF_PERSIST_MAX_B=0 in a
-    subprocess), so an instance's result does not depend on its batch."""
+@pytest.mark.parametrize("n,B", [(1024, 4), (4096, 3), (512, 300)])
+def test_half_persistent_kernel_bit_identical(n, B):
+    """The half-length engine runs the whole solve in one persistent kernel
+    per instance (k_krylov_persist_h: the same phase bodies in a loop, its hot
+    vectors in shared memory); its results must equal the phase kernels' bit
+    for bit (TSF_PERSIST_MAX_B=0 in a subprocess).  (512, 300): more CTAs than
+    SMs, so finished instances' SMs are back-filled."""
     import tempfile
-    n, B = 1024, 4
     out = {}
     with tempfile.TemporaryDirectory() as td:
-        for tag, mb in (("persist", "148"), ("phases", "0")):
+        for tag, mb in (("persist", "1000000"), ("phases", "0")):
             f = Path(td) / f"{tag}.npz"
             env = dict(os.environ, TSF_PERSIST_MAX_B=mb)
             subprocess.run([sys.executable, "-c", _solve_script(n, B), str(f)], check=True, env=env)
