@@ -279,11 +279,20 @@ int solve_t(int B, const KrylovArgs& a, cudaStream_t st) {
         const char* s = getenv("TSF_PERSIST_CTAS");
         return s && s[0] == '2';
       }();
-      SolveKernel kp = two ? k_krylov_persist_h<N, (HShape<N>::MIN_BLOCKS > 1 ? HShape<N>::MIN_BLOCKS : 1)>
-                           : k_krylov_persist_h<N, 1>;
-      const int smem = two ? HShape<N>::SMEM : HPersist<N>::BYTES;
-      static cudaError_t prep = prep_kernel(kp, smem);
-      if (prep != cudaSuccess) return launch_error(prep);
+      // batches of at most one CTA per SM keep every vector that fits on chip
+      static const int sms = [] {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+          n = 148;
+        return n;
+      }();
+      const bool full = !two && B <= sms && HPersist<N>::NV > 3;
+      SolveKernel kp = two    ? k_krylov_persist_h<N, (HShape<N>::MIN_BLOCKS > 1 ? HShape<N>::MIN_BLOCKS : 1), false>
+                       : full ? k_krylov_persist_h<N, 1, true>
+                              : k_krylov_persist_h<N, 1, false>;
+      const int smem = two ? HShape<N>::SMEM : full ? HPersist<N>::BYTES : HPersist<N>::bytes(HPersist<N>::NV >= 3 ? 3 : 0);
+      if ((e = prep_kernel(kp, smem)) != cudaSuccess) return launch_error(e);
       k_set_int<<<1, 1, 0, st>>>(a.active, B);
       kp<<<B, HShape<N>::BLOCK, smem, st>>>(a, a.kst, a.active);
       return launch_error(cudaGetLastError());

@@ -247,18 +247,57 @@ TSF_D void apply_level_op_half(const double* __restrict__ xg, const double* __re
   }
 }
 
-// Where an instance's p_hat, s_hat and stored half spectrum live: the plan's
-// global workspaces (phase kernels) or the CTA's shared memory (persistent
-// kernel) — generic pointers either way.
+// Where an instance's vectors live: the plan's global workspaces (phase
+// kernels) or the CTA's shared memory (persistent kernel: as many as fit,
+// hottest first) — generic pointers either way.  xg: the caller's solution
+// vector, written when the instance finishes if x lives on chip (x != xg).
 struct HVec {
   double* ph;
   double* sh;
   double2* hs;
+  double* s;
+  double* v;
+  double* p;
+  double* r;
+  const double* r0;
+  double* x;
+  double* xg;
+  const double* kap;
+  double* pspec;
+  bool onchip;      // every vector above the solve reads is in shared memory: no L2 prefetch
+  bool kap_copy;    // kap points at a shared-memory copy begin has to fill
+  bool r0_copy;     // likewise r0
 };
 template <int N>
 TSF_D HVec hvec_global(const KrylovArgs& a) {
   const int b = blockIdx.x;
-  return HVec{a.ph + (long)b * N, a.sh + (long)b * N, a.hspec + (long)b * (N / 2 + 1)};
+  const long ow = (long)b * N;
+  HVec h;
+  h.ph = a.ph + ow;
+  h.sh = a.sh + ow;
+  h.hs = a.hspec + (long)b * (N / 2 + 1);
+  h.s = a.s + ow;
+  h.v = a.v + ow;
+  h.p = a.p + ow;
+  h.r = a.r + ow;
+  h.r0 = a.r0w + ow;
+  h.x = a.xw + ow;
+  h.xg = a.x + ow;
+  h.kap = (a.kappa ? a.kappa : (const double*)a.kwork) + ow;
+  h.pspec = a.pspec + ow;
+  h.onchip = false;
+  h.kap_copy = false;
+  h.r0_copy = false;
+  return h;
+}
+// the caller's x from the on-chip iterate, before an instance finishes
+template <int N>
+TSF_D void publish_x_h(const HVec& hv) {
+  if (hv.x != hv.xg) {
+    double2 t[8];
+    ld2<N>(t, hv.x);
+    st2<N>(hv.xg, t);
+  }
 }
 
 // Every multiply-add of the phase bodies below is written out (fma /
@@ -297,6 +336,7 @@ TSF_D bool dev_begin_h(const KrylovArgs& a, KState* st, int* active, double2* sm
       }
       st2<N>(a.kwork + ow, kk);
     }
+    if (hv.kap_copy) st2<N>(const_cast<double*>(hv.kap), kk);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       ksum += kk[c].x;
@@ -322,7 +362,7 @@ TSF_D bool dev_begin_h(const KrylovArgs& a, KState* st, int* active, double2* sm
   // the level's Strang filter (even part of 1/total, 1/n folded in), k < n
   for (int k = tid; k < N; k += blockDim.x) {
     const double2 lam = ldt(&a.tab.pclam[k]);
-    a.pspec[ow + k] = 0.5 * (1.0 / fma(kbar, lam.x, d) + 1.0 / fma(kbar, lam.y, d)) / N;
+    hv.pspec[k] = 0.5 * (1.0 / fma(kbar, lam.x, d) + 1.0 / fma(kbar, lam.y, d)) / N;
   }
   double2 u[8];
   ld2<N>(u, a.rhs + ow);
@@ -337,14 +377,16 @@ TSF_D bool dev_begin_h(const KrylovArgs& a, KState* st, int* active, double2* sm
     double2 zero[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) zero[c] = make_double2(0.0, 0.0);
-    st2<N>(a.x + ow, zero);
+    st2<N>(hv.x, zero);
+    if (hv.x != hv.xg) st2<N>(hv.xg, zero);
   }
+  if (hv.r0_copy) st2<N>(const_cast<double*>(hv.r0), u);
   if (sqrt(ss) == 0.0) {
     finish_instance(a, st, active, b, 0, 0.0, TSF_OK, sm);
     return true;
   }
-  st2<N>(a.p + ow, u);
-  strang_half<N>(u, sm, tw, SpecTable{a.pspec + ow}, hv.hs);
+  st2<N>(hv.p, u);
+  strang_half<N>(u, sm, tw, SpecTable{hv.pspec}, hv.hs);
   st2<N>(hv.ph, u);
   if (tid == 0) {
     KState s;
@@ -381,18 +423,20 @@ TSF_D bool dev_bicg_v_h(const KrylovArgs& a, KState* st, int* active, double2* s
   const int tid = threadIdx.x;
   const long ow = (long)b * N;
   const double* phg = hv.ph;
-  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + ow;
+  const double* kg = hv.kap;
   double2* hs = hv.hs;
-  prefetch_l2(kg, N);
-  prefetch_l2(a.r0w + ow, N);
-  if (s.it != 1) prefetch_l2(a.r + ow, N);
+  if (!hv.onchip) {
+    prefetch_l2(kg, N);
+    prefetch_l2(hv.r0, N);
+    if (s.it != 1) prefetch_l2(hv.r, N);
+  }
   double2 u[8];
   apply_level_op_half<N, true>(phg, kg, a.shift, u, sm, aux, tab, hs);   // u = v = M p_hat
-  const double* rc = (s.it == 1 ? a.r0w : a.r) + ow;
+  const double* rc = s.it == 1 ? hv.r0 : (const double*)hv.r;
   double2 r0v[8], rv[8];
-  ld2<N>(r0v, a.r0w + ow);
+  ld2<N>(r0v, hv.r0);
   ld2<N>(rv, rc);
-  st2<N>(a.v + ow, u);
+  st2<N>(hv.v, u);
   double part = 0.0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -401,6 +445,7 @@ TSF_D bool dev_bicg_v_h(const KrylovArgs& a, KState* st, int* active, double2* s
   }
   const double denom = block_sum1(part, red);
   if (denom == 0.0) {
+    publish_x_h<N>(hv);
     finish_instance(a, st, active, b, s.it, s.rnorm / s.nrm0, TSF_BD_R0V, sm);
     return true;
   }
@@ -417,19 +462,19 @@ TSF_D bool dev_bicg_v_h(const KrylovArgs& a, KState* st, int* active, double2* s
   if (snorm / s.nrm0 < a.tol) {
     // x += alpha p_hat (early exit counts as a full iteration, krylov.py:135-137)
     double2 xv[8], pv[8];
-    ld2<N>(xv, a.xw + ow);
+    ld2<N>(xv, hv.x);
     ld2<N>(pv, phg);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       xv[c].x = fma(alpha, pv[c].x, xv[c].x);
       xv[c].y = fma(alpha, pv[c].y, xv[c].y);
     }
-    st2<N>(a.x + ow, xv);
+    st2<N>(hv.xg, xv);
     finish_instance(a, st, active, b, s.it, snorm / s.nrm0, TSF_OK, sm);
     return true;
   }
-  st2<N>(a.s + ow, u);
-  strang_half<N>(u, sm, tab.tw, SpecTable{a.pspec + ow}, hs);
+  st2<N>(hv.s, u);
+  strang_half<N>(u, sm, tab.tw, SpecTable{hv.pspec}, hs);
   st2<N>(hv.sh, u);
   if (tid == 0) {
     st[b].alpha = alpha;
@@ -449,19 +494,21 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
   const int tid = threadIdx.x;
   const long ow = (long)b * N;
   const double* shg = hv.sh;
-  const double* kg = (a.kappa ? a.kappa : (const double*)a.kwork) + ow;
+  const double* kg = hv.kap;
   double2* hs = hv.hs;
-  prefetch_l2(kg, N);
-  prefetch_l2(a.s + ow, N);
-  prefetch_l2(a.xw + ow, N);
-  if (!SMV) prefetch_l2(hv.ph, N);
-  prefetch_l2(a.r0w + ow, N);
-  prefetch_l2(a.p + ow, N);
-  prefetch_l2(a.v + ow, N);
+  if (!hv.onchip) {
+    prefetch_l2(kg, N);
+    prefetch_l2(hv.s, N);
+    prefetch_l2(hv.x, N);
+    if (!SMV) prefetch_l2(hv.ph, N);
+    prefetch_l2(hv.r0, N);
+    prefetch_l2(hv.p, N);
+    prefetch_l2(hv.v, N);
+  }
   double2 u[8];
   apply_level_op_half<N, true>(shg, kg, a.shift, u, sm, aux, tab, hs);   // u = t = M s_hat
   double2 sv[8];
-  ld2<N>(sv, a.s + ow);
+  ld2<N>(sv, hv.s);
   Vals<2> red2;
   red2.v[0] = 0.0;
   red2.v[1] = 0.0;
@@ -474,16 +521,17 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
   }
   red2 = block_sum<2>(red2, red);
   if (red2.v[0] == 0.0) {
+    publish_x_h<N>(hv);
     finish_instance(a, st, active, b, s.it, s.snorm / s.nrm0, TSF_BD_OMEGA_DEN, sm);
     return true;
   }
   const double omega = red2.v[1] / red2.v[0];
   // x += alpha p_hat + omega s_hat
   {
-    const double2* x2 = reinterpret_cast<const double2*>(a.xw + ow);
+    const double2* x2 = reinterpret_cast<const double2*>(hv.x);
     const double2* p2 = reinterpret_cast<const double2*>(hv.ph);
     const double2* h2 = reinterpret_cast<const double2*>(shg);
-    double2* xo = reinterpret_cast<double2*>(a.xw + ow);
+    double2* xo = reinterpret_cast<double2*>(hv.x);
     // XC slots' operands before their stores (TSF_H_XUPD_CHUNK above)
 #pragma unroll
     constexpr int XC = TSF_H_XUPD_CHUNK;
@@ -508,7 +556,7 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
   }
   // r = s - omega t
   double2 r0v[8];
-  ld2<N>(r0v, a.r0w + ow);
+  ld2<N>(r0v, hv.r0);
   red2.v[0] = 0.0;
   red2.v[1] = 0.0;
 #pragma unroll
@@ -520,11 +568,11 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
     red2.v[1] = fma(r0v[c].x, u[c].x, red2.v[1]);
     red2.v[1] = fma(r0v[c].y, u[c].y, red2.v[1]);
   }
-  st2<N>(a.r + ow, u);
+  st2<N>(hv.r, u);
   // operands of the next p: in flight during the reduction
   double2 qv[8], vv[8];
-  ld2<N>(qv, a.p + ow);
-  ld2<N>(vv, a.v + ow);
+  ld2<N>(qv, hv.p);
+  ld2<N>(vv, hv.v);
   red2 = block_sum<2>(red2, red);
   const double rnorm = sqrt(red2.v[0]);
   const double rel = rnorm / s.nrm0;
@@ -532,6 +580,10 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
   const int fin = rel < a.tol ? 1 : omega == 0.0 ? 2 : s.it >= a.max_iters ? 3
                   : rho_new == 0.0 ? 4 : 0;
   if (fin) {
+    if (hv.x != hv.xg) {
+      __syncthreads();   // every thread's slots of the on-chip x
+      publish_x_h<N>(hv);
+    }
     if (fin == 1) finish_instance(a, st, active, b, s.it, rel, TSF_OK, sm);
     else if (fin == 2) finish_instance(a, st, active, b, s.it, rel, TSF_BD_OMEGA, sm);
     else if (fin == 3) finish_instance(a, st, active, b, a.max_iters, rel, TSF_NOT_CONVERGED, sm);
@@ -545,8 +597,8 @@ TSF_D bool dev_bicg_t_h(const KrylovArgs& a, KState* st, int* active, double2* s
     u[c].x = fma(beta, fma(-omega, vv[c].x, qv[c].x), u[c].x);
     u[c].y = fma(beta, fma(-omega, vv[c].y, qv[c].y), u[c].y);
   }
-  st2<N>(a.p + ow, u);
-  strang_half<N>(u, sm, tab.tw, SpecTable{a.pspec + ow}, hs);
+  st2<N>(hv.p, u);
+  strang_half<N>(u, sm, tab.tw, SpecTable{hv.pspec}, hs);
   st2<N>(hv.ph, u);
   if (tid == 0) {
     st[b].rho = s.rho_new;
@@ -591,35 +643,62 @@ k_bicg_h(KrylovArgs a, KState* st, int* active) {
 // addressing: the phase bodies see ordinary pointers).
 template <int N>
 struct HPersist {
-  static constexpr int VEC_OFF = HShape<N>::SMEM;                    // p_hat | s_hat | spectrum
-  static constexpr int SMEM = VEC_OFF + 2 * N * 8 + (N / 2 + 2) * 16;
+  static constexpr int VEC_OFF = HShape<N>::SMEM;
 #ifndef TSF_PERSIST_SMV
 #define TSF_PERSIST_SMV 1
 #endif
-  static constexpr bool SMV = TSF_PERSIST_SMV && SMEM <= kSmemCap;
-  static constexpr int BYTES = SMV ? SMEM : HShape<N>::SMEM;
+  // shared-memory residents in order of traffic per iteration: p_hat, s_hat,
+  // half spectrum (NV >= 3: n = 4096), then s, v, p, r, x, r0, kappa (NV = 10:
+  // n <= 2048) and the Strang filter (NV = 11: n <= 1024)
+  static constexpr int HS_BYTES = (N / 2 + 2) * 16;
+  static constexpr int bytes(int nv) { return VEC_OFF + (nv >= 3 ? HS_BYTES + (nv - 1) * N * 8 : nv * N * 8); }
+  static constexpr int NV = !TSF_PERSIST_SMV            ? 0
+                            : bytes(11) <= kSmemCap     ? 11
+                            : bytes(10) <= kSmemCap     ? 10
+                            : bytes(3) <= kSmemCap      ? 3
+                                                        : 0;
+  static constexpr int BYTES = bytes(NV);
 };
-template <int N, int MB>
+// FULL: every vector that fits on chip (small batches: one CTA per SM anyway);
+// otherwise only p_hat / s_hat / spectrum, so that several CTAs of a small
+// grid size still share an SM.  Same arithmetic either way.
+template <int N, int MB, bool FULL>
 __global__ void __launch_bounds__(HShape<N>::BLOCK, MB)
 k_krylov_persist_h(KrylovArgs a, KState* st, int* active) {
   using S = HShape<N>;
-  constexpr bool SMV = HPersist<N>::SMV && MB == 1;
+  constexpr int NV = MB != 1 ? 0 : FULL ? HPersist<N>::NV : (HPersist<N>::NV >= 3 ? 3 : 0);
   extern __shared__ double2 sm[];
   __shared__ double red[4 * 32];
   double* aux = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::FFT_BYTES);
   FilterTables tab = a.tab;
   tab.tw = stage_tw_half<N>(a.tab.tw, reinterpret_cast<double2*>(aux + N));
   HVec hv = hvec_global<N>(a);
-  if constexpr (SMV) {
+  if constexpr (NV >= 3) {
     double* vec = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + HPersist<N>::VEC_OFF);
-    hv = HVec{vec, vec + N, reinterpret_cast<double2*>(vec + 2 * N)};
+    hv.ph = vec;
+    hv.sh = vec + N;
+    hv.hs = reinterpret_cast<double2*>(vec + 2 * N);
+    if constexpr (NV >= 10) {
+      double* w = vec + 2 * N + HPersist<N>::HS_BYTES / 8;
+      hv.s = w;
+      hv.v = w + N;
+      hv.p = w + 2 * N;
+      hv.r = w + 3 * N;
+      hv.x = w + 4 * N;
+      hv.r0 = w + 5 * N;
+      hv.r0_copy = true;
+      hv.kap = w + 6 * N;
+      hv.kap_copy = true;
+      hv.onchip = true;
+      if constexpr (NV >= 11) hv.pspec = w + 7 * N;
+    }
   }
   if (dev_begin_h<N>(a, st, active, sm, red, tab.tw, hv)) return;
   for (;;) {
     __syncthreads();   // st[b] and the previous phase's vectors (other threads' slots)
     if (dev_bicg_v_h<N>(a, st, active, sm, red, aux, tab, hv)) return;
     __syncthreads();
-    if (dev_bicg_t_h<N, SMV>(a, st, active, sm, red, aux, tab, hv)) return;
+    if (dev_bicg_t_h<N, (NV >= 3)>(a, st, active, sm, red, aux, tab, hv)) return;
   }
 }
 
