@@ -530,12 +530,14 @@ def main():
              "algorithmic_bytes": soe_bytes}
     dom = k_solve if solve_ms >= soe_ms else k_soe
     # ncu DRAM bytes of the same kernels, from a capture of THIS build only
-    # (profiles/ncu_traffic.json, keyed by workload and the library's sha256;
+    # (profiles/ncu_traffic.json, keyed by workload and the sha256 of the kernel
+    # sources — nvcc output is not bit-reproducible — or of the library file;
     # tools/ncu_traffic.py writes it): per instance-iteration of the level solve
     traffic, traffic_src = None, "no ncu capture of this build for this workload"
     try:
         tr = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())[args.workload]
-        if tr.get("lib_sha256") == _native.lib_sha256():
+        if (tr.get("src_sha256") == _native.src_sha256() and "TSF_LIB" not in os.environ) or \
+                tr.get("lib_sha256") == _native.lib_sha256():
             traffic = (tr["dram_bytes_per_instance_iteration"] * its_sum / K
                        if dom is k_solve else tr["soe_dram_bytes_per_level"] * B / tr["B"])
             traffic_src = (f"ncu dram__bytes_read+write of the same kernels ({tr['capture']}) "

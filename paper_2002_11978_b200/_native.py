@@ -182,6 +182,22 @@ class Plan:
             pass
 
 
+def src_sha256() -> str:
+    """sha256 over the kernel sources the library is built from (csrc/, the C
+    header, the Makefile): ties a profile to the CODE it measured.  nvcc's
+    output is not bit-reproducible (a fresh build of the same sources has a
+    different file hash), so the library file's own hash cannot do that."""
+    import hashlib
+    root = Path(__file__).resolve().parent
+    files = sorted(p for p in (root / "csrc").rglob("*") if p.is_file())
+    files += [root.parent / "include" / "tsfrac_b200.h", root.parent / "Makefile"]
+    h = hashlib.sha256()
+    for p in files:
+        h.update(str(p.relative_to(root.parent)).encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()
+
+
 def lib_sha256(path: Optional[os.PathLike] = None) -> str:
     """sha256 of the loaded library file (ties profiles to the build they measured)."""
     import hashlib

@@ -8,8 +8,8 @@ runs `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,...` over
 by one, so every launch is captured), sums the bytes of the solve kernels and
 of the SOE kernels over the timed levels, normalises by the instance-
 iterations the bench line reports, and records the result with the
-library's sha256 in profiles/ncu_traffic.json — bench.py quotes
-roofline.traffic only when the sha matches the library it runs.
+library's and the kernel sources' sha256 in profiles/ncu_traffic.json —
+bench.py quotes roofline.traffic only when one of them matches what it runs.
 """
 import argparse
 import csv
@@ -80,7 +80,8 @@ def main():
     soe = sum(nbytes(v) for _, nm, v in launches[start:] if any(s in nm for s in SOE))
     K = bl["steps"]
     its = bl["kernels"]["level_solve"]["iterations_per_launch"] * K
-    rec = {"lib_sha256": _native.lib_sha256(), "B": bl["config"]["instances_per_gpu"],
+    rec = {"lib_sha256": _native.lib_sha256(), "src_sha256": _native.src_sha256(),
+           "B": bl["config"]["instances_per_gpu"],
            "dram_bytes_per_instance_iteration": solve / its,
            "soe_dram_bytes_per_level": soe / K,
            "algorithmic_bytes_per_instance_iteration": 216 * bl["config"]["n"],
